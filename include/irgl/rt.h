@@ -1,0 +1,235 @@
+/*
+ * irgl/rt.h — C-ABI of the B200-native IrGL worklist graph runtime (libirgl_rt.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 1607.05707 ("Lowering IrGL to CUDA"):
+ * worklist-driven irregular graph operators over CSR behind IrGL's operator API.  The reference
+ * ships the operator vocabulary as an AST (reference/proj/core/include/irgl/ast.hpp:97-233) and
+ * specifies — but does not ship — its executors:
+ *   run_host(module, entry, bindings, config)
+ *   launch_kernel(kernel, args, pipe_state, config)
+ *   run_pipe(pipe_stmt, machine, config)
+ *   lower_orchestration / outline_pipe
+ * Each entry point below names the construct it replaces.  Plain pointers and sizes only; no
+ * torch or CUDA types cross the boundary.
+ *
+ * Conventions (kept from the reference):
+ *   - errors are values: every call returns irgl_status_t and never throws or aborts
+ *     (reference diag.hpp:20-27); irgl_last_error() gives "RULE: message";
+ *   - single-threaded orchestration: one host thread per irgl_ctx;
+ *   - INF is INT32_MAX in int32 storage;
+ *   - work items cross the ABI as int64 and are stored as uint32 on the device;
+ *     ids >= 2^32 are rejected with IRGL_E_INVALID.
+ * Ownership: host arrays are borrowed for the duration of a call and copied; handles own their
+ * device memory; *_destroy frees it; results are copied into caller buffers.
+ */
+#ifndef IRGL_RT_H
+#define IRGL_RT_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IRGL_ABI_VERSION 1
+#define IRGL_INF 2147483647
+
+typedef int32_t irgl_status_t;
+enum {
+  IRGL_OK = 0,
+  IRGL_E_INVALID = 1,        /* bad argument / id out of range                                */
+  IRGL_E_USAGE = 2,          /* API misuse (wrong handle, op needs a graph / a pipe, ...)      */
+  IRGL_E_OOM = 3,            /* device allocation failed                                       */
+  IRGL_E_WL_OVERFLOW = 4,    /* worklist initialiser / push beyond WorklistInit.size */
+  IRGL_E_OCCUPANCY = 5,      /* barrier launch > co-resident threads  */
+  IRGL_E_OUTLINE_EMPTY = 6,  /* T_control = empty set                     */
+  IRGL_E_CUDA = 7,           /* CUDA runtime error (message in irgl_last_error)                */
+  IRGL_E_NCCL = 8,           /* NCCL error / async error                                       */
+  IRGL_E_UNSUPPORTED = 9     /* combination not supported by this build                        */
+};
+
+/* ast.hpp:90 Reduction {Any, All}; NONE = invocation without a return cell. */
+typedef enum { IRGL_RED_NONE = 0, IRGL_RED_ANY = 1, IRGL_RED_ALL = 2 } irgl_reduction;
+/* PAPER.md:363 pipe context worklists in / out / retry. */
+typedef enum { IRGL_WL_IN = 0, IRGL_WL_OUT = 1, IRGL_WL_RETRY = 2 } irgl_wl;
+/* ast.hpp:193 IterateCond {While|Until}; NONE = no reduction condition. */
+typedef enum { IRGL_COND_NONE = 0, IRGL_COND_WHILE = 1, IRGL_COND_UNTIL = 2 } irgl_cond_mode;
+/* ast.hpp:91 CondCombiner {And, Or} for ExtraCond. */
+typedef enum { IRGL_COMB_OR = 0, IRGL_COMB_AND = 1 } irgl_combiner;
+/* ast.hpp:89 ForAllMapping {Consecutive, Blocked}. */
+typedef enum { IRGL_MAP_CONSECUTIVE = 0, IRGL_MAP_BLOCKED = 1 } irgl_mapping;
+
+/* The plain (device) kernels this runtime implements — the north-star operators in IrGL form
+ * plus the tiny operators the SPEC's own examples are phrased in. */
+typedef enum {
+  IRGL_OP_BFS = 0,   /* Listing 2: level[dst]==INF -> level=LEVEL; push */
+  IRGL_OP_SSSP = 1,  /* data-driven Bellman-Ford: atomicMin(dist[dst], dist[n]+w) < old -> push */
+  IRGL_OP_CC = 2,    /* topology-driven hook (CAS larger root onto smaller) + pointer jumping,
+                        Iterate While Any; labels = min vertex id per component          */
+  IRGL_OP_PR = 3,    /* topology-driven pull Jacobi PageRank, fp64, ReduceAndReturn(|d|>tol) */
+  IRGL_OP_TC = 4,    /* degree-oriented intersection triangle count (Sum: extension, App. B6) */
+  IRGL_OP_CC_LP = 5, /* data-driven min-label propagation (worklist form of CC)              */
+  /* SPEC example operators (tests): */
+  IRGL_OP_TEST_COUNTDOWN = 100, /* pop x; if x+1 < guard: push x+1 */
+  IRGL_OP_TEST_RETRY_ODD = 101, /* odd x retried `guard` times, then pushed */
+  IRGL_OP_TEST_REDUCE = 102,    /* ReduceAndReturn(values[x]) */
+  IRGL_OP_TEST_NOPUSH = 103,    /* pops, never pushes */
+  IRGL_OP_TEST_PUSHPOP = 104,   /* records popped_at[x]=launch; push x+guard */
+  IRGL_OP_TEST_FORALL_MAP = 105 /* records thread_of[x] = global thread id */
+} irgl_op;
+
+typedef struct irgl_ctx irgl_ctx;
+typedef struct irgl_graph irgl_graph;
+typedef struct irgl_pipe irgl_pipe;
+
+/* Runtime configuration (the reference's SimConfig / CLI flags). */
+typedef struct irgl_config {
+  int32_t outline;               /* default for irgl_iterate: 0 host loop, 1 outlined, -1 auto */
+  int32_t blocks_per_sm;         /* FixedFromSM multiplier; 0 = occupancy    */
+  int32_t retry_serialize_after; /* Retry conflict management; 0 -> 4          */
+  int32_t warp_threshold;        /* degree >= -> warp-cooperative expansion; 0 -> 32            */
+  int32_t cta_threshold;         /* degree >= -> CTA chunk list (grid edge-balanced); 0 -> 1024 */
+  int32_t chunk_edges;           /* edges per CTA chunk; 0 -> 2048                              */
+  int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
+  int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
+  int32_t reserved[8];
+} irgl_config;
+
+/* Kernel arguments (the Invoke/Iterate `args`). */
+typedef struct irgl_op_args {
+  int64_t round_start;   /* value of the round counter (LEVEL) at the first invocation; 0 -> 1 */
+  int64_t guard;         /* test operators                                                   */
+  double pr_damping;     /* 0 -> 0.85                                                          */
+  double pr_tol;         /* 0 -> 1e-6 (absolute, per vertex)                                   */
+  const int32_t* values; /* IRGL_OP_TEST_REDUCE: per-item booleans (copied)                   */
+  int64_t nvalues;
+  int32_t mapping;       /* irgl_mapping of the outer ForAll (test operators)                  */
+  int32_t threads;       /* test operators: total CUDA threads (0 = planner's choice)          */
+  int32_t reserved[6];
+} irgl_op_args;
+
+/* Iterate [While|Until Any|All] kernel(args) [ExtraCond] (ast.hpp:186-204). */
+typedef struct irgl_iterate_opts {
+  int32_t cond_mode;   /* irgl_cond_mode                                                      */
+  int32_t reduction;   /* irgl_reduction of the cond (and the invocation's return cell)        */
+  int32_t extra_comb;  /* irgl_combiner joining ExtraCond with the empty-worklist test         */
+  int32_t outline;     /* -1 ctx default, 0 host-orchestrated, 1 outlined persistent kernel    */
+  int64_t max_rounds;  /* ExtraCond: exit when rounds >= max_rounds (0 = none)                 */
+  int32_t reset;       /* 1: (re)initialise the operator's node state from the pipe first      */
+  int32_t reserved[5];
+} irgl_iterate_opts;
+
+typedef struct irgl_iter_stats {
+  int64_t rounds;          /* invocations (between_rounds executions)                          */
+  int64_t launches;        /* kernel launches incl. retry relaunches (outlined: 1)             */
+  int64_t popped;          /* items popped                                                     */
+  int64_t pushes;          /* items pushed to out (local + remote-applied)                     */
+  int64_t retries;         /* items routed through the retry worklist                          */
+  int64_t edges;           /* directed edges scanned                                           */
+  int64_t remote_updates;  /* updates sent to other partitions                                 */
+  int64_t exchange_bytes;  /* bytes moved between partitions                                   */
+  int64_t serial_launches; /* retry launches executed serialised                               */
+  int32_t last_reduced;    /* last invocation's Any/All value, -1 if none                      */
+  int32_t outlined;        /* 1 if the loop ran as one persistent kernel                       */
+  double device_ms;        /* CUDA-event time of the whole iterate on the ctx stream           */
+} irgl_iter_stats;
+
+/* Device graph generator (§8d synthetic inputs). */
+typedef enum { IRGL_GEN_RMAT = 0, IRGL_GEN_GRID = 1 } irgl_gen_kind;
+typedef struct irgl_gen_spec {
+  int32_t kind;          /* irgl_gen_kind                                                       */
+  int32_t scale;         /* RMAT: N = 2^scale                                                   */
+  int32_t edge_factor;   /* RMAT: 16                                                            */
+  int32_t width, height; /* GRID                                                                */
+  int32_t diag;          /* GRID: add (x,y)-(x+1,y+1)                                           */
+  int32_t cut_period;    /* GRID: cut vertical edges between rows r,r+1 when r%p == p-1         */
+  int32_t perc_keep_ppm; /* GRID: keep probability in ppm (1000000 = all)                       */
+  uint64_t seed;         /* RMAT graph seed                                                     */
+  uint64_t wseed;        /* weight seed (11)                                                    */
+  uint64_t perc_seed;    /* GRID percolation seed (5)                                           */
+  int32_t reserved[8];
+} irgl_gen_spec;
+
+typedef struct irgl_graph_info {
+  int64_t n, m;                 /* global vertices / directed edges                            */
+  int64_t local_n, local_m;     /* this process's partition(s)                                 */
+  int64_t lo, hi;               /* owned vertex range of the first local partition             */
+  int32_t partitions;           /* total partitions                                            */
+  int32_t has_weights;
+  int64_t max_degree;
+} irgl_graph_info;
+
+/* ---- context ------------------------------------------------------------------------------ */
+/* Single process.  ndev devices; the graph is split into max(ndev, cfg->logical_partitions)
+ * vertex partitions, partition p on devices[p % ndev]. */
+irgl_status_t irgl_ctx_create(const int* devices, int ndev, const irgl_config* cfg, irgl_ctx** out);
+/* One process per GPU (torchrun): rank `rank` of `nranks`, NCCL unique id from rank 0. */
+irgl_status_t irgl_nccl_unique_id(void* id128);
+irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void* id128,
+                                   const irgl_config* cfg, irgl_ctx** out);
+irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx);
+irgl_status_t irgl_ctx_sync(irgl_ctx* ctx);
+const char* irgl_last_error(const irgl_ctx* ctx); /* ctx may be NULL: last global error */
+int irgl_abi_version(void);
+
+/* ---- graph (reference Value::Graph; builtins edges/dst/weight) ----- */
+irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const int64_t* row_ptr,
+                                    const int32_t* col, const int32_t* weight /*nullable*/,
+                                    irgl_graph** out);
+irgl_status_t irgl_graph_generate(irgl_ctx* ctx, const irgl_gen_spec* spec, irgl_graph** out);
+irgl_status_t irgl_graph_info_get(const irgl_graph* g, irgl_graph_info* info);
+/* Copies the CSR of the local partitions back (single-process: the whole graph). */
+irgl_status_t irgl_graph_download(irgl_graph* g, int64_t* row_ptr, int32_t* col, int32_t* weight);
+irgl_status_t irgl_graph_destroy(irgl_graph* g);
+
+/* ---- pipe context {in, out, retry} ------------------------ */
+irgl_status_t irgl_pipe_create(irgl_ctx* ctx, int64_t capacity /*WorklistInit.size*/,
+                               irgl_pipe** out);
+/* WorklistInit Scalars (ast.hpp:101) / FromArray (ast.hpp:104).  With a graph of P>1
+ * partitions each item is routed to its owner partition. */
+irgl_status_t irgl_pipe_init_scalars(irgl_pipe* p, const int64_t* items, int64_t count);
+irgl_status_t irgl_pipe_init_from_array(irgl_pipe* p, const int64_t* arr, int64_t len);
+irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end); /* iota */
+irgl_status_t irgl_pipe_size(const irgl_pipe* p, irgl_wl which, int64_t* out);
+irgl_status_t irgl_pipe_read(irgl_pipe* p, irgl_wl which, int64_t* items, int64_t cap,
+                             int64_t* count);
+irgl_status_t irgl_pipe_destroy(irgl_pipe* p);
+
+/* ---- operator state -------------------------------------------------------------------------- */
+/* Initialise node properties for `op` (level/dist = INF except the pipe's in-items = 0; CC label
+ * = id; PR rank = 1/N).  pipe may be NULL for topology-driven operators. */
+irgl_status_t irgl_op_reset(irgl_ctx* ctx, irgl_graph* g, irgl_op op, const irgl_op_args* args,
+                            irgl_pipe* pipe);
+
+/* ---- orchestration ------------------------------------------------------------------------- */
+/* [Any|All(] Invoke kernel(args) [)] — PAPER.md:88-90: launch; while retry is
+ * non-empty swap in<->retry and relaunch (out kept); then swap in<->out and clear out.
+ * `reduced` receives the return cell (identity Any->0, All->1 when nothing was evaluated). */
+irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe /*NULL: non-worklist op*/, irgl_graph* g,
+                          irgl_op op, const irgl_op_args* args, irgl_reduction red,
+                          int32_t* reduced /*nullable*/, irgl_iter_stats* stats /*nullable*/);
+/* Iterate ...: repeat Invoke until `in` is empty (worklist
+ * ops) combined with cond/extra_cond; between_rounds = round counter ++.  outline=1 runs the
+ * whole loop as one cooperative persistent kernel with a grid barrier (SyncRunningThreads). */
+irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
+                           const irgl_op_args* args, const irgl_iterate_opts* opts,
+                           irgl_iter_stats* stats);
+/* Copies the operator's node result to the host: BFS/SSSP/CC/CC_LP int32[n], PR double[n],
+ * TC uint64[1]; test ops: PUSHPOP/FORALL_MAP int32[capacity] (g may be NULL). */
+irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out,
+                               size_t bytes);
+
+/* ---- launch planning ------------------------------------------------------ */
+/* Block-size constraint of a kernel: Elastic [1,1024], Shrinkable(max) [1,max], Fixed(n) {n}. */
+typedef enum { IRGL_BLOCK_ELASTIC = 0, IRGL_BLOCK_SHRINKABLE = 1, IRGL_BLOCK_FIXED = 2 } irgl_block_kind;
+typedef struct irgl_block_constraint { int32_t kind; int32_t value; } irgl_block_constraint;
+/* T_control = max(intersection of domains).  IRGL_E_OUTLINE_EMPTY if empty. */
+irgl_status_t irgl_t_control(const irgl_block_constraint* cs, int n, int32_t* out);
+/* The block constraint of this build's kernel for `op` (Fixed(256) for the nested-parallelism
+ * kernels) and the co-resident grid of its outlined variant. */
+irgl_status_t irgl_op_plan(irgl_ctx* ctx, irgl_op op, irgl_block_constraint* block,
+                           int32_t* grid_outlined, int32_t* grid_fixed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1362 @@
+// api.cu — C-ABI (include/irgl/rt.h): contexts, graphs, pipe contexts and the orchestration
+// constructs Invoke / Iterate / Pipe with the in/out/retry swap protocol (PAPER.md:358-381,
+// SPEC.md:359-381, :459-467) over the device kernels of expand.cu / topo.cu / testops.cu.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "nccl_dyn.h"
+
+// ----------------------------------------------------------------------------------------------
+// Handles
+namespace irgl {
+struct PartRT {  // one vertex partition hosted by this process
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  int sms = 0;
+  uint32_t* h_pin = nullptr;  // pinned scratch (counts readback)
+};
+}  // namespace irgl
+
+struct irgl_ctx {
+  irgl_config cfg{};
+  std::vector<irgl::PartRT> parts;  // local partitions
+  int rank = 0, nranks = 1;         // NCCL world (1 = single process)
+  ncclComm_t comm = nullptr;
+  const irgl::NcclApi* nccl = nullptr;
+  int64_t route_size = INT64_MAX;   // partition size of the last graph (pipe routing)
+  std::string err;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // test-operator state (partition 0)
+  int32_t* test_log = nullptr;
+  int64_t test_log_cap = 0;
+  int32_t* test_rcount = nullptr;
+  int64_t test_rcount_cap = 0;
+  int32_t test_launch_no = 0;
+  irgl::Ctl* test_ctl = nullptr;
+  int ptotal() const { return nranks * (int)parts.size(); }
+  int gpart(int l) const { return rank * (int)parts.size() + l; }
+};
+
+namespace irgl {
+struct GraphPart {
+  int64_t lo = 0, hi = 0, m = 0, maxdeg = 0;
+  int64_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  int32_t* w = nullptr;
+  int32_t* lab = nullptr;     // level / dist / label [N]
+  int32_t* stamp = nullptr;   // push dedupe [N]
+  double* pr[4] = {nullptr, nullptr, nullptr, nullptr};  // rank a, rank b, contrib a, contrib b
+  int pr_cur = 0;
+  int64_t* tc_rp = nullptr;
+  int32_t* tc_cl = nullptr;
+  int64_t tc_m = -1;
+  ChunkDesc* chunks = nullptr;
+  uint32_t chunk_cap = 0;
+  Ctl* ctl = nullptr;
+  // multi-partition exchange
+  uint32_t* send = nullptr;
+  uint32_t* send_cnt = nullptr;
+  int32_t* send_val = nullptr;
+  uint32_t* recv = nullptr;
+  int32_t* recv_val = nullptr;
+  DevCSR csr() const { return DevCSR{row_ptr, col, w, lo, hi}; }
+};
+struct PipePart {
+  uint32_t* buf[3] = {nullptr, nullptr, nullptr};
+  Ctl* ctl = nullptr;
+  int b_in = 0, b_out = 1, b_retry = 2;
+  int c_in = 0, c_out = 1, c_retry = 2, c_spare = 3;
+  uint32_t n_in = 0;  // host mirror of the in-count
+};
+}  // namespace irgl
+
+struct irgl_graph {
+  irgl_ctx* ctx = nullptr;
+  int64_t n = 0, m = 0;
+  bool has_w = false;
+  int64_t part_size = 1;
+  std::vector<irgl::GraphPart> parts;
+  int lab_op = -1;
+  int64_t stamp_epoch = 0;
+  uint64_t tc_count = 0;
+  int64_t maxdeg = 0;
+};
+
+struct irgl_pipe {
+  irgl_ctx* ctx = nullptr;
+  int64_t cap = 0;
+  std::vector<irgl::PipePart> parts;
+};
+
+// ----------------------------------------------------------------------------------------------
+namespace irgl {
+static std::string g_err;  // last error without a ctx
+
+void set_error(irgl_ctx* ctx, irgl_status_t st, const char* rule, const std::string& msg) {
+  (void)st;
+  std::string s = std::string(rule) + ": " + msg;
+  if (ctx) ctx->err = s;
+  g_err = s;
+}
+irgl_status_t cuda_status(irgl_ctx* ctx, cudaError_t e, const char* where) {
+  const irgl_status_t st = (e == cudaErrorMemoryAllocation) ? IRGL_E_OOM : IRGL_E_CUDA;
+  set_error(ctx, st, st == IRGL_E_OOM ? "E_OOM" : "E_CUDA",
+            std::string(cudaGetErrorString(e)) + " at " + where);
+  cudaGetLastError();  // clear sticky non-fatal errors
+  return st;
+}
+static irgl_status_t fail(irgl_ctx* ctx, irgl_status_t st, const char* rule, const std::string& m) {
+  set_error(ctx, st, rule, m);
+  return st;
+}
+
+static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
+  ExpandCfg ec;
+  ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 32;
+  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 1024;
+  ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 2048;
+  if (ec.warp_t < 1) ec.warp_t = 1;
+  if (ec.cta_t < ec.warp_t) ec.cta_t = ec.warp_t;
+  return ec;
+}
+
+static bool is_wl_graph_op(int op) {
+  return op == IRGL_OP_BFS || op == IRGL_OP_SSSP || op == IRGL_OP_CC_LP;
+}
+static bool is_test_op(int op) { return op >= IRGL_OP_TEST_COUNTDOWN && op <= IRGL_OP_TEST_FORALL_MAP; }
+static bool is_known_op(int op) {
+  return (op >= IRGL_OP_BFS && op <= IRGL_OP_CC_LP) || is_test_op(op);
+}
+
+#define CK(expr)                                                 \
+  do {                                                           \
+    cudaError_t _e = (expr);                                     \
+    if (_e != cudaSuccess) return cuda_status(ctx, _e, #expr);   \
+  } while (0)
+
+#define NCK(expr)                                                                   \
+  do {                                                                              \
+    ncclResult_t _r = (expr);                                                       \
+    if (_r != ncclSuccess)                                                          \
+      return fail(ctx, IRGL_E_NCCL, "E_NCCL",                                       \
+                  std::string(ctx->nccl->GetErrorString(_r)) + " at " #expr);       \
+  } while (0)
+
+static int grid_max(const irgl_ctx* ctx, const PartRT& pr, int op) {
+  int bps = ctx->cfg.blocks_per_sm > 0 ? ctx->cfg.blocks_per_sm : expand_blocks_per_sm(op);
+  if (bps <= 0) bps = 1;
+  return bps * pr.sms;
+}
+
+// ---- worklist helpers ------------------------------------------------------------------------
+static irgl_status_t pipe_set_in(irgl_ctx* ctx, irgl_pipe* p, int l, const std::vector<uint32_t>& items) {
+  PipePart& pp = p->parts[l];
+  PartRT& pr = ctx->parts[l];
+  CK(cudaSetDevice(pr.dev));
+  if (!items.empty())
+    CK(cudaMemcpyAsync(pp.buf[pp.b_in], items.data(), items.size() * 4, cudaMemcpyHostToDevice, pr.st));
+  uint32_t zeros[4] = {0, 0, 0, 0};
+  zeros[pp.c_in] = (uint32_t)items.size();
+  CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+  CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
+  CK(cudaMemsetAsync(&pp.ctl->overflow, 0, sizeof(uint32_t), pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  pp.n_in = (uint32_t)items.size();
+  return IRGL_OK;
+}
+
+static irgl_status_t pipe_init_items(irgl_pipe* p, const int64_t* items, int64_t count) {
+  irgl_ctx* ctx = p->ctx;
+  if (count < 0 || (count > 0 && !items)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "bad init array");
+  const int L = (int)ctx->parts.size();
+  std::vector<std::vector<uint32_t>> per(L);
+  for (int64_t i = 0; i < count; ++i) {
+    if (items[i] < 0 || items[i] > 0xffffffffll)
+      return fail(ctx, IRGL_E_INVALID, "E_INVALID", "work item id out of uint32 range (App. B5)");
+    // one partition: no routing.  P > 1: the owner of vertex id x is x / part_size.
+    const bool route = ctx->ptotal() > 1 && ctx->route_size != INT64_MAX;
+    const int64_t owner = route ? items[i] / ctx->route_size : 0;
+    const int64_t l = route ? owner - (int64_t)ctx->rank * L : 0;
+    if (l < 0 || l >= L) continue;  // owned by another rank
+    per[l].push_back((uint32_t)items[i]);
+  }
+  for (int l = 0; l < L; ++l) {
+    if ((int64_t)per[l].size() > p->cap)
+      return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
+                  "WorklistInit has more items than its size (SPEC.md:463)");
+    irgl_status_t s = pipe_set_in(ctx, p, l, per[l]);
+    if (s != IRGL_OK) return s;
+  }
+  return IRGL_OK;
+}
+
+// swap in <-> out and clear the new out
+static irgl_status_t pipe_swap_in_out(irgl_ctx* ctx, PipePart& pp, PartRT& pr, uint32_t nout) {
+  std::swap(pp.b_in, pp.b_out);
+  std::swap(pp.c_in, pp.c_out);
+  pp.n_in = nout;
+  CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_out], 0, 4, pr.st));
+  return IRGL_OK;
+}
+
+// ---- operator state ---------------------------------------------------------------------------
+static irgl_status_t ensure_lab(irgl_ctx* ctx, irgl_graph* g, bool need_stamp) {
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    if (!gp.lab) CK(cudaMalloc(&gp.lab, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
+    if (need_stamp && !gp.stamp) {
+      CK(cudaMalloc(&gp.stamp, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
+      CK(cudaMemset(gp.stamp, 0, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
+    }
+  }
+  return IRGL_OK;
+}
+
+static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* pipe) {
+  if (is_test_op(op)) {
+    ctx->test_launch_no = 0;
+    if (ctx->test_rcount) CK(cudaMemset(ctx->test_rcount, 0, ctx->test_rcount_cap * 4));
+    if (ctx->test_log) CK(cudaMemset(ctx->test_log, 0xff, ctx->test_log_cap * 4));
+    return IRGL_OK;
+  }
+  if (!g) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph operator needs a graph");
+  if (op == IRGL_OP_BFS || op == IRGL_OP_SSSP || op == IRGL_OP_CC_LP || op == IRGL_OP_CC) {
+    irgl_status_t s = ensure_lab(ctx, g, op != IRGL_OP_BFS && op != IRGL_OP_CC);
+    if (s != IRGL_OK) return s;
+    for (size_t l = 0; l < g->parts.size(); ++l) {
+      GraphPart& gp = g->parts[l];
+      PartRT& pr = ctx->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      if (op == IRGL_OP_BFS || op == IRGL_OP_SSSP) {
+        CK(launch_fill_i32(gp.lab, kInf, g->n, pr.st));
+      } else {
+        // label[v] = v (iota over int32 as uint32)
+        CK(launch_iota_u32(reinterpret_cast<uint32_t*>(gp.lab), 0u, (uint32_t)g->n, pr.st));
+      }
+      if (gp.stamp) CK(cudaMemsetAsync(gp.stamp, 0, g->n * sizeof(int32_t), pr.st));
+      if ((op == IRGL_OP_BFS || op == IRGL_OP_SSSP) && pipe) {
+        // level/dist[src] = 0 for the initial items (App. B2); items were routed to owners
+        PipePart& pp = pipe->parts[l];
+        CK(launch_scatter_zero(gp.lab, pp.buf[pp.b_in], pp.n_in, pr.st));
+      }
+      CK(cudaStreamSynchronize(pr.st));
+    }
+    // NCCL mode: every rank's ghost copy must also see the sources as 0 (they are owned elsewhere
+    // but never pushed back) — handled because the owner applies; remote ghosts stay INF.
+    g->lab_op = op;
+    g->stamp_epoch = 0;
+    return IRGL_OK;
+  }
+  if (op == IRGL_OP_PR) {
+    if (ctx->ptotal() > 1) return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED", "PR runs on one partition");
+    GraphPart& gp = g->parts[0];
+    PartRT& pr = ctx->parts[0];
+    CK(cudaSetDevice(pr.dev));
+    for (int k = 0; k < 4; ++k)
+      if (!gp.pr[k]) CK(cudaMalloc(&gp.pr[k], std::max<int64_t>(g->n, 1) * sizeof(double)));
+    CK(launch_pr_init(gp.pr[0], gp.pr[2], gp.row_ptr, g->n, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    gp.pr_cur = 0;
+    g->lab_op = op;
+    return IRGL_OK;
+  }
+  if (op == IRGL_OP_TC) {
+    g->tc_count = 0;
+    g->lab_op = op;
+    return IRGL_OK;
+  }
+  return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown operator");
+}
+
+// ---- multi-partition exchange (E5) -------------------------------------------------------------
+// After every local expansion: bucket counts -> (pack values) -> transport -> owner-side apply.
+static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pipe, int op,
+                                        int32_t level, int32_t stamp_id, irgl_iter_stats* stt) {
+  const int L = (int)ctx->parts.size();
+  const int P = ctx->ptotal();
+  const int64_t ps = g->part_size;
+  const bool vals = op != IRGL_OP_BFS;
+  // 1. send counts of local partitions -> host (P x P matrix, row = sender)
+  std::vector<uint32_t> cnt((size_t)P * P, 0);
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaMemcpyAsync(pr.h_pin, g->parts[l].send_cnt, P * 4, cudaMemcpyDeviceToHost, pr.st));
+  }
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaStreamSynchronize(pr.st));
+    std::memcpy(&cnt[(size_t)ctx->gpart(l) * P], pr.h_pin, P * 4);
+  }
+  // 2. pack values (SSSP / CC_LP): current ghost label of each bucket entry
+  if (vals)
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      for (int q = 0; q < P; ++q) {
+        const uint32_t c = cnt[(size_t)ctx->gpart(l) * P + q];
+        if (c) CK(launch_pack_values(gp.lab, gp.send + (int64_t)q * ps, gp.send_val + (int64_t)q * ps, c, pr.st));
+      }
+    }
+  // 3. transport
+  if (ctx->nranks > 1) {
+    // counts of the other ranks: all-gather the local rows (device buffer send_cnt of part 0)
+    PartRT& pr = ctx->parts[0];
+    GraphPart& gp = g->parts[0];
+    CK(cudaSetDevice(pr.dev));
+    uint32_t* dmat = reinterpret_cast<uint32_t*>(gp.recv_val ? (void*)gp.recv_val : (void*)gp.recv);
+    // use the tail of the recv buffer region sized P*P as scratch: recv is [P*ps] >= P*P
+    uint32_t* scratch = gp.recv + ((int64_t)P * ps - (int64_t)P * P);
+    (void)dmat;
+    NCK(ctx->nccl->AllGather(gp.send_cnt, scratch, P, ncclUint32, ctx->comm, pr.st));
+    CK(cudaMemcpyAsync(cnt.data(), scratch, (size_t)P * P * 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    // payloads: grouped send/recv (all-to-all v), one partition per rank
+    const int me = ctx->rank;
+    NCK(ctx->nccl->GroupStart());
+    for (int q = 0; q < P; ++q) {
+      if (q == me) continue;
+      const uint32_t cs = cnt[(size_t)me * P + q], cr = cnt[(size_t)q * P + me];
+      if (cs) {
+        NCK(ctx->nccl->Send(gp.send + (int64_t)q * ps, cs, ncclUint32, q, ctx->comm, pr.st));
+        if (vals) NCK(ctx->nccl->Send(gp.send_val + (int64_t)q * ps, cs, ncclInt32, q, ctx->comm, pr.st));
+      }
+      if (cr) {
+        NCK(ctx->nccl->Recv(gp.recv + (int64_t)q * ps, cr, ncclUint32, q, ctx->comm, pr.st));
+        if (vals) NCK(ctx->nccl->Recv(gp.recv_val + (int64_t)q * ps, cr, ncclInt32, q, ctx->comm, pr.st));
+      }
+      stt->exchange_bytes += (int64_t)(cs + cr) * (vals ? 8 : 4);
+    }
+    NCK(ctx->nccl->GroupEnd());
+  } else {
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      CK(cudaStreamSynchronize(pr.st));  // packs done
+    }
+    for (int q = 0; q < L; ++q) {
+      PartRT& dst = ctx->parts[q];
+      CK(cudaSetDevice(dst.dev));
+      for (int p = 0; p < L; ++p) {
+        if (p == q) continue;
+        const uint32_t c = cnt[(size_t)p * P + q];
+        if (!c) continue;
+        CK(cudaMemcpyPeerAsync(g->parts[q].recv + (int64_t)p * ps, dst.dev,
+                               g->parts[p].send + (int64_t)q * ps, ctx->parts[p].dev, (size_t)c * 4, dst.st));
+        if (vals)
+          CK(cudaMemcpyPeerAsync(g->parts[q].recv_val + (int64_t)p * ps, dst.dev,
+                                 g->parts[p].send_val + (int64_t)q * ps, ctx->parts[p].dev,
+                                 (size_t)c * 4, dst.st));
+        stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
+      }
+    }
+  }
+  // 4. owner-side apply (min-reduce) into the local out worklist; reset send counts
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    GraphPart& gp = g->parts[l];
+    PipePart& pp = pipe->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    const int q = ctx->gpart(l);
+    for (int p = 0; p < P; ++p) {
+      if (p == q) continue;
+      const uint32_t c = cnt[(size_t)p * P + q];
+      if (!c) continue;
+      CK(launch_apply_remote(op, gp.lab, gp.stamp, pp.ctl, gp.recv + (int64_t)p * ps,
+                             vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, pp.buf[pp.b_out],
+                             &pp.ctl->cnt[pp.c_out], (uint32_t)pipe->cap, level, stamp_id, pr.st));
+    }
+    CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
+  }
+  return IRGL_OK;
+}
+
+static irgl_status_t allreduce_sum_u64(irgl_ctx* ctx, uint64_t* v) {
+  if (ctx->nranks <= 1) return IRGL_OK;
+  PartRT& pr = ctx->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  unsigned long long* d = nullptr;
+  CK(cudaMallocAsync(&d, 8, pr.st));
+  CK(cudaMemcpyAsync(d, v, 8, cudaMemcpyHostToDevice, pr.st));
+  NCK(ctx->nccl->AllReduce(d, d, 1, ncclUint64, ncclSum, ctx->comm, pr.st));
+  CK(cudaMemcpyAsync(v, d, 8, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaFreeAsync(d, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  return IRGL_OK;
+}
+
+// ---- data-driven graph operators: host-orchestrated rounds ----------------------------------
+static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                                     int64_t level0, const irgl_iterate_opts& o, bool once,
+                                     irgl_iter_stats* stt) {
+  const int L = (int)ctx->parts.size();
+  const int P = ctx->ptotal();
+  const ExpandCfg ec = expand_cfg(ctx);
+  int64_t level = level0;
+  for (;;) {
+    uint64_t total_in = 0;
+    for (int l = 0; l < L; ++l) total_in += pipe->parts[l].n_in;
+    irgl_status_t s = allreduce_sum_u64(ctx, &total_in);
+    if (s != IRGL_OK) return s;
+    // termination: in empty [comb] rounds >= max_rounds
+    const bool empty = total_in == 0;
+    const bool extra = o.max_rounds > 0 && stt->rounds >= o.max_rounds;
+    const bool stop = o.max_rounds > 0 ? (o.extra_comb == IRGL_COMB_AND ? (empty && extra) : (empty || extra))
+                                       : empty;
+    if (stop || (once && stt->rounds >= 1)) break;
+    const int32_t stamp_id = (int32_t)(++g->stamp_epoch);
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      RoundBufs rb;
+      rb.in = pp.buf[pp.b_in];
+      rb.nin = pp.n_in;
+      rb.out = pp.buf[pp.b_out];
+      rb.out_cnt = &pp.ctl->cnt[pp.c_out];
+      rb.cap = (uint32_t)pipe->cap;
+      rb.chunks = gp.chunks;
+      rb.chunk_cnt = &pp.ctl->chunk_cnt[0];
+      rb.chunk_cap = gp.chunk_cap;
+      rb.level = (int32_t)level;
+      rb.stamp_id = stamp_id;
+      DistRoute dr{P, ctx->gpart(l), g->part_size, gp.send, gp.send_cnt};
+      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rb, dr, ec, grid_max(ctx, pr, op), pr.st));
+      stt->launches += 2;
+    }
+    if (P > 1) {
+      s = exchange_and_apply(ctx, g, pipe, op, (int32_t)level, stamp_id, stt);
+      if (s != IRGL_OK) return s;
+    }
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_out], 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemcpyAsync(pr.h_pin + 1, &pp.ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(uint32_t), pr.st));
+    }
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      CK(cudaStreamSynchronize(pr.st));
+      if (pr.h_pin[1]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+      const uint32_t nout = pr.h_pin[0];
+      stt->popped += pp.n_in;
+      stt->pushes += nout;
+      irgl_status_t s2 = pipe_swap_in_out(ctx, pp, pr, nout);
+      if (s2 != IRGL_OK) return s2;
+    }
+    stt->rounds++;
+    ++level;  // between_rounds { LEVEL++ }
+  }
+  return IRGL_OK;
+}
+
+// ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
+static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                                       int64_t level0, const irgl_iterate_opts& o,
+                                       irgl_iter_stats* stt) {
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  PipePart& pp = pipe->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  if (pp.n_in == 0) return IRGL_OK;
+  const int bps = persistent_blocks_per_sm(op);
+  if (bps <= 0)
+    return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY",
+                "outlined kernel cannot be co-resident (SyncRunningThreads would deadlock, PAPER.md:248)");
+  const int grid = bps * pr.sms;
+  PersistArgs pa;
+  pa.buf_a = pp.buf[pp.b_in];
+  pa.buf_b = pp.buf[pp.b_out];
+  pa.slot[0] = pp.c_in;
+  pa.slot[1] = pp.c_out;
+  pa.slot[2] = pp.c_spare;
+  pa.cap = (uint32_t)pipe->cap;
+  pa.chunks = gp.chunks;
+  pa.chunk_cap = gp.chunk_cap;
+  pa.level0 = (int32_t)level0;
+  pa.stamp0 = (int32_t)(g->stamp_epoch + 1);
+  pa.max_rounds = o.max_rounds > 0 ? std::max<int64_t>(o.max_rounds - stt->rounds, 0) : 0;
+  if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
+  CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
+  CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
+  CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
+  CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
+  Ctl h;
+  CK(cudaMemcpyAsync(&h, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+  const int64_t K = (int64_t)h.rounds;
+  // rotate the host view: buffers by parity, counters by K mod 3 (see persistent_kernel)
+  const int slots[3] = {pp.c_in, pp.c_out, pp.c_spare};
+  if (K & 1) std::swap(pp.b_in, pp.b_out);
+  pp.c_in = slots[K % 3];
+  pp.c_out = slots[(K + 1) % 3];
+  pp.c_spare = slots[(K + 2) % 3];
+  pp.n_in = h.cnt[pp.c_in];
+  g->stamp_epoch += K;
+  stt->rounds += K;
+  stt->launches += 1;
+  stt->popped += (int64_t)h.popped;
+  stt->pushes += (int64_t)h.pushes;
+  stt->outlined = 1;
+  return IRGL_OK;
+}
+
+// Read (stt != null) and zero the edges / remote counters of the pipe's control blocks.
+static irgl_status_t pipe_counters(irgl_ctx* ctx, irgl_pipe* pipe, irgl_iter_stats* stt) {
+  for (size_t l = 0; l < pipe->parts.size(); ++l) {
+    PartRT& pr = ctx->parts[l];
+    PipePart& pp = pipe->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    if (stt) {
+      unsigned long long hv[4] = {0, 0, 0, 0};
+      CK(cudaMemcpy(hv, &pp.ctl->edges, sizeof(hv), cudaMemcpyDeviceToHost));
+      stt->edges += (int64_t)hv[0];
+      stt->remote_updates += (int64_t)hv[3];
+    }
+    CK(cudaMemsetAsync(&pp.ctl->edges, 0, 8, pr.st));
+    CK(cudaMemsetAsync(&pp.ctl->remote, 0, 8, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+  }
+  return IRGL_OK;
+}
+
+// ---- test operators (partition 0): full swap protocol with retry -----------
+static irgl_status_t test_ensure(irgl_ctx* ctx, int64_t cap) {
+  if (ctx->test_log_cap < cap) {
+    if (ctx->test_log) cudaFree(ctx->test_log);
+    CK(cudaMalloc(&ctx->test_log, cap * 4));
+    CK(cudaMemset(ctx->test_log, 0xff, cap * 4));
+    ctx->test_log_cap = cap;
+  }
+  if (ctx->test_rcount_cap < cap) {
+    if (ctx->test_rcount) cudaFree(ctx->test_rcount);
+    CK(cudaMalloc(&ctx->test_rcount, cap * 4));
+    CK(cudaMemset(ctx->test_rcount, 0, cap * 4));
+    ctx->test_rcount_cap = cap;
+  }
+  if (!ctx->test_ctl) {
+    CK(cudaMalloc(&ctx->test_ctl, sizeof(Ctl)));
+    CK(cudaMemset(ctx->test_ctl, 0, sizeof(Ctl)));
+  }
+  return IRGL_OK;
+}
+
+static irgl_status_t test_invoke(irgl_ctx* ctx, irgl_pipe* pipe, int op, const irgl_op_args* a,
+                                 int red, int32_t* reduced, irgl_iter_stats* stt,
+                                 const int32_t* dvalues) {
+  PartRT& pr = ctx->parts[0];
+  PipePart& pp = pipe->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  irgl_status_t s = test_ensure(ctx, pipe->cap);
+  if (s != IRGL_OK) return s;
+  const uint32_t ident = red == IRGL_RED_ALL ? 1u : 0u;
+  CK(cudaMemcpyAsync(&ctx->test_ctl->red[0], &ident, 4, cudaMemcpyHostToDevice, pr.st));
+  CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_retry], 0, 4, pr.st));
+  const int rsa = ctx->cfg.retry_serialize_after > 0 ? ctx->cfg.retry_serialize_after : 4;
+  int retry_rounds = 0;
+  for (;;) {
+    TestArgs ta;
+    ta.op = op;
+    ta.in = pp.buf[pp.b_in];
+    ta.nin = pp.n_in;
+    ta.out = pp.buf[pp.b_out];
+    ta.out_cnt = &pp.ctl->cnt[pp.c_out];
+    ta.retry = pp.buf[pp.b_retry];
+    ta.retry_cnt = &pp.ctl->cnt[pp.c_retry];
+    ta.cap = (uint32_t)pipe->cap;
+    ta.guard = a ? a->guard : 0;
+    ta.values = dvalues;
+    ta.rcount = ctx->test_rcount;
+    ta.log = ctx->test_log;
+    ta.launch_no = ++ctx->test_launch_no;
+    ta.mapping = a ? a->mapping : 0;
+    ta.red = &ctx->test_ctl->red[0];
+    ta.reduction = red;
+    ta.overflow = &ctx->test_ctl->overflow;
+    // Retry beyond retry_serialize_after rounds: serial execution
+    const bool serial = retry_rounds > rsa;
+    int threads = a && a->threads > 0 ? a->threads : 148 * 256;
+    if (serial) {
+      threads = 1;
+      stt->serial_launches++;
+    }
+    if (ta.nin > 0 || red != IRGL_RED_NONE) CK(launch_test_op(ta, threads, pr.st));
+    stt->launches++;
+    stt->popped += pp.n_in;
+    CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_retry], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    const uint32_t nretry = pr.h_pin[0];
+    if (nretry == 0) break;
+    // while retry != {}: swap in <-> retry, clear retry, relaunch; out preserved
+    std::swap(pp.b_in, pp.b_retry);
+    std::swap(pp.c_in, pp.c_retry);
+    pp.n_in = nretry;
+    CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_retry], 0, 4, pr.st));
+    stt->retries += nretry;
+    ++retry_rounds;
+  }
+  uint32_t h[3];
+  CK(cudaMemcpyAsync(&h[0], &pp.ctl->cnt[pp.c_out], 4, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaMemcpyAsync(&h[1], &ctx->test_ctl->red[0], 4, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaMemcpyAsync(&h[2], &ctx->test_ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  if (h[2]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+  stt->pushes += h[0];
+  s = pipe_swap_in_out(ctx, pp, pr, h[0]);
+  if (s != IRGL_OK) return s;
+  if (reduced) *reduced = red == IRGL_RED_NONE ? -1 : (int32_t)h[1];
+  stt->last_reduced = red == IRGL_RED_NONE ? -1 : (int32_t)h[1];
+  return IRGL_OK;
+}
+
+// ---- topology-driven invocations ---------------------------------------------------------------
+static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irgl_op_args* a,
+                                 int red, int32_t* reduced, irgl_iter_stats* stt) {
+  if (ctx->ptotal() > 1)
+    return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED", "CC/PR/TC run on one partition (SURVEY §8e)");
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  if (g->lab_op != op) {
+    irgl_status_t s = op_reset(ctx, g, op, nullptr);
+    if (s != IRGL_OK) return s;
+  }
+  const int gm = grid_max(ctx, pr, op);
+  uint32_t cell = 0;
+  if (op == IRGL_OP_CC || op == IRGL_OP_PR) {
+    const uint32_t ident = red == IRGL_RED_ALL ? 1u : 0u;
+    CK(cudaMemcpyAsync(&gp.ctl->red[0], &ident, 4, cudaMemcpyHostToDevice, pr.st));
+  }
+  if (op == IRGL_OP_CC) {
+    // hook's ReduceAndReturn(changed) — fold into Any (All over "changed" is its negation)
+    CK(cudaMemsetAsync(&gp.ctl->red[1], 0, 4, pr.st));
+    CK(launch_cc_hook(gp.csr(), gp.lab, gp.ctl, 1, gm, pr.st));
+    CK(launch_cc_compress(gp.lab, g->n, pr.st));
+    stt->launches += 2;
+    CK(cudaMemcpyAsync(&cell, &gp.ctl->red[1], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    stt->edges += g->m;
+    if (red == IRGL_RED_ALL) cell = cell ? 1u : 0u;  // every evaluated value true iff any hooked
+  } else if (op == IRGL_OP_PR) {
+    const double d = a && a->pr_damping > 0 ? a->pr_damping : 0.85;
+    const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
+    const int c = gp.pr_cur;
+    CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c], gp.pr[3 - c], d, tol, g->n,
+                       gp.ctl, 0, gm, pr.st));
+    stt->launches += 1;
+    CK(cudaMemcpyAsync(&cell, &gp.ctl->red[0], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    gp.pr_cur = 1 - c;
+    stt->edges += g->m;
+  } else if (op == IRGL_OP_TC) {
+    if (gp.tc_m < 0) CK(tc_orient(gp.csr(), g->n, &gp.tc_rp, &gp.tc_cl, &gp.tc_m, pr.st));
+    CK(launch_tc_count(gp.tc_rp, gp.tc_cl, g->n, gp.ctl, pr.st));
+    unsigned long long c = 0;
+    CK(cudaMemcpyAsync(&c, &gp.ctl->tc_count, 8, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    g->tc_count = c;
+    stt->launches += 1;
+    stt->edges += gp.tc_m;
+    red = IRGL_RED_NONE;
+  }
+  if (reduced) *reduced = red == IRGL_RED_NONE ? -1 : (int32_t)cell;
+  stt->last_reduced = red == IRGL_RED_NONE ? -1 : (int32_t)cell;
+  stt->rounds++;
+  return IRGL_OK;
+}
+
+static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_args* a,
+                                 const irgl_iterate_opts& o, irgl_iter_stats* stt) {
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  if (g->lab_op != IRGL_OP_PR) {
+    irgl_status_t s = op_reset(ctx, g, IRGL_OP_PR, nullptr);
+    if (s != IRGL_OK) return s;
+  }
+  const int bps = pr_persistent_blocks_per_sm();
+  if (bps <= 0) return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "PR control kernel not co-resident");
+  const double d = a && a->pr_damping > 0 ? a->pr_damping : 0.85;
+  const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
+  const int c = gp.pr_cur;
+  CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
+  CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c], gp.pr[3 - c], d, tol, g->n,
+                          gp.ctl, o.max_rounds, o.cond_mode, bps * pr.sms, pr.st));
+  Ctl h;
+  CK(cudaMemcpyAsync(&h, gp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  const int64_t K = (int64_t)h.rounds;
+  if (K & 1) gp.pr_cur = 1 - c;
+  stt->rounds += K;
+  stt->launches += 1;
+  stt->edges += K * g->m;
+  stt->last_reduced = h.last_red;
+  stt->outlined = 1;
+  return IRGL_OK;
+}
+
+static irgl_status_t upload_values(irgl_ctx* ctx, const irgl_op_args* a, int32_t** d) {
+  *d = nullptr;
+  if (!a || !a->values || a->nvalues <= 0) return IRGL_OK;
+  CK(cudaMalloc(d, a->nvalues * 4));
+  CK(cudaMemcpy(*d, a->values, a->nvalues * 4, cudaMemcpyHostToDevice));
+  return IRGL_OK;
+}
+
+static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
+  const int P = ctx->ptotal();
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    CK(cudaMalloc(&gp.ctl, sizeof(Ctl)));
+    CK(cudaMemset(gp.ctl, 0, sizeof(Ctl)));
+    CK(max_degree(gp.row_ptr, gp.hi - gp.lo, &gp.maxdeg, ctx->parts[l].st));
+    g->maxdeg = std::max(g->maxdeg, gp.maxdeg);
+    const ExpandCfg ec = expand_cfg(ctx);
+    const int64_t nch = gp.m / ec.chunk_edges + gp.m / ec.cta_t + 1024;
+    gp.chunk_cap = (uint32_t)std::min<int64_t>(nch, 0xffffffffll);
+    CK(cudaMalloc(&gp.chunks, (size_t)gp.chunk_cap * sizeof(ChunkDesc)));
+    if (P > 1) {
+      const int64_t tot = (int64_t)P * g->part_size;
+      CK(cudaMalloc(&gp.send, tot * 4));
+      CK(cudaMalloc(&gp.send_val, tot * 4));
+      CK(cudaMalloc(&gp.recv, tot * 4));
+      CK(cudaMalloc(&gp.recv_val, tot * 4));
+      CK(cudaMalloc(&gp.send_cnt, P * 4));
+      CK(cudaMemset(gp.send_cnt, 0, P * 4));
+    }
+  }
+  ctx->route_size = g->part_size;
+  return IRGL_OK;
+}
+
+static void partition_ranges(int64_t n, int P, int64_t* ps) { *ps = std::max<int64_t>((n + P - 1) / P, 1); }
+
+}  // namespace irgl
+
+using namespace irgl;
+
+// ==============================================================================================
+extern "C" {
+
+int irgl_abi_version(void) { return IRGL_ABI_VERSION; }
+
+const char* irgl_last_error(const irgl_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : irgl::g_err.c_str();
+}
+
+static irgl_status_t ctx_init_parts(irgl_ctx* c, const int* devices, int ndev, int L) {
+  irgl_ctx* ctx = c;
+  c->parts.resize(L);
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = c->parts[l];
+    pr.dev = devices ? devices[l % ndev] : 0;
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaStreamCreateWithFlags(&pr.st, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&pr.sms, cudaDevAttrMultiProcessorCount, pr.dev));
+    CK(cudaMallocHost(&pr.h_pin, 4096));
+  }
+  CK(cudaSetDevice(c->parts[0].dev));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  // peer access for the loopback exchange across devices
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      const int da = c->parts[a].dev, db = c->parts[b].dev;
+      if (da == db) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, da, db);
+      if (can) {
+        cudaSetDevice(da);
+        cudaDeviceEnablePeerAccess(db, 0);
+        cudaGetLastError();
+      }
+    }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_ctx_create(const int* devices, int ndev, const irgl_config* cfg, irgl_ctx** out) {
+  if (!out || ndev < 0 || (ndev > 0 && !devices)) {
+    set_error(nullptr, IRGL_E_INVALID, "E_INVALID", "irgl_ctx_create: bad arguments");
+    return IRGL_E_INVALID;
+  }
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    set_error(nullptr, IRGL_E_CUDA, "E_CUDA", "no CUDA device available (no CPU fallback exists)");
+    return IRGL_E_CUDA;
+  }
+  auto c = std::make_unique<irgl_ctx>();
+  if (cfg) c->cfg = *cfg;
+  int zero = 0;
+  if (ndev == 0) { devices = &zero; ndev = 1; }
+  const int L = std::max(ndev, c->cfg.logical_partitions > 1 ? c->cfg.logical_partitions : 1);
+  irgl_status_t s = ctx_init_parts(c.get(), devices, ndev, L);
+  if (s != IRGL_OK) return s;
+  *out = c.release();
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_nccl_unique_id(void* id128) {
+  std::string why;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) { set_error(nullptr, IRGL_E_NCCL, "E_NCCL", why); return IRGL_E_NCCL; }
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) {
+    set_error(nullptr, IRGL_E_NCCL, "E_NCCL", "ncclGetUniqueId failed");
+    return IRGL_E_NCCL;
+  }
+  std::memcpy(id128, &id, sizeof(id));
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void* id128,
+                                   const irgl_config* cfg, irgl_ctx** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || !id128) {
+    set_error(nullptr, IRGL_E_INVALID, "E_INVALID", "irgl_ctx_create_nccl: bad arguments");
+    return IRGL_E_INVALID;
+  }
+  auto c = std::make_unique<irgl_ctx>();
+  if (cfg) c->cfg = *cfg;
+  c->cfg.logical_partitions = 1;  // one partition per rank
+  irgl_status_t s = ctx_init_parts(c.get(), &device, 1, 1);
+  if (s != IRGL_OK) return s;
+  std::string why;
+  c->nccl = nccl_api(&why);
+  if (!c->nccl) { set_error(nullptr, IRGL_E_NCCL, "E_NCCL", why); return IRGL_E_NCCL; }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  cudaSetDevice(device);
+  ncclResult_t r = c->nccl->CommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    set_error(nullptr, IRGL_E_NCCL, "E_NCCL", std::string("ncclCommInitRank: ") + c->nccl->GetErrorString(r));
+    return IRGL_E_NCCL;
+  }
+  c->rank = rank;
+  c->nranks = nranks;
+  *out = c.release();
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_ctx_sync(irgl_ctx* ctx) {
+  if (!ctx) return IRGL_E_INVALID;
+  for (auto& p : ctx->parts) {
+    CK(cudaSetDevice(p.dev));
+    CK(cudaStreamSynchronize(p.st));
+  }
+  if (ctx->comm) {
+    ncclResult_t ae = ncclSuccess;
+    ctx->nccl->CommGetAsyncError(ctx->comm, &ae);
+    if (ae != ncclSuccess) return fail(ctx, IRGL_E_NCCL, "E_NCCL", ctx->nccl->GetErrorString(ae));
+  }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
+  if (!ctx) return IRGL_E_INVALID;
+  for (auto& p : ctx->parts) {
+    cudaSetDevice(p.dev);
+    cudaStreamSynchronize(p.st);
+  }
+  if (ctx->comm) ctx->nccl->CommDestroy(ctx->comm);
+  cudaSetDevice(ctx->parts[0].dev);
+  if (ctx->test_log) cudaFree(ctx->test_log);
+  if (ctx->test_rcount) cudaFree(ctx->test_rcount);
+  if (ctx->test_ctl) cudaFree(ctx->test_ctl);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (auto& p : ctx->parts) {
+    cudaSetDevice(p.dev);
+    if (p.st) cudaStreamDestroy(p.st);
+    if (p.h_pin) cudaFreeHost(p.h_pin);
+  }
+  delete ctx;
+  return IRGL_OK;
+}
+
+// ---- graphs ------------------------------------------------------------------------------------
+irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const int64_t* row_ptr,
+                                    const int32_t* col, const int32_t* weight, irgl_graph** out) {
+  if (!ctx || !out || n < 1 || m < 0 || !row_ptr || (m > 0 && !col))
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID", "irgl_graph_create_csr: bad arguments");
+  if (n > 0x7fffffffll) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "n must fit int32 vertex ids");
+  if (row_ptr[0] != 0 || row_ptr[n] != m)
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID", "row_ptr must start at 0 and end at m");
+  for (int64_t i = 0; i < n; ++i)
+    if (row_ptr[i + 1] < row_ptr[i]) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "row_ptr not monotone");
+  for (int64_t e = 0; e < m; ++e)
+    if (col[e] < 0 || col[e] >= n) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "column id out of range");
+  auto g = std::make_unique<irgl_graph>();
+  g->ctx = ctx;
+  g->n = n;
+  g->m = m;
+  g->has_w = weight != nullptr;
+  const int L = (int)ctx->parts.size();
+  const int P = ctx->ptotal();
+  partition_ranges(n, P, &g->part_size);
+  g->parts.resize(L);
+  for (int l = 0; l < L; ++l) {
+    GraphPart& gp = g->parts[l];
+    PartRT& pr = ctx->parts[l];
+    const int gpi = ctx->gpart(l);
+    gp.lo = std::min<int64_t>((int64_t)gpi * g->part_size, n);
+    gp.hi = std::min<int64_t>(gp.lo + g->part_size, n);
+    const int64_t nloc = gp.hi - gp.lo;
+    const int64_t e0 = row_ptr[gp.lo], e1 = row_ptr[gp.hi];
+    gp.m = e1 - e0;
+    CK(cudaSetDevice(pr.dev));
+    std::vector<int64_t> rp(nloc + 1);
+    for (int64_t i = 0; i <= nloc; ++i) rp[i] = row_ptr[gp.lo + i] - e0;
+    CK(cudaMalloc(&gp.row_ptr, (nloc + 1) * 8));
+    CK(cudaMemcpy(gp.row_ptr, rp.data(), (nloc + 1) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&gp.col, std::max<int64_t>(gp.m, 4) * 4));
+    CK(cudaMalloc(&gp.w, std::max<int64_t>(gp.m, 4) * 4));
+    if (gp.m > 0) {
+      CK(cudaMemcpy(gp.col, col + e0, gp.m * 4, cudaMemcpyHostToDevice));
+      if (weight) CK(cudaMemcpy(gp.w, weight + e0, gp.m * 4, cudaMemcpyHostToDevice));
+      else CK(launch_fill_i32(gp.w, 1, gp.m, pr.st));
+    }
+  }
+  irgl_status_t s = graph_alloc_exchange(ctx, g.get());
+  if (s != IRGL_OK) return s;
+  *out = g.release();
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_generate(irgl_ctx* ctx, const irgl_gen_spec* spec, irgl_graph** out) {
+  if (!ctx || !spec || !out) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "irgl_graph_generate: bad arguments");
+  int64_t n = 0;
+  if (spec->kind == IRGL_GEN_RMAT) {
+    if (spec->scale < 1 || spec->scale > 30) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "scale out of range");
+    n = 1ll << spec->scale;
+  } else if (spec->kind == IRGL_GEN_GRID) {
+    if (spec->width < 1 || spec->height < 1) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "bad grid size");
+    n = (int64_t)spec->width * spec->height;
+  } else {
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown generator");
+  }
+  if (n > 0x7fffffffll) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "n must fit int32 vertex ids");
+  auto g = std::make_unique<irgl_graph>();
+  g->ctx = ctx;
+  g->n = n;
+  g->has_w = true;
+  const int L = (int)ctx->parts.size();
+  const int P = ctx->ptotal();
+  partition_ranges(n, P, &g->part_size);
+  g->parts.resize(L);
+  int64_t mloc = 0;
+  for (int l = 0; l < L; ++l) {
+    GraphPart& gp = g->parts[l];
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    const int gpi = ctx->gpart(l);
+    gp.lo = std::min<int64_t>((int64_t)gpi * g->part_size, n);
+    gp.hi = std::min<int64_t>(gp.lo + g->part_size, n);
+    std::string where;
+    cudaError_t e = gen_partition(*spec, n, gp.lo, gp.hi, &gp.row_ptr, &gp.col, &gp.w, &gp.m, pr.st, &where);
+    if (e != cudaSuccess) return cuda_status(ctx, e, where.c_str());
+    mloc += gp.m;
+  }
+  uint64_t mtot = (uint64_t)mloc;
+  irgl_status_t s = allreduce_sum_u64(ctx, &mtot);
+  if (s != IRGL_OK) return s;
+  g->m = (int64_t)mtot;
+  s = graph_alloc_exchange(ctx, g.get());
+  if (s != IRGL_OK) return s;
+  *out = g.release();
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_info_get(const irgl_graph* g, irgl_graph_info* info) {
+  if (!g || !info) return IRGL_E_INVALID;
+  std::memset(info, 0, sizeof(*info));
+  info->n = g->n;
+  info->m = g->m;
+  for (auto& p : g->parts) {
+    info->local_n += p.hi - p.lo;
+    info->local_m += p.m;
+  }
+  info->lo = g->parts[0].lo;
+  info->hi = g->parts[0].hi;
+  info->partitions = g->ctx->ptotal();
+  info->has_weights = g->has_w ? 1 : 0;
+  info->max_degree = g->maxdeg;
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_download(irgl_graph* g, int64_t* row_ptr, int32_t* col, int32_t* weight) {
+  if (!g) return IRGL_E_INVALID;
+  irgl_ctx* ctx = g->ctx;
+  int64_t eoff = 0;
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    const int64_t nloc = gp.hi - gp.lo;
+    std::vector<int64_t> rp(nloc + 1);
+    CK(cudaMemcpy(rp.data(), gp.row_ptr, (nloc + 1) * 8, cudaMemcpyDeviceToHost));
+    if (row_ptr) {
+      const int64_t base = (ctx->nranks > 1) ? 0 : eoff;
+      const int64_t ro = (ctx->nranks > 1) ? 0 : gp.lo;
+      for (int64_t i = 0; i <= nloc; ++i) row_ptr[ro + i] = base + rp[i];
+    }
+    if (col && gp.m) CK(cudaMemcpy(col + eoff, gp.col, gp.m * 4, cudaMemcpyDeviceToHost));
+    if (weight && gp.m) CK(cudaMemcpy(weight + eoff, gp.w, gp.m * 4, cudaMemcpyDeviceToHost));
+    eoff += gp.m;
+  }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_destroy(irgl_graph* g) {
+  if (!g) return IRGL_E_INVALID;
+  irgl_ctx* ctx = g->ctx;
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    cudaSetDevice(ctx->parts[l].dev);
+    cudaStreamSynchronize(ctx->parts[l].st);
+    void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
+                  gp.tc_rp, gp.tc_cl, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
+                  gp.recv_val};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  }
+  delete g;
+  return IRGL_OK;
+}
+
+// ---- pipes -------------------------------------------------------------------------------------
+irgl_status_t irgl_pipe_create(irgl_ctx* ctx, int64_t capacity, irgl_pipe** out) {
+  if (!ctx || !out || capacity < 1 || capacity > 0xffffffffll)
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID", "irgl_pipe_create: capacity must be in [1, 2^32)");
+  auto p = std::make_unique<irgl_pipe>();
+  p->ctx = ctx;
+  p->cap = capacity;
+  p->parts.resize(ctx->parts.size());
+  for (size_t l = 0; l < ctx->parts.size(); ++l) {
+    PipePart& pp = p->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    for (int k = 0; k < 3; ++k) CK(cudaMalloc(&pp.buf[k], capacity * 4));
+    CK(cudaMalloc(&pp.ctl, sizeof(Ctl)));
+    CK(cudaMemset(pp.ctl, 0, sizeof(Ctl)));
+  }
+  *out = p.release();
+  return IRGL_OK;
+}
+irgl_status_t irgl_pipe_init_scalars(irgl_pipe* p, const int64_t* items, int64_t count) {
+  if (!p) return IRGL_E_INVALID;
+  return pipe_init_items(p, items, count);
+}
+irgl_status_t irgl_pipe_init_from_array(irgl_pipe* p, const int64_t* arr, int64_t len) {
+  if (!p) return IRGL_E_INVALID;
+  return pipe_init_items(p, arr, len);
+}
+irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end) {
+  if (!p || begin < 0 || end < begin || end > 0xffffffffll) return IRGL_E_INVALID;
+  irgl_ctx* ctx = p->ctx;
+  const int L = (int)ctx->parts.size();
+  for (int l = 0; l < L; ++l) {
+    int64_t b = begin, e = end;
+    if (ctx->ptotal() > 1 && ctx->route_size != INT64_MAX) {
+      const int64_t lo = (int64_t)ctx->gpart(l) * ctx->route_size, hi = lo + ctx->route_size;
+      b = std::max(b, lo);
+      e = std::min(e, hi);
+    } else if (l > 0) {
+      b = e = 0;
+    }
+    if (e < b) e = b;
+    if (e - b > p->cap) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "WorklistInit larger than size");
+    PipePart& pp = p->parts[l];
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    CK(launch_iota_u32(pp.buf[pp.b_in], (uint32_t)b, (uint32_t)(e - b), pr.st));
+    uint32_t zeros[4] = {0, 0, 0, 0};
+    zeros[pp.c_in] = (uint32_t)(e - b);
+    CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    pp.n_in = (uint32_t)(e - b);
+  }
+  return IRGL_OK;
+}
+irgl_status_t irgl_pipe_size(const irgl_pipe* p, irgl_wl which, int64_t* out) {
+  if (!p || !out) return IRGL_E_INVALID;
+  irgl_ctx* ctx = p->ctx;
+  int64_t tot = 0;
+  for (size_t l = 0; l < p->parts.size(); ++l) {
+    const PipePart& pp = p->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    const int slot = which == IRGL_WL_IN ? pp.c_in : which == IRGL_WL_OUT ? pp.c_out : pp.c_retry;
+    uint32_t c = 0;
+    CK(cudaMemcpy(&c, &pp.ctl->cnt[slot], 4, cudaMemcpyDeviceToHost));
+    tot += c;
+  }
+  *out = tot;
+  return IRGL_OK;
+}
+irgl_status_t irgl_pipe_read(irgl_pipe* p, irgl_wl which, int64_t* items, int64_t cap, int64_t* count) {
+  if (!p || !count) return IRGL_E_INVALID;
+  irgl_ctx* ctx = p->ctx;
+  int64_t tot = 0;
+  for (size_t l = 0; l < p->parts.size(); ++l) {
+    const PipePart& pp = p->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    const int slot = which == IRGL_WL_IN ? pp.c_in : which == IRGL_WL_OUT ? pp.c_out : pp.c_retry;
+    const int buf = which == IRGL_WL_IN ? pp.b_in : which == IRGL_WL_OUT ? pp.b_out : pp.b_retry;
+    uint32_t c = 0;
+    CK(cudaMemcpy(&c, &pp.ctl->cnt[slot], 4, cudaMemcpyDeviceToHost));
+    c = (uint32_t)std::min<int64_t>(c, p->cap);
+    std::vector<uint32_t> h(c);
+    if (c) CK(cudaMemcpy(h.data(), pp.buf[buf], c * 4, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < c; ++i)
+      if (tot + i < cap && items) items[tot + i] = h[i];
+    tot += c;
+  }
+  *count = tot;
+  return IRGL_OK;
+}
+irgl_status_t irgl_pipe_destroy(irgl_pipe* p) {
+  if (!p) return IRGL_E_INVALID;
+  for (size_t l = 0; l < p->parts.size(); ++l) {
+    cudaSetDevice(p->ctx->parts[l].dev);
+    cudaStreamSynchronize(p->ctx->parts[l].st);
+    for (int k = 0; k < 3; ++k)
+      if (p->parts[l].buf[k]) cudaFree(p->parts[l].buf[k]);
+    if (p->parts[l].ctl) cudaFree(p->parts[l].ctl);
+  }
+  delete p;
+  return IRGL_OK;
+}
+
+// ---- operators ---------------------------------------------------------------------------------
+irgl_status_t irgl_op_reset(irgl_ctx* ctx, irgl_graph* g, irgl_op op, const irgl_op_args* args,
+                            irgl_pipe* pipe) {
+  (void)args;
+  if (!ctx || !is_known_op(op)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown operator");
+  if (g && g->ctx != ctx) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph belongs to another ctx");
+  return op_reset(ctx, g, op, pipe);
+}
+
+static irgl_status_t check_call(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op) {
+  if (!ctx) return IRGL_E_INVALID;
+  if (!is_known_op(op)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown operator");
+  if (g && g->ctx != ctx) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph belongs to another ctx");
+  if (pipe && pipe->ctx != ctx) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "pipe belongs to another ctx");
+  if ((is_wl_graph_op(op) || is_test_op(op)) && !pipe)
+    return fail(ctx, IRGL_E_USAGE, "E_USAGE",
+                "Invoke of a worklist-using kernel outside any Pipe/Iterate context (SPEC.md:187)");
+  if (!is_test_op(op) && !g) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph operator needs a graph");
+  if (op == IRGL_OP_SSSP && g && !g->has_w)
+    return fail(ctx, IRGL_E_USAGE, "E_USAGE", "SSSP needs edge weights");
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
+                          const irgl_op_args* args, irgl_reduction red, int32_t* reduced,
+                          irgl_iter_stats* stats) {
+  irgl_status_t s = check_call(ctx, pipe, g, op);
+  if (s != IRGL_OK) return s;
+  irgl_iter_stats st{};
+  st.last_reduced = -1;
+  if (is_test_op(op)) {
+    int32_t* dv = nullptr;
+    s = upload_values(ctx, args, &dv);
+    if (s == IRGL_OK) s = test_invoke(ctx, pipe, op, args, red, reduced, &st, dv);
+    if (dv) cudaFree(dv);
+  } else if (is_wl_graph_op(op)) {
+    if (g->lab_op != op) {
+      s = op_reset(ctx, g, op, pipe);
+      if (s != IRGL_OK) return s;
+    }
+    irgl_iterate_opts o{};
+    const int64_t level = args && args->round_start > 0 ? args->round_start : 1;
+    s = pipe_counters(ctx, pipe, nullptr);
+    if (s == IRGL_OK) s = wl_graph_rounds(ctx, pipe, g, op, level, o, true, &st);
+    if (s == IRGL_OK) s = pipe_counters(ctx, pipe, &st);
+    if (reduced) *reduced = red == IRGL_RED_ALL ? 1 : red == IRGL_RED_ANY ? 0 : -1;  // identity
+  } else {
+    s = topo_invoke(ctx, g, op, args, red, reduced, &st);
+  }
+  if (stats) *stats = st;
+  return s;
+}
+
+irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
+                           const irgl_op_args* args, const irgl_iterate_opts* opts,
+                           irgl_iter_stats* stats) {
+  irgl_status_t s = check_call(ctx, pipe, g, op);
+  if (s != IRGL_OK) return s;
+  irgl_iterate_opts o{};
+  o.outline = -1;
+  o.reset = 1;
+  if (opts) o = *opts;
+  irgl_iter_stats st{};
+  st.last_reduced = -1;
+  int outline = o.outline >= 0 ? o.outline : ctx->cfg.outline;
+  if (outline < 0) outline = 1;  // auto: outline whenever the planner allows it
+  const PartRT& pr0 = ctx->parts[0];
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaEventRecord(ctx->ev0, pr0.st));
+  if (is_wl_graph_op(op)) {
+    if (o.reset || g->lab_op != op) {
+      s = op_reset(ctx, g, op, pipe);
+      if (s != IRGL_OK) return s;
+      CK(cudaSetDevice(pr0.dev));
+      CK(cudaEventRecord(ctx->ev0, pr0.st));
+    }
+    s = pipe_counters(ctx, pipe, nullptr);  // zero edges / remote counters
+    if (s != IRGL_OK) return s;
+    const int64_t level = args && args->round_start > 0 ? args->round_start : 1;
+    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, &st);
+    else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, &st);
+    if (s != IRGL_OK) return s;
+    s = pipe_counters(ctx, pipe, &st);  // edges scanned / remote updates
+    if (s != IRGL_OK) return s;
+  } else if (op == IRGL_OP_PR && outline && ctx->ptotal() == 1 &&
+             (o.cond_mode != IRGL_COND_NONE || o.max_rounds > 0)) {
+    if (o.reset) {
+      s = op_reset(ctx, g, op, nullptr);
+      if (s != IRGL_OK) return s;
+      CK(cudaSetDevice(pr0.dev));
+      CK(cudaEventRecord(ctx->ev0, pr0.st));
+    }
+    s = pr_outlined(ctx, g, args, o, &st);
+    if (s != IRGL_OK) return s;
+  } else {
+    // host loop over Invoke: test operators and topology-driven operators
+    if (o.reset && g && !is_test_op(op)) {
+      s = op_reset(ctx, g, op, nullptr);
+      if (s != IRGL_OK) return s;
+    }
+    const int red = o.cond_mode != IRGL_COND_NONE ? (o.reduction ? o.reduction : IRGL_RED_ANY) : IRGL_RED_NONE;
+    int32_t* dv = nullptr;
+    if (is_test_op(op)) {
+      s = upload_values(ctx, args, &dv);
+      if (s != IRGL_OK) return s;
+    }
+    for (;;) {
+      const bool wl = is_test_op(op);
+      const bool empty = wl && pipe->parts[0].n_in == 0;
+      const bool extra = o.max_rounds > 0 && st.rounds >= o.max_rounds;
+      bool stop = o.max_rounds > 0 ? (o.extra_comb == IRGL_COMB_AND ? (empty && extra) : (empty || extra)) : empty;
+      if (stop) break;
+      int32_t r = -1;
+      if (wl) {
+        s = test_invoke(ctx, pipe, op, args, red, &r, &st, dv);
+        st.rounds++;
+      } else {
+        s = topo_invoke(ctx, g, op, args, red, &r, &st);
+      }
+      if (s != IRGL_OK) break;
+      if (o.cond_mode == IRGL_COND_WHILE && r == 0) break;
+      if (o.cond_mode == IRGL_COND_UNTIL && r == 1) break;
+      if (!wl && o.cond_mode == IRGL_COND_NONE && o.max_rounds <= 0) break;  // plain Invoke
+    }
+    if (dv) cudaFree(dv);
+    if (s != IRGL_OK) return s;
+  }
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaEventRecord(ctx->ev1, pr0.st));
+  CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  st.device_ms = ms;
+  if (stats) *stats = st;
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out, size_t bytes) {
+  if (!ctx || !host_out) return IRGL_E_INVALID;
+  if (is_test_op(op)) {
+    if (!ctx->test_log) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "no test operator has run");
+    const size_t nb = std::min(bytes, (size_t)ctx->test_log_cap * 4);
+    CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaMemcpy(host_out, ctx->test_log, nb, cudaMemcpyDeviceToHost));
+    return IRGL_OK;
+  }
+  if (!g) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph operator result needs the graph");
+  if (op == IRGL_OP_TC) {
+    if (bytes < 8) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "TC result is one uint64");
+    std::memcpy(host_out, &g->tc_count, 8);
+    return IRGL_OK;
+  }
+  if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
+  const size_t esz = op == IRGL_OP_PR ? 8 : 4;
+  if (bytes < (size_t)g->n * esz) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    CK(cudaStreamSynchronize(ctx->parts[l].st));
+    const int64_t nloc = gp.hi - gp.lo;
+    if (nloc <= 0) continue;
+    if (op == IRGL_OP_PR) {
+      CK(cudaMemcpy((double*)host_out + gp.lo, gp.pr[gp.pr_cur] + gp.lo, nloc * 8, cudaMemcpyDeviceToHost));
+    } else {
+      CK(cudaMemcpy((int32_t*)host_out + gp.lo, gp.lab + gp.lo, nloc * 4, cudaMemcpyDeviceToHost));
+    }
+  }
+  return IRGL_OK;
+}
+
+// ---- launch planning ----------------------------------------------------------------------------
+irgl_status_t irgl_t_control(const irgl_block_constraint* cs, int n, int32_t* out) {
+  if (!cs || n < 1 || !out) return IRGL_E_INVALID;
+  // domains are intervals [lo, hi] inside [1, 1024]; T_control = max of the intersection
+  int lo = 1, hi = 1024;
+  for (int i = 0; i < n; ++i) {
+    int a = 1, b = 1024;
+    if (cs[i].kind == IRGL_BLOCK_SHRINKABLE) {
+      if (cs[i].value < 1 || cs[i].value > 1024) return IRGL_E_INVALID;
+      b = cs[i].value;
+    } else if (cs[i].kind == IRGL_BLOCK_FIXED) {
+      if (cs[i].value < 1 || cs[i].value > 1024) return IRGL_E_INVALID;
+      a = b = cs[i].value;
+    } else if (cs[i].kind != IRGL_BLOCK_ELASTIC) {
+      return IRGL_E_INVALID;
+    }
+    lo = std::max(lo, a);
+    hi = std::min(hi, b);
+  }
+  if (lo > hi) {
+    set_error(nullptr, IRGL_E_OUTLINE_EMPTY, "E_OUTLINE_EMPTY",
+              "iteration outlining cannot be performed on this Pipe (PAPER.md:438)");
+    return IRGL_E_OUTLINE_EMPTY;
+  }
+  *out = hi;
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_op_plan(irgl_ctx* ctx, irgl_op op, irgl_block_constraint* block,
+                           int32_t* grid_outlined, int32_t* grid_fixed) {
+  if (!ctx || !is_known_op(op)) return IRGL_E_INVALID;
+  CK(cudaSetDevice(ctx->parts[0].dev));
+  const int sms = ctx->parts[0].sms;
+  if (block) {
+    if (is_test_op(op)) {
+      block->kind = IRGL_BLOCK_ELASTIC;
+      block->value = 0;
+    } else {
+      block->kind = IRGL_BLOCK_FIXED;  // smem sized by the block
+      block->value = kBlock;
+    }
+  }
+  int bps_o = 0;
+  if (is_wl_graph_op(op)) bps_o = persistent_blocks_per_sm(op);
+  else if (op == IRGL_OP_PR) bps_o = pr_persistent_blocks_per_sm();
+  if (grid_outlined) *grid_outlined = bps_o * sms;
+  if (grid_fixed) *grid_fixed = grid_max(ctx, ctx->parts[0], op);
+  return IRGL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// internal.cuh — shared host/device definitions of the B200 IrGL runtime (libirgl_rt.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "irgl/rt.h"
+
+namespace irgl {
+
+// Fixed(256): the nested-parallelism / cooperative-conversion kernels use shared memory sized by
+// the block, so their block constraint is Fixed.
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int32_t kInf = 0x7fffffff;
+constexpr int kPushBuf = 2048;  // per-CTA shared-memory push staging (cooperative conversion)
+
+// CTA-chunk descriptor: `len` (<= chunk_edges) edges of vertex v starting at edge `beg`.
+struct ChunkDesc {
+  int64_t beg;
+  uint32_t v;
+  uint32_t len;
+};
+
+// Device-resident control block of one pipe partition.  Counter slots are addressed by index so
+// the persistent kernel can rotate them (see persistent loop in expand.cu).
+struct Ctl {
+  uint32_t cnt[4];        // worklist counters: in / out / retry / spare (slots named by the host)
+  uint32_t chunk_cnt[3];  // CTA-chunk list counters, rotated by round
+  uint32_t red[3];        // ReduceAndReturn cells, rotated by round
+  uint32_t overflow;      // push beyond capacity (IRGL_E_WL_OVERFLOW)
+  uint32_t pad;
+  unsigned long long edges;    // directed edges scanned
+  unsigned long long popped;   // items popped (persistent mode)
+  unsigned long long pushes;   // items pushed (persistent mode)
+  unsigned long long remote;   // remote updates emitted
+  unsigned long long rounds;   // persistent: rounds executed
+  int32_t last_red;            // persistent: last round's reduced value
+  int32_t exit_in_slot;        // persistent: buffer parity at exit
+  unsigned long long tc_count; // TC: Sum reduction (extension)
+};
+
+// ---------------------------------------------------------------------------------------------
+// Device helpers.
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// 128-bit streaming load of CSR column / weight data: read-only for the kernel's lifetime, so
+// the non-coherent path with L1 no-allocate (stream, do not pollute L1 with col data).
+__device__ __forceinline__ int4 ld_stream_v4(const int32_t* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+// Label/distance gathers: coherent global loads.  A stale (larger / INF) value is benign for
+// every operator here: it only causes an atomic that then returns the true value.
+__device__ __forceinline__ int32_t ld_label(const int32_t* p) {
+  int32_t r;
+  asm volatile("ld.global.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+}  // namespace irgl
+
+// ---------------------------------------------------------------------------------------------
+// Host-side error plumbing: every API call returns a status; the message goes to the ctx
+// (or a global slot) as "RULE: message" (reference diag.hpp:20-27 convention).
+namespace irgl {
+void set_error(irgl_ctx* ctx, irgl_status_t st, const char* rule, const std::string& msg);
+irgl_status_t cuda_status(irgl_ctx* ctx, cudaError_t e, const char* where);
+}  // namespace irgl
+
+#define IRGL_CUDA(ctx, expr)                                              \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) return ::irgl::cuda_status((ctx), _e, #expr);  \
+  } while (0)

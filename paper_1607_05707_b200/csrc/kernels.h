@@ -1,0 +1,127 @@
+// kernels.h — host-side launchers of the device kernels (one translation unit per family).
+#pragma once
+#include "internal.cuh"
+
+namespace irgl {
+
+// One partition's CSR rows [lo, hi) with global column ids.
+struct DevCSR {
+  const int64_t* row_ptr;  // [hi-lo+1]
+  const int32_t* col;      // [m_local]
+  const int32_t* w;        // [m_local] or nullptr
+  int64_t lo, hi;
+};
+
+// Routing of pushes whose destination is owned by another partition (1D vertex partition).
+struct DistRoute {
+  int nparts;          // 1 => no routing
+  int me;
+  int64_t part_size;   // ceil(N / nparts); owner(v) = v / part_size
+  uint32_t* send;      // [N]: bucket of peer q is send[q*part_size ...]
+  uint32_t* send_cnt;  // [nparts]
+};
+
+struct ExpandCfg {
+  int32_t warp_t, cta_t, chunk_edges;
+};
+
+// Worklist view of one round.
+struct RoundBufs {
+  const uint32_t* in;
+  uint32_t nin;
+  uint32_t* out;
+  uint32_t* out_cnt;
+  uint32_t cap;
+  ChunkDesc* chunks;
+  uint32_t* chunk_cnt;
+  uint32_t chunk_cap;
+  int32_t level;     // BFS LEVEL of this round
+  int32_t stamp_id;  // unique round id (push dedupe)
+};
+
+// ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
+// One host-orchestrated round: expansion of `in` plus the CTA-chunk (hub) phase.
+cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+                                const RoundBufs& rb, const DistRoute& dr, const ExpandCfg& ec,
+                                int grid_max, cudaStream_t st);
+// Apply received remote updates (owner side min-reduce): items[i] with values[i] (BFS: level).
+cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, const uint32_t* items,
+                                const int32_t* values, uint32_t n, uint32_t* out, uint32_t* out_cnt,
+                                uint32_t cap, int32_t level, int32_t stamp_id, cudaStream_t st);
+// Gather current label values of the send buckets (SSSP / CC_LP pack step).
+cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
+                               uint32_t n, cudaStream_t st);
+
+struct PersistArgs {
+  uint32_t* buf_a;   // in buffer at round 0
+  uint32_t* buf_b;   // out buffer at round 0
+  int32_t slot[3];   // counter slots in Ctl::cnt: in, out, spare at round 0
+  uint32_t cap;
+  ChunkDesc* chunks;
+  uint32_t chunk_cap;
+  int32_t level0;
+  int32_t stamp0;
+  int64_t max_rounds;  // 0 = until empty
+};
+// Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
+cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+                              const PersistArgs& pa, const ExpandCfg& ec, int grid,
+                              cudaStream_t st);
+// Co-resident CTAs/SM of the persistent kernel for `op` (occupancy API).
+int persistent_blocks_per_sm(int op);
+int expand_blocks_per_sm(int op);
+
+// ---- topology-driven operators (topo.cu) ----------------------------------------------------
+cudaError_t launch_cc_hook(const DevCSR& g, int32_t* parent, Ctl* ctl, int red_slot, int grid,
+                           cudaStream_t st);
+cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st);
+cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
+                           cudaStream_t st);
+cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
+                            const double* contrib, double* contrib_next, double d, double tol,
+                            int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st);
+cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double* ca, double* cb,
+                                 double d, double tol, int64_t n_global, Ctl* ctl,
+                                 int64_t max_rounds, int cond_mode, int grid, cudaStream_t st);
+int pr_persistent_blocks_per_sm();
+cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out, int64_t* m_out,
+                      cudaStream_t st);
+cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl* ctl,
+                            cudaStream_t st);
+
+// ---- misc (util.cu) ---------------------------------------------------------------------------
+cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);
+cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st);
+cudaError_t launch_iota_u32(uint32_t* p, uint32_t begin, uint32_t n, cudaStream_t st);
+cudaError_t launch_set_red(Ctl* ctl, int slot, uint32_t v, cudaStream_t st);
+
+// ---- test operators (testops.cu) ----------------------------------------------------------------
+struct TestArgs {
+  int op;
+  const uint32_t* in;
+  uint32_t nin;
+  uint32_t* out;
+  uint32_t* out_cnt;
+  uint32_t* retry;
+  uint32_t* retry_cnt;
+  uint32_t cap;
+  int64_t guard;
+  const int32_t* values;
+  int32_t* rcount;    // per item retry counts
+  int32_t* log;       // PUSHPOP: popped_at; FORALL_MAP: thread id
+  int32_t launch_no;
+  int mapping;
+  uint32_t* red;      // return cell
+  int reduction;
+  uint32_t* overflow;
+};
+cudaError_t launch_test_op(const TestArgs& a, int threads, cudaStream_t st);
+
+// ---- graph generation (gen.cu) ------------------------------------------------------------------
+// Builds the CSR rows [lo, hi) of the generated graph on the device.
+cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t hi,
+                          int64_t** row_ptr, int32_t** col, int32_t** w, int64_t* m_local,
+                          cudaStream_t st, std::string* err);
+cudaError_t max_degree(const int64_t* row_ptr, int64_t nrows, int64_t* out, cudaStream_t st);
+
+}  // namespace irgl

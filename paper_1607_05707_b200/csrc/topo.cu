@@ -1,0 +1,396 @@
+// topo.cu — topology-driven operators (no worklist; Iterate is a plain loop):
+//   CC  : hook (CAS the larger root onto the smaller) + pointer jumping, Iterate While Any.
+//   PR  : pull Jacobi PageRank in fp64 with a fused contrib_next write and the E4 warp-reduced
+//         ReduceAndReturn(|new-old| > tol) flag; outlined variant = one persistent kernel.
+//   TC  : degree-ordered orientation + warp-cooperative sorted-list intersection, warp-reduced
+//         64-bit Sum (an extension: IrGL's ReduceAndReturn has only Any/All).
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace irgl {
+namespace {
+constexpr unsigned FULL = 0xffffffffu;
+
+// E4: warp-reduced ReduceAndReturn.  Threads that evaluated `value` fold it; one idempotent store
+// per warp (Any writes 1 into a cell initialised to 0, All writes 0 into a cell initialised to 1)
+// — no atomics, no per-thread traffic.
+__device__ __forceinline__ void reduce_and_return(bool evaluated, bool value, int reduction,
+                                                  uint32_t* cell) {
+  if (reduction == IRGL_RED_ANY) {
+    if (__any_sync(FULL, evaluated && value) && lane_id() == 0) *(volatile uint32_t*)cell = 1u;
+  } else if (reduction == IRGL_RED_ALL) {
+    if (!__all_sync(FULL, !evaluated || value) && lane_id() == 0) *(volatile uint32_t*)cell = 0u;
+  }
+}
+
+__device__ __forceinline__ int32_t cc_find(const int32_t* par, int32_t x) {
+  int32_t p = ld_label(par + x);
+  while (p != x) {
+    x = p;
+    p = ld_label(par + x);
+  }
+  return x;
+}
+
+// Hook edge (u, v): ECL-CC style CAS retry so each edge needs one visit.
+__device__ __forceinline__ bool cc_hook_edge(int32_t* par, int32_t u, int32_t v) {
+  int32_t a = cc_find(par, u), b = cc_find(par, v);
+  bool changed = false;
+  while (a != b) {
+    const int32_t hi = max(a, b), lo = min(a, b);
+    const int32_t old = atomicCAS(par + hi, hi, lo);
+    if (old == hi) {
+      changed = true;
+      break;
+    }
+    a = cc_find(par, old);
+    b = cc_find(par, lo);
+  }
+  return changed;
+}
+
+__global__ void __launch_bounds__(kBlock) cc_hook_kernel(DevCSR g, int32_t* par, uint32_t* cell) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nloc = g.hi - g.lo;
+  for (int64_t t0 = (int64_t)blockIdx.x * kBlock; t0 < nloc; t0 += (int64_t)gridDim.x * kBlock) {
+    const int64_t i = t0 + threadIdx.x;
+    const bool valid = i < nloc;
+    int64_t beg = 0, end = 0;
+    if (valid) {
+      beg = g.row_ptr[i];
+      end = g.row_ptr[i + 1];
+    }
+    const int32_t u = (int32_t)(g.lo + i);
+    bool changed = false;
+    // warp-cooperative for high degree
+    int64_t deg = end - beg;
+    uint32_t wm = __ballot_sync(FULL, deg >= 32);
+    while (wm) {
+      const int leader = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const int64_t b = __shfl_sync(FULL, beg, leader), e = __shfl_sync(FULL, end, leader);
+      const int32_t uu = __shfl_sync(FULL, u, leader);
+      if (lane == leader) deg = 0;
+      for (int64_t k = b + lane; k < e; k += 32) {
+        const int32_t v = ld_stream(g.col + k);
+        if (v < uu) changed |= cc_hook_edge(par, uu, v);
+      }
+    }
+    if (deg > 0)
+      for (int64_t k = beg; k < end; ++k) {
+        const int32_t v = ld_stream(g.col + k);
+        if (v < u) changed |= cc_hook_edge(par, u, v);
+      }
+    reduce_and_return(true, changed, IRGL_RED_ANY, cell);
+  }
+}
+
+__global__ void cc_compress_kernel(int32_t* par, int64_t n) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    par[v] = cc_find(par, (int32_t)v);
+}
+
+// ---------------------------------------------------------------------------------------------
+// PageRank.  rank(v) = (1-d)/N + d * sum_{u in N(v)} contrib(u), contrib(u) = rank(u)/deg(u).
+struct PrSmem {
+  double red[kWarps];
+  int32_t owner;
+  int64_t b, e;
+};
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+  return x;
+}
+
+// One PR sweep over the local vertex range (tile per CTA-iteration).  Deterministic per-vertex
+// summation order (fixed by the code path chosen by degree).
+__device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
+                               double* __restrict__ rank_new, const double* __restrict__ contrib,
+                               double* __restrict__ contrib_next, double d, double tol,
+                               double base, int red, uint32_t* cell) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t nloc = g.hi - g.lo;
+  for (int64_t t0 = (int64_t)blockIdx.x * kBlock; t0 < nloc; t0 += (int64_t)gridDim.x * kBlock) {
+    const int64_t i = t0 + tid;
+    const bool valid = i < nloc;
+    int64_t beg = 0, end = 0;
+    if (valid) {
+      beg = __ldg(g.row_ptr + i);
+      end = __ldg(g.row_ptr + i + 1);
+    }
+    const int64_t deg0 = end - beg;
+    int64_t deg = deg0;
+    double mysum = 0.0;
+    // CTA level (deg >= 1024): whole CTA sums one vertex at a time
+    while (__syncthreads_or(deg >= 1024)) {
+      if (deg >= 1024) sm.owner = tid;  // any winner
+      __syncthreads();
+      const int own = sm.owner;
+      if (tid == own) {
+        sm.b = beg;
+        sm.e = end;
+        deg = 0;
+      }
+      __syncthreads();
+      double s = 0.0;
+      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += contrib[ld_stream(g.col + k)];
+      s = warp_sum(s);
+      if (lane == 0) sm.red[warp] = s;
+      __syncthreads();
+      if (tid == own) {
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < kWarps; ++k) t += sm.red[k];
+        mysum = t;
+      }
+      __syncthreads();
+    }
+    // warp level
+    uint32_t wm = __ballot_sync(FULL, deg >= 32);
+    while (wm) {
+      const int leader = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const int64_t b = __shfl_sync(FULL, beg, leader), e = __shfl_sync(FULL, end, leader);
+      double s = 0.0;
+      for (int64_t k = b + lane; k < e; k += 32) s += contrib[ld_stream(g.col + k)];
+      s = warp_sum(s);
+      if (lane == leader) {
+        mysum = s;
+        deg = 0;
+      }
+    }
+    // thread level
+    if (deg > 0) {
+      double s = 0.0;
+      for (int64_t k = beg; k < end; ++k) s += contrib[ld_stream(g.col + k)];
+      mysum = s;
+    }
+    bool changed = false;
+    if (valid) {
+      const int64_t v = g.lo + i;
+      const double r = base + d * mysum;
+      rank_new[v] = r;
+      contrib_next[v] = deg0 > 0 ? r / (double)deg0 : 0.0;
+      changed = fabs(r - rank_old[v]) > tol;
+    }
+    reduce_and_return(valid, changed, red, cell);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) pr_sweep_kernel(DevCSR g, const double* rank_old,
+                                                          double* rank_new, const double* contrib,
+                                                          double* contrib_next, double d,
+                                                          double tol, double base, uint32_t* cell) {
+  __shared__ PrSmem sm;
+  pr_sweep_tiles(sm, g, rank_old, rank_new, contrib, contrib_next, d, tol, base, IRGL_RED_ANY,
+                 cell);
+}
+
+__global__ void pr_init_kernel(double* rank, double* contrib, const int64_t* row_ptr, int64_t n) {
+  const double r0 = 1.0 / (double)n;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    rank[v] = r0;
+    const int64_t deg = row_ptr[v + 1] - row_ptr[v];
+    contrib[v] = deg > 0 ? r0 / (double)deg : 0.0;
+  }
+}
+
+// Outlined PR: Iterate While Any PR(graph) [Or rounds >= max] as one persistent kernel.
+// Cells rotate over 3 slots: cell (r+1)%3 is reset during round r (last read at the start of r-1).
+__global__ void __launch_bounds__(kBlock) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
+                                                               double* ca, double* cb, double d,
+                                                               double tol, double base, Ctl* ctl,
+                                                               int64_t max_rounds, int cond_mode) {
+  __shared__ PrSmem sm;
+  cg::grid_group grid = cg::this_grid();
+  for (int64_t r = 0;; ++r) {
+    double* ro = (r & 1) ? rb : ra;
+    double* rn = (r & 1) ? ra : rb;
+    double* co = (r & 1) ? cb : ca;
+    double* cn = (r & 1) ? ca : cb;
+    uint32_t* cell = &ctl->red[r % 3];
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->red[(r + 1) % 3] = 0u;
+    pr_sweep_tiles(sm, g, ro, rn, co, cn, d, tol, base, IRGL_RED_ANY, cell);
+    grid.sync();
+    const uint32_t any = *(volatile uint32_t*)cell;
+    bool stop = false;
+    if (cond_mode == IRGL_COND_WHILE) stop = (any == 0u);
+    if (cond_mode == IRGL_COND_UNTIL) stop = (any == 1u);
+    if (max_rounds > 0 && r + 1 >= max_rounds) stop = true;
+    if (stop) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->rounds = (unsigned long long)(r + 1);
+        ctl->last_red = (int32_t)any;
+        ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+      }
+      break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// TC: orientation u -> v iff (deg u, u) < (deg v, v); warp per vertex, order-preserving
+// ballot compaction keeps each N+(u) sorted.
+__device__ __forceinline__ bool tc_less(const int64_t* rp, int64_t u, int64_t v) {
+  const int64_t du = rp[u + 1] - rp[u], dv = rp[v + 1] - rp[v];
+  return du < dv || (du == dv && u < v);
+}
+
+__global__ void tc_count_out_kernel(const int64_t* rp, const int32_t* col, int64_t n,
+                                    int64_t* dout) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t c = 0;
+    for (int64_t k0 = rp[u]; k0 < rp[u + 1]; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool p = k < rp[u + 1] && tc_less(rp, u, col[k]);
+      c += __popc(__ballot_sync(FULL, p));
+    }
+    if (lane == 0) dout[u] = c;
+  }
+}
+
+__global__ void tc_fill_kernel(const int64_t* rp, const int32_t* col, int64_t n, const int64_t* orp,
+                               int32_t* ocl) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    int64_t o = orp[u];
+    for (int64_t k0 = rp[u]; k0 < rp[u + 1]; k0 += 32) {
+      const int64_t k = k0 + lane;
+      int32_t v = 0;
+      bool p = false;
+      if (k < rp[u + 1]) {
+        v = col[k];
+        p = tc_less(rp, u, v);
+      }
+      const uint32_t m = __ballot_sync(FULL, p);
+      if (p) ocl[o + __popc(m & lanemask_lt())] = v;
+      o += __popc(m);
+    }
+  }
+}
+
+__device__ __forceinline__ bool bsearch_i32(const int32_t* a, int64_t n, int32_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int32_t y = a[mid];
+    if (y == x) return true;
+    if (y < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return false;
+}
+
+// warp per vertex u; for each v in N+(u): lanes stride the shorter of N+(u), N+(v) and binary
+// search the longer.  Warp-reduced 64-bit count, one atomic per warp.
+__global__ void tc_count_kernel(const int64_t* orp, const int32_t* ocl, int64_t n,
+                                unsigned long long* total) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long cnt = 0;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t ub = orp[u], ue = orp[u + 1];
+    for (int64_t k = ub; k < ue; ++k) {
+      const int32_t v = ocl[k];
+      const int64_t vb = orp[v], ve = orp[v + 1];
+      const int64_t du = ue - ub, dv = ve - vb;
+      const int32_t* S = du <= dv ? ocl + ub : ocl + vb;
+      const int32_t* L = du <= dv ? ocl + vb : ocl + ub;
+      const int64_t ns = du <= dv ? du : dv, nl = du <= dv ? dv : du;
+      for (int64_t j = lane; j < ns; j += 32) cnt += bsearch_i32(L, nl, S[j]) ? 1 : 0;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(FULL, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(total, cnt);
+}
+
+}  // namespace
+
+cudaError_t launch_cc_hook(const DevCSR& g, int32_t* parent, Ctl* ctl, int red_slot, int grid,
+                           cudaStream_t st) {
+  cc_hook_kernel<<<grid, kBlock, 0, st>>>(g, parent, &ctl->red[red_slot]);
+  return cudaGetLastError();
+}
+cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  cc_compress_kernel<<<grid, 256, 0, st>>>(parent, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
+                           cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  pr_init_kernel<<<grid, 256, 0, st>>>(rank, contrib, row_ptr, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
+                            const double* contrib, double* contrib_next, double d, double tol,
+                            int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st) {
+  const double base = (1.0 - d) / (double)n_global;
+  pr_sweep_kernel<<<grid, kBlock, 0, st>>>(g, rank_old, rank_new, contrib, contrib_next, d, tol,
+                                           base, &ctl->red[red_slot]);
+  return cudaGetLastError();
+}
+int pr_persistent_blocks_per_sm() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pr_persistent_kernel, kBlock, 0);
+  return nb;
+}
+cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double* ca, double* cb,
+                                 double d, double tol, int64_t n_global, Ctl* ctl,
+                                 int64_t max_rounds, int cond_mode, int grid, cudaStream_t st) {
+  double base = (1.0 - d) / (double)n_global;
+  DevCSR gg = g;
+  void* args[] = {&gg, &ra, &rb, &ca, &cb, &d, &tol, &base, &ctl, &max_rounds, &cond_mode};
+  return cudaLaunchCooperativeKernel((void*)pr_persistent_kernel, grid, kBlock, args, 0, st);
+}
+
+cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out,
+                      int64_t* m_out, cudaStream_t st) {
+  int64_t* dout = nullptr;
+  int64_t* orp = nullptr;
+  int32_t* ocl = nullptr;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&dout, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&orp, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
+  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  tc_count_out_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, dout);
+  cudaMemsetAsync(dout + n, 0, sizeof(int64_t), st);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, dout, orp, n + 1, st);
+  void* t = nullptr;
+  if ((e = cudaMallocAsync(&t, tmp, st)) != cudaSuccess) return e;
+  cub::DeviceScan::ExclusiveSum(t, tmp, dout, orp, n + 1, st);
+  int64_t mo = 0;
+  cudaMemcpyAsync(&mo, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&ocl, (mo > 0 ? mo : 1) * sizeof(int32_t), st)) != cudaSuccess) return e;
+  tc_fill_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, orp, ocl);
+  cudaFreeAsync(t, st);
+  cudaFreeAsync(dout, st);
+  *rp_out = orp;
+  *cl_out = ocl;
+  *m_out = mo;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl* ctl,
+                            cudaStream_t st) {
+  cudaMemsetAsync(&ctl->tc_count, 0, sizeof(unsigned long long), st);
+  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  tc_count_kernel<<<grid, 256, 0, st>>>(rp, cl, n, &ctl->tc_count);
+  return cudaGetLastError();
+}
+
+}  // namespace irgl

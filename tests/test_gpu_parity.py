@@ -1,0 +1,239 @@
+"""GPU parity tests: the sm_100a runtime (through the C-ABI) against the CPU oracle on identical
+inputs.  Integer results bit-exact; PageRank within 1e-6 L1-relative (north_star).
+
+Reference pins: SPEC.md:438 (path-5 BFS), :549 (random graphs, rounds = ecc+1); the SSSP / CC /
+PR / TC operators are pinned by the oracle and SURVEY Appendix C known answers."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------------------------------------
+# device graph generator == oracle graph generator (F2: GPU Philox RMAT / grids)
+@pytest.mark.parametrize("scale", [6, 10, 14])
+def test_device_rmat_matches_oracle(ctx, oracle, scale):
+    og = oracle.rmat(scale)
+    g = ctx.generate_rmat(scale)
+    assert g.n == og.n and g.m == og.m
+    rp, col, w = g.download()
+    np.testing.assert_array_equal(rp, og.row_ptr)
+    np.testing.assert_array_equal(col, og.col)
+    np.testing.assert_array_equal(w, og.weight)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(diag=True), dict(cut_period=3),
+                                dict(perc_keep=0.5), dict(diag=True, cut_period=4, perc_keep=0.7)])
+def test_device_grid_matches_oracle(ctx, oracle, kw):
+    og = oracle.grid(13, 11, **kw)
+    g = ctx.generate_grid(13, 11, **kw)
+    rp, col, w = g.download()
+    np.testing.assert_array_equal(rp, og.row_ptr)
+    np.testing.assert_array_equal(col, og.col)
+    np.testing.assert_array_equal(w, og.weight)
+
+
+def _upload(ctx, og):
+    return ctx.graph_from_csr(og.row_ptr, og.col, og.weight)
+
+
+# ---------------------------------------------------------------------------------------------
+# BFS — Listing 2
+def test_bfs_path5_golden(ctx, irgl, oracle):
+    og = oracle.grid(5, 1)
+    g = _upload(ctx, og)
+    for outline in (0, 1):
+        lv, st = irgl.bfs(ctx, g, 0, outline=outline)
+        assert lv.tolist() == [0, 1, 2, 3, 4]
+        assert st.rounds == 5                 # ecc(src)+1 invocations (App. B1)
+
+
+@pytest.mark.parametrize("outline", [0, 1])
+def test_bfs_rmat_parity(ctx, irgl, oracle, outline):
+    og = oracle.rmat(14)
+    g = _upload(ctx, og)
+    for s in og.sources(4):
+        ref, ecc = oracle.bfs(og, int(s))
+        lv, st = irgl.bfs(ctx, g, int(s), outline=outline)
+        np.testing.assert_array_equal(lv, ref)
+        assert st.rounds == ecc + 1
+        reached = ref < oracle.INF
+        assert st.edges == int(og.degrees()[reached].sum())
+
+
+def test_bfs_random_small_graphs(ctx, irgl, oracle):
+    """random connected graphs (<= 64 nodes), levels == sequential BFS."""
+    rng = np.random.default_rng(3)
+    for t in range(20):
+        n = int(rng.integers(2, 65))
+        # random spanning tree + extra edges => connected
+        u = [int(rng.integers(0, i)) for i in range(1, n)]
+        v = list(range(1, n))
+        k = int(rng.integers(0, 2 * n))
+        u += rng.integers(0, n, k).tolist()
+        v += rng.integers(0, n, k).tolist()
+        og = oracle.from_edges(n, u, v)
+        g = _upload(ctx, og)
+        src = int(rng.integers(0, n))
+        ref, ecc = oracle.bfs(og, src)
+        for outline in (0, 1):
+            lv, st = irgl.bfs(ctx, g, src, outline=outline)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1
+
+
+def test_bfs_grid_known_answer(ctx, irgl, oracle):
+    W, H = 64, 48
+    g = ctx.generate_grid(W, H)
+    lv, st = irgl.bfs(ctx, g, 0, outline=1)
+    x, y = np.meshgrid(np.arange(W), np.arange(H))
+    np.testing.assert_array_equal(lv.reshape(H, W), x + y)  # App. C: level(x,y) = x + y
+    assert st.rounds == (W - 1) + (H - 1) + 1
+    gt = ctx.generate_grid(W, H, diag=True)
+    lv, _ = irgl.bfs(ctx, gt, 0)
+    np.testing.assert_array_equal(lv.reshape(H, W), np.maximum(x, y))
+
+
+def test_bfs_isolated_source_and_unreachable(ctx, irgl, oracle):
+    og = oracle.from_edges(6, [0, 1], [1, 2])  # 3,4,5 isolated
+    g = _upload(ctx, og)
+    lv, st = irgl.bfs(ctx, g, 4)
+    assert lv.tolist() == [irgl.INF, irgl.INF, irgl.INF, irgl.INF, 0, irgl.INF]
+    assert st.rounds == 1
+
+
+# ---------------------------------------------------------------------------------------------
+# nested-parallelism scheduler edge cases: force every level (thread / warp / CTA chunk)
+@pytest.mark.parametrize("cfg", [dict(warp_threshold=1, cta_threshold=1, chunk_edges=5),
+                                 dict(warp_threshold=4, cta_threshold=16, chunk_edges=8),
+                                 dict(warp_threshold=1000000, cta_threshold=1000000),
+                                 dict(warp_threshold=32, cta_threshold=64, chunk_edges=64)])
+def test_scheduler_thresholds_parity(irgl, oracle, cfg):
+    og = oracle.rmat(13)
+    with irgl.Context(**cfg) as c:
+        g = _upload(c, og)
+        s = int(og.sources(1)[0])
+        ref, _ = oracle.bfs(og, s)
+        dref = oracle.sssp(og, s)
+        for outline in (0, 1):
+            lv, _ = irgl.bfs(c, g, s, outline=outline)
+            np.testing.assert_array_equal(lv, ref)
+            d, _ = irgl.sssp(c, g, s, outline=outline)
+            np.testing.assert_array_equal(d, dref)
+
+
+# ---------------------------------------------------------------------------------------------
+# SSSP (data-driven Bellman-Ford, integer weights)
+@pytest.mark.parametrize("outline", [0, 1])
+def test_sssp_rmat_parity(ctx, irgl, oracle, outline):
+    og = oracle.rmat(14)
+    g = _upload(ctx, og)
+    for s in og.sources(3):
+        ref = oracle.sssp(og, int(s))
+        d, st = irgl.sssp(ctx, g, int(s), outline=outline)
+        np.testing.assert_array_equal(d, ref)
+
+
+def test_sssp_device_generated_graph(ctx, irgl, oracle):
+    og = oracle.rmat(15)
+    g = ctx.generate_rmat(15)
+    s = int(og.sources(1)[0])
+    d, _ = irgl.sssp(ctx, g, s)
+    np.testing.assert_array_equal(d, oracle.sssp(og, s))
+
+
+def test_sssp_path_known_answer(ctx, irgl, oracle):
+    n = 40
+    og = oracle.from_edges(n, list(range(n - 1)), list(range(1, n)), w=[7] * (n - 1))
+    g = _upload(ctx, og)
+    d, st = irgl.sssp(ctx, g, 0)
+    assert d.tolist() == [7 * i for i in range(n)]  # App. C
+
+
+# ---------------------------------------------------------------------------------------------
+# CC
+def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):
+    og = oracle.rmat(14)
+    lab, st = irgl.cc(ctx, _upload(ctx, og))
+    np.testing.assert_array_equal(lab, oracle.cc(og))
+    W, H, P = 64, 64, 16
+    og = oracle.grid(W, H, cut_period=P)
+    lab, st = irgl.cc(ctx, ctx.generate_grid(W, H, cut_period=P))
+    np.testing.assert_array_equal(lab, oracle.cc(og))
+    assert sorted(set(lab.tolist())) == [k * P * W for k in range(H // P)]  # App. C stripes
+    og = oracle.grid(W, H, perc_keep=0.5)
+    lab, _ = irgl.cc(ctx, ctx.generate_grid(W, H, perc_keep=0.5))
+    np.testing.assert_array_equal(lab, oracle.cc(og))
+
+
+def test_cc_lp_parity(ctx, irgl, oracle):
+    og = oracle.rmat(13)
+    g = _upload(ctx, og)
+    for outline in (0, 1):
+        lab, st = irgl.cc_lp(ctx, g, outline=outline)
+        np.testing.assert_array_equal(lab, oracle.cc(og))
+
+
+# ---------------------------------------------------------------------------------------------
+# PageRank (fp64, tolerance 1e-6 L1 relative per north_star)
+@pytest.mark.parametrize("outline", [0, 1])
+def test_pagerank_parity(ctx, irgl, oracle, outline):
+    og = oracle.rmat(14)
+    g = _upload(ctx, og)
+    ref, it = oracle.pagerank(og)
+    r, st = irgl.pagerank(ctx, g, outline=outline)
+    assert np.abs(r - ref).sum() / np.abs(ref).sum() <= 1e-6
+    assert abs(st.rounds - it) <= 1
+    assert r.sum() <= 1.0 + 1e-9  # App. C: sum(rank) <= 1
+
+
+def test_pagerank_regular_graph_uniform(ctx, irgl, oracle):
+    og = oracle.from_edges(10, list(range(10)), [(i + 1) % 10 for i in range(10)])  # cycle
+    r, _ = irgl.pagerank(ctx, _upload(ctx, og))
+    np.testing.assert_allclose(r, 0.1, rtol=1e-12)
+
+
+# ---------------------------------------------------------------------------------------------
+# TC
+def test_tc_parity(ctx, irgl, oracle):
+    og = oracle.rmat(13)
+    c, _ = irgl.triangle_count(ctx, _upload(ctx, og))
+    assert c == oracle.tc(og)
+    W, H = 50, 40
+    c, _ = irgl.triangle_count(ctx, ctx.generate_grid(W, H, diag=True))
+    assert c == 2 * (W - 1) * (H - 1)  # App. C
+    n = 12
+    u, v = zip(*[(a, b) for a in range(n) for b in range(a + 1, n)])
+    c, _ = irgl.triangle_count(ctx, _upload(ctx, oracle.from_edges(n, u, v)))
+    assert c == n * (n - 1) * (n - 2) // 6  # C(n,3)
+
+
+# ---------------------------------------------------------------------------------------------
+# multi-partition (1D vertex partition + exchange + owner-side min-reduce), loopback transport
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_partitioned_bfs_sssp_parity(irgl, oracle, P):
+    og = oracle.rmat(13)
+    with irgl.Context(logical_partitions=P) as c:
+        g = _upload(c, og)
+        for s in og.sources(2):
+            s = int(s)
+            ref, ecc = oracle.bfs(og, s)
+            lv, st = irgl.bfs(c, g, s)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1
+            d, st = irgl.sssp(c, g, s)
+            np.testing.assert_array_equal(d, oracle.sssp(og, s))
+            assert st.remote_updates > 0
+
+
+def test_partitioned_generated_graph(irgl, oracle):
+    og = oracle.rmat(12)
+    with irgl.Context(logical_partitions=4) as c:
+        g = c.generate_rmat(12)
+        assert g.m == og.m
+        rp, col, w = g.download()
+        np.testing.assert_array_equal(rp, og.row_ptr)
+        np.testing.assert_array_equal(col, og.col)
+        s = int(og.sources(1)[0])
+        lv, _ = irgl.bfs(c, g, s)
+        np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
