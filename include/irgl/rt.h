@@ -104,7 +104,9 @@ typedef struct irgl_op_args {
   int64_t nvalues;
   int32_t mapping;       /* irgl_mapping of the outer ForAll (test operators)                  */
   int32_t threads;       /* test operators: total CUDA threads (0 = planner's choice)          */
-  int32_t reserved[6];
+  int32_t delta;         /* SSSP: near-far bucket width; 0 = plain data-driven Bellman-Ford,
+                            <0 = runtime default.  Same distances either way.                 */
+  int32_t reserved[5];
 } irgl_op_args;
 
 /* Iterate [While|Until Any|All] kernel(args) [ExtraCond] (ast.hpp:186-204). */
@@ -131,6 +133,7 @@ typedef struct irgl_iter_stats {
   int32_t last_reduced;    /* last invocation's Any/All value, -1 if none                      */
   int32_t outlined;        /* 1 if the loop ran as one persistent kernel                       */
   double device_ms;        /* CUDA-event time of the whole iterate on the ctx stream           */
+  double kernel_ms;        /* CUDA-event time of the hot kernels (expand/chunk or persistent)  */
 } irgl_iter_stats;
 
 /* Device graph generator (§8d synthetic inputs). */
@@ -217,6 +220,14 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
  * TC uint64[1]; test ops: PUSHPOP/FORALL_MAP int32[capacity] (g may be NULL). */
 irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out,
                                size_t bytes);
+
+/* ---- measurement --------------------------------------------------------------------------- */
+/* CUDA events on the stream of the ctx's first partition (the stream every kernel of this ctx is
+ * ordered on), slots 0..7; elapsed time between two recorded slots in ms. */
+irgl_status_t irgl_event_record(irgl_ctx* ctx, int slot);
+irgl_status_t irgl_event_elapsed(irgl_ctx* ctx, int slot_a, int slot_b, double* ms);
+/* Process-wide count of kernels this library has launched (all ctxs). */
+int64_t irgl_launch_count(void);
 
 /* ---- launch planning ------------------------------------------------------ */
 /* Block-size constraint of a kernel: Elastic [1,1024], Shrinkable(max) [1,max], Fixed(n) {n}. */

@@ -2,6 +2,7 @@
 // constructs Invoke / Iterate / Pipe with the in/out/retry swap protocol (PAPER.md:358-381,
 // SPEC.md:359-381, :459-467) over the device kernels of expand.cu / topo.cu / testops.cu.
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -30,6 +31,8 @@ struct irgl_ctx {
   int64_t route_size = INT64_MAX;   // partition size of the last graph (pipe routing)
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // hot-kernel timing (iter_stats.kernel_ms)
+  cudaEvent_t user_ev[8] = {};                  // irgl_event_record slots
   // test-operator state (partition 0)
   int32_t* test_log = nullptr;
   int64_t test_log_cap = 0;
@@ -56,6 +59,8 @@ struct GraphPart {
   int64_t tc_m = -1;
   ChunkDesc* chunks = nullptr;
   uint32_t chunk_cap = 0;
+  uint32_t* far[2] = {nullptr, nullptr};  // SSSP near-far piles
+  uint32_t far_cap = 0;
   Ctl* ctl = nullptr;
   // multi-partition exchange
   uint32_t* send = nullptr;
@@ -95,6 +100,8 @@ struct irgl_pipe {
 // ----------------------------------------------------------------------------------------------
 namespace irgl {
 static std::string g_err;  // last error without a ctx
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(irgl_ctx* ctx, irgl_status_t st, const char* rule, const std::string& msg) {
   (void)st;
@@ -276,7 +283,7 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
 // ---- multi-partition exchange (E5) -------------------------------------------------------------
 // After every local expansion: bucket counts -> (pack values) -> transport -> owner-side apply.
 static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pipe, int op,
-                                        int32_t level, int32_t stamp_id, irgl_iter_stats* stt) {
+                                        const std::vector<RoundBufs>& rbs, irgl_iter_stats* stt) {
   const int L = (int)ctx->parts.size();
   const int P = ctx->ptotal();
   const int64_t ps = g->part_size;
@@ -370,8 +377,7 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       const uint32_t c = cnt[(size_t)p * P + q];
       if (!c) continue;
       CK(launch_apply_remote(op, gp.lab, gp.stamp, pp.ctl, gp.recv + (int64_t)p * ps,
-                             vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, pp.buf[pp.b_out],
-                             &pp.ctl->cnt[pp.c_out], (uint32_t)pipe->cap, level, stamp_id, pr.st));
+                             vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
     }
     CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
   }
@@ -392,14 +398,149 @@ static irgl_status_t allreduce_sum_u64(irgl_ctx* ctx, uint64_t* v) {
   return IRGL_OK;
 }
 
+static irgl_status_t allreduce_min_u64(irgl_ctx* ctx, uint64_t* v) {
+  if (ctx->nranks <= 1) return IRGL_OK;
+  PartRT& pr = ctx->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  unsigned long long* d = nullptr;
+  CK(cudaMallocAsync(&d, 8, pr.st));
+  CK(cudaMemcpyAsync(d, v, 8, cudaMemcpyHostToDevice, pr.st));
+  NCK(ctx->nccl->AllReduce(d, d, 1, ncclUint64, ncclMin, ctx->comm, pr.st));
+  CK(cudaMemcpyAsync(v, d, 8, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaFreeAsync(d, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  return IRGL_OK;
+}
+
 // ---- data-driven graph operators: host-orchestrated rounds ----------------------------------
+// SSSP near-far state of one iterate (delta <= 0: plain Bellman-Ford).
+struct NearFar {
+  int32_t delta = 0;
+  int32_t threshold = kInf;
+  int fsel = 0;  // current far pile
+};
+
+static int32_t default_delta(const irgl_graph* g) {
+  (void)g;
+  return 8;  // bucket width for [1,255] weights; tuned on RMAT-22
+}
+
+static irgl_status_t ensure_far(irgl_ctx* ctx, irgl_graph* g) {
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    if (gp.far[0]) continue;
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    const int64_t nloc = std::max<int64_t>(gp.hi - gp.lo, 1);
+    gp.far_cap = (uint32_t)std::min<int64_t>(4 * nloc + 4096, 0xffffffffll);
+    for (int k = 0; k < 2; ++k) CK(cudaMalloc(&gp.far[k], (size_t)gp.far_cap * 4));
+  }
+  return IRGL_OK;
+}
+
+static RoundBufs round_bufs(irgl_pipe* pipe, GraphPart& gp, PipePart& pp, int32_t level,
+                            int32_t stamp_id, const NearFar& nf) {
+  RoundBufs rb;
+  rb.in = pp.buf[pp.b_in];
+  rb.nin = pp.n_in;
+  rb.out = pp.buf[pp.b_out];
+  rb.out_cnt = &pp.ctl->cnt[pp.c_out];
+  rb.cap = (uint32_t)pipe->cap;
+  rb.chunks = gp.chunks;
+  rb.chunk_cnt = &pp.ctl->chunk_cnt[0];
+  rb.chunk_cap = gp.chunk_cap;
+  rb.level = level;
+  rb.stamp_id = stamp_id;
+  rb.tile_ctr = &pp.ctl->tile_ctr[0];
+  rb.far = gp.far[nf.fsel];
+  rb.far_cnt = &pp.ctl->far_cnt[nf.fsel];
+  rb.far_cap = gp.far_cap;
+  rb.threshold = nf.delta > 0 ? nf.threshold : kInf;
+  return rb;
+}
+
+static irgl_status_t allreduce_min_u64(irgl_ctx* ctx, uint64_t* v);
+
+// Near-far: when the near frontier is globally empty, advance the threshold and split every
+// partition's far pile into its out worklist / next pile (SPEC-level semantics unchanged: the
+// split only reorders relaxations).  Also compacts a pile that grew past half its capacity.
+static irgl_status_t near_far_split(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pipe, NearFar& nf,
+                                    std::vector<uint32_t>& nout, int32_t level) {
+  const int L = (int)ctx->parts.size();
+  std::vector<uint32_t> nfar(L, 0);
+  auto read_counts = [&]() -> irgl_status_t {
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_out], 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemcpyAsync(pr.h_pin + 1, &pp.ctl->far_cnt[nf.fsel], 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemcpyAsync(pr.h_pin + 2, &pp.ctl->minkeep, 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+      nout[l] = pr.h_pin[0];
+      nfar[l] = pr.h_pin[1];
+    }
+    return IRGL_OK;
+  };
+  irgl_status_t s = read_counts();
+  if (s != IRGL_OK) return s;
+  uint64_t tout = 0, tfar = 0;
+  bool compact = false;
+  for (int l = 0; l < L; ++l) {
+    tout += nout[l];
+    tfar += nfar[l];
+    compact |= nfar[l] > g->parts[l].far_cap / 2;
+  }
+  if ((s = allreduce_sum_u64(ctx, &tout)) != IRGL_OK) return s;
+  if ((s = allreduce_sum_u64(ctx, &tfar)) != IRGL_OK) return s;
+  uint64_t anycompact = compact ? 1 : 0;
+  if ((s = allreduce_sum_u64(ctx, &anycompact)) != IRGL_OK) return s;
+  bool advance = tout == 0;
+  if (!(advance && tfar > 0) && !anycompact) return IRGL_OK;
+  for (;;) {
+    const int32_t t_old = nf.threshold;  // below it: already expanded (dropped)
+    if (advance) nf.threshold += nf.delta;
+    const int32_t sid = (int32_t)(++g->stamp_epoch);
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      CK(cudaMemsetAsync(&pp.ctl->far_cnt[nf.fsel ^ 1], 0, 4, pr.st));
+      CK(cudaMemsetAsync(&pp.ctl->minkeep, 0xff, 4, pr.st));
+      NearFar nx = nf;
+      nx.fsel ^= 1;
+      RoundBufs rb = round_bufs(pipe, gp, pp, level, sid, nx);
+      CK(launch_far_split(gp.csr(), gp.lab, gp.stamp, pp.ctl, rb, gp.far[nf.fsel],
+                          &pp.ctl->far_cnt[nf.fsel], t_old, &pp.ctl->minkeep,
+                          grid_max(ctx, pr, IRGL_OP_SSSP), pr.st));
+    }
+    nf.fsel ^= 1;
+    if ((s = read_counts()) != IRGL_OK) return s;
+    tout = tfar = 0;
+    uint64_t mk = ~0ull;
+    for (int l = 0; l < L; ++l) {
+      tout += nout[l];
+      tfar += nfar[l];
+      mk = std::min<uint64_t>(mk, ctx->parts[l].h_pin[2]);
+    }
+    if ((s = allreduce_sum_u64(ctx, &tout)) != IRGL_OK) return s;
+    if ((s = allreduce_sum_u64(ctx, &tfar)) != IRGL_OK) return s;
+    if (tout > 0 || tfar == 0) break;
+    if ((s = allreduce_min_u64(ctx, &mk)) != IRGL_OK) return s;
+    nf.threshold = (int32_t)mk;  // next pass moves at least the minimum kept distance
+    advance = true;
+  }
+  return IRGL_OK;
+}
+
 static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                      int64_t level0, const irgl_iterate_opts& o, bool once,
-                                     irgl_iter_stats* stt) {
+                                     NearFar& nf, irgl_iter_stats* stt) {
   const int L = (int)ctx->parts.size();
   const int P = ctx->ptotal();
   const ExpandCfg ec = expand_cfg(ctx);
   int64_t level = level0;
+  std::vector<uint32_t> nout(L, 0);
   for (;;) {
     uint64_t total_in = 0;
     for (int l = 0; l < L; ++l) total_in += pipe->parts[l].n_in;
@@ -412,28 +553,21 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
                                        : empty;
     if (stop || (once && stt->rounds >= 1)) break;
     const int32_t stamp_id = (int32_t)(++g->stamp_epoch);
+    std::vector<RoundBufs> rbs(L);
     for (int l = 0; l < L; ++l) {
       PartRT& pr = ctx->parts[l];
       GraphPart& gp = g->parts[l];
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
-      RoundBufs rb;
-      rb.in = pp.buf[pp.b_in];
-      rb.nin = pp.n_in;
-      rb.out = pp.buf[pp.b_out];
-      rb.out_cnt = &pp.ctl->cnt[pp.c_out];
-      rb.cap = (uint32_t)pipe->cap;
-      rb.chunks = gp.chunks;
-      rb.chunk_cnt = &pp.ctl->chunk_cnt[0];
-      rb.chunk_cap = gp.chunk_cap;
-      rb.level = (int32_t)level;
-      rb.stamp_id = stamp_id;
+      rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       DistRoute dr{P, ctx->gpart(l), g->part_size, gp.send, gp.send_cnt};
-      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rb, dr, ec, grid_max(ctx, pr, op), pr.st));
+      if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
+      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
+      if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
     }
     if (P > 1) {
-      s = exchange_and_apply(ctx, g, pipe, op, (int32_t)level, stamp_id, stt);
+      s = exchange_and_apply(ctx, g, pipe, op, rbs, stt);
       if (s != IRGL_OK) return s;
     }
     for (int l = 0; l < L; ++l) {
@@ -443,6 +577,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_out], 4, cudaMemcpyDeviceToHost, pr.st));
       CK(cudaMemcpyAsync(pr.h_pin + 1, &pp.ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
       CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(uint32_t), pr.st));
+      CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(uint32_t), pr.st));
     }
     for (int l = 0; l < L; ++l) {
       PartRT& pr = ctx->parts[l];
@@ -450,10 +585,21 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       CK(cudaSetDevice(pr.dev));
       CK(cudaStreamSynchronize(pr.st));
       if (pr.h_pin[1]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
-      const uint32_t nout = pr.h_pin[0];
+      if (l == 0) {
+        float kms = 0.f;
+        CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
+        stt->kernel_ms += kms;
+      }
+      nout[l] = pr.h_pin[0];
       stt->popped += pp.n_in;
-      stt->pushes += nout;
-      irgl_status_t s2 = pipe_swap_in_out(ctx, pp, pr, nout);
+    }
+    if (nf.delta > 0) {
+      s = near_far_split(ctx, g, pipe, nf, nout, (int32_t)level);
+      if (s != IRGL_OK) return s;
+    }
+    for (int l = 0; l < L; ++l) {
+      stt->pushes += nout[l];
+      irgl_status_t s2 = pipe_swap_in_out(ctx, pipe->parts[l], ctx->parts[l], nout[l]);
       if (s2 != IRGL_OK) return s2;
     }
     stt->rounds++;
@@ -465,7 +611,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
 // ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
 static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                        int64_t level0, const irgl_iterate_opts& o,
-                                       irgl_iter_stats* stt) {
+                                       const NearFar& nf, irgl_iter_stats* stt) {
   PartRT& pr = ctx->parts[0];
   GraphPart& gp = g->parts[0];
   PipePart& pp = pipe->parts[0];
@@ -488,14 +634,27 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.level0 = (int32_t)level0;
   pa.stamp0 = (int32_t)(g->stamp_epoch + 1);
   pa.max_rounds = o.max_rounds > 0 ? std::max<int64_t>(o.max_rounds - stt->rounds, 0) : 0;
+  pa.far_a = gp.far[0];
+  pa.far_b = gp.far[1];
+  pa.far_cap = gp.far_cap;
+  pa.delta = nf.delta;
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
+  CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(pp.ctl->tile_ctr), pr.st));
+  CK(cudaMemsetAsync(pp.ctl->far_cnt, 0, sizeof(pp.ctl->far_cnt), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
+  CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
+  CK(cudaEventRecord(ctx->kev1, pr.st));
   Ctl h;
   CK(cudaMemcpyAsync(&h, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
   CK(cudaStreamSynchronize(pr.st));
+  {
+    float kms = 0.f;
+    CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
+    stt->kernel_ms += kms;
+  }
   if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
   const int64_t K = (int64_t)h.rounds;
   // rotate the host view: buffers by parity, counters by K mod 3 (see persistent_kernel)
@@ -505,7 +664,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pp.c_out = slots[(K + 1) % 3];
   pp.c_spare = slots[(K + 2) % 3];
   pp.n_in = h.cnt[pp.c_in];
-  g->stamp_epoch += K;
+  g->stamp_epoch += h.stamp_used;
   stt->rounds += K;
   stt->launches += 1;
   stt->popped += (int64_t)h.popped;
@@ -693,11 +852,18 @@ static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_arg
   const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
   const int c = gp.pr_cur;
   CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
+  CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c], gp.pr[3 - c], d, tol, g->n,
                           gp.ctl, o.max_rounds, o.cond_mode, bps * pr.sms, pr.st));
+  CK(cudaEventRecord(ctx->kev1, pr.st));
   Ctl h;
   CK(cudaMemcpyAsync(&h, gp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
   CK(cudaStreamSynchronize(pr.st));
+  {
+    float kms = 0.f;
+    CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
+    stt->kernel_ms += kms;
+  }
   const int64_t K = (int64_t)h.rounds;
   if (K & 1) gp.pr_cur = 1 - c;
   stt->rounds += K;
@@ -772,6 +938,9 @@ static irgl_status_t ctx_init_parts(irgl_ctx* c, const int* devices, int ndev, i
   CK(cudaSetDevice(c->parts[0].dev));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
+  CK(cudaEventCreate(&c->kev0));
+  CK(cudaEventCreate(&c->kev1));
+  for (auto& e : c->user_ev) CK(cudaEventCreate(&e));
   // peer access for the loopback exchange across devices
   for (int a = 0; a < L; ++a)
     for (int b = 0; b < L; ++b) {
@@ -877,8 +1046,10 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
   if (ctx->test_log) cudaFree(ctx->test_log);
   if (ctx->test_rcount) cudaFree(ctx->test_rcount);
   if (ctx->test_ctl) cudaFree(ctx->test_ctl);
-  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
-  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->kev0, ctx->kev1})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->user_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& p : ctx->parts) {
     cudaSetDevice(p.dev);
     if (p.st) cudaStreamDestroy(p.st);
@@ -1029,7 +1200,7 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     cudaStreamSynchronize(ctx->parts[l].st);
     void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
                   gp.tc_rp, gp.tc_cl, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
-                  gp.recv_val};
+                  gp.recv_val, gp.far[0], gp.far[1]};
     for (void* p : ps)
       if (p) cudaFree(p);
   }
@@ -1181,8 +1352,9 @@ irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op
     }
     irgl_iterate_opts o{};
     const int64_t level = args && args->round_start > 0 ? args->round_start : 1;
+    NearFar nf;  // a single Invoke is one plain round
     s = pipe_counters(ctx, pipe, nullptr);
-    if (s == IRGL_OK) s = wl_graph_rounds(ctx, pipe, g, op, level, o, true, &st);
+    if (s == IRGL_OK) s = wl_graph_rounds(ctx, pipe, g, op, level, o, true, nf, &st);
     if (s == IRGL_OK) s = pipe_counters(ctx, pipe, &st);
     if (reduced) *reduced = red == IRGL_RED_ALL ? 1 : red == IRGL_RED_ANY ? 0 : -1;  // identity
   } else {
@@ -1218,8 +1390,22 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     s = pipe_counters(ctx, pipe, nullptr);  // zero edges / remote counters
     if (s != IRGL_OK) return s;
     const int64_t level = args && args->round_start > 0 ? args->round_start : 1;
-    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, &st);
-    else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, &st);
+    NearFar nf;
+    if (op == IRGL_OP_SSSP) {
+      nf.delta = !args ? 0 : (args->delta < 0 ? default_delta(g) : args->delta);
+      nf.threshold = nf.delta;
+      if (nf.delta > 0) {
+        s = ensure_far(ctx, g);
+        if (s != IRGL_OK) return s;
+        for (size_t l = 0; l < pipe->parts.size(); ++l) {
+          CK(cudaSetDevice(ctx->parts[l].dev));
+          CK(cudaMemset(pipe->parts[l].ctl->far_cnt, 0, sizeof(uint32_t) * 2));
+        }
+        CK(cudaSetDevice(pr0.dev));
+      }
+    }
+    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, &st);
+    else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s != IRGL_OK) return s;
     s = pipe_counters(ctx, pipe, &st);  // edges scanned / remote updates
     if (s != IRGL_OK) return s;
@@ -1308,6 +1494,24 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
   }
   return IRGL_OK;
 }
+
+// ---- measurement --------------------------------------------------------------------------------
+irgl_status_t irgl_event_record(irgl_ctx* ctx, int slot) {
+  if (!ctx || slot < 0 || slot >= 8) return IRGL_E_INVALID;
+  CK(cudaSetDevice(ctx->parts[0].dev));
+  CK(cudaEventRecord(ctx->user_ev[slot], ctx->parts[0].st));
+  return IRGL_OK;
+}
+irgl_status_t irgl_event_elapsed(irgl_ctx* ctx, int a, int b, double* ms) {
+  if (!ctx || !ms || a < 0 || a >= 8 || b < 0 || b >= 8) return IRGL_E_INVALID;
+  CK(cudaSetDevice(ctx->parts[0].dev));
+  CK(cudaEventSynchronize(ctx->user_ev[b]));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, ctx->user_ev[a], ctx->user_ev[b]));
+  *ms = f;
+  return IRGL_OK;
+}
+int64_t irgl_launch_count(void) { return g_launches.load(); }
 
 // ---- launch planning ----------------------------------------------------------------------------
 irgl_status_t irgl_t_control(const irgl_block_constraint* cs, int n, int32_t* out) {

@@ -1,17 +1,23 @@
 // expand.cu — the data-driven hot path: ForAll over the in-worklist x ForAll over edges(n)
 // for BFS (Listing 2), SSSP and CC_LP, lowered B200-first:
 //
-//  E1  nested-parallelism edge scheduler.  Each popped vertex's edges go to
-//        - one thread          (degree < warp_t): CTA-wide scan, edge ids staged in smem and
-//                              processed one edge per thread ("fine-grained" gather);
+//  E1  nested-parallelism edge scheduler.  Work is handed out in warp tiles of 32 popped
+//      vertices (first tile static, then dynamic from a per-round counter); each vertex's edges go
+//      to
+//        - one thread          (degree < warp_t): warp-wide scan of the small degrees, each lane
+//                              finds the owner of its edge slot with a 5-step shuffle search
+//                              ("fine-grained" gather, no shared memory, no CTA barrier);
 //        - one warp            (warp_t <= degree < cta_t), 128-bit col/weight loads;
 //        - CTA chunks          (degree >= cta_t): split into chunk_edges-sized descriptors that
 //                              every CTA of the grid drains in a second phase (edge-balanced,
 //                              so super-hubs do not serialise on one CTA).
-//  E2  cooperative conversion of pushes: warp __ballot_sync/__popc aggregation into a per-CTA
-//      shared-memory staging queue, flushed with ONE global atomic reservation per tile.
+//  E2  cooperative conversion of pushes: warp __ballot_sync/__popc aggregation into a per-warp
+//      shared-memory staging queue; one global atomic reservation per 224+ staged items.
 //  E3  iteration outlining: the Iterate loop as one cooperative persistent kernel with a grid
 //      barrier (SyncRunningThreads) instead of per-round host launches.
+//  SSSP near-far (delta > 0): pushes with dist >= threshold go to a far pile that is split back
+//      into the worklist when the near frontier empties (same fixed point as Bellman-Ford, less
+//      re-relaxation).
 //
 // Reference semantics (SPEC.md:317-322 ForAll lowering; :425 bulk-synchronous worklists: pops
 // read `in`, pushes append to `out`, never visible in the same launch).
@@ -25,21 +31,14 @@ namespace irgl {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWBuf = 256;  // per-warp push staging entries
+#ifndef IRGL_MINB
+#define IRGL_MINB 4  // min co-resident CTAs per SM requested from ptxas (register budget)
+#endif
 
 struct Smem {
-  // cooperative-conversion push staging
-  uint32_t push_cnt;
-  uint32_t push_base;
-  uint32_t push_buf[kPushBuf];
-  // fine-grained gather window
-  int64_t fg_edge[kBlock];
-  int32_t fg_src[kBlock];
-  // block scan scratch
-  uint32_t warp_tot[kWarps];
-  unsigned long long warp_edges[kWarps];
-  // chunk descriptor broadcast
-  ChunkDesc chunk;
-  int32_t chunk_src;
+  uint32_t wbuf[kWarps][kWBuf];   // near pushes (E2)
+  uint32_t fbuf[kWarps][kWBuf];   // far pushes (SSSP near-far)
 };
 
 struct KParams {
@@ -51,147 +50,12 @@ struct KParams {
   ExpandCfg ec;
 };
 
-// ---- relax: the operator body for one edge (n -> dst) ----------------------------------------
-// BFS   : if level[dst]==INF { level[dst]=LEVEL; push(dst) }   CAS dedupes the push.
-// SSSP  : nd = dist[n]+w;  if atomicMin(dist[dst],nd) > nd and stamp[dst] != round: push(dst)
-// CC_LP : nd = label[n];   same as SSSP.
-template <int OP>
-__device__ __forceinline__ bool relax_with(const KParams& p, int32_t cur, int32_t sv, int32_t wt,
-                                           uint32_t dst, int32_t level, int32_t stamp_id) {
-  if (OP == IRGL_OP_BFS) {
-    if (cur != kInf) return false;
-    return atomicCAS(p.lab + dst, kInf, level) == kInf;
-  } else {
-    const int32_t nd = (OP == IRGL_OP_SSSP) ? sv + wt : sv;
-    if (nd >= cur) return false;
-    const int32_t old = atomicMin(p.lab + dst, nd);
-    if (nd >= old) return false;
-    return atomicExch(p.stamp + dst, stamp_id) != stamp_id;
-  }
-}
-
-// ---- push: E2 cooperative conversion ----------------------------------------------------------
-// Every lane of the warp must call this (converged).  Local destinations are staged in shared
-// memory (one smem atomic per warp); a full staging buffer spills straight to global with one
-// atomic per warp.  Remote destinations (multi-partition) go to the owner's bucket, grouped
-// per owner with __match_any_sync.
-template <bool DIST>
-__device__ __forceinline__ void push(Smem& sm, const KParams& p, const RoundBufs& rb, bool pred,
-                                     uint32_t v) {
-  uint32_t m = __ballot_sync(FULL, pred);
-  if (m == 0) return;
-  const uint32_t lane = lane_id();
-  if (DIST) {
-    const int owner = pred ? (int)((int64_t)v / p.dr.part_size) : -1;
-    const bool remote = pred && owner != p.dr.me;
-    const uint32_t rm = __ballot_sync(FULL, remote);
-    if (rm) {
-      if (remote) {
-        const uint32_t grp = __match_any_sync(rm, owner);
-        const uint32_t leader = __ffs(grp) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(p.dr.send_cnt + owner, __popc(grp));
-        base = __shfl_sync(grp, base, leader);
-        const uint32_t pos = base + __popc(grp & lanemask_lt());
-        if (pos < (uint32_t)p.dr.part_size)
-          p.dr.send[(int64_t)owner * p.dr.part_size + pos] = v;
-        else
-          atomicOr(&p.ctl->overflow, 1u);
-      }
-      if (lane == __ffs(rm) - 1) atomicAdd(&p.ctl->remote, (unsigned long long)__popc(rm));
-      pred = pred && !remote;
-      m = __ballot_sync(FULL, pred);
-      if (m == 0) return;
-    }
-  }
-  const uint32_t n = __popc(m);
-  const uint32_t leader = __ffs(m) - 1;
-  uint32_t pos = 0;
-  if (lane == leader) pos = atomicAdd(&sm.push_cnt, n);
-  pos = __shfl_sync(FULL, pos, leader);
-  const uint32_t rank = __popc(m & lanemask_lt());
-  // slots [pos, kPushBuf) go to smem, the remainder spills to global
-  const uint32_t in_smem = pos >= (uint32_t)kPushBuf ? 0u : min(n, (uint32_t)kPushBuf - pos);
-  uint32_t gbase = 0;
-  if (in_smem < n) {
-    if (lane == leader) gbase = atomicAdd(rb.out_cnt, n - in_smem);
-    gbase = __shfl_sync(FULL, gbase, leader);
-  }
-  if (pred) {
-    if (rank < in_smem) {
-      sm.push_buf[pos + rank] = v;
-    } else {
-      const uint32_t q = gbase + (rank - in_smem);
-      if (q < rb.cap) rb.out[q] = v;
-      else atomicOr(&p.ctl->overflow, 1u);
-    }
-  }
-}
-
-// Flush the CTA's staged pushes: one global reservation per tile (CTA-uniform call site).
-__device__ __forceinline__ void flush_pushes(Smem& sm, const KParams& p, const RoundBufs& rb) {
-  __syncthreads();  // all pushes of the tile are staged
-  const uint32_t c = min(sm.push_cnt, (uint32_t)kPushBuf);
-  if (threadIdx.x == 0) sm.push_base = c ? atomicAdd(rb.out_cnt, c) : 0u;
-  __syncthreads();  // push_base visible; nobody reads push_cnt past this point
-  if (threadIdx.x == 0) sm.push_cnt = 0;
-  const uint32_t base = sm.push_base;
-  for (uint32_t i = threadIdx.x; i < c; i += kBlock) {
-    const uint32_t q = base + i;
-    if (q < rb.cap) rb.out[q] = sm.push_buf[i];
-    else atomicOr(&p.ctl->overflow, 1u);
-  }
-  __syncthreads();  // staging buffer and counter reusable
-}
-
-// ---- edge-range processing by a group of G lanes (G = 32 warp, G = kBlock CTA) -------------------
-// Head/tail (misaligned) edges in one predicated step, the aligned body with 128-bit loads:
-// each lane issues 4 independent label gathers before its 4 decisions (ILP).
-template <int OP, bool DIST, int G>
-__device__ __forceinline__ void process_range(Smem& sm, const KParams& p, const RoundBufs& rb,
-                                              int64_t b, int64_t e, int32_t sv, int gl) {
-  const int32_t* __restrict__ col = p.g.col;
-  const int32_t* __restrict__ w = p.g.w;
-  const int64_t a0 = min((b + 3) & ~int64_t(3), e);
-  const int64_t a1 = max(e & ~int64_t(3), a0);
-  {
-    const int nh = (int)(a0 - b), nt = (int)(e - a1);
-    const bool act = gl < nh + nt;
-    const int64_t ed = gl < nh ? b + gl : a1 + (gl - nh);
-    uint32_t dst = 0;
-    int32_t wt = 0, cur = 0;
-    if (act) {
-      dst = (uint32_t)ld_stream(col + ed);
-      if (OP == IRGL_OP_SSSP) wt = ld_stream(w + ed);
-      cur = ld_label(p.lab + dst);
-    }
-    const bool pr = act && relax_with<OP>(p, cur, sv, wt, dst, rb.level, rb.stamp_id);
-    push<DIST>(sm, p, rb, pr, dst);
-  }
-  const int64_t q1 = a1 >> 2;
-  for (int64_t q0 = a0 >> 2; q0 < q1; q0 += G) {
-    const int64_t q = q0 + gl;
-    const bool act = q < q1;
-    int4 c4 = make_int4(0, 0, 0, 0), w4 = make_int4(0, 0, 0, 0);
-    int32_t l0 = 0, l1 = 0, l2 = 0, l3 = 0;
-    if (act) {
-      c4 = ld_stream_v4(col + 4 * q);
-      if (OP == IRGL_OP_SSSP) w4 = ld_stream_v4(w + 4 * q);
-      l0 = ld_label(p.lab + c4.x);
-      l1 = ld_label(p.lab + c4.y);
-      l2 = ld_label(p.lab + c4.z);
-      l3 = ld_label(p.lab + c4.w);
-    }
-    const bool p0 = act && relax_with<OP>(p, l0, sv, w4.x, (uint32_t)c4.x, rb.level, rb.stamp_id);
-    const bool p1 = act && relax_with<OP>(p, l1, sv, w4.y, (uint32_t)c4.y, rb.level, rb.stamp_id);
-    const bool p2 = act && relax_with<OP>(p, l2, sv, w4.z, (uint32_t)c4.z, rb.level, rb.stamp_id);
-    const bool p3 = act && relax_with<OP>(p, l3, sv, w4.w, (uint32_t)c4.w, rb.level, rb.stamp_id);
-    push<DIST>(sm, p, rb, p0, (uint32_t)c4.x);
-    push<DIST>(sm, p, rb, p1, (uint32_t)c4.y);
-    push<DIST>(sm, p, rb, p2, (uint32_t)c4.z);
-    push<DIST>(sm, p, rb, p3, (uint32_t)c4.w);
-  }
-}
+// Register-resident, warp-uniform state of a warp's staging queues.
+struct WarpQ {
+  uint32_t n = 0;   // staged near pushes
+  uint32_t nf = 0;  // staged far pushes
+  unsigned long long edges = 0;
+};
 
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
   uint32_t r;
@@ -204,12 +68,160 @@ __device__ __forceinline__ uint32_t ld_ctl(const uint32_t* p) {
   return r;
 }
 
-// ---- one tile of kBlock worklist items (consecutive mapping) ------------------------
+// ---- relax: the operator body for one edge (n -> dst) ----------------------------------------
+// BFS   : if level[dst]==INF { level[dst]=LEVEL; push(dst) }   CAS dedupes the push.
+// SSSP  : nd = dist[n]+w;  if atomicMin(dist[dst],nd) > nd and stamp[dst] != round: push(dst)
+// CC_LP : nd = label[n];   same as SSSP.
+// Returns 0 (no push), 1 (near push) or 2 (far push: nd >= threshold).
+template <int OP>
+__device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb, int32_t cur,
+                                          int32_t sv, int32_t wt, uint32_t dst) {
+  if (OP == IRGL_OP_BFS) {
+    if (cur != kInf) return 0;
+    return atomicCAS(p.lab + dst, kInf, rb.level) == kInf ? 1 : 0;
+  } else {
+    const int32_t nd = (OP == IRGL_OP_SSSP) ? sv + wt : sv;
+    if (nd >= cur) return 0;
+    const int32_t old = atomicMin(p.lab + dst, nd);
+    if (nd >= old) return 0;
+    // push dedupe per round and per pile: stamp code = 2*round_id + (far ? 1 : 0).  A vertex
+    // first pushed far and then improved below the threshold in the same round is pushed near
+    // too; its stale far entry is dropped by the split (dist < old threshold).
+    const int kind = (OP == IRGL_OP_SSSP && nd >= rb.threshold) ? 2 : 1;
+    const int32_t code = (rb.stamp_id << 1) | (kind - 1);
+    if (atomicExch(p.stamp + dst, code) == code) return 0;
+    return kind;
+  }
+}
+
+// ---- E2: per-warp staging --------------------------------------------------------------------
+__device__ __forceinline__ void wflush(uint32_t* buf, uint32_t& n, uint32_t* out, uint32_t* cnt,
+                                       uint32_t cap, uint32_t* overflow) {
+  if (n == 0) return;
+  __syncwarp();
+  uint32_t base = 0;
+  if (lane_id() == 0) base = atomicAdd(cnt, n);
+  base = __shfl_sync(FULL, base, 0);
+  for (uint32_t i = lane_id(); i < n; i += 32) {
+    const uint32_t q = base + i;
+    if (q < cap) out[q] = buf[i];
+    else atomicOr(overflow, 1u);
+  }
+  __syncwarp();
+  n = 0;
+}
+
+// Every lane of the warp must call this (converged).  kind: 0 none, 1 near, 2 far.
+template <bool DIST>
+__device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
+                                      int kind, uint32_t v) {
+  uint32_t m = __ballot_sync(FULL, kind != 0);
+  if (m == 0) return;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  if (DIST) {
+    const int owner = kind ? (int)((int64_t)v / p.dr.part_size) : -1;
+    const bool remote = kind && owner != p.dr.me;
+    const uint32_t rm = __ballot_sync(FULL, remote);
+    if (rm) {
+      if (remote) {
+        const uint32_t grp = __match_any_sync(rm, owner);
+        const uint32_t leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(p.dr.send_cnt + owner, __popc(grp));
+        base = __shfl_sync(grp, base, leader);
+        const uint32_t pos = base + __popc(grp & lanemask_lt());
+        if (pos < (uint32_t)p.dr.part_size) p.dr.send[(int64_t)owner * p.dr.part_size + pos] = v;
+        else atomicOr(&p.ctl->overflow, 1u);
+      }
+      if (lane == __ffs(rm) - 1) atomicAdd(&p.ctl->remote, (unsigned long long)__popc(rm));
+      if (remote) kind = 0;
+      m = __ballot_sync(FULL, kind != 0);
+      if (m == 0) return;
+    }
+  }
+  const uint32_t mn = __ballot_sync(FULL, kind == 1);
+  const uint32_t mf = m & ~mn;
+  const uint32_t lt = lanemask_lt();
+  if (mn) {
+    if (kind == 1) sm.wbuf[warp][q.n + __popc(mn & lt)] = v;
+    q.n += __popc(mn);
+    if (q.n > kWBuf - 32) wflush(sm.wbuf[warp], q.n, rb.out, rb.out_cnt, rb.cap, &p.ctl->overflow);
+  }
+  if (mf) {
+    if (kind == 2) sm.fbuf[warp][q.nf + __popc(mf & lt)] = v;
+    q.nf += __popc(mf);
+    if (q.nf > kWBuf - 32) wflush(sm.fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
+  }
+}
+
+__device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
+  const uint32_t warp = threadIdx.x >> 5;
+  wflush(sm.wbuf[warp], q.n, rb.out, rb.out_cnt, rb.cap, &p.ctl->overflow);
+  wflush(sm.fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
+  if (q.edges) {
+    if (lane_id() == 0) atomicAdd(&p.ctl->edges, q.edges);
+    q.edges = 0;
+  }
+}
+
+// ---- edge-range processing by a group of G lanes (G = 32 warp, G = kBlock CTA) -------------------
+// Head/tail (misaligned) edges in one predicated step, the aligned body with 128-bit loads:
+// each lane issues 4 independent label gathers before its 4 decisions (ILP).
+template <int OP, bool DIST, int G>
+__device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams& p,
+                                              const RoundBufs& rb, int64_t b, int64_t e,
+                                              int32_t sv, int gl) {
+  const int32_t* __restrict__ col = p.g.col;
+  const int32_t* __restrict__ w = p.g.w;
+  const int64_t a0 = min((b + 3) & ~int64_t(3), e);
+  const int64_t a1 = max(e & ~int64_t(3), a0);
+  const int nh = (int)(a0 - b), nt = (int)(e - a1);
+  if (nh + nt > 0 && (G == 32 || (threadIdx.x >> 5) == 0)) {  // warp-uniform condition
+    const bool act = gl < nh + nt;
+    const int64_t ed = gl < nh ? b + gl : a1 + (gl - nh);
+    uint32_t dst = 0;
+    int32_t wt = 0, cur = 0;
+    if (act) {
+      dst = (uint32_t)ld_stream(col + ed);
+      if (OP == IRGL_OP_SSSP) wt = ld_stream(w + ed);
+      cur = ld_label(p.lab + dst);
+    }
+    const int k = act ? relax_with<OP>(p, rb, cur, sv, wt, dst) : 0;
+    wpush<DIST>(sm, q, p, rb, k, dst);
+  }
+  const int64_t q1 = a1 >> 2;
+  for (int64_t q0 = a0 >> 2; q0 < q1; q0 += G) {
+    const int64_t qi = q0 + gl;
+    // a warp whose 32 lanes are all past the end skips the body (stays warp-uniform)
+    if (G > 32 && q0 + (gl & ~31) >= q1) break;
+    const bool act = qi < q1;
+    int4 c4 = make_int4(0, 0, 0, 0), w4 = make_int4(0, 0, 0, 0);
+    int32_t l0 = 0, l1 = 0, l2 = 0, l3 = 0;
+    if (act) {
+      c4 = ld_stream_v4(col + 4 * qi);
+      if (OP == IRGL_OP_SSSP) w4 = ld_stream_v4(w + 4 * qi);
+      l0 = ld_label(p.lab + c4.x);
+      l1 = ld_label(p.lab + c4.y);
+      l2 = ld_label(p.lab + c4.z);
+      l3 = ld_label(p.lab + c4.w);
+    }
+    const int k0 = act ? relax_with<OP>(p, rb, l0, sv, w4.x, (uint32_t)c4.x) : 0;
+    const int k1 = act ? relax_with<OP>(p, rb, l1, sv, w4.y, (uint32_t)c4.y) : 0;
+    const int k2 = act ? relax_with<OP>(p, rb, l2, sv, w4.z, (uint32_t)c4.z) : 0;
+    const int k3 = act ? relax_with<OP>(p, rb, l3, sv, w4.w, (uint32_t)c4.w) : 0;
+    wpush<DIST>(sm, q, p, rb, k0, (uint32_t)c4.x);
+    wpush<DIST>(sm, q, p, rb, k1, (uint32_t)c4.y);
+    wpush<DIST>(sm, q, p, rb, k2, (uint32_t)c4.z);
+    wpush<DIST>(sm, q, p, rb, k3, (uint32_t)c4.w);
+  }
+}
+
+// ---- one warp tile of 32 worklist items (consecutive mapping inside the tile) --------------------
 template <int OP, bool DIST>
-__device__ void expand_tile(Smem& sm, const KParams& p, const RoundBufs& rb, uint32_t tile_base) {
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const uint32_t i = tile_base + tid;
+__device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
+                                 uint32_t base) {
+  const int lane = lane_id();
+  const uint32_t i = base + lane;
   const bool valid = i < rb.nin;
   uint32_t v = 0;
   int64_t beg = 0, end = 0;
@@ -222,13 +234,11 @@ __device__ void expand_tile(Smem& sm, const KParams& p, const RoundBufs& rb, uin
     if (OP != IRGL_OP_BFS) sv = ld_label(p.lab + v);
   }
   int64_t deg = end - beg;
-
-  // stats: edges scanned per tile (one 64-bit atomic per CTA tile)
   {
     unsigned long long de = (unsigned long long)deg;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) de += __shfl_xor_sync(FULL, de, o);
-    if (lane == 0) sm.warp_edges[warp] = de;
+    q.edges += de;
   }
 
   // ---- CTA-chunk level: degree >= cta_t -> chunk descriptors (warp-cooperative emission)
@@ -243,11 +253,11 @@ __device__ void expand_tile(Smem& sm, const KParams& p, const RoundBufs& rb, uin
       const uint32_t vv = __shfl_sync(FULL, v, leader);
       const int64_t ce = p.ec.chunk_edges;
       const uint32_t nch = (uint32_t)((e - b + ce - 1) / ce);
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(rb.chunk_cnt, nch);
-      base = __shfl_sync(FULL, base, 0);
+      uint32_t cbase = 0;
+      if (lane == 0) cbase = atomicAdd(rb.chunk_cnt, nch);
+      cbase = __shfl_sync(FULL, cbase, 0);
       for (uint32_t k = lane; k < nch; k += 32) {
-        const uint32_t pos = base + k;
+        const uint32_t pos = cbase + k;
         const int64_t cb = b + (int64_t)k * ce;
         if (pos < rb.chunk_cap) {
           ChunkDesc d;
@@ -273,11 +283,11 @@ __device__ void expand_tile(Smem& sm, const KParams& p, const RoundBufs& rb, uin
       const int64_t e = __shfl_sync(FULL, end, leader);
       const int32_t s = __shfl_sync(FULL, sv, leader);
       if (lane == leader) deg = 0;
-      process_range<OP, DIST, 32>(sm, p, rb, b, e, s, lane);
+      process_range<OP, DIST, 32>(sm, q, p, rb, b, e, s, lane);
     }
   }
 
-  // ---- thread level (fine-grained): CTA exclusive scan of the remaining small degrees
+  // ---- thread level (fine-grained): warp scan of the small degrees, shuffle owner search
   const uint32_t d = (uint32_t)deg;
   uint32_t incl = d;
 #pragma unroll
@@ -285,98 +295,146 @@ __device__ void expand_tile(Smem& sm, const KParams& p, const RoundBufs& rb, uin
     const uint32_t t = __shfl_up_sync(FULL, incl, o);
     if (lane >= o) incl += t;
   }
-  if (lane == 31) sm.warp_tot[warp] = incl;
-  __syncthreads();
-  uint32_t wpre = 0, total = 0;
+  const uint32_t total = __shfl_sync(FULL, incl, 31);
+  const int64_t off = beg - (int64_t)(incl - d);  // edge of slot k (owned here) = off + k
+  for (uint32_t wb = 0; wb < total; wb += 32) {
+    const uint32_t k = wb + lane;
+    const bool act = k < total;
+    uint32_t o = 0;
 #pragma unroll
-  for (int k = 0; k < kWarps; ++k) {
-    const uint32_t t = sm.warp_tot[k];
-    if (k < warp) wpre += t;
-    total += t;
-  }
-  if (tid == 0) {
-    unsigned long long te = 0;
-#pragma unroll
-    for (int k = 0; k < kWarps; ++k) te += sm.warp_edges[k];
-    if (te) atomicAdd(&p.ctl->edges, te);
-  }
-  const uint32_t off = wpre + incl - d;
-  for (uint32_t wbase = 0; wbase < total; wbase += kBlock) {
-    const uint32_t s0 = max(off, wbase), s1 = min(off + d, wbase + (uint32_t)kBlock);
-    for (uint32_t k = s0; k < s1; ++k) {
-      sm.fg_edge[k - wbase] = beg + (int64_t)(k - off);
-      sm.fg_src[k - wbase] = sv;
+    for (uint32_t s = 16; s > 0; s >>= 1) {
+      const uint32_t t = __shfl_sync(FULL, incl, o + s - 1);
+      if (t <= k) o += s;
     }
-    __syncthreads();
-    const uint32_t cnt = min((uint32_t)kBlock, total - wbase);
-    const bool act = (uint32_t)tid < cnt;
+    o = min(o, 31u);
+    const int64_t eo = __shfl_sync(FULL, off, o);
+    const int32_t s = __shfl_sync(FULL, sv, o);
     uint32_t dst = 0;
-    int32_t wt = 0, s = 0, cur = 0;
+    int32_t wt = 0, cur = 0;
     if (act) {
-      const int64_t ed = sm.fg_edge[tid];
-      s = sm.fg_src[tid];
+      const int64_t ed = eo + k;
       dst = (uint32_t)ld_stream(p.g.col + ed);
       if (OP == IRGL_OP_SSSP) wt = ld_stream(p.g.w + ed);
       cur = ld_label(p.lab + dst);
     }
-    const bool pr = act && relax_with<OP>(p, cur, s, wt, dst, rb.level, rb.stamp_id);
-    push<DIST>(sm, p, rb, pr, dst);
-    __syncthreads();
+    const int kk = act ? relax_with<OP>(p, rb, cur, s, wt, dst) : 0;
+    wpush<DIST>(sm, q, p, rb, kk, dst);
   }
-  flush_pushes(sm, p, rb);
 }
 
-// ---- CTA-chunk phase: every CTA drains chunk descriptors (grid-stride) ------------------------
+// Item phase: warp tiles, the first static (global warp id), the rest dynamic from tile_ctr.
 template <int OP, bool DIST>
-__device__ void chunk_phase(Smem& sm, const KParams& p, const RoundBufs& rb, uint32_t nch) {
+__device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t ntiles = (rb.nin + 31) >> 5;
+  uint32_t t = gw;
+  while (t < ntiles) {
+    expand_warp_tile<OP, DIST>(sm, q, p, rb, t << 5);
+    uint32_t nt = 0;
+    if (lane_id() == 0) nt = nwarps + atomicAdd(rb.tile_ctr, 1u);
+    t = __shfl_sync(FULL, nt, 0);
+  }
+}
+
+// ---- CTA-chunk phase: every CTA drains chunk descriptors (grid-stride); each thread reads the
+// descriptor itself (broadcast load), so no CTA barrier is needed between chunks.
+template <int OP, bool DIST>
+__device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, uint32_t nch) {
   nch = min(nch, rb.chunk_cap);
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    if (threadIdx.x == 0) {
-      sm.chunk = rb.chunks[c];
-      sm.chunk_src = (OP != IRGL_OP_BFS) ? ld_label(p.lab + sm.chunk.v) : 0;
-    }
-    __syncthreads();
-    const int64_t b = sm.chunk.beg, e = b + sm.chunk.len;
-    const int32_t s = sm.chunk_src;
-    process_range<OP, DIST, kBlock>(sm, p, rb, b, e, s, threadIdx.x);
-    flush_pushes(sm, p, rb);  // begins with __syncthreads: chunk smem reuse is safe
+    const ChunkDesc dsc = rb.chunks[c];
+    const int32_t s = (OP != IRGL_OP_BFS) ? ld_label(p.lab + dsc.v) : 0;
+    process_range<OP, DIST, kBlock>(sm, q, p, rb, dsc.beg, dsc.beg + dsc.len, s, threadIdx.x);
   }
 }
 
-template <int OP, bool DIST>
-__global__ void __launch_bounds__(kBlock, 4) expand_kernel(KParams p, RoundBufs rb) {
-  __shared__ Smem sm;
-  if (threadIdx.x == 0) sm.push_cnt = 0;
-  __syncthreads();
-  for (uint32_t t = blockIdx.x * kBlock; t < rb.nin; t += gridDim.x * kBlock)
-    expand_tile<OP, DIST>(sm, p, rb, t);
+// ---- near-far split: far pile -> near worklist / next far pile / dropped --------------------------
+//   dist <  t_old            : already expanded when it dropped below the old threshold -> drop
+//   t_old <= dist < threshold: near worklist
+//   dist >= threshold        : next far pile (min kept distance -> minkeep)
+__device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
+                          const uint32_t* far_in, uint32_t nfar, int32_t t_old,
+                          unsigned int* minkeep) {
+  uint32_t mymin = 0xffffffffu;
+  const uint32_t T = (gridDim.x * blockDim.x);
+  for (uint32_t i0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; i0 < nfar; i0 += T) {
+    const uint32_t i = i0 + lane_id();
+    int kind = 0;
+    uint32_t v = 0;
+    if (i < nfar) {
+      v = ld_item(far_in + i);
+      const int32_t dv = ld_label(p.lab + v);
+      if (dv >= t_old) {
+        const int k = dv < rb.threshold ? 1 : 2;
+        const int32_t code = (rb.stamp_id << 1) | (k - 1);
+        if (atomicExch(p.stamp + v, code) != code) {
+          kind = k;
+          if (kind == 2) mymin = min(mymin, (uint32_t)dv);
+        }
+      }
+    }
+    wpush<false>(sm, q, p, rb, kind, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mymin = min(mymin, __shfl_xor_sync(FULL, mymin, o));
+  if (lane_id() == 0 && mymin != 0xffffffffu) atomicMin(minkeep, mymin);
 }
 
 template <int OP, bool DIST>
-__global__ void __launch_bounds__(kBlock, 4) chunk_kernel(KParams p, RoundBufs rb) {
+__global__ void __launch_bounds__(kBlock, IRGL_MINB) expand_kernel(KParams p, RoundBufs rb) {
   __shared__ Smem sm;
-  if (threadIdx.x == 0) sm.push_cnt = 0;
-  __syncthreads();
-  chunk_phase<OP, DIST>(sm, p, rb, ld_ctl(rb.chunk_cnt));
+  WarpQ q;
+  item_phase<OP, DIST>(sm, q, p, rb);
+  wflush_all(sm, q, p, rb);
+}
+
+template <int OP, bool DIST>
+__global__ void __launch_bounds__(kBlock, IRGL_MINB) chunk_kernel(KParams p, RoundBufs rb) {
+  __shared__ Smem sm;
+  WarpQ q;
+  chunk_phase<OP, DIST>(sm, q, p, rb, ld_ctl(rb.chunk_cnt));
+  wflush_all(sm, q, p, rb);
+}
+
+__global__ void __launch_bounds__(kBlock, IRGL_MINB) far_split_kernel(KParams p, RoundBufs rb,
+                                                              const uint32_t* far_in,
+                                                              const uint32_t* nfar_ptr,
+                                                              int32_t t_old,
+                                                              unsigned int* minkeep) {
+  __shared__ Smem sm;
+  WarpQ q;
+  far_split(sm, q, p, rb, far_in, ld_ctl(nfar_ptr), t_old, minkeep);
+  wflush_all(sm, q, p, rb);
 }
 
 // ---- E3: outlined Iterate.  One cooperative launch; rounds separated by grid.sync() --------------
 // Worklist buffers alternate by round parity; counters rotate over three slots so the counter
 // cleared during round r (slot (r+2)%3, last read during round r-1) is the out-counter of round
 // r+1: no extra barrier is needed to reset it ("swap in/out and reset out").
+__device__ __forceinline__ int slot3(const PersistArgs& a, uint32_t i) {
+  const uint32_t m = i % 3;
+  return m == 0 ? a.slot[0] : (m == 1 ? a.slot[1] : a.slot[2]);
+}
+
 template <int OP>
-__global__ void __launch_bounds__(kBlock, 4) persistent_kernel(KParams p, PersistArgs a) {
+__global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
   cg::grid_group grid = cg::this_grid();
-  if (threadIdx.x == 0) sm.push_cnt = 0;
-  __syncthreads();
+  WarpQ q;
   uint32_t* cnt = p.ctl->cnt;
+  const bool nf = (OP == IRGL_OP_SSSP) && a.delta > 0;
+  int32_t threshold = nf ? a.delta : kInf;
+  int32_t sid = a.stamp0;       // unique stamp ids: rounds and splits
+  uint32_t fsel = 0;            // which far buffer is current
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   for (uint32_t r = 0;; ++r) {
-    uint32_t* cin = cnt + a.slot[r % 3];
-    uint32_t* cout = cnt + a.slot[(r + 1) % 3];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      cnt[a.slot[(r + 2) % 3]] = 0;
+    uint32_t* cin = cnt + slot3(a, r);
+    uint32_t* cout = cnt + slot3(a, r + 1);
+    if (leader) {
+      cnt[slot3(a, r + 2)] = 0;
       p.ctl->chunk_cnt[(r + 1) % 3] = 0;
+      p.ctl->tile_ctr[(r + 1) % 3] = 0;
     }
     RoundBufs rb;
     rb.in = (r & 1) ? a.buf_b : a.buf_a;
@@ -387,26 +445,67 @@ __global__ void __launch_bounds__(kBlock, 4) persistent_kernel(KParams p, Persis
     rb.chunks = a.chunks;
     rb.chunk_cnt = &p.ctl->chunk_cnt[r % 3];
     rb.chunk_cap = a.chunk_cap;
+    rb.tile_ctr = &p.ctl->tile_ctr[r % 3];
     rb.level = a.level0 + (int32_t)r;
-    rb.stamp_id = a.stamp0 + (int32_t)r;
-    for (uint32_t t = blockIdx.x * kBlock; t < rb.nin; t += gridDim.x * kBlock)
-      expand_tile<OP, false>(sm, p, rb, t);
+    rb.stamp_id = sid++;
+    rb.far = fsel ? a.far_b : a.far_a;
+    rb.far_cnt = &p.ctl->far_cnt[fsel];
+    rb.far_cap = a.far_cap;
+    rb.threshold = threshold;
+    item_phase<OP, false>(sm, q, p, rb);
+    wflush_all(sm, q, p, rb);
     grid.sync();  // SyncRunningThreads
     const uint32_t nch = ld_ctl(rb.chunk_cnt);
     if (nch) {
-      chunk_phase<OP, false>(sm, p, rb, nch);
+      chunk_phase<OP, false>(sm, q, p, rb, nch);
+      wflush_all(sm, q, p, rb);
       grid.sync();
     }
-    const uint32_t nout = ld_ctl(cout);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t nout = ld_ctl(cout);
+    if (nf) {
+      // near frontier exhausted: advance the threshold and split the far pile; a pile past half
+      // its capacity is compacted (split at the unchanged threshold) even when near is not empty
+      uint32_t nfar = ld_ctl(rb.far_cnt);
+      bool advance = nout == 0;
+      if ((advance && nfar > 0) || nfar > a.far_cap / 2) {
+        for (;;) {
+          const int32_t t_old = threshold;
+          if (advance) threshold += a.delta;
+          if (leader) {
+            p.ctl->far_cnt[fsel ^ 1] = 0;
+            p.ctl->minkeep = 0xffffffffu;
+          }
+          grid.sync();
+          RoundBufs sb = rb;
+          sb.far = fsel ? a.far_a : a.far_b;  // next far pile
+          sb.far_cnt = &p.ctl->far_cnt[fsel ^ 1];
+          sb.threshold = threshold;
+          sb.stamp_id = sid++;
+          far_split(sm, q, p, sb, rb.far, nfar, t_old, &p.ctl->minkeep);
+          wflush_all(sm, q, p, sb);
+          grid.sync();
+          fsel ^= 1;
+          rb.far = sb.far;
+          rb.far_cnt = sb.far_cnt;
+          nout = ld_ctl(cout);
+          nfar = ld_ctl(rb.far_cnt);
+          if (nout > 0 || nfar == 0) break;
+          threshold = (int32_t)ld_ctl(&p.ctl->minkeep);  // next pass moves at least the minimum
+          advance = true;
+        }
+      }
+    }
+    if (leader) {
       p.ctl->popped += rb.nin;
       p.ctl->pushes += nout;
     }
     // Iterate termination: in empty (next round) [Or rounds >= max_rounds]
     if (nout == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds)) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (leader) {
         p.ctl->rounds = r + 1;
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+        p.ctl->stamp_used = (uint32_t)(sid - a.stamp0);
+        p.ctl->far_sel = fsel;
       }
       break;
     }
@@ -415,40 +514,23 @@ __global__ void __launch_bounds__(kBlock, 4) persistent_kernel(KParams p, Persis
 
 // ---- owner-side application of remote updates (E5 min-reduce) ---------------------------------
 template <int OP>
-__global__ void __launch_bounds__(kBlock) apply_remote_kernel(int32_t* lab, int32_t* stamp, Ctl* ctl,
+__global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBufs rb,
                                                            const uint32_t* items,
-                                                           const int32_t* values, uint32_t n,
-                                                           uint32_t* out, uint32_t* out_cnt,
-                                                           uint32_t cap, int32_t level,
-                                                           int32_t stamp_id) {
-  const uint32_t lane = lane_id();
-  for (uint32_t i0 = blockIdx.x * kBlock; i0 < n; i0 += gridDim.x * kBlock) {
-    const uint32_t i = i0 + threadIdx.x;
-    bool pr = false;
+                                                           const int32_t* values, uint32_t n) {
+  __shared__ Smem sm;
+  WarpQ q;
+  for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < n; i0 += gridDim.x * kBlock) {
+    const uint32_t i = i0 + lane_id();
+    int kind = 0;
     uint32_t v = 0;
     if (i < n) {
       v = items[i];
-      if (OP == IRGL_OP_BFS) {
-        pr = ld_label(lab + v) == kInf && atomicCAS(lab + v, kInf, level) == kInf;
-      } else {
-        const int32_t nd = values[i];
-        pr = nd < ld_label(lab + v) && atomicMin(lab + v, nd) > nd &&
-             atomicExch(stamp + v, stamp_id) != stamp_id;
-      }
+      const int32_t cur = ld_label(p.lab + v);
+      kind = relax_with<OP>(p, rb, cur, OP == IRGL_OP_BFS ? 0 : values[i], 0, v);
     }
-    const uint32_t m = __ballot_sync(FULL, pr);
-    if (m) {
-      const uint32_t leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(out_cnt, __popc(m));
-      base = __shfl_sync(FULL, base, leader);
-      if (pr) {
-        const uint32_t q = base + __popc(m & lanemask_lt());
-        if (q < cap) out[q] = v;
-        else atomicOr(&ctl->overflow, 1u);
-      }
-    }
+    wpush<false>(sm, q, p, rb, kind, v);
   }
+  wflush_all(sm, q, p, rb);
 }
 
 __global__ void pack_values_kernel(const int32_t* lab, const uint32_t* items, int32_t* values,
@@ -460,9 +542,12 @@ __global__ void pack_values_kernel(const int32_t* lab, const uint32_t* items, in
 template <int OP, bool DIST>
 cudaError_t round_impl(const KParams& kp, const RoundBufs& rb, int grid_max, cudaStream_t st) {
   if (rb.nin > 0) {
-    const int tiles = (int)((rb.nin + kBlock - 1) / kBlock);
-    expand_kernel<OP, DIST><<<min(tiles, grid_max), kBlock, 0, st>>>(kp, rb);
+    const int wtiles = (int)((rb.nin + 31) / 32);
+    const int blocks = min((wtiles + kWarps - 1) / kWarps, grid_max);
+    note_launch();
+    expand_kernel<OP, DIST><<<blocks, kBlock, 0, st>>>(kp, rb);
   }
+  note_launch();
   chunk_kernel<OP, DIST><<<grid_max, kBlock, 0, st>>>(kp, rb);
   return cudaGetLastError();
 }
@@ -488,23 +573,32 @@ cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* 
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+                             const RoundBufs& rb, const uint32_t* far_in, const uint32_t* nfar_ptr,
+                             int32_t t_old, unsigned int* minkeep, int grid, cudaStream_t st) {
+  KParams kp{g, lab, stamp, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
+  note_launch();
+  far_split_kernel<<<grid, kBlock, 0, st>>>(kp, rb, far_in, nfar_ptr, t_old, minkeep);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, const uint32_t* items,
-                                const int32_t* values, uint32_t n, uint32_t* out, uint32_t* out_cnt,
-                                uint32_t cap, int32_t level, int32_t stamp_id, cudaStream_t st) {
+                                const int32_t* values, uint32_t n, const RoundBufs& rb,
+                                cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const int grid = (int)min((n + kBlock - 1) / kBlock, 148u * 8u);
+  KParams kp{DevCSR{nullptr, nullptr, nullptr, 0, 0}, lab, stamp, ctl,
+             DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
+  note_launch();
   switch (op) {
     case IRGL_OP_BFS:
-      apply_remote_kernel<IRGL_OP_BFS><<<grid, kBlock, 0, st>>>(lab, stamp, ctl, items, values, n,
-                                                                out, out_cnt, cap, level, stamp_id);
+      apply_remote_kernel<IRGL_OP_BFS><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
       break;
     case IRGL_OP_SSSP:
-      apply_remote_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(lab, stamp, ctl, items, values, n,
-                                                                 out, out_cnt, cap, level, stamp_id);
+      apply_remote_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
       break;
     case IRGL_OP_CC_LP:
-      apply_remote_kernel<IRGL_OP_CC_LP><<<grid, kBlock, 0, st>>>(lab, stamp, ctl, items, values, n,
-                                                                  out, out_cnt, cap, level, stamp_id);
+      apply_remote_kernel<IRGL_OP_CC_LP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
       break;
     default:
       return cudaErrorInvalidValue;
@@ -515,6 +609,7 @@ cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, 
 cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
                                uint32_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  note_launch();
   pack_values_kernel<<<(int)min((n + 255) / 256, 4096u), 256, 0, st>>>(lab, items, values, n);
   return cudaGetLastError();
 }
@@ -557,6 +652,7 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
   KParams kp{g, lab, stamp, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ec};
   PersistArgs a = pa;
   void* args[] = {&kp, &a};
+  note_launch();
   switch (op) {
     case IRGL_OP_BFS:
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_BFS>, grid, kBlock, args, 0, st);

@@ -222,6 +222,7 @@ cudaError_t max_degree(const int64_t* row_ptr, int64_t nrows, int64_t* out, cuda
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(d, 0, 8, st);
   if (nrows > 0)
+    note_launch();
     max_deg_kernel<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 8), 256, 0, st>>>(row_ptr, nrows, d);
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
@@ -247,7 +248,10 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     GridSpec g{s.width, s.height, s.diag, s.cut_period,
                s.perc_keep_ppm > 0 ? s.perc_keep_ppm : 1000000, s.perc_seed};
     const int grid = (int)std::min<int64_t>((nloc + 255) / 256, 148 * 16);
-    if (nloc > 0) grid_deg_kernel<<<grid, 256, 0, st>>>(g, lo, hi, deg);
+    if (nloc > 0) {
+      note_launch();
+      grid_deg_kernel<<<grid, 256, 0, st>>>(g, lo, hi, deg);
+    }
     size_t tmp = 0;
     GEN_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg, rp, nloc + 1, st));
     void* t = nullptr;
@@ -258,7 +262,10 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     cudaFreeAsync(t, st);
     GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * sizeof(int32_t), st));
     GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * sizeof(int32_t), st));
-    if (nloc > 0) grid_fill_kernel<<<grid, 256, 0, st>>>(g, lo, hi, rp, s.wseed, dc, dw);
+    if (nloc > 0) {
+      note_launch();
+      grid_fill_kernel<<<grid, 256, 0, st>>>(g, lo, hi, rp, s.wseed, dc, dw);
+    }
   } else {
     const int scale = s.scale;
     const uint64_t ne = (uint64_t)(s.edge_factor > 0 ? s.edge_factor : 16) << scale;
@@ -270,6 +277,7 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     GEN_CK(cudaMallocAsync(&ctr, 8, st));
     GEN_CK(cudaMemsetAsync(ctr, 0, 8, st));
     const int ggrid = 148 * 16;
+    note_launch();
     rmat_keys_kernel<false><<<ggrid, 256, 0, st>>>(ne, scale, s.seed, scr, lo, hi, ctr, nullptr);
     unsigned long long nk = 0;
     GEN_CK(cudaMemcpyAsync(&nk, ctr, 8, cudaMemcpyDeviceToHost, st));
@@ -279,6 +287,7 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     GEN_CK(cudaMallocAsync(&ka, (nk > 0 ? nk : 1) * sizeof(uint64_t), st));
     GEN_CK(cudaMallocAsync(&kb, (nk > 0 ? nk : 1) * sizeof(uint64_t), st));
     GEN_CK(cudaMemsetAsync(ctr, 0, 8, st));
+    note_launch();
     rmat_keys_kernel<true><<<ggrid, 256, 0, st>>>(ne, scale, s.seed, scr, lo, hi, ctr, ka);
     const int end_bit = bits_for(nloc > 1 ? nloc : 2) + scale;
     cub::DoubleBuffer<uint64_t> db(ka, kb);
@@ -301,11 +310,17 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     GEN_CK(cudaStreamSynchronize(st));
     cudaFreeAsync(sorted, st);
     const int fgrid = (int)std::min<int64_t>((m + 255) / 256, 148 * 32);
-    if (m > 0) row_count_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, deg);
+    if (m > 0) {
+      note_launch();
+      row_count_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, deg);
+    }
     GEN_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg, rp, nloc + 1, st));
     GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * sizeof(int32_t), st));
     GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * sizeof(int32_t), st));
-    if (m > 0) fill_csr_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, lo, s.wseed, dc, dw);
+    if (m > 0) {
+      note_launch();
+      fill_csr_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, lo, s.wseed, dc, dw);
+    }
     cudaFreeAsync(uniq, st);
     cudaFreeAsync(t, st);
     cudaFreeAsync(nsel, st);

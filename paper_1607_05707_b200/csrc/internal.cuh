@@ -41,6 +41,12 @@ struct Ctl {
   int32_t last_red;            // persistent: last round's reduced value
   int32_t exit_in_slot;        // persistent: buffer parity at exit
   unsigned long long tc_count; // TC: Sum reduction (extension)
+  uint32_t tile_ctr[3];        // dynamic warp-tile counters, rotated by round
+  uint32_t far_cnt[2];         // SSSP near-far pile counters (double-buffered)
+  uint32_t minkeep;            // min dist kept in the far pile by the last split
+  uint32_t stamp_used;         // persistent: stamp ids consumed (rounds + splits)
+  uint32_t far_sel;            // persistent: current far pile at exit
+  uint32_t pad2;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -81,6 +87,8 @@ __device__ __forceinline__ int32_t ld_label(const int32_t* p) {
 // (or a global slot) as "RULE: message" (reference diag.hpp:20-27 convention).
 namespace irgl {
 void set_error(irgl_ctx* ctx, irgl_status_t st, const char* rule, const std::string& msg);
+// every kernel launch site calls this (irgl_launch_count evidence for the bench)
+void note_launch(int n = 1);
 irgl_status_t cuda_status(irgl_ctx* ctx, cudaError_t e, const char* where);
 }  // namespace irgl
 

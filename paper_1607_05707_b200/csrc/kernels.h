@@ -37,6 +37,12 @@ struct RoundBufs {
   uint32_t chunk_cap;
   int32_t level;     // BFS LEVEL of this round
   int32_t stamp_id;  // unique round id (push dedupe)
+  uint32_t* tile_ctr;  // dynamic warp-tile counter of this round (zeroed before the round)
+  // SSSP near-far: pushes with dist >= threshold go to the far pile
+  uint32_t* far;
+  uint32_t* far_cnt;
+  uint32_t far_cap;
+  int32_t threshold;  // INT32_MAX: near-far off
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
@@ -46,8 +52,12 @@ cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* 
                                 int grid_max, cudaStream_t st);
 // Apply received remote updates (owner side min-reduce): items[i] with values[i] (BFS: level).
 cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, const uint32_t* items,
-                                const int32_t* values, uint32_t n, uint32_t* out, uint32_t* out_cnt,
-                                uint32_t cap, int32_t level, int32_t stamp_id, cudaStream_t st);
+                                const int32_t* values, uint32_t n, const RoundBufs& rb,
+                                cudaStream_t st);
+// Near-far split of a far pile into rb.out (dist < rb.threshold) / rb.far (the next pile).
+cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+                             const RoundBufs& rb, const uint32_t* far_in, const uint32_t* nfar_ptr,
+                             int32_t t_old, unsigned int* minkeep, int grid, cudaStream_t st);
 // Gather current label values of the send buckets (SSSP / CC_LP pack step).
 cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
                                uint32_t n, cudaStream_t st);
@@ -62,6 +72,10 @@ struct PersistArgs {
   int32_t level0;
   int32_t stamp0;
   int64_t max_rounds;  // 0 = until empty
+  uint32_t* far_a;     // SSSP near-far piles (current at round 0 = far_a)
+  uint32_t* far_b;
+  uint32_t far_cap;
+  int32_t delta;       // 0: plain data-driven Bellman-Ford
 };
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,

@@ -102,26 +102,31 @@ cudaError_t launch_test_op(const TestArgs& a, int threads, cudaStream_t st) {
   // T = grid*bs threads; T == threads whenever threads <= 256 or a multiple of 256
   const int bs = threads <= 256 ? (threads > 0 ? threads : 1) : 256;
   const int grid = (threads + bs - 1) / bs;
+  note_launch();
   test_op_kernel<<<grid, bs, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  note_launch();
   fill_i32_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(p, v, n);
   return cudaGetLastError();
 }
 cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  note_launch();
   scatter_zero_kernel<<<(int)std::min<uint32_t>((n + 255) / 256, 1024), 256, 0, st>>>(lab, items, n);
   return cudaGetLastError();
 }
 cudaError_t launch_iota_u32(uint32_t* p, uint32_t begin, uint32_t n, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
+  note_launch();
   iota_kernel<<<(int)std::min<uint32_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(p, begin, n);
   return cudaGetLastError();
 }
 cudaError_t launch_set_red(Ctl* ctl, int slot, uint32_t v, cudaStream_t st) {
+  note_launch();
   set_red_kernel<<<1, 1, 0, st>>>(ctl, slot, v);
   return cudaGetLastError();
 }

@@ -320,17 +320,20 @@ __global__ void tc_count_kernel(const int64_t* orp, const int32_t* ocl, int64_t 
 
 cudaError_t launch_cc_hook(const DevCSR& g, int32_t* parent, Ctl* ctl, int red_slot, int grid,
                            cudaStream_t st) {
+  note_launch();
   cc_hook_kernel<<<grid, kBlock, 0, st>>>(g, parent, &ctl->red[red_slot]);
   return cudaGetLastError();
 }
 cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  note_launch();
   cc_compress_kernel<<<grid, 256, 0, st>>>(parent, n);
   return cudaGetLastError();
 }
 cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
                            cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  note_launch();
   pr_init_kernel<<<grid, 256, 0, st>>>(rank, contrib, row_ptr, n);
   return cudaGetLastError();
 }
@@ -338,6 +341,7 @@ cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* ran
                             const double* contrib, double* contrib_next, double d, double tol,
                             int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st) {
   const double base = (1.0 - d) / (double)n_global;
+  note_launch();
   pr_sweep_kernel<<<grid, kBlock, 0, st>>>(g, rank_old, rank_new, contrib, contrib_next, d, tol,
                                            base, &ctl->red[red_slot]);
   return cudaGetLastError();
@@ -353,6 +357,7 @@ cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double
   double base = (1.0 - d) / (double)n_global;
   DevCSR gg = g;
   void* args[] = {&gg, &ra, &rb, &ca, &cb, &d, &tol, &base, &ctl, &max_rounds, &cond_mode};
+  note_launch();
   return cudaLaunchCooperativeKernel((void*)pr_persistent_kernel, grid, kBlock, args, 0, st);
 }
 
@@ -365,6 +370,7 @@ cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl
   if ((e = cudaMallocAsync(&dout, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&orp, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
   const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  note_launch();
   tc_count_out_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, dout);
   cudaMemsetAsync(dout + n, 0, sizeof(int64_t), st);
   size_t tmp = 0;
@@ -376,6 +382,7 @@ cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl
   cudaMemcpyAsync(&mo, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&ocl, (mo > 0 ? mo : 1) * sizeof(int32_t), st)) != cudaSuccess) return e;
+  note_launch();
   tc_fill_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, orp, ocl);
   cudaFreeAsync(t, st);
   cudaFreeAsync(dout, st);
@@ -389,6 +396,7 @@ cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl
                             cudaStream_t st) {
   cudaMemsetAsync(&ctl->tc_count, 0, sizeof(unsigned long long), st);
   const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  note_launch();
   tc_count_kernel<<<grid, 256, 0, st>>>(rp, cl, n, &ctl->tc_count);
   return cudaGetLastError();
 }

@@ -65,7 +65,8 @@ class Config(C.Structure):
 class OpArgs(C.Structure):
     _fields_ = [("round_start", C.c_int64), ("guard", C.c_int64), ("pr_damping", C.c_double),
                 ("pr_tol", C.c_double), ("values", C.POINTER(C.c_int32)), ("nvalues", C.c_int64),
-                ("mapping", C.c_int32), ("threads", C.c_int32), ("reserved", C.c_int32 * 6)]
+                ("mapping", C.c_int32), ("threads", C.c_int32), ("delta", C.c_int32),
+                ("reserved", C.c_int32 * 5)]
 
 
 class IterateOpts(C.Structure):
@@ -79,7 +80,7 @@ class IterStats(C.Structure):
                 ("pushes", C.c_int64), ("retries", C.c_int64), ("edges", C.c_int64),
                 ("remote_updates", C.c_int64), ("exchange_bytes", C.c_int64),
                 ("serial_launches", C.c_int64), ("last_reduced", C.c_int32),
-                ("outlined", C.c_int32), ("device_ms", C.c_double)]
+                ("outlined", C.c_int32), ("device_ms", C.c_double), ("kernel_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -110,7 +111,7 @@ EXPORTS = [
     "irgl_pipe_create", "irgl_pipe_init_scalars", "irgl_pipe_init_from_array",
     "irgl_pipe_init_range", "irgl_pipe_size", "irgl_pipe_read", "irgl_pipe_destroy",
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
-    "irgl_op_plan",
+    "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
 ]
 
 _lib = None
@@ -121,7 +122,8 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    # IRGL_LIB: load an alternative build (tuning experiments only; same C-ABI)
+    path = path or os.environ.get("IRGL_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`"
                           " (there is no CPU fallback for the IrGL GPU runtime)")
@@ -157,6 +159,9 @@ def load_library(path: str | None = None):
         "irgl_read_result": ([P, P, C.c_int, P, C.c_size_t], i32),
         "irgl_t_control": ([C.POINTER(BlockConstraint), C.c_int, i32p], i32),
         "irgl_op_plan": ([P, C.c_int, C.POINTER(BlockConstraint), i32p, i32p], i32),
+        "irgl_event_record": ([P, C.c_int], i32),
+        "irgl_event_elapsed": ([P, C.c_int, C.c_int, C.POINTER(C.c_double)], i32),
+        "irgl_launch_count": ([], i64),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -192,6 +197,11 @@ def t_control(constraints) -> int:
     return out.value
 
 
+def launch_count() -> int:
+    """Kernels launched by libirgl_rt.so in this process so far."""
+    return int(load_library().irgl_launch_count())
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(load_library().irgl_nccl_unique_id(buf))
@@ -199,8 +209,9 @@ def nccl_unique_id() -> bytes:
 
 
 def _op_args(round_start=0, guard=0, pr_damping=0.0, pr_tol=0.0, values=None, mapping=0,
-             threads=0):
+             threads=0, delta=-1):
     a = OpArgs()
+    a.delta = delta
     a.round_start = round_start
     a.guard = guard
     a.pr_damping = pr_damping
@@ -229,6 +240,7 @@ class Stats:
     last_reduced: int
     outlined: int
     device_ms: float
+    kernel_ms: float
 
 
 class Context:
@@ -371,6 +383,14 @@ class Context:
                                              out.ctypes.data_as(C.c_void_p), out.nbytes))
         return out
 
+    def event_record(self, slot):
+        self._chk(self._lib.irgl_event_record(self._h, slot))
+
+    def event_elapsed(self, a, b) -> float:
+        ms = C.c_double(0)
+        self._chk(self._lib.irgl_event_elapsed(self._h, a, b, C.byref(ms)))
+        return ms.value
+
     def op_plan(self, op):
         bc = BlockConstraint()
         go, gf = C.c_int32(0), C.c_int32(0)
@@ -474,10 +494,11 @@ def bfs(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outli
     return ctx.read_result(BFS, graph), st
 
 
-def sssp(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outline=-1):
+def sssp(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outline=-1,
+         delta=-1):
     p = pipe or ctx.pipe(graph.n)
     p.init_scalars([src])
-    st = ctx.iterate(SSSP, graph, p, outline=outline)
+    st = ctx.iterate(SSSP, graph, p, outline=outline, delta=delta)
     return ctx.read_result(SSSP, graph), st
 
 

@@ -134,6 +134,17 @@ def test_sssp_rmat_parity(ctx, irgl, oracle, outline):
         np.testing.assert_array_equal(d, ref)
 
 
+@pytest.mark.parametrize("delta", [0, 1, 7, 96, 100000])
+@pytest.mark.parametrize("outline", [0, 1])
+def test_sssp_near_far_parity(ctx, irgl, oracle, delta, outline):
+    """Near-far (delta > 0) reorders relaxations only: distances stay bit-exact."""
+    og = oracle.rmat(13)
+    g = _upload(ctx, og)
+    s = int(og.sources(1)[0])
+    d, st = irgl.sssp(ctx, g, s, outline=outline, delta=delta)
+    np.testing.assert_array_equal(d, oracle.sssp(og, s))
+
+
 def test_sssp_device_generated_graph(ctx, irgl, oracle):
     og = oracle.rmat(15)
     g = ctx.generate_rmat(15)
@@ -221,9 +232,10 @@ def test_partitioned_bfs_sssp_parity(irgl, oracle, P):
             lv, st = irgl.bfs(c, g, s)
             np.testing.assert_array_equal(lv, ref)
             assert st.rounds == ecc + 1
-            d, st = irgl.sssp(c, g, s)
-            np.testing.assert_array_equal(d, oracle.sssp(og, s))
-            assert st.remote_updates > 0
+            for delta in (0, 64):
+                d, st = irgl.sssp(c, g, s, delta=delta)
+                np.testing.assert_array_equal(d, oracle.sssp(og, s))
+                assert st.remote_updates > 0
 
 
 def test_partitioned_generated_graph(irgl, oracle):
