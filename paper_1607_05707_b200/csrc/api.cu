@@ -29,6 +29,7 @@ struct irgl_ctx {
   ncclComm_t comm = nullptr;
   const irgl::NcclApi* nccl = nullptr;
   int64_t route_size = INT64_MAX;   // partition size of the last graph (pipe routing)
+  uint32_t* cnt_dev = nullptr;      // NCCL count exchange scratch [L*P + P*P]
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // hot-kernel timing (iter_stats.kernel_ms)
@@ -313,35 +314,46 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       }
     }
   // 3. transport
-  if (ctx->nranks > 1) {
-    // counts of the other ranks: all-gather the local rows (device buffer send_cnt of part 0)
+  if (ctx->comm) {
+    // NCCL transport (R ranks x L partitions; all partitions of a rank share its device).
+    for (int l = 0; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // packs done
     PartRT& pr = ctx->parts[0];
-    GraphPart& gp = g->parts[0];
     CK(cudaSetDevice(pr.dev));
-    uint32_t* dmat = reinterpret_cast<uint32_t*>(gp.recv_val ? (void*)gp.recv_val : (void*)gp.recv);
-    // use the tail of the recv buffer region sized P*P as scratch: recv is [P*ps] >= P*P
-    uint32_t* scratch = gp.recv + ((int64_t)P * ps - (int64_t)P * P);
-    (void)dmat;
-    NCK(ctx->nccl->AllGather(gp.send_cnt, scratch, P, ncclUint32, ctx->comm, pr.st));
-    CK(cudaMemcpyAsync(cnt.data(), scratch, (size_t)P * P * 4, cudaMemcpyDeviceToHost, pr.st));
+    // (i) counts: every rank contributes its L rows of the P x P matrix (ncclAllGather)
+    for (int l = 0; l < L; ++l)
+      CK(cudaMemcpyAsync(ctx->cnt_dev + (size_t)l * P, g->parts[l].send_cnt, P * 4,
+                         cudaMemcpyDeviceToDevice, pr.st));
+    NCK(ctx->nccl->AllGather(ctx->cnt_dev, ctx->cnt_dev + (size_t)L * P, (size_t)L * P, ncclUint32,
+                             ctx->comm, pr.st));
+    CK(cudaMemcpyAsync(cnt.data(), ctx->cnt_dev + (size_t)L * P, (size_t)P * P * 4,
+                       cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
-    // payloads: grouped send/recv (all-to-all v), one partition per rank
-    const int me = ctx->rank;
+    // (ii) payloads: grouped send/recv (all-to-all-v).  Every rank walks the (src, dst) partition
+    // pairs in the same global order, so the per-peer order of sends matches the receiver's
+    // order of recvs (NCCL matches point-to-point calls per peer in issue order).
+    const int lo_part = ctx->gpart(0);
     NCK(ctx->nccl->GroupStart());
-    for (int q = 0; q < P; ++q) {
-      if (q == me) continue;
-      const uint32_t cs = cnt[(size_t)me * P + q], cr = cnt[(size_t)q * P + me];
-      if (cs) {
-        NCK(ctx->nccl->Send(gp.send + (int64_t)q * ps, cs, ncclUint32, q, ctx->comm, pr.st));
-        if (vals) NCK(ctx->nccl->Send(gp.send_val + (int64_t)q * ps, cs, ncclInt32, q, ctx->comm, pr.st));
+    for (int p = 0; p < P; ++p)
+      for (int q = 0; q < P; ++q) {
+        if (p == q) continue;
+        const uint32_t c = cnt[(size_t)p * P + q];
+        if (!c) continue;
+        const bool src_local = p >= lo_part && p < lo_part + L;
+        const bool dst_local = q >= lo_part && q < lo_part + L;
+        if (src_local) {
+          GraphPart& sp = g->parts[p - lo_part];
+          NCK(ctx->nccl->Send(sp.send + (int64_t)q * ps, c, ncclUint32, q / L, ctx->comm, pr.st));
+          if (vals) NCK(ctx->nccl->Send(sp.send_val + (int64_t)q * ps, c, ncclInt32, q / L, ctx->comm, pr.st));
+          stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
+        }
+        if (dst_local) {
+          GraphPart& dp = g->parts[q - lo_part];
+          NCK(ctx->nccl->Recv(dp.recv + (int64_t)p * ps, c, ncclUint32, p / L, ctx->comm, pr.st));
+          if (vals) NCK(ctx->nccl->Recv(dp.recv_val + (int64_t)p * ps, c, ncclInt32, p / L, ctx->comm, pr.st));
+        }
       }
-      if (cr) {
-        NCK(ctx->nccl->Recv(gp.recv + (int64_t)q * ps, cr, ncclUint32, q, ctx->comm, pr.st));
-        if (vals) NCK(ctx->nccl->Recv(gp.recv_val + (int64_t)q * ps, cr, ncclInt32, q, ctx->comm, pr.st));
-      }
-      stt->exchange_bytes += (int64_t)(cs + cr) * (vals ? 8 : 4);
-    }
     NCK(ctx->nccl->GroupEnd());
+    CK(cudaStreamSynchronize(pr.st));  // payloads landed before the per-partition applies
   } else {
     for (int l = 0; l < L; ++l) {
       PartRT& pr = ctx->parts[l];
@@ -385,7 +397,7 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
 }
 
 static irgl_status_t allreduce_sum_u64(irgl_ctx* ctx, uint64_t* v) {
-  if (ctx->nranks <= 1) return IRGL_OK;
+  if (!ctx->comm) return IRGL_OK;
   PartRT& pr = ctx->parts[0];
   CK(cudaSetDevice(pr.dev));
   unsigned long long* d = nullptr;
@@ -399,7 +411,7 @@ static irgl_status_t allreduce_sum_u64(irgl_ctx* ctx, uint64_t* v) {
 }
 
 static irgl_status_t allreduce_min_u64(irgl_ctx* ctx, uint64_t* v) {
-  if (ctx->nranks <= 1) return IRGL_OK;
+  if (!ctx->comm) return IRGL_OK;
   PartRT& pr = ctx->parts[0];
   CK(cudaSetDevice(pr.dev));
   unsigned long long* d = nullptr;
@@ -474,7 +486,7 @@ static irgl_status_t near_far_split(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pip
       CK(cudaSetDevice(pr.dev));
       CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_out], 4, cudaMemcpyDeviceToHost, pr.st));
       CK(cudaMemcpyAsync(pr.h_pin + 1, &pp.ctl->far_cnt[nf.fsel], 4, cudaMemcpyDeviceToHost, pr.st));
-      CK(cudaMemcpyAsync(pr.h_pin + 2, &pp.ctl->minkeep, 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemcpyAsync(pr.h_pin + 2, &pp.ctl->minkeep[0], 4, cudaMemcpyDeviceToHost, pr.st));
       CK(cudaStreamSynchronize(pr.st));
       nout[l] = pr.h_pin[0];
       nfar[l] = pr.h_pin[1];
@@ -506,12 +518,12 @@ static irgl_status_t near_far_split(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pip
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
       CK(cudaMemsetAsync(&pp.ctl->far_cnt[nf.fsel ^ 1], 0, 4, pr.st));
-      CK(cudaMemsetAsync(&pp.ctl->minkeep, 0xff, 4, pr.st));
+      CK(cudaMemsetAsync(&pp.ctl->minkeep[0], 0xff, 4, pr.st));
       NearFar nx = nf;
       nx.fsel ^= 1;
       RoundBufs rb = round_bufs(pipe, gp, pp, level, sid, nx);
       CK(launch_far_split(gp.csr(), gp.lab, gp.stamp, pp.ctl, rb, gp.far[nf.fsel],
-                          &pp.ctl->far_cnt[nf.fsel], t_old, &pp.ctl->minkeep,
+                          &pp.ctl->far_cnt[nf.fsel], t_old, &pp.ctl->minkeep[0],
                           grid_max(ctx, pr, IRGL_OP_SSSP), pr.st));
     }
     nf.fsel ^= 1;
@@ -1001,8 +1013,10 @@ irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void*
   }
   auto c = std::make_unique<irgl_ctx>();
   if (cfg) c->cfg = *cfg;
-  c->cfg.logical_partitions = 1;  // one partition per rank
-  irgl_status_t s = ctx_init_parts(c.get(), &device, 1, 1);
+  // one partition per rank by default; logical_partitions > 1 hosts L partitions per rank on the
+  // rank's device (their exchange still goes through NCCL, self send/recv included)
+  const int L = c->cfg.logical_partitions > 1 ? c->cfg.logical_partitions : 1;
+  irgl_status_t s = ctx_init_parts(c.get(), &device, 1, L);
   if (s != IRGL_OK) return s;
   std::string why;
   c->nccl = nccl_api(&why);
@@ -1017,6 +1031,11 @@ irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void*
   }
   c->rank = rank;
   c->nranks = nranks;
+  const int P = nranks * L;
+  if (cudaMalloc(&c->cnt_dev, ((size_t)L * P + (size_t)P * P) * 4) != cudaSuccess) {
+    set_error(nullptr, IRGL_E_OOM, "E_OOM", "count exchange scratch");
+    return IRGL_E_OOM;
+  }
   *out = c.release();
   return IRGL_OK;
 }
@@ -1046,6 +1065,7 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
   if (ctx->test_log) cudaFree(ctx->test_log);
   if (ctx->test_rcount) cudaFree(ctx->test_rcount);
   if (ctx->test_ctl) cudaFree(ctx->test_ctl);
+  if (ctx->cnt_dev) cudaFree(ctx->cnt_dev);
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->kev0, ctx->kev1})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->user_ev)
@@ -1179,10 +1199,9 @@ irgl_status_t irgl_graph_download(irgl_graph* g, int64_t* row_ptr, int32_t* col,
     const int64_t nloc = gp.hi - gp.lo;
     std::vector<int64_t> rp(nloc + 1);
     CK(cudaMemcpy(rp.data(), gp.row_ptr, (nloc + 1) * 8, cudaMemcpyDeviceToHost));
-    if (row_ptr) {
-      const int64_t base = (ctx->nranks > 1) ? 0 : eoff;
-      const int64_t ro = (ctx->nranks > 1) ? 0 : gp.lo;
-      for (int64_t i = 0; i <= nloc; ++i) row_ptr[ro + i] = base + rp[i];
+    if (row_ptr) {  // local partitions are contiguous: rows relative to the first local one
+      const int64_t ro = gp.lo - g->parts[0].lo;
+      for (int64_t i = 0; i <= nloc; ++i) row_ptr[ro + i] = eoff + rp[i];
     }
     if (col && gp.m) CK(cudaMemcpy(col + eoff, gp.col, gp.m * 4, cudaMemcpyDeviceToHost));
     if (weight && gp.m) CK(cudaMemcpy(weight + eoff, gp.w, gp.m * 4, cudaMemcpyDeviceToHost));

@@ -39,6 +39,9 @@ constexpr int kWBuf = 256;  // per-warp push staging entries
 struct Smem {
   uint32_t wbuf[kWarps][kWBuf];   // near pushes (E2)
   uint32_t fbuf[kWarps][kWBuf];   // far pushes (SSSP near-far)
+  uint32_t fl_cnt[2][kWarps];     // CTA flush: per-warp staged counts (near, far)
+  uint32_t fl_off[2][kWarps];     // CTA flush: per-warp global offsets
+  unsigned long long fl_edges[kWarps];
 };
 
 struct KParams {
@@ -154,14 +157,49 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
   }
 }
 
+// CTA-level flush at a CTA-uniform point (every thread calls it): one global reservation per pile
+// and one stats atomic per CTA instead of one per warp (E2 at CTA granularity).
 __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
-  const uint32_t warp = threadIdx.x >> 5;
-  wflush(sm.wbuf[warp], q.n, rb.out, rb.out_cnt, rb.cap, &p.ctl->overflow);
-  wflush(sm.fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
-  if (q.edges) {
-    if (lane_id() == 0) atomicAdd(&p.ctl->edges, q.edges);
-    q.edges = 0;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  if (lane == 0) {
+    sm.fl_cnt[0][warp] = q.n;
+    sm.fl_cnt[1][warp] = q.nf;
+    sm.fl_edges[warp] = q.edges;
   }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    const int k = threadIdx.x;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      sm.fl_off[k][w] = tot;
+      tot += sm.fl_cnt[k][w];
+    }
+    const uint32_t base = tot ? atomicAdd(k == 0 ? rb.out_cnt : rb.far_cnt, tot) : 0u;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) sm.fl_off[k][w] += base;
+    if (k == 0) {
+      unsigned long long te = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) te += sm.fl_edges[w];
+      if (te) atomicAdd(&p.ctl->edges, te);
+    }
+  }
+  __syncthreads();
+  const uint32_t o0 = sm.fl_off[0][warp], o1 = sm.fl_off[1][warp];
+  for (uint32_t i = lane; i < q.n; i += 32) {
+    const uint32_t qq = o0 + i;
+    if (qq < rb.cap) rb.out[qq] = sm.wbuf[warp][i];
+    else atomicOr(&p.ctl->overflow, 1u);
+  }
+  for (uint32_t i = lane; i < q.nf; i += 32) {
+    const uint32_t qq = o1 + i;
+    if (qq < rb.far_cap) rb.far[qq] = sm.fbuf[warp][i];
+    else atomicOr(&p.ctl->overflow, 1u);
+  }
+  __syncwarp();
+  q.n = q.nf = 0;
+  q.edges = 0;
 }
 
 // ---- edge-range processing by a group of G lanes (G = 32 warp, G = kBlock CTA) -------------------
@@ -219,10 +257,10 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
 // ---- one warp tile of 32 worklist items (consecutive mapping inside the tile) --------------------
 template <int OP, bool DIST>
 __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
-                                 uint32_t base) {
+                                 uint32_t base, uint32_t width) {
   const int lane = lane_id();
   const uint32_t i = base + lane;
-  const bool valid = i < rb.nin;
+  const bool valid = (uint32_t)lane < width && i < rb.nin;
   uint32_t v = 0;
   int64_t beg = 0, end = 0;
   int32_t sv = 0;
@@ -231,7 +269,7 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     const int64_t lv = (int64_t)v - p.g.lo;
     beg = __ldg(p.g.row_ptr + lv);
     end = __ldg(p.g.row_ptr + lv + 1);
-    if (OP != IRGL_OP_BFS) sv = ld_label(p.lab + v);
+    if (OP != IRGL_OP_BFS) sv = ld_label_cg(p.lab + v);
   }
   int64_t deg = end - beg;
   {
@@ -322,15 +360,21 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   }
 }
 
-// Item phase: warp tiles, the first static (global warp id), the rest dynamic from tile_ctr.
+// Item phase: warp tiles of `width` items — 32 for large frontiers, fewer when the frontier is
+// smaller than the grid's warps so that more warps share a small round (shorter critical path).
+// The first tile of each warp is static (global warp id); when there are more tiles than warps
+// the rest are fetched dynamically from tile_ctr (no atomics otherwise).
 template <int OP, bool DIST>
 __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t ntiles = (rb.nin + 31) >> 5;
+  uint32_t width = 32;
+  while (width > 1 && (uint64_t)(width >> 1) * nwarps >= rb.nin) width >>= 1;
+  const uint32_t ntiles = (rb.nin + width - 1) / width;
   uint32_t t = gw;
   while (t < ntiles) {
-    expand_warp_tile<OP, DIST>(sm, q, p, rb, t << 5);
+    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width);
+    if (ntiles <= nwarps) break;
     uint32_t nt = 0;
     if (lane_id() == 0) nt = nwarps + atomicAdd(rb.tile_ctr, 1u);
     t = __shfl_sync(FULL, nt, 0);
@@ -343,8 +387,18 @@ template <int OP, bool DIST>
 __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, uint32_t nch) {
   nch = min(nch, rb.chunk_cap);
   for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    const ChunkDesc dsc = rb.chunks[c];
-    const int32_t s = (OP != IRGL_OP_BFS) ? ld_label(p.lab + dsc.v) : 0;
+    // descriptors are rewritten every round: L2-coherent load (grid.sync() does not invalidate
+    // L1, so a plain load could return a previous round's descriptor in the persistent kernel)
+    ChunkDesc dsc;
+    {
+      uint32_t a0, a1, a2, a3;
+      asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(rb.chunks + c));
+      dsc.beg = (int64_t)(((uint64_t)a1 << 32) | a0);
+      dsc.v = a2;
+      dsc.len = a3;
+    }
+    const int32_t s = (OP != IRGL_OP_BFS) ? ld_label_cg(p.lab + dsc.v) : 0;
     process_range<OP, DIST, kBlock>(sm, q, p, rb, dsc.beg, dsc.beg + dsc.len, s, threadIdx.x);
   }
 }
@@ -364,7 +418,7 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
     uint32_t v = 0;
     if (i < nfar) {
       v = ld_item(far_in + i);
-      const int32_t dv = ld_label(p.lab + v);
+      const int32_t dv = ld_label_cg(p.lab + v);
       if (dv >= t_old) {
         const int k = dv < rb.threshold ? 1 : 2;
         const int32_t code = (rb.stamp_id << 1) | (k - 1);
@@ -427,6 +481,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
   int32_t threshold = nf ? a.delta : kInf;
   int32_t sid = a.stamp0;       // unique stamp ids: rounds and splits
   uint32_t fsel = 0;            // which far buffer is current
+  uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   for (uint32_t r = 0;; ++r) {
     uint32_t* cin = cnt + slot3(a, r);
@@ -471,9 +526,13 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
         for (;;) {
           const int32_t t_old = threshold;
           if (advance) threshold += a.delta;
+          // slot nsplit&1 was last read after split nsplit-2, i.e. before the barrier every CTA
+          // passed on its way here: safe to reset (the other slot may still be being read)
+          unsigned int* mk = &p.ctl->minkeep[nsplit & 1];
+          ++nsplit;
           if (leader) {
             p.ctl->far_cnt[fsel ^ 1] = 0;
-            p.ctl->minkeep = 0xffffffffu;
+            *mk = 0xffffffffu;
           }
           grid.sync();
           RoundBufs sb = rb;
@@ -481,7 +540,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
           sb.far_cnt = &p.ctl->far_cnt[fsel ^ 1];
           sb.threshold = threshold;
           sb.stamp_id = sid++;
-          far_split(sm, q, p, sb, rb.far, nfar, t_old, &p.ctl->minkeep);
+          far_split(sm, q, p, sb, rb.far, nfar, t_old, mk);
           wflush_all(sm, q, p, sb);
           grid.sync();
           fsel ^= 1;
@@ -490,7 +549,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
           nout = ld_ctl(cout);
           nfar = ld_ctl(rb.far_cnt);
           if (nout > 0 || nfar == 0) break;
-          threshold = (int32_t)ld_ctl(&p.ctl->minkeep);  // next pass moves at least the minimum
+          threshold = (int32_t)ld_ctl(mk);  // next pass moves at least the minimum
           advance = true;
         }
       }

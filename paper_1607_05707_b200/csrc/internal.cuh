@@ -43,10 +43,10 @@ struct Ctl {
   unsigned long long tc_count; // TC: Sum reduction (extension)
   uint32_t tile_ctr[3];        // dynamic warp-tile counters, rotated by round
   uint32_t far_cnt[2];         // SSSP near-far pile counters (double-buffered)
-  uint32_t minkeep;            // min dist kept in the far pile by the last split
+  uint32_t minkeep[2];         // min dist kept in the far pile by a split (double-buffered: the
+                               // persistent kernel resets one slot while CTAs may still read the other)
   uint32_t stamp_used;         // persistent: stamp ids consumed (rounds + splits)
   uint32_t far_sel;            // persistent: current far pile at exit
-  uint32_t pad2;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -70,6 +70,13 @@ __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p) {
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
   int32_t r;
   asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+// L2-coherent read (never an L1 line that predates a grid barrier): used where a stale value is
+// NOT benign — the popped vertex's own distance and the near-far split's drop test.
+__device__ __forceinline__ int32_t ld_label_cg(const int32_t* p) {
+  int32_t r;
+  asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 // Label/distance gathers: coherent global loads.  A stale (larger / INF) value is benign for

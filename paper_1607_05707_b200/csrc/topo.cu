@@ -103,6 +103,14 @@ struct PrSmem {
   int64_t b, e;
 };
 
+// contrib / rank arrays are rewritten every sweep; in the persistent kernel a plain load could hit
+// an L1 line from two sweeps ago (grid.sync() does not invalidate L1): read them through L2.
+__device__ __forceinline__ double ld_cg_f64(const double* p) {
+  double r;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
@@ -140,7 +148,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       }
       __syncthreads();
       double s = 0.0;
-      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += contrib[ld_stream(g.col + k)];
+      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += ld_cg_f64(contrib + ld_stream(g.col + k));
       s = warp_sum(s);
       if (lane == 0) sm.red[warp] = s;
       __syncthreads();
@@ -159,7 +167,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       wm &= wm - 1;
       const int64_t b = __shfl_sync(FULL, beg, leader), e = __shfl_sync(FULL, end, leader);
       double s = 0.0;
-      for (int64_t k = b + lane; k < e; k += 32) s += contrib[ld_stream(g.col + k)];
+      for (int64_t k = b + lane; k < e; k += 32) s += ld_cg_f64(contrib + ld_stream(g.col + k));
       s = warp_sum(s);
       if (lane == leader) {
         mysum = s;
@@ -169,7 +177,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
     // thread level
     if (deg > 0) {
       double s = 0.0;
-      for (int64_t k = beg; k < end; ++k) s += contrib[ld_stream(g.col + k)];
+      for (int64_t k = beg; k < end; ++k) s += ld_cg_f64(contrib + ld_stream(g.col + k));
       mysum = s;
     }
     bool changed = false;
@@ -178,7 +186,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       const double r = base + d * mysum;
       rank_new[v] = r;
       contrib_next[v] = deg0 > 0 ? r / (double)deg0 : 0.0;
-      changed = fabs(r - rank_old[v]) > tol;
+      changed = fabs(r - ld_cg_f64(rank_old + v)) > tol;
     }
     reduce_and_return(valid, changed, red, cell);
   }

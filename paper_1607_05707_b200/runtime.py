@@ -365,6 +365,21 @@ class Context:
                                          C.byref(o), C.byref(st)))
         return Stats(**st.as_dict())
 
+    def run_pipe(self, pipe, body, once=False, max_rounds=None):
+        """Pipe [Once] { body }: `body(ctx, pipe)` issues the
+        Invokes/Iterates of the pipe, which all share the pipe context.  A looping Pipe repeats
+        the body while `in` is non-empty at the start of the body; `Pipe Once` runs it once.
+        Returns the number of body executions."""
+        n = 0
+        while True:
+            if not once and pipe.size() == 0:
+                break
+            body(self, pipe)
+            n += 1
+            if once or (max_rounds is not None and n >= max_rounds):
+                break
+        return n
+
     def read_result(self, op, graph=None, size=None):
         if op == TC:
             out = np.zeros(1, dtype=np.uint64)

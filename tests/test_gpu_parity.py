@@ -249,3 +249,27 @@ def test_partitioned_generated_graph(irgl, oracle):
         s = int(og.sources(1)[0])
         lv, _ = irgl.bfs(c, g, s)
         np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
+
+
+# ---------------------------------------------------------------------------------------------
+# NCCL transport on one GPU: a 1-rank communicator hosting P logical partitions exchanges
+# through ncclAllGather + grouped ncclSend/ncclRecv (self send/recv), the same code path the
+# 8-GPU run takes with one partition per rank.
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_nccl_transport_single_rank(irgl, oracle, P):
+    og = oracle.rmat(12)
+    uid = irgl.nccl_unique_id()
+    with irgl.Context(nccl=(0, 0, 1, uid), logical_partitions=P) as c:
+        g = c.generate_rmat(12)
+        assert g.m == og.m and g.info.partitions == P
+        rp, col, w = g.download()
+        np.testing.assert_array_equal(rp, og.row_ptr)
+        for s in og.sources(2):
+            s = int(s)
+            lv, st = irgl.bfs(c, g, s)
+            np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
+            for delta in (0, 8):
+                d, st = irgl.sssp(c, g, s, delta=delta)
+                np.testing.assert_array_equal(d, oracle.sssp(og, s))
+            if P > 1:
+                assert st.exchange_bytes > 0

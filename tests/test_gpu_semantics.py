@@ -154,3 +154,24 @@ def test_invoke_level_by_level_bfs_matches_iterate(ctx, irgl, oracle):
         ctx.invoke(irgl.BFS, g, p, round_start=LEVEL)
         LEVEL += 1
     np.testing.assert_array_equal(ctx.read_result(irgl.BFS, g), oracle.bfs(og, s)[0])
+
+
+def test_looping_pipe_and_pipe_once(ctx, irgl):
+    """Listing-3/4 shapes: a looping Pipe repeats its body while `in` is non-empty; Pipe Once
+    runs it once; Invokes inside share the pipe context."""
+    p = ctx.pipe(64)
+    p.init_scalars([0, 1])
+    seen = []
+
+    def body(c, pp):
+        seen.append(sorted(pp.read().tolist()))
+        c.invoke(irgl.TEST_COUNTDOWN, None, pp, guard=4)   # A: pushes x+1 while x+1 < 4
+        c.invoke(irgl.TEST_COUNTDOWN, None, pp, guard=4)   # B consumes A's worklist
+
+    n = ctx.run_pipe(p, body)
+    # [0,1] -A-> [1,2] -B-> [2,3];  [2,3] -A-> [3] -B-> []
+    assert n == 2 and seen == [[0, 1], [2, 3]]
+    q = ctx.pipe(8)
+    q.init_scalars([5])
+    assert ctx.run_pipe(q, lambda c, pp: c.invoke(irgl.TEST_NOPUSH, None, pp), once=True) == 1
+    assert q.size() == 0

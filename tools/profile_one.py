@@ -14,6 +14,7 @@ op = {"sssp": irgl.SSSP, "bfs": irgl.BFS, "cc_lp": irgl.CC_LP}[sys.argv[1] if le
 scale = int(sys.argv[2]) if len(sys.argv) > 2 else 22
 outline = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+delta = int(sys.argv[5]) if len(sys.argv) > 5 else -1
 ctx = irgl.Context(outline=outline)
 g = ctx.generate_rmat(scale)
 rp = np.zeros(g.n + 1, dtype=np.int64)
@@ -22,5 +23,5 @@ src = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=1)[0]
 p = ctx.pipe(g.n)
 for _ in range(reps):
     p.init_scalars([src])
-    st = ctx.iterate(op, g, p)
+    st = ctx.iterate(op, g, p, delta=delta)
 print("src", src, st)
