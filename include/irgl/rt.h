@@ -87,8 +87,8 @@ typedef struct irgl_config {
   int32_t blocks_per_sm;         /* FixedFromSM multiplier; 0 = occupancy    */
   int32_t retry_serialize_after; /* Retry conflict management; 0 -> 4          */
   int32_t warp_threshold;        /* degree >= -> warp-cooperative expansion; 0 -> 32            */
-  int32_t cta_threshold;         /* degree >= -> CTA chunk list (grid edge-balanced); 0 -> 1024 */
-  int32_t chunk_edges;           /* edges per CTA chunk; 0 -> 2048                              */
+  int32_t cta_threshold;         /* degree >= -> CTA chunk list (grid edge-balanced); 0 -> 512  */
+  int32_t chunk_edges;           /* edges per CTA chunk; 0 -> 1024                              */
   int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
   int32_t reserved[8];

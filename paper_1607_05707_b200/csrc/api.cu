@@ -125,8 +125,8 @@ static irgl_status_t fail(irgl_ctx* ctx, irgl_status_t st, const char* rule, con
 static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   ExpandCfg ec;
   ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 32;
-  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 1024;
-  ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 2048;
+  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 512;        // RMAT-22 sweep
+  ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 1024;
   if (ec.warp_t < 1) ec.warp_t = 1;
   if (ec.cta_t < ec.warp_t) ec.cta_t = ec.warp_t;
   return ec;
@@ -434,7 +434,10 @@ struct NearFar {
 
 static int32_t default_delta(const irgl_graph* g) {
   (void)g;
-  return 8;  // bucket width for [1,255] weights; tuned on RMAT-22
+  // plain data-driven Bellman-Ford (the IrGL form) is the default: on RMAT-22 it beat near-far
+  // at every bucket width measured (profiles/r1_tune_*.txt), the extra rounds costing more than the
+  // re-relaxation they save
+  return 0;
 }
 
 static irgl_status_t ensure_far(irgl_ctx* ctx, irgl_graph* g) {

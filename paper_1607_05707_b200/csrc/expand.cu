@@ -33,7 +33,7 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int kWBuf = 256;  // per-warp push staging entries
 #ifndef IRGL_MINB
-#define IRGL_MINB 4  // min co-resident CTAs per SM requested from ptxas (register budget)
+#define IRGL_MINB 6  // min co-resident CTAs per SM requested from ptxas: 40 registers, 48 warps/SM (tools/sweep.py)
 #endif
 
 struct Smem {
@@ -227,30 +227,57 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
     const int k = act ? relax_with<OP>(p, rb, cur, sv, wt, dst) : 0;
     wpush<DIST>(sm, q, p, rb, k, dst);
   }
+  // aligned body: two int4 groups per lane per iteration -> 8 independent label gathers in
+  // flight per lane (memory-level parallelism for the latency-bound gathers)
   const int64_t q1 = a1 >> 2;
-  for (int64_t q0 = a0 >> 2; q0 < q1; q0 += G) {
-    const int64_t qi = q0 + gl;
+  for (int64_t q0 = a0 >> 2; q0 < q1; q0 += 2 * G) {
     // a warp whose 32 lanes are all past the end skips the body (stays warp-uniform)
     if (G > 32 && q0 + (gl & ~31) >= q1) break;
-    const bool act = qi < q1;
-    int4 c4 = make_int4(0, 0, 0, 0), w4 = make_int4(0, 0, 0, 0);
-    int32_t l0 = 0, l1 = 0, l2 = 0, l3 = 0;
-    if (act) {
-      c4 = ld_stream_v4(col + 4 * qi);
-      if (OP == IRGL_OP_SSSP) w4 = ld_stream_v4(w + 4 * qi);
-      l0 = ld_label(p.lab + c4.x);
-      l1 = ld_label(p.lab + c4.y);
-      l2 = ld_label(p.lab + c4.z);
-      l3 = ld_label(p.lab + c4.w);
+    const int64_t qa = q0 + gl, qb = q0 + G + gl;
+    const bool aa = qa < q1, ab = qb < q1;
+    int4 ca = make_int4(0, 0, 0, 0), wa = make_int4(0, 0, 0, 0);
+    int4 cb = make_int4(0, 0, 0, 0), wb = make_int4(0, 0, 0, 0);
+    if (aa) {
+      ca = ld_stream_v4(col + 4 * qa);
+      if (OP == IRGL_OP_SSSP) wa = ld_stream_v4(w + 4 * qa);
     }
-    const int k0 = act ? relax_with<OP>(p, rb, l0, sv, w4.x, (uint32_t)c4.x) : 0;
-    const int k1 = act ? relax_with<OP>(p, rb, l1, sv, w4.y, (uint32_t)c4.y) : 0;
-    const int k2 = act ? relax_with<OP>(p, rb, l2, sv, w4.z, (uint32_t)c4.z) : 0;
-    const int k3 = act ? relax_with<OP>(p, rb, l3, sv, w4.w, (uint32_t)c4.w) : 0;
-    wpush<DIST>(sm, q, p, rb, k0, (uint32_t)c4.x);
-    wpush<DIST>(sm, q, p, rb, k1, (uint32_t)c4.y);
-    wpush<DIST>(sm, q, p, rb, k2, (uint32_t)c4.z);
-    wpush<DIST>(sm, q, p, rb, k3, (uint32_t)c4.w);
+    if (ab) {
+      cb = ld_stream_v4(col + 4 * qb);
+      if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(w + 4 * qb);
+    }
+    int32_t la0 = 0, la1 = 0, la2 = 0, la3 = 0, lb0 = 0, lb1 = 0, lb2 = 0, lb3 = 0;
+    if (aa) {
+      la0 = ld_label(p.lab + ca.x);
+      la1 = ld_label(p.lab + ca.y);
+      la2 = ld_label(p.lab + ca.z);
+      la3 = ld_label(p.lab + ca.w);
+    }
+    if (ab) {
+      lb0 = ld_label(p.lab + cb.x);
+      lb1 = ld_label(p.lab + cb.y);
+      lb2 = ld_label(p.lab + cb.z);
+      lb3 = ld_label(p.lab + cb.w);
+    }
+    {
+      const int k0 = aa ? relax_with<OP>(p, rb, la0, sv, wa.x, (uint32_t)ca.x) : 0;
+      const int k1 = aa ? relax_with<OP>(p, rb, la1, sv, wa.y, (uint32_t)ca.y) : 0;
+      const int k2 = aa ? relax_with<OP>(p, rb, la2, sv, wa.z, (uint32_t)ca.z) : 0;
+      const int k3 = aa ? relax_with<OP>(p, rb, la3, sv, wa.w, (uint32_t)ca.w) : 0;
+      wpush<DIST>(sm, q, p, rb, k0, (uint32_t)ca.x);
+      wpush<DIST>(sm, q, p, rb, k1, (uint32_t)ca.y);
+      wpush<DIST>(sm, q, p, rb, k2, (uint32_t)ca.z);
+      wpush<DIST>(sm, q, p, rb, k3, (uint32_t)ca.w);
+    }
+    if (__any_sync(FULL, ab)) {
+      const int k0 = ab ? relax_with<OP>(p, rb, lb0, sv, wb.x, (uint32_t)cb.x) : 0;
+      const int k1 = ab ? relax_with<OP>(p, rb, lb1, sv, wb.y, (uint32_t)cb.y) : 0;
+      const int k2 = ab ? relax_with<OP>(p, rb, lb2, sv, wb.z, (uint32_t)cb.z) : 0;
+      const int k3 = ab ? relax_with<OP>(p, rb, lb3, sv, wb.w, (uint32_t)cb.w) : 0;
+      wpush<DIST>(sm, q, p, rb, k0, (uint32_t)cb.x);
+      wpush<DIST>(sm, q, p, rb, k1, (uint32_t)cb.y);
+      wpush<DIST>(sm, q, p, rb, k2, (uint32_t)cb.z);
+      wpush<DIST>(sm, q, p, rb, k3, (uint32_t)cb.w);
+    }
   }
 }
 
@@ -483,6 +510,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
   uint32_t fsel = 0;            // which far buffer is current
   uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));  // round r's in-count = round r-1's out-count
   for (uint32_t r = 0;; ++r) {
     uint32_t* cin = cnt + slot3(a, r);
     uint32_t* cout = cnt + slot3(a, r + 1);
@@ -493,7 +521,8 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     }
     RoundBufs rb;
     rb.in = (r & 1) ? a.buf_b : a.buf_a;
-    rb.nin = ld_ctl(cin);
+    rb.nin = nin_next;
+    (void)cin;
     rb.out = (r & 1) ? a.buf_a : a.buf_b;
     rb.out_cnt = cout;
     rb.cap = a.cap;
@@ -510,13 +539,15 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     item_phase<OP, false>(sm, q, p, rb);
     wflush_all(sm, q, p, rb);
     grid.sync();  // SyncRunningThreads
+    // both counters in flight together (one L2 round trip on the round's critical path)
     const uint32_t nch = ld_ctl(rb.chunk_cnt);
+    uint32_t nout = ld_ctl(cout);
     if (nch) {
       chunk_phase<OP, false>(sm, q, p, rb, nch);
       wflush_all(sm, q, p, rb);
       grid.sync();
+      nout = ld_ctl(cout);
     }
-    uint32_t nout = ld_ctl(cout);
     if (nf) {
       // near frontier exhausted: advance the threshold and split the far pile; a pile past half
       // its capacity is compacted (split at the unchanged threshold) even when near is not empty
@@ -558,6 +589,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
       p.ctl->popped += rb.nin;
       p.ctl->pushes += nout;
     }
+    nin_next = nout;
     // Iterate termination: in empty (next round) [Or rounds >= max_rounds]
     if (nout == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds)) {
       if (leader) {

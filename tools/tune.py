@@ -22,7 +22,7 @@ for cfg in CFGS:
     for outline in (1, 0):
         t, k, e, r = run(ctx, g, srcs, irgl.BFS, outline=outline)
         print(f"{cfg} BFS outline={outline}: {t:.3f} ms (kernel {k:.3f}) GTEPS={E/2/t/1e6:.1f} rounds={r}", flush=True)
-        for delta in ([0, 4, 8, 16, 32] if cfg == {} else [8]):
+        for delta in ([0, 2, 4, 8, 16, 32, 64] if cfg == {} else [8]):
             t, k, e, r = run(ctx, g, srcs, irgl.SSSP, outline=outline, delta=delta)
             print(f"{cfg} SSSP outline={outline} delta={delta}: {t:.3f} ms (kernel {k:.3f}) GTEPS={E/2/t/1e6:.1f} scans/E={e/E:.2f} rounds={r}", flush=True)
     ctx.close()
