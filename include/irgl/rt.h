@@ -74,7 +74,8 @@ typedef enum {
   IRGL_OP_TEST_REDUCE = 102,    /* ReduceAndReturn(values[x]) */
   IRGL_OP_TEST_NOPUSH = 103,    /* pops, never pushes */
   IRGL_OP_TEST_PUSHPOP = 104,   /* records popped_at[x]=launch; push x+guard */
-  IRGL_OP_TEST_FORALL_MAP = 105 /* records thread_of[x] = global thread id */
+  IRGL_OP_TEST_FORALL_MAP = 105, /* records thread_of[x] = global thread id */
+  IRGL_OP_TEST_RESPAWN_ODD = 106  /* as RETRY_ODD with Respawn: never serialised */
 } irgl_op;
 
 typedef struct irgl_ctx irgl_ctx;
@@ -179,6 +180,11 @@ irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const i
                                     const int32_t* col, const int32_t* weight /*nullable*/,
                                     irgl_graph** out);
 irgl_status_t irgl_graph_generate(irgl_ctx* ctx, const irgl_gen_spec* spec, irgl_graph** out);
+/* Text edge list: first line "N M", then M lines "u v [w]" (0-based ids, '#' and
+ * blank lines ignored).  symmetrise=1 adds reverse edges; self loops dropped, duplicates merged
+ * (minimum weight); missing weights = 1.  The CSR is built on the device (sort + unique). */
+irgl_status_t irgl_graph_read_edgelist(irgl_ctx* ctx, const char* path, int symmetrise,
+                                       irgl_graph** out);
 irgl_status_t irgl_graph_info_get(const irgl_graph* g, irgl_graph_info* info);
 /* Copies the CSR of the local partitions back (single-process: the whole graph). */
 irgl_status_t irgl_graph_download(irgl_graph* g, int64_t* row_ptr, int32_t* col, int32_t* weight);

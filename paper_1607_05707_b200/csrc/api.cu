@@ -135,7 +135,7 @@ static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
 static bool is_wl_graph_op(int op) {
   return op == IRGL_OP_BFS || op == IRGL_OP_SSSP || op == IRGL_OP_CC_LP;
 }
-static bool is_test_op(int op) { return op >= IRGL_OP_TEST_COUNTDOWN && op <= IRGL_OP_TEST_FORALL_MAP; }
+static bool is_test_op(int op) { return op >= IRGL_OP_TEST_COUNTDOWN && op <= IRGL_OP_TEST_RESPAWN_ODD; }
 static bool is_known_op(int op) {
   return (op >= IRGL_OP_BFS && op <= IRGL_OP_CC_LP) || is_test_op(op);
 }
@@ -761,7 +761,7 @@ static irgl_status_t test_invoke(irgl_ctx* ctx, irgl_pipe* pipe, int op, const i
     ta.reduction = red;
     ta.overflow = &ctx->test_ctl->overflow;
     // Retry beyond retry_serialize_after rounds: serial execution
-    const bool serial = retry_rounds > rsa;
+    const bool serial = op != IRGL_OP_TEST_RESPAWN_ODD && retry_rounds > rsa;  // Respawn: never
     int threads = a && a->threads > 0 ? a->threads : 148 * 256;
     if (serial) {
       threads = 1;
@@ -1173,6 +1173,65 @@ irgl_status_t irgl_graph_generate(irgl_ctx* ctx, const irgl_gen_spec* spec, irgl
   if (s != IRGL_OK) return s;
   *out = g.release();
   return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_read_edgelist(irgl_ctx* ctx, const char* path, int symmetrise,
+                                       irgl_graph** out) {
+  if (!ctx || !path || !out) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "irgl_graph_read_edgelist: bad arguments");
+  FILE* f = std::fopen(path, "r");
+  if (!f) return fail(ctx, IRGL_E_INVALID, "E_INVALID", std::string("cannot open ") + path);
+  char line[512];
+  int64_t n = -1, m = -1, lineno = 0;
+  std::vector<EdgeRec> edges;
+  while (std::fgets(line, sizeof(line), f)) {
+    ++lineno;
+    const char* s = line;
+    while (*s == ' ' || *s == '\t') ++s;
+    if (*s == '#' || *s == '\n' || *s == '\r' || *s == 0) continue;
+    long long a = 0, b = 0, c = 1;
+    const int k = std::sscanf(s, "%lld %lld %lld", &a, &b, &c);
+    if (n < 0) {
+      if (k < 2 || a < 1 || b < 0) {
+        std::fclose(f);
+        return fail(ctx, IRGL_E_INVALID, "E_INVALID", "edge list header must be 'N M'");
+      }
+      n = a;
+      m = b;
+      edges.reserve((size_t)m * (symmetrise ? 2 : 1));
+      continue;
+    }
+    if (k < 2 || a < 0 || b < 0 || a >= n || b >= n) {
+      std::fclose(f);
+      return fail(ctx, IRGL_E_INVALID, "E_INVALID",
+                  "bad edge at line " + std::to_string(lineno) + " (ids must be in [0, N))");
+    }
+    if (a == b) continue;
+    edges.push_back({(uint32_t)a, (uint32_t)b, (int32_t)c});
+    if (symmetrise) edges.push_back({(uint32_t)b, (uint32_t)a, (int32_t)c});
+  }
+  std::fclose(f);
+  if (n < 0) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "empty edge list");
+  if (n > 0x7fffffffll) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "n must fit int32 vertex ids");
+  int64_t* rp = nullptr;
+  int32_t* col = nullptr;
+  int32_t* w = nullptr;
+  int64_t mm = 0;
+  PartRT& pr = ctx->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  cudaError_t e = csr_from_edges_device(edges.data(), (int64_t)edges.size(), n, &rp, &col, &w, &mm, pr.st);
+  if (e != cudaSuccess) return cuda_status(ctx, e, "csr_from_edges_device");
+  std::vector<int64_t> hrp(n + 1);
+  std::vector<int32_t> hcol(mm), hw(mm);
+  CK(cudaMemcpy(hrp.data(), rp, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  if (mm) {
+    CK(cudaMemcpy(hcol.data(), col, mm * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hw.data(), w, mm * 4, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(rp);
+  cudaFree(col);
+  cudaFree(w);
+  // one code path for partitioning / validation: the CSR entry point
+  return irgl_graph_create_csr(ctx, n, mm, hrp.data(), hcol.data(), hw.data(), out);
 }
 
 irgl_status_t irgl_graph_info_get(const irgl_graph* g, irgl_graph_info* info) {

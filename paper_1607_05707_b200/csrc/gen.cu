@@ -214,7 +214,90 @@ int bits_for(int64_t x) {
     }                                    \
   } while (0)
 
+__global__ void edge_keys_kernel(const EdgeRec* e, int64_t ne, uint64_t* keys, int32_t* w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = ((uint64_t)e[i].u << 32) | e[i].v;
+    w[i] = e[i].w;
+  }
+}
+__global__ void split_keys_kernel(const uint64_t* keys, int64_t m, int32_t* col) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    col[i] = (int32_t)(keys[i] & 0xffffffffull);
+}
+struct MinOp {
+  __device__ __forceinline__ int32_t operator()(int32_t a, int32_t b) const { return a < b ? a : b; }
+};
 }  // namespace
+
+cudaError_t csr_from_edges_device(const EdgeRec* host_edges, int64_t ne, int64_t n,
+                                  int64_t** row_ptr, int32_t** col, int32_t** w, int64_t* m_out,
+                                  cudaStream_t st) {
+  std::string* err = nullptr;
+  EdgeRec* de = nullptr;
+  uint64_t *ka = nullptr, *kb = nullptr;
+  int32_t *wa = nullptr, *wb = nullptr;
+  const int64_t cap = ne > 0 ? ne : 1;
+  GEN_CK(cudaMallocAsync(&de, cap * sizeof(EdgeRec), st));
+  GEN_CK(cudaMallocAsync(&ka, cap * 8, st));
+  GEN_CK(cudaMallocAsync(&kb, cap * 8, st));
+  GEN_CK(cudaMallocAsync(&wa, cap * 4, st));
+  GEN_CK(cudaMallocAsync(&wb, cap * 4, st));
+  if (ne) GEN_CK(cudaMemcpyAsync(de, host_edges, ne * sizeof(EdgeRec), cudaMemcpyHostToDevice, st));
+  const int grid = (int)std::min<int64_t>((cap + 255) / 256, 148 * 16);
+  if (ne) {
+    note_launch();
+    edge_keys_kernel<<<grid, 256, 0, st>>>(de, ne, ka, wa);
+  }
+  cub::DoubleBuffer<uint64_t> dk(ka, kb);
+  cub::DoubleBuffer<int32_t> dv(wa, wb);
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  int64_t* nrun = nullptr;
+  GEN_CK(cudaMallocAsync(&nrun, 8, st));
+  GEN_CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, dk, dv, ne, 0, 64, st));
+  GEN_CK(cub::DeviceReduce::ReduceByKey(nullptr, t2, ka, kb, wa, wb, nrun, MinOp(), ne, st));
+  int64_t* deg = nullptr;
+  int64_t* rp = nullptr;
+  GEN_CK(cudaMallocAsync(&deg, (n + 1) * 8, st));
+  GEN_CK(cudaMallocAsync(&rp, (n + 1) * 8, st));
+  GEN_CK(cudaMemsetAsync(deg, 0, (n + 1) * 8, st));
+  GEN_CK(cub::DeviceScan::ExclusiveSum(nullptr, t3, deg, rp, n + 1, st));
+  size_t tmp = std::max(t1, std::max(t2, t3));
+  void* t = nullptr;
+  GEN_CK(cudaMallocAsync(&t, tmp > 0 ? tmp : 1, st));
+  GEN_CK(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, ne, 0, 64, st));
+  uint64_t* uk = dk.Alternate();
+  int32_t* uw = dv.Alternate();
+  GEN_CK(cub::DeviceReduce::ReduceByKey(t, tmp, dk.Current(), uk, dv.Current(), uw, nrun, MinOp(), ne, st));
+  int64_t m = 0;
+  GEN_CK(cudaMemcpyAsync(&m, nrun, 8, cudaMemcpyDeviceToHost, st));
+  GEN_CK(cudaStreamSynchronize(st));
+  if (ne == 0) m = 0;
+  const int fgrid = (int)std::min<int64_t>((m + 255) / 256, 148 * 32);
+  if (m > 0) {
+    note_launch();
+    row_count_kernel<<<fgrid, 256, 0, st>>>(uk, m, 32, deg);
+  }
+  GEN_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg, rp, n + 1, st));
+  int32_t* dc = nullptr;
+  int32_t* dw = nullptr;
+  GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * 4, st));
+  GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * 4, st));
+  if (m > 0) {
+    note_launch();
+    split_keys_kernel<<<fgrid, 256, 0, st>>>(uk, m, dc);
+    GEN_CK(cudaMemcpyAsync(dw, uw, m * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  GEN_CK(cudaStreamSynchronize(st));
+  for (void* p : {(void*)de, (void*)ka, (void*)kb, (void*)wa, (void*)wb, (void*)nrun, (void*)deg, t})
+    cudaFree(p);
+  *row_ptr = rp;
+  *col = dc;
+  *w = dw;
+  *m_out = m;
+  return cudaGetLastError();
+}
 
 cudaError_t max_degree(const int64_t* row_ptr, int64_t nrows, int64_t* out, cudaStream_t st) {
   unsigned long long* d = nullptr;

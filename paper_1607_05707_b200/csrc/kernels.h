@@ -137,5 +137,13 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
                           int64_t** row_ptr, int32_t** col, int32_t** w, int64_t* m_local,
                           cudaStream_t st, std::string* err);
 cudaError_t max_degree(const int64_t* row_ptr, int64_t nrows, int64_t* out, cudaStream_t st);
+// Directed edge records -> CSR on the device (sort by (u, v), keep the minimum weight per pair).
+struct EdgeRec {
+  uint32_t u, v;
+  int32_t w;
+};
+cudaError_t csr_from_edges_device(const EdgeRec* host_edges, int64_t ne, int64_t n,
+                                  int64_t** row_ptr, int32_t** col, int32_t** w, int64_t* m,
+                                  cudaStream_t st);
 
 }  // namespace irgl

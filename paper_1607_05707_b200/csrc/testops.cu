@@ -47,6 +47,7 @@ __global__ void test_op_kernel(TestArgs a) {
       case IRGL_OP_TEST_COUNTDOWN:
         wl_append((int64_t)x + 1 < a.guard, x + 1, a.out, a.out_cnt, a.cap, a.overflow);
         break;
+      case IRGL_OP_TEST_RESPAWN_ODD:
       case IRGL_OP_TEST_RETRY_ODD: {
         const int64_t g = a.guard > 0 ? a.guard : 1;
         bool retry = false;

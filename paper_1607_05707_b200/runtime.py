@@ -43,6 +43,7 @@ MAP_CONSECUTIVE, MAP_BLOCKED = 0, 1
 BFS, SSSP, CC, PR, TC, CC_LP = 0, 1, 2, 3, 4, 5
 TEST_COUNTDOWN, TEST_RETRY_ODD, TEST_REDUCE, TEST_NOPUSH, TEST_PUSHPOP, TEST_FORALL_MAP = (
     100, 101, 102, 103, 104, 105)
+TEST_RESPAWN_ODD = 106
 GEN_RMAT, GEN_GRID = 0, 1
 BLOCK_ELASTIC, BLOCK_SHRINKABLE, BLOCK_FIXED = 0, 1, 2
 
@@ -107,7 +108,7 @@ class BlockConstraint(C.Structure):
 EXPORTS = [
     "irgl_ctx_create", "irgl_nccl_unique_id", "irgl_ctx_create_nccl", "irgl_ctx_destroy",
     "irgl_ctx_sync", "irgl_last_error", "irgl_abi_version", "irgl_graph_create_csr",
-    "irgl_graph_generate", "irgl_graph_info_get", "irgl_graph_download", "irgl_graph_destroy",
+    "irgl_graph_generate", "irgl_graph_read_edgelist", "irgl_graph_info_get", "irgl_graph_download", "irgl_graph_destroy",
     "irgl_pipe_create", "irgl_pipe_init_scalars", "irgl_pipe_init_from_array",
     "irgl_pipe_init_range", "irgl_pipe_size", "irgl_pipe_read", "irgl_pipe_destroy",
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
@@ -141,6 +142,7 @@ def load_library(path: str | None = None):
         "irgl_abi_version": ([], C.c_int),
         "irgl_graph_create_csr": ([P, i64, i64, i64p, i32p, i32p, pp], i32),
         "irgl_graph_generate": ([P, C.POINTER(GenSpec), pp], i32),
+        "irgl_graph_read_edgelist": ([P, C.c_char_p, C.c_int, pp], i32),
         "irgl_graph_info_get": ([P, C.POINTER(GraphInfo)], i32),
         "irgl_graph_download": ([P, i64p, i32p, i32p], i32),
         "irgl_graph_destroy": ([P], i32),
@@ -322,6 +324,13 @@ class Context:
         s.perc_keep_ppm = int(round(perc_keep * 1e6))
         s.perc_seed, s.wseed = perc_seed, wseed
         return self._generate(s)
+
+    def read_edgelist(self, path, symmetrise=True) -> "Graph":
+        """Text edge list: 'N M' then 'u v [w]' lines; CSR built on the device."""
+        h = C.c_void_p()
+        self._chk(self._lib.irgl_graph_read_edgelist(self._h, str(path).encode(), int(symmetrise),
+                                                     C.byref(h)))
+        return Graph(self, h)
 
     def _generate(self, spec) -> "Graph":
         h = C.c_void_p()

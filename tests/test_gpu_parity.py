@@ -273,3 +273,35 @@ def test_nccl_transport_single_rank(irgl, oracle, P):
                 np.testing.assert_array_equal(d, oracle.sssp(og, s))
             if P > 1:
                 assert st.exchange_bytes > 0
+
+
+# ---------------------------------------------------------------------------------------------
+# F2 ingestion: text edge list -> device CSR
+def test_edgelist_reader(ctx, irgl, oracle, tmp_path):
+    f = tmp_path / "path5.txt"
+    f.write_text("# SPEC.md:523 path graph\n5 4\n0 1\n1 2\n\n2 3\n3 4\n")
+    g = ctx.read_edgelist(f)
+    lv, st = irgl.bfs(ctx, g, 0)
+    assert lv.tolist() == [0, 1, 2, 3, 4] and st.rounds == 5
+    og = oracle.rmat(10)
+    src = np.repeat(np.arange(og.n), og.degrees())
+    f2 = tmp_path / "rmat10.txt"
+    with open(f2, "w") as fh:
+        fh.write(f"{og.n} {og.m}\n")
+        for a, b, w in zip(src, og.col, og.weight):
+            fh.write(f"{a} {b} {w}\n")
+    g2 = ctx.read_edgelist(f2, symmetrise=False)
+    rp, col, w = g2.download()
+    np.testing.assert_array_equal(rp, og.row_ptr)
+    np.testing.assert_array_equal(col, og.col)
+    np.testing.assert_array_equal(w, og.weight)
+    f3 = tmp_path / "dup.txt"
+    f3.write_text("3 4\n0 1 9\n1 0 4\n0 1 7\n1 1 3\n")  # duplicates -> min weight, self loop dropped
+    g3 = ctx.read_edgelist(f3)
+    rp, col, w = g3.download()
+    assert rp.tolist() == [0, 1, 2, 2] and col.tolist() == [1, 0] and w.tolist() == [4, 4]
+    f4 = tmp_path / "bad.txt"
+    f4.write_text("3 1\n0 7\n")
+    with pytest.raises(irgl.IrglError) as e:
+        ctx.read_edgelist(f4)
+    assert e.value.status == 1

@@ -175,3 +175,15 @@ def test_looping_pipe_and_pipe_once(ctx, irgl):
     q.init_scalars([5])
     assert ctx.run_pipe(q, lambda c, pp: c.invoke(irgl.TEST_NOPUSH, None, pp), once=True) == 1
     assert q.size() == 0
+
+
+def test_respawn_is_never_serialised(irgl):
+    """Respawn pushes to the retry worklist like Retry but never triggers conflict management
+    (SPEC.md:88, :462): same launches, no serial launch."""
+    with irgl.Context(retry_serialize_after=2) as c:
+        p = c.pipe(64)
+        p.init_scalars([1, 3, 5])
+        c.op_reset(irgl.TEST_RESPAWN_ODD)
+        _, st = c.invoke(irgl.TEST_RESPAWN_ODD, None, p, guard=5)
+        assert st.launches == 6 and st.serial_launches == 0
+        assert sorted(p.read().tolist()) == [1, 3, 5]
