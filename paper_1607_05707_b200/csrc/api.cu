@@ -124,7 +124,9 @@ static irgl_status_t fail(irgl_ctx* ctx, irgl_status_t st, const char* rule, con
 
 static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   ExpandCfg ec;
-  ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 32;
+  // degree < warp_t: warp-scan gather (4 windows / lane in flight); < cta_t: one warp per vertex
+  // (int4); >= cta_t: CTA chunks.  Defaults from the RMAT-22 sweep (profiles/r1_sweep.txt).
+  ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 128;
   ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 512;        // RMAT-22 sweep
   ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 1024;
   if (ec.warp_t < 1) ec.warp_t = 1;

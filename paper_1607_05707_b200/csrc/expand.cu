@@ -214,7 +214,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
   const int64_t a0 = min((b + 3) & ~int64_t(3), e);
   const int64_t a1 = max(e & ~int64_t(3), a0);
   const int nh = (int)(a0 - b), nt = (int)(e - a1);
-  if (nh + nt > 0 && (G == 32 || (threadIdx.x >> 5) == 0)) {  // warp-uniform condition
+  if (nh + nt > 0 && (G == 32 || (gl >> 5) == 0)) {  // first warp of the group (warp-uniform)
     const bool act = gl < nh + nt;
     const int64_t ed = gl < nh ? b + gl : a1 + (gl - nh);
     uint32_t dst = 0;
@@ -362,28 +362,42 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   }
   const uint32_t total = __shfl_sync(FULL, incl, 31);
   const int64_t off = beg - (int64_t)(incl - d);  // edge of slot k (owned here) = off + k
-  for (uint32_t wb = 0; wb < total; wb += 32) {
-    const uint32_t k = wb + lane;
-    const bool act = k < total;
-    uint32_t o = 0;
+  // 4 windows of 32 edge slots per iteration: each lane has 4 independent col/label chains in
+  // flight (memory-level parallelism); owner of slot k = #lanes with inclusive prefix <= k
+  constexpr int kWin = 4;
+  for (uint32_t wb = 0; wb < total; wb += 32 * kWin) {
+    uint32_t dst[kWin];
+    int32_t wt[kWin], s[kWin], cur[kWin];
+    bool act[kWin];
 #pragma unroll
-    for (uint32_t s = 16; s > 0; s >>= 1) {
-      const uint32_t t = __shfl_sync(FULL, incl, o + s - 1);
-      if (t <= k) o += s;
+    for (int j = 0; j < kWin; ++j) {
+      const uint32_t k = wb + 32 * j + lane;
+      act[j] = k < total;
+      uint32_t o = 0;
+#pragma unroll
+      for (uint32_t st = 16; st > 0; st >>= 1) {
+        const uint32_t t = __shfl_sync(FULL, incl, o + st - 1);
+        if (t <= k) o += st;
+      }
+      o = min(o, 31u);
+      const int64_t eo = __shfl_sync(FULL, off, o);
+      s[j] = __shfl_sync(FULL, sv, o);
+      dst[j] = 0;
+      wt[j] = 0;
+      if (act[j]) {
+        const int64_t ed = eo + k;
+        dst[j] = (uint32_t)ld_stream(p.g.col + ed);
+        if (OP == IRGL_OP_SSSP) wt[j] = ld_stream(p.g.w + ed);
+      }
     }
-    o = min(o, 31u);
-    const int64_t eo = __shfl_sync(FULL, off, o);
-    const int32_t s = __shfl_sync(FULL, sv, o);
-    uint32_t dst = 0;
-    int32_t wt = 0, cur = 0;
-    if (act) {
-      const int64_t ed = eo + k;
-      dst = (uint32_t)ld_stream(p.g.col + ed);
-      if (OP == IRGL_OP_SSSP) wt = ld_stream(p.g.w + ed);
-      cur = ld_label(p.lab + dst);
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) cur[j] = act[j] ? ld_label(p.lab + dst[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < kWin; ++j) {
+      if (wb + 32 * j >= total) break;  // warp-uniform
+      const int kk = act[j] ? relax_with<OP>(p, rb, cur[j], s[j], wt[j], dst[j]) : 0;
+      wpush<DIST>(sm, q, p, rb, kk, dst[j]);
     }
-    const int kk = act ? relax_with<OP>(p, rb, cur, s, wt, dst) : 0;
-    wpush<DIST>(sm, q, p, rb, kk, dst);
   }
 }
 
@@ -413,9 +427,12 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
 template <int OP, bool DIST>
 __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, uint32_t nch) {
   nch = min(nch, rb.chunk_cap);
-  for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-    // descriptors are rewritten every round: L2-coherent load (grid.sync() does not invalidate
-    // L1, so a plain load could return a previous round's descriptor in the persistent kernel)
+  // two chunks per CTA at a time (128-thread halves) -> twice the independent chains per SM
+  constexpr int kHalf = kBlock / 2;
+  const uint32_t half = threadIdx.x / kHalf;
+  const int gl = threadIdx.x % kHalf;
+  for (uint32_t c = 2 * blockIdx.x + half; c < nch; c += 2 * gridDim.x) {
+    // descriptors are rewritten every round: L2-coherent load
     ChunkDesc dsc;
     {
       uint32_t a0, a1, a2, a3;
@@ -426,7 +443,7 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
       dsc.len = a3;
     }
     const int32_t s = (OP != IRGL_OP_BFS) ? ld_label_cg(p.lab + dsc.v) : 0;
-    process_range<OP, DIST, kBlock>(sm, q, p, rb, dsc.beg, dsc.beg + dsc.len, s, threadIdx.x);
+    process_range<OP, DIST, kHalf>(sm, q, p, rb, dsc.beg, dsc.beg + dsc.len, s, gl);
   }
 }
 

@@ -11,8 +11,10 @@ def run(ctx, g, srcs, op, **kw):
         p.init_scalars([s]); st = ctx.iterate(op, g, p, **kw); t += st.kernel_ms
     return t / len(srcs)
 base = None
-for warp_t in (32, 16):
-    for cta_t, chunk in ((1024, 2048), (512, 1024), (256, 1024), (256, 512), (128, 512), (128, 256), (64, 256)):
+CFG = [(w, c, k) for w in (32, 64, 128, 256) for c, k in ((512, 1024), (1024, 2048), (1024, 1024))]
+for warp_t, cta_t, chunk in CFG:
+    if warp_t > cta_t: continue
+    if True:
         ctx = irgl.Context(warp_threshold=warp_t, cta_threshold=cta_t, chunk_edges=chunk)
         g = ctx.generate_rmat(scale)
         if base is None:
