@@ -220,7 +220,8 @@ def run_reference(args, d):
 
 
 def workload_config(args, g):
-    cfg = {"workload": f"{args.op.upper()} on RMAT-{args.scale} (edge factor 16, weights [1,255]), "
+    cfg = {"workload": f"{args.op.upper()}{'-DO' if args.direction and args.op == 'bfs' else ''} "
+                       f"on RMAT-{args.scale} (edge factor 16, weights [1,255]), "
                        f"one traversal per step over 16 sources",
            "op": args.op, "graph": "rmat", "scale": args.scale, "edge_factor": 16,
            "sources": 16, "partitions": args.gpus, "outline": args.outline,
@@ -262,10 +263,12 @@ def run_irgl(args, d):
         er.append(d.reduce(st.edges, "sum"))
         vr.append(d.reduce(st.popped, "sum"))
 
+    kw = {"direction": 1} if (args.op == "bfs" and args.direction) else {}
+
     def step(i):
         s = cand[i % 16]
         p.init_scalars([s])
-        return ctx.iterate(op_id, g, p)
+        return ctx.iterate(op_id, g, p, **kw)
 
     for i in range(args.warmup):
         step(i)
@@ -281,7 +284,10 @@ def run_irgl(args, d):
         k = (args.warmup + i) % 16
         kms += st.kernel_ms
         tot_e += er[k]
-        tot_b += algorithmic_bytes(args.op, vr[k], er[k])
+        # direction-optimising BFS examines fewer edges than E_r: bytes from the actual counter
+        # (SURVEY §8f F1); otherwise the fixed work-efficient formula of §8d
+        e_bytes = d.reduce(st.edges, "sum") if kw else er[k]
+        tot_b += algorithmic_bytes(args.op, vr[k], e_bytes)
         stats.append(st)
     ctx.event_record(1)
     ctx.sync()
@@ -322,8 +328,9 @@ def run_irgl(args, d):
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
                      "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "persistent_kernel<SSSP> (outlined Iterate)" if args.outline != 0
-                     else "expand_kernel + chunk_kernel",
+                     "kernel": (f"persistent_kernel<{args.op.upper()}> (outlined Iterate)"
+                                if not kw else "persistent_bfs_do_kernel (outlined, direction-optimising)")
+                     if args.outline != 0 else "expand_kernel + chunk_kernel",
                      "algorithmic_bytes_per_step": round(tot_b / args.steps),
                      "kernel_ms_per_step": round(kms / args.steps, 4)},
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": 8,
@@ -377,6 +384,8 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--direction", type=int, default=0,
+                    help="BFS: 1 = direction-optimising (SURVEY §8f F1), 0 = Listing-2 top-down")
     args = ap.parse_args()
     d = Dist()
     if d.world > 1:

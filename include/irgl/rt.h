@@ -107,7 +107,10 @@ typedef struct irgl_op_args {
   int32_t threads;       /* test operators: total CUDA threads (0 = planner's choice)          */
   int32_t delta;         /* SSSP: near-far bucket width; 0 = plain data-driven Bellman-Ford,
                             <0 = runtime default.  Same distances either way.                 */
-  int32_t reserved[5];
+  int32_t direction;     /* BFS: 0 = top-down worklist (Listing 2); 1 = direction-optimising
+                            (bottom-up rounds when the frontier is large; outlined, 1 partition;
+                            SURVEY §8f F1).  Same levels either way.                          */
+  int32_t reserved[4];
 } irgl_op_args;
 
 /* Iterate [While|Until Any|All] kernel(args) [ExtraCond] (ast.hpp:186-204). */

@@ -472,6 +472,7 @@ static RoundBufs round_bufs(irgl_pipe* pipe, GraphPart& gp, PipePart& pp, int32_
   rb.far_cnt = &pp.ctl->far_cnt[nf.fsel];
   rb.far_cap = gp.far_cap;
   rb.threshold = nf.delta > 0 ? nf.threshold : kInf;
+  rb.mf_acc = nullptr;
   return rb;
 }
 
@@ -628,7 +629,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
 // ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
 static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                        int64_t level0, const irgl_iterate_opts& o,
-                                       const NearFar& nf, irgl_iter_stats* stt) {
+                                       const NearFar& nf, int dir_opt, irgl_iter_stats* stt) {
   PartRT& pr = ctx->parts[0];
   GraphPart& gp = g->parts[0];
   PipePart& pp = pipe->parts[0];
@@ -655,12 +656,16 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.far_b = gp.far[1];
   pa.far_cap = gp.far_cap;
   pa.delta = nf.delta;
+  pa.dir_opt = (op == IRGL_OP_BFS && dir_opt) ? 1 : 0;
+  pa.n = g->n;
+  pa.m = g->m;
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
   CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(pp.ctl->tile_ctr), pr.st));
   CK(cudaMemsetAsync(pp.ctl->far_cnt, 0, sizeof(pp.ctl->far_cnt), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
+  CK(cudaMemsetAsync(pp.ctl->mf, 0, sizeof(pp.ctl->mf) + sizeof(pp.ctl->bu_found) + 8, pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
@@ -682,6 +687,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pp.c_spare = slots[(K + 2) % 3];
   pp.n_in = h.cnt[pp.c_in];
   g->stamp_epoch += h.stamp_used;
+  stt->edges += (int64_t)h.bu_scanned;  // pipe_counters adds the top-down scans
   stt->rounds += K;
   stt->launches += 1;
   stt->popped += (int64_t)h.popped;
@@ -1487,7 +1493,11 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
         CK(cudaSetDevice(pr0.dev));
       }
     }
-    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, &st);
+    const int dir_opt = args ? args->direction : 0;
+    if (dir_opt && !(outline && ctx->ptotal() == 1))
+      return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
+                  "direction-optimising BFS runs outlined on one partition");
+    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s != IRGL_OK) return s;
     s = pipe_counters(ctx, pipe, &st);  // edges scanned / remote updates

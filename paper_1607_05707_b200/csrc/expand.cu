@@ -58,6 +58,7 @@ struct WarpQ {
   uint32_t n = 0;   // staged near pushes
   uint32_t nf = 0;  // staged far pushes
   unsigned long long edges = 0;
+  unsigned long long mf = 0;  // DO-BFS: degrees of pushed vertices
 };
 
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
@@ -145,6 +146,13 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
   const uint32_t mn = __ballot_sync(FULL, kind == 1);
   const uint32_t mf = m & ~mn;
   const uint32_t lt = lanemask_lt();
+  if (mn && rb.mf_acc) {  // DO-BFS: edges of the next frontier
+    unsigned long long dg = 0;
+    if (kind == 1) dg = (unsigned long long)(__ldg(p.g.row_ptr + v - p.g.lo + 1) - __ldg(p.g.row_ptr + v - p.g.lo));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dg += __shfl_xor_sync(FULL, dg, o);
+    q.mf += dg;
+  }
   if (mn) {
     if (kind == 1) sm.wbuf[warp][q.n + __popc(mn & lt)] = v;
     q.n += __popc(mn);
@@ -161,6 +169,10 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
 // and one stats atomic per CTA instead of one per warp (E2 at CTA granularity).
 __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  if (q.mf) {
+    if (lane == 0) atomicAdd(rb.mf_acc, q.mf);
+    q.mf = 0;
+  }
   if (lane == 0) {
     sm.fl_cnt[0][warp] = q.n;
     sm.fl_cnt[1][warp] = q.nf;
@@ -553,6 +565,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     rb.far_cnt = &p.ctl->far_cnt[fsel];
     rb.far_cap = a.far_cap;
     rb.threshold = threshold;
+    rb.mf_acc = nullptr;
     item_phase<OP, false>(sm, q, p, rb);
     wflush_all(sm, q, p, rb);
     grid.sync();  // SyncRunningThreads
@@ -614,6 +627,147 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
         p.ctl->stamp_used = (uint32_t)(sid - a.stamp0);
         p.ctl->far_sel = fsel;
+      }
+      break;
+    }
+  }
+}
+
+// ---- F1: direction-optimising BFS (outlined, one partition) -----------------------------------------
+// Bottom-up round at level L: every unvisited vertex scans its neighbours for a parent at level
+// L-1 and stops at the first one (Beamer et al.).  Only the owning thread writes level[v], so a
+// plain store suffices; a neighbour already set to L in this round is not a parent.
+__device__ void bu_phase(const KParams& p, int64_t n, int32_t L, unsigned long long* found,
+                         unsigned long long* found_deg, unsigned long long* scanned) {
+  unsigned long long f = 0, fd = 0, sc = 0;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += T) {
+    if (ld_label(p.lab + v) != kInf) continue;
+    const int64_t b = __ldg(p.g.row_ptr + v), e = __ldg(p.g.row_ptr + v + 1);
+    for (int64_t k = b; k < e; ++k) {
+      const int32_t u = ld_stream(p.g.col + k);
+      if (ld_label(p.lab + u) == L - 1) {
+        p.lab[v] = L;
+        ++f;
+        fd += (unsigned long long)(e - b);
+        sc += (unsigned long long)(k - b + 1);
+        break;
+      }
+      if (k + 1 == e) sc += (unsigned long long)(e - b);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    f += __shfl_xor_sync(FULL, f, o);
+    fd += __shfl_xor_sync(FULL, fd, o);
+    sc += __shfl_xor_sync(FULL, sc, o);
+  }
+  if (lane_id() == 0) {
+    if (f) atomicAdd(found, f);
+    if (fd) atomicAdd(found_deg, fd);
+    if (sc) atomicAdd(scanned, sc);
+  }
+}
+
+// Bottom-up -> top-down: materialise the frontier (level == L) as the out worklist.
+__device__ void bu_compact(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, int64_t n,
+                           int32_t L) {
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); v0 < n; v0 += T) {
+    const int64_t v = v0 + lane_id();
+    const int kind = (v < n && ld_label(p.lab + v) == L) ? 1 : 0;
+    wpush<false>(sm, q, p, rb, kind, (uint32_t)v);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KParams p, PersistArgs a) {
+  __shared__ Smem sm;
+  cg::grid_group grid = cg::this_grid();
+  WarpQ q;
+  uint32_t* cnt = p.ctl->cnt;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  constexpr double kAlpha = 14.0, kBeta = 24.0;  // Beamer's switching constants
+  bool bottom_up = false;
+  uint32_t nbu = 0;
+  unsigned long long explored = 0;               // edges of vertices already discovered
+  uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));
+  for (uint32_t r = 0;; ++r) {
+    uint32_t* cout = cnt + slot3(a, r + 1);
+    if (leader) {
+      cnt[slot3(a, r + 2)] = 0;
+      p.ctl->chunk_cnt[(r + 1) % 3] = 0;
+      p.ctl->tile_ctr[(r + 1) % 3] = 0;
+      p.ctl->mf[(r + 1) % 3] = 0;
+      p.ctl->bu_found[(r + 1) % 3] = 0;
+    }
+    RoundBufs rb;
+    rb.in = (r & 1) ? a.buf_b : a.buf_a;
+    rb.nin = nin_next;
+    rb.out = (r & 1) ? a.buf_a : a.buf_b;
+    rb.out_cnt = cout;
+    rb.cap = a.cap;
+    rb.chunks = a.chunks;
+    rb.chunk_cnt = &p.ctl->chunk_cnt[r % 3];
+    rb.chunk_cap = a.chunk_cap;
+    rb.tile_ctr = &p.ctl->tile_ctr[r % 3];
+    rb.level = a.level0 + (int32_t)r;
+    rb.stamp_id = a.stamp0 + (int32_t)r;
+    rb.far = nullptr;
+    rb.far_cnt = nullptr;
+    rb.far_cap = 0;
+    rb.threshold = kInf;
+    rb.mf_acc = &p.ctl->mf[r % 3];
+    uint64_t nf, mf;
+    if (!bottom_up) {
+      item_phase<IRGL_OP_BFS, false>(sm, q, p, rb);
+      wflush_all(sm, q, p, rb);
+      grid.sync();
+      const uint32_t nch = ld_ctl(rb.chunk_cnt);
+      nf = ld_ctl(cout);
+      if (nch) {
+        chunk_phase<IRGL_OP_BFS, false>(sm, q, p, rb, nch);
+        wflush_all(sm, q, p, rb);
+        grid.sync();
+        nf = ld_ctl(cout);
+      }
+      mf = *(volatile unsigned long long*)&p.ctl->mf[r % 3];
+    } else {
+      bu_phase(p, a.n, rb.level, &p.ctl->bu_found[r % 3], &p.ctl->mf[r % 3], &p.ctl->bu_scanned);
+      grid.sync();
+      nf = *(volatile unsigned long long*)&p.ctl->bu_found[r % 3];
+      mf = *(volatile unsigned long long*)&p.ctl->mf[r % 3];
+      ++nbu;
+    }
+    explored += mf;
+    if (leader) {
+      p.ctl->popped += rb.nin;
+      p.ctl->pushes += nf;
+    }
+    const bool done = nf == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
+    if (!done) {
+      // direction for the next round (uniform: every thread reads the same counters)
+      const double mu = (double)a.m - (double)explored;
+      bool next_bu = bottom_up;
+      if (!bottom_up && (double)mf > mu / kAlpha) next_bu = true;
+      else if (bottom_up && (double)nf < (double)a.n / kBeta) next_bu = false;
+      if (bottom_up && !next_bu) {
+        // materialise the level-L frontier as the next round's worklist
+        RoundBufs cb = rb;
+        cb.mf_acc = nullptr;
+        bu_compact(sm, q, p, cb, a.n, rb.level);
+        wflush_all(sm, q, p, cb);
+        grid.sync();
+        nf = ld_ctl(cout);
+      }
+      bottom_up = next_bu;
+    }
+    nin_next = (uint32_t)nf;
+    if (done) {
+      if (leader) {
+        p.ctl->rounds = r + 1;
+        p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+        p.ctl->stamp_used = r + 1;
+        p.ctl->bu_rounds = nbu;
       }
       break;
     }
@@ -725,9 +879,12 @@ cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_
 int persistent_blocks_per_sm(int op) {
   int nb = 0;
   switch (op) {
-    case IRGL_OP_BFS:
+    case IRGL_OP_BFS: {
+      int nd = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_BFS>, kBlock, 0);
-      break;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nd, persistent_bfs_do_kernel, kBlock, 0);
+      nb = min(nb, nd);
+    } break;
     case IRGL_OP_SSSP:
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
       break;
@@ -763,6 +920,8 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
   note_launch();
   switch (op) {
     case IRGL_OP_BFS:
+      if (a.dir_opt)
+        return cudaLaunchCooperativeKernel((void*)persistent_bfs_do_kernel, grid, kBlock, args, 0, st);
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_BFS>, grid, kBlock, args, 0, st);
     case IRGL_OP_SSSP:
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_SSSP>, grid, kBlock, args, 0, st);

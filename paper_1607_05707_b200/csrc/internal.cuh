@@ -47,6 +47,10 @@ struct Ctl {
                                // persistent kernel resets one slot while CTAs may still read the other)
   uint32_t stamp_used;         // persistent: stamp ids consumed (rounds + splits)
   uint32_t far_sel;            // persistent: current far pile at exit
+  uint32_t bu_rounds;          // direction-optimising BFS: bottom-up rounds executed
+  unsigned long long mf[3];    // DO-BFS: edges of the next frontier (rotated by round)
+  unsigned long long bu_found[3];  // DO-BFS: vertices discovered by a bottom-up round
+  unsigned long long bu_scanned;   // DO-BFS: edges examined by bottom-up rounds
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -43,6 +43,7 @@ struct RoundBufs {
   uint32_t* far_cnt;
   uint32_t far_cap;
   int32_t threshold;  // INT32_MAX: near-far off
+  unsigned long long* mf_acc;  // DO-BFS: sum of degrees of pushed vertices (null: off)
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
@@ -76,6 +77,9 @@ struct PersistArgs {
   uint32_t* far_b;
   uint32_t far_cap;
   int32_t delta;       // 0: plain data-driven Bellman-Ford
+  int32_t dir_opt;     // BFS: 1 = direction-optimising (top-down / bottom-up switching)
+  int64_t n;           // vertices (bottom-up sweeps)
+  int64_t m;           // directed edges
 };
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,

@@ -67,7 +67,7 @@ class OpArgs(C.Structure):
     _fields_ = [("round_start", C.c_int64), ("guard", C.c_int64), ("pr_damping", C.c_double),
                 ("pr_tol", C.c_double), ("values", C.POINTER(C.c_int32)), ("nvalues", C.c_int64),
                 ("mapping", C.c_int32), ("threads", C.c_int32), ("delta", C.c_int32),
-                ("reserved", C.c_int32 * 5)]
+                ("direction", C.c_int32), ("reserved", C.c_int32 * 4)]
 
 
 class IterateOpts(C.Structure):
@@ -211,9 +211,10 @@ def nccl_unique_id() -> bytes:
 
 
 def _op_args(round_start=0, guard=0, pr_damping=0.0, pr_tol=0.0, values=None, mapping=0,
-             threads=0, delta=-1):
+             threads=0, delta=-1, direction=0):
     a = OpArgs()
     a.delta = delta
+    a.direction = direction
     a.round_start = round_start
     a.guard = guard
     a.pr_damping = pr_damping
@@ -510,11 +511,13 @@ class Pipe:
 
 
 # ---- convenience drivers (the IrGL programs of the north star, in host form) ------------------
-def bfs(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outline=-1):
-    """Listing 2: LEVEL=0; Iterate BFS(graph, LEVEL) Initial [src] { LEVEL++ }."""
+def bfs(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outline=-1,
+        direction=0):
+    """Listing 2: LEVEL=0; Iterate BFS(graph, LEVEL) Initial [src] { LEVEL++ }.
+    direction=1: direction-optimising variant (same levels)."""
     p = pipe or ctx.pipe(graph.n)
     p.init_scalars([src])
-    st = ctx.iterate(BFS, graph, p, outline=outline, round_start=1)
+    st = ctx.iterate(BFS, graph, p, outline=outline, round_start=1, direction=direction)
     return ctx.read_result(BFS, graph), st
 
 

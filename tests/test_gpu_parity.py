@@ -305,3 +305,32 @@ def test_edgelist_reader(ctx, irgl, oracle, tmp_path):
     with pytest.raises(irgl.IrglError) as e:
         ctx.read_edgelist(f4)
     assert e.value.status == 1
+
+
+# ---------------------------------------------------------------------------------------------
+# F1: direction-optimising BFS (outlined): same levels as Listing 2, fewer edges examined
+def test_bfs_direction_optimising_parity(ctx, irgl, oracle):
+    for og in (oracle.rmat(14), oracle.rmat(16), oracle.grid(40, 30), oracle.grid(33, 17, diag=True)):
+        g = _upload(ctx, og)
+        for s in og.sources(3):
+            s = int(s)
+            ref, ecc = oracle.bfs(og, s)
+            lv, st = irgl.bfs(ctx, g, s, outline=1, direction=1)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1
+    og = oracle.rmat(16)
+    g = _upload(ctx, og)
+    s = int(og.sources(1)[0])
+    ref, _ = oracle.bfs(og, s)
+    E = int(og.degrees()[ref < oracle.INF].sum())
+    lv, st = irgl.bfs(ctx, g, s, outline=1, direction=1)
+    assert st.edges < E  # bottom-up rounds stop at the first parent
+
+
+def test_bfs_direction_optimising_needs_outlined(irgl, oracle):
+    og = oracle.rmat(10)
+    with irgl.Context(logical_partitions=2) as c:
+        g = c.graph_from_csr(og.row_ptr, og.col, og.weight)
+        with pytest.raises(irgl.IrglError) as e:
+            irgl.bfs(c, g, 0, direction=1)
+        assert e.value.status == 9

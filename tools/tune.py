@@ -22,6 +22,9 @@ for cfg in CFGS:
     for outline in (1, 0):
         t, k, e, r = run(ctx, g, srcs, irgl.BFS, outline=outline)
         print(f"{cfg} BFS outline={outline}: {t:.3f} ms (kernel {k:.3f}) GTEPS={E/2/t/1e6:.1f} rounds={r}", flush=True)
+        if outline:
+            t, k, e, r = run(ctx, g, srcs, irgl.BFS, outline=1, direction=1)
+            print(f"{cfg} BFS-DO outline=1: {t:.3f} ms (kernel {k:.3f}) GTEPS={E/2/t/1e6:.1f} rounds={r} scanned/E={e/E:.3f}", flush=True)
         for delta in ([0, 2, 4, 8, 16, 32, 64] if cfg == {} else [8]):
             t, k, e, r = run(ctx, g, srcs, irgl.SSSP, outline=outline, delta=delta)
             print(f"{cfg} SSSP outline={outline} delta={delta}: {t:.3f} ms (kernel {k:.3f}) GTEPS={E/2/t/1e6:.1f} scans/E={e/E:.2f} rounds={r}", flush=True)
