@@ -68,6 +68,9 @@ typedef enum {
   IRGL_OP_PR = 3,    /* topology-driven pull Jacobi PageRank, fp64, ReduceAndReturn(|d|>tol) */
   IRGL_OP_TC = 4,    /* degree-oriented intersection triangle count (Sum: extension, App. B6) */
   IRGL_OP_CC_LP = 5, /* data-driven min-label propagation (worklist form of CC)              */
+  IRGL_OP_MST = 6,   /* Boruvka minimum spanning forest, Listing 1: find-min
+                        edge per component under Atomic, hook + pointer jumping, Iterate While
+                        Any; result uint64[2] = {forest weight, forest edges} */
   /* SPEC example operators (tests): */
   IRGL_OP_TEST_COUNTDOWN = 100, /* pop x; if x+1 < guard: push x+1 */
   IRGL_OP_TEST_RETRY_ODD = 101, /* odd x retried `guard` times, then pushed */
@@ -75,7 +78,10 @@ typedef enum {
   IRGL_OP_TEST_NOPUSH = 103,    /* pops, never pushes */
   IRGL_OP_TEST_PUSHPOP = 104,   /* records popped_at[x]=launch; push x+guard */
   IRGL_OP_TEST_FORALL_MAP = 105, /* records thread_of[x] = global thread id */
-  IRGL_OP_TEST_RESPAWN_ODD = 106  /* as RETRY_ODD with Respawn: never serialised */
+  IRGL_OP_TEST_RESPAWN_ODD = 106, /* as RETRY_ODD with Respawn: never serialised */
+  IRGL_OP_TEST_ATOMIC = 107,      /* blocking Atomic increment of one counter */
+  IRGL_OP_TEST_ATOMIC_ELSE = 108, /* Atomic/Else single attempt; guard=1: lock held SPEC.md:551 */
+  IRGL_OP_TEST_EXCLUSIVE = 109    /* Exclusive over values[x*guard..] lock sets */
 } irgl_op;
 
 typedef struct irgl_ctx irgl_ctx;

@@ -347,6 +347,49 @@ extern "C" uint64_t orc_tc_merge(const orc_graph* g) {
   return total;
 }
 
+extern "C" void orc_mst_kruskal(const orc_graph* g, uint64_t* weight, int64_t* nedges) {
+  struct E { int32_t w, a, b; };
+  std::vector<E> es;
+  for (int64_t u = 0; u < g->n; ++u)
+    for (int64_t e = g->row_ptr[u]; e < g->row_ptr[u + 1]; ++e)
+      if (g->col[e] > u) es.push_back({g->w[e], (int32_t)u, g->col[e]});
+  std::sort(es.begin(), es.end(), [](const E& x, const E& y) {
+    return x.w != y.w ? x.w < y.w : (x.a != y.a ? x.a < y.a : x.b < y.b);
+  });
+  std::vector<int64_t> p(g->n);
+  for (int64_t i = 0; i < g->n; ++i) p[i] = i;
+  uint64_t tot = 0;
+  int64_t cnt = 0;
+  for (const E& e : es) {
+    int64_t a = uf_find(p, e.a), b = uf_find(p, e.b);
+    if (a == b) continue;
+    if (a < b) p[b] = a; else p[a] = b;
+    tot += (uint64_t)e.w;
+    ++cnt;
+  }
+  *weight = tot;
+  *nedges = cnt;
+}
+
+extern "C" void orc_exclusive(const int32_t* locks, int64_t nitems, int k, int32_t* won) {
+  int32_t maxl = -1;
+  for (int64_t i = 0; i < nitems * k; ++i) maxl = std::max(maxl, locks[i]);
+  std::vector<int64_t> owner(maxl + 1, INT64_MAX);
+  for (int64_t x = 0; x < nitems; ++x)  // claim: priority-min per lock slot
+    for (int j = 0; j < k; ++j) {
+      const int32_t l = locks[x * k + j];
+      if (l >= 0) owner[l] = std::min<int64_t>(owner[l], x);
+    }
+  for (int64_t x = 0; x < nitems; ++x) {  // check / confirm
+    bool all = true;
+    for (int j = 0; j < k; ++j) {
+      const int32_t l = locks[x * k + j];
+      if (l >= 0 && owner[l] != x) all = false;
+    }
+    won[x] = all ? 1 : 0;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // IrGL bulk-synchronous executor.
 //

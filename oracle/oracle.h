@@ -73,6 +73,14 @@ void orc_cc_unionfind(const orc_graph* g, int32_t* label); /* label = min vertex
 int orc_pagerank(const orc_graph* g, double d, double tol, int max_iter, double* rank);
 uint64_t orc_tc_merge(const orc_graph* g);
 
+/* MST forest by Kruskal (edges ordered by (w, min(u,v), max(u,v))): total weight and edge count
+ * (SPEC.md:550 acceptance item 2 oracle for Boruvka, Listing 1). */
+void orc_mst_kruskal(const orc_graph* g, uint64_t* weight, int64_t* nedges);
+/* Exclusive protocol oracle: item x claims locks[x*k .. x*k+k)
+ * (-1 = unused) with priority x (lower wins); x wins iff it holds every lock it claimed after the
+ * claim phase.  won[x] = 1/0. */
+void orc_exclusive(const int32_t* locks, int64_t nitems, int k, int32_t* won);
+
 /* ---- IrGL bulk-synchronous worklist executor (restates SPEC.md:423-467) ----------------- */
 enum { ORC_OP_BFS = 0, ORC_OP_SSSP = 1, ORC_OP_CC = 2, ORC_OP_PR = 3, ORC_OP_TC = 4,
        ORC_OP_CC_LP = 5,

@@ -87,6 +87,8 @@ def lib():
         L.orc_cc_unionfind.argtypes = [P, i32p]
         L.orc_pagerank.restype = C.c_int
         L.orc_pagerank.argtypes = [P, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double)]
+        L.orc_mst_kruskal.argtypes = [P, C.POINTER(C.c_uint64), i64p]
+        L.orc_exclusive.argtypes = [i32p, C.c_int64, C.c_int, i32p]
         L.orc_tc_merge.restype = C.c_uint64
         L.orc_tc_merge.argtypes = [P]
         L.orc_iterate.restype = C.c_int
@@ -199,6 +201,20 @@ def pagerank(g: Graph, d=0.85, tol=1e-6, max_iter=100):
 
 def tc(g: Graph) -> int:
     return int(lib().orc_tc_merge(g.handle))
+
+
+def mst(g: Graph):
+    w, n = C.c_uint64(0), C.c_int64(0)
+    lib().orc_mst_kruskal(g.handle, C.byref(w), C.byref(n))
+    return int(w.value), int(n.value)
+
+
+def exclusive(locks):
+    """locks: int32 [nitems, k] (-1 unused); returns won[nitems] (priority = item index)."""
+    lk = np.ascontiguousarray(locks, dtype=np.int32)
+    won = np.zeros(lk.shape[0], dtype=np.int32)
+    lib().orc_exclusive(_p(lk, C.c_int32), lk.shape[0], lk.shape[1], _p(won, C.c_int32))
+    return won
 
 
 def reduce(values, reduction):

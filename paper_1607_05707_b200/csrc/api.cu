@@ -41,6 +41,7 @@ struct irgl_ctx {
   int64_t test_rcount_cap = 0;
   int32_t test_launch_no = 0;
   irgl::Ctl* test_ctl = nullptr;
+  int32_t* test_lock = nullptr;
   int ptotal() const { return nranks * (int)parts.size(); }
   int gpart(int l) const { return rank * (int)parts.size() + l; }
 };
@@ -62,6 +63,9 @@ struct GraphPart {
   uint32_t chunk_cap = 0;
   uint32_t* far[2] = {nullptr, nullptr};  // SSSP near-far piles
   uint32_t far_cap = 0;
+  int32_t* mst[6] = {};          // MST: parent, comp, lock, best w / a / b
+  uint32_t* mst_wl[2] = {};      // MST: node worklist (Listing 1)
+  int mst_sel = 0;
   Ctl* ctl = nullptr;
   // multi-partition exchange
   uint32_t* send = nullptr;
@@ -137,9 +141,9 @@ static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
 static bool is_wl_graph_op(int op) {
   return op == IRGL_OP_BFS || op == IRGL_OP_SSSP || op == IRGL_OP_CC_LP;
 }
-static bool is_test_op(int op) { return op >= IRGL_OP_TEST_COUNTDOWN && op <= IRGL_OP_TEST_RESPAWN_ODD; }
+static bool is_test_op(int op) { return op >= IRGL_OP_TEST_COUNTDOWN && op <= IRGL_OP_TEST_EXCLUSIVE; }
 static bool is_known_op(int op) {
-  return (op >= IRGL_OP_BFS && op <= IRGL_OP_CC_LP) || is_test_op(op);
+  return (op >= IRGL_OP_BFS && op <= IRGL_OP_MST) || is_test_op(op);
 }
 
 #define CK(expr)                                                 \
@@ -277,6 +281,26 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
   }
   if (op == IRGL_OP_TC) {
     g->tc_count = 0;
+    g->lab_op = op;
+    return IRGL_OK;
+  }
+  if (op == IRGL_OP_MST) {
+    if (ctx->ptotal() > 1) return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED", "MST runs on one partition");
+    GraphPart& gp = g->parts[0];
+    PartRT& pr = ctx->parts[0];
+    CK(cudaSetDevice(pr.dev));
+    const int64_t n1 = std::max<int64_t>(g->n, 1);
+    for (int k = 0; k < 6; ++k)
+      if (!gp.mst[k]) CK(cudaMalloc(&gp.mst[k], n1 * 4));
+    for (int k = 0; k < 2; ++k)
+      if (!gp.mst_wl[k]) CK(cudaMalloc(&gp.mst_wl[k], n1 * 4));
+    CK(launch_mst_init(gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3], gp.mst[4], gp.mst[5], gp.mst_wl[0],
+                       g->n, pr.st));
+    CK(cudaMemsetAsync(&gp.ctl->mst_w, 0, 16, pr.st));
+    const uint32_t cnts[2] = {(uint32_t)g->n, 0u};
+    CK(cudaMemcpyAsync(gp.ctl->mst_cnt, cnts, 8, cudaMemcpyHostToDevice, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    gp.mst_sel = 0;
     g->lab_op = op;
     return IRGL_OK;
   }
@@ -744,6 +768,39 @@ static irgl_status_t test_invoke(irgl_ctx* ctx, irgl_pipe* pipe, int op, const i
   CK(cudaSetDevice(pr.dev));
   irgl_status_t s = test_ensure(ctx, pipe->cap);
   if (s != IRGL_OK) return s;
+  if (op == IRGL_OP_TEST_ATOMIC || op == IRGL_OP_TEST_ATOMIC_ELSE || op == IRGL_OP_TEST_EXCLUSIVE) {
+    // Atomic / Exclusive constructs: one launch over the in-worklist
+    CK(cudaMemsetAsync(ctx->test_log, 0, ctx->test_log_cap * 4, pr.st));
+    if (op == IRGL_OP_TEST_EXCLUSIVE) {
+      const int k = a && a->guard > 0 ? (int)a->guard : 1;
+      if (!dvalues || !a || a->nvalues < (int64_t)pp.n_in * k)
+        return fail(ctx, IRGL_E_INVALID, "E_INVALID", "EXCLUSIVE needs values[items*guard] lock ids");
+      int32_t maxl = 0;
+      for (int64_t i = 0; i < a->nvalues; ++i) maxl = std::max(maxl, a->values[i]);
+      int32_t *owner = nullptr, *won = nullptr;
+      CK(cudaMalloc(&owner, ((size_t)maxl + 1) * 4));
+      CK(cudaMalloc(&won, pipe->cap * 4));
+      CK(cudaMemset(owner, 0x7f, ((size_t)maxl + 1) * 4));  // INT32_MAX-ish: priority-min identity
+      const int bps = exclusive_blocks_per_sm();
+      if (bps <= 0) return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "Exclusive needs a co-resident grid");
+      CK(launch_exclusive_test(pp.buf[pp.b_in], pp.n_in, dvalues, k, owner, won, ctx->test_log,
+                               bps * pr.sms, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+      cudaFree(owner);
+      cudaFree(won);
+    } else {
+      if (!ctx->test_lock) CK(cudaMalloc(&ctx->test_lock, 4));
+      const int32_t held = (op == IRGL_OP_TEST_ATOMIC_ELSE && a && a->guard) ? 1 : 0;
+      CK(cudaMemcpyAsync(ctx->test_lock, &held, 4, cudaMemcpyHostToDevice, pr.st));
+      const int threads = a && a->threads > 0 ? a->threads : 148 * 256;
+      CK(launch_atomic_test(pp.buf[pp.b_in], pp.n_in, ctx->test_lock, ctx->test_log,
+                            op == IRGL_OP_TEST_ATOMIC_ELSE, threads, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+    }
+    stt->launches++;
+    stt->popped += pp.n_in;
+    return pipe_swap_in_out(ctx, pp, pr, 0);
+  }
   const uint32_t ident = red == IRGL_RED_ALL ? 1u : 0u;
   CK(cudaMemcpyAsync(&ctx->test_ctl->red[0], &ident, 4, cudaMemcpyHostToDevice, pr.st));
   CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_retry], 0, 4, pr.st));
@@ -843,6 +900,23 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     CK(cudaStreamSynchronize(pr.st));
     gp.pr_cur = 1 - c;
     stt->edges += g->m;
+  } else if (op == IRGL_OP_MST) {
+    // one invocation = find-min (Atomic) + hook + pointer jumping; ReduceAndReturn(hooked)
+    const int sel = gp.mst_sel;
+    uint32_t nin = 0;
+    CK(cudaMemcpyAsync(&nin, &gp.ctl->mst_cnt[sel], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaMemsetAsync(&gp.ctl->mst_cnt[sel ^ 1], 0, 4, pr.st));
+    CK(cudaMemsetAsync(&gp.ctl->red[1], 0, 4, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    CK(launch_mst_round(gp.csr(), gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3], gp.mst[4], gp.mst[5],
+                        gp.mst_wl[sel], nin, gp.mst_wl[sel ^ 1], &gp.ctl->mst_cnt[sel ^ 1],
+                        &gp.ctl->mst_w, &gp.ctl->mst_e, &gp.ctl->red[1], g->n, gm, pr.st));
+    stt->launches += 3;
+    stt->popped += nin;
+    CK(cudaMemcpyAsync(&cell, &gp.ctl->red[1], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    gp.mst_sel = sel ^ 1;
+    if (red == IRGL_RED_ALL) cell = cell ? 1u : 0u;
   } else if (op == IRGL_OP_TC) {
     if (gp.tc_m < 0) CK(tc_orient(gp.csr(), g->n, &gp.tc_rp, &gp.tc_cl, &gp.tc_m, pr.st));
     CK(launch_tc_count(gp.tc_rp, gp.tc_cl, g->n, gp.ctl, pr.st));
@@ -1076,6 +1150,7 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
   if (ctx->test_log) cudaFree(ctx->test_log);
   if (ctx->test_rcount) cudaFree(ctx->test_rcount);
   if (ctx->test_ctl) cudaFree(ctx->test_ctl);
+  if (ctx->test_lock) cudaFree(ctx->test_lock);
   if (ctx->cnt_dev) cudaFree(ctx->cnt_dev);
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->kev0, ctx->kev1})
     if (e) cudaEventDestroy(e);
@@ -1289,7 +1364,8 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     cudaStreamSynchronize(ctx->parts[l].st);
     void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
                   gp.tc_rp, gp.tc_cl, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
-                  gp.recv_val, gp.far[0], gp.far[1]};
+                  gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
+                  gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
     for (void* p : ps)
       if (p) cudaFree(p);
   }
@@ -1568,6 +1644,13 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
   if (op == IRGL_OP_TC) {
     if (bytes < 8) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "TC result is one uint64");
     std::memcpy(host_out, &g->tc_count, 8);
+    return IRGL_OK;
+  }
+  if (op == IRGL_OP_MST) {
+    if (bytes < 16) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "MST result is uint64[2]");
+    if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "MST has not run on this graph");
+    CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaMemcpy(host_out, &g->parts[0].ctl->mst_w, 16, cudaMemcpyDeviceToHost));
     return IRGL_OK;
   }
   if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");

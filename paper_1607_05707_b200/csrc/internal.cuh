@@ -51,6 +51,8 @@ struct Ctl {
   unsigned long long mf[3];    // DO-BFS: edges of the next frontier (rotated by round)
   unsigned long long bu_found[3];  // DO-BFS: vertices discovered by a bottom-up round
   unsigned long long bu_scanned;   // DO-BFS: edges examined by bottom-up rounds
+  unsigned long long mst_w, mst_e; // MST: forest weight / edges
+  uint32_t mst_cnt[2];             // MST: internal worklist counters
 };
 
 // ---------------------------------------------------------------------------------------------

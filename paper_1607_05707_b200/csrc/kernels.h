@@ -107,6 +107,21 @@ cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl
 cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl* ctl,
                             cudaStream_t st);
 
+// ---- Atomic / Exclusive constructs and Boruvka MST (mst.cu) -----------------------------------
+cudaError_t launch_mst_init(int32_t* parent, int32_t* comp, int32_t* lock, int32_t* bw, int32_t* ba,
+                            int32_t* bb, uint32_t* wl, int64_t n, cudaStream_t st);
+cudaError_t launch_mst_round(const DevCSR& g, int32_t* parent, int32_t* comp, int32_t* lock,
+                             int32_t* bw, int32_t* ba, int32_t* bb, const uint32_t* in, uint32_t nin,
+                             uint32_t* out, uint32_t* out_cnt, unsigned long long* wsum,
+                             unsigned long long* esum, uint32_t* cell, int64_t n, int grid,
+                             cudaStream_t st);
+cudaError_t launch_atomic_test(const uint32_t* in, uint32_t nin, int32_t* lock, int32_t* log,
+                               int else_form, int threads, cudaStream_t st);
+int exclusive_blocks_per_sm();
+cudaError_t launch_exclusive_test(const uint32_t* in, uint32_t nin, const int32_t* locks, int k,
+                                  int32_t* owner, int32_t* won, int32_t* log, int grid,
+                                  cudaStream_t st);
+
 // ---- misc (util.cu) ---------------------------------------------------------------------------
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);
 cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st);
