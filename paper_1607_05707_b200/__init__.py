@@ -5,11 +5,11 @@ include/irgl/rt.h); this package is its host-side mirror of the IrGL operator AP
 package loads the shared library and fails loudly if it has not been built.
 """
 from .runtime import (  # noqa: F401
-    BFS, CC, CC_LP, COMB_AND, COMB_OR, COND_NONE, COND_UNTIL, COND_WHILE, INF, MAP_BLOCKED,
+    BFS, CC, CC_LP, MST, TEST_ATOMIC, TEST_ATOMIC_ELSE, TEST_EXCLUSIVE, COMB_AND, COMB_OR, COND_NONE, COND_UNTIL, COND_WHILE, INF, MAP_BLOCKED,
     MAP_CONSECUTIVE, PR, RED_ALL, RED_ANY, RED_NONE, SSSP, TC, TEST_COUNTDOWN, TEST_FORALL_MAP,
     TEST_NOPUSH, TEST_PUSHPOP, TEST_REDUCE, TEST_RESPAWN_ODD, TEST_RETRY_ODD, WL_IN, WL_OUT, WL_RETRY,
     BLOCK_ELASTIC, BLOCK_FIXED, BLOCK_SHRINKABLE, EXPORTS, LIB_PATH, Context, Graph, IrglError,
-    Pipe, Stats, bfs, cc, cc_lp, launch_count, load_library, nccl_unique_id, pagerank, sssp, t_control,
+    Pipe, Stats, bfs, cc, cc_lp, launch_count, load_library, mst, nccl_unique_id, pagerank, sssp, t_control,
     triangle_count,
 )
 

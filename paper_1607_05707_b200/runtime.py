@@ -40,10 +40,11 @@ WL_IN, WL_OUT, WL_RETRY = 0, 1, 2
 COND_NONE, COND_WHILE, COND_UNTIL = 0, 1, 2
 COMB_OR, COMB_AND = 0, 1
 MAP_CONSECUTIVE, MAP_BLOCKED = 0, 1
-BFS, SSSP, CC, PR, TC, CC_LP = 0, 1, 2, 3, 4, 5
+BFS, SSSP, CC, PR, TC, CC_LP, MST = 0, 1, 2, 3, 4, 5, 6
 TEST_COUNTDOWN, TEST_RETRY_ODD, TEST_REDUCE, TEST_NOPUSH, TEST_PUSHPOP, TEST_FORALL_MAP = (
     100, 101, 102, 103, 104, 105)
 TEST_RESPAWN_ODD = 106
+TEST_ATOMIC, TEST_ATOMIC_ELSE, TEST_EXCLUSIVE = 107, 108, 109
 GEN_RMAT, GEN_GRID = 0, 1
 BLOCK_ELASTIC, BLOCK_SHRINKABLE, BLOCK_FIXED = 0, 1, 2
 
@@ -393,6 +394,8 @@ class Context:
     def read_result(self, op, graph=None, size=None):
         if op == TC:
             out = np.zeros(1, dtype=np.uint64)
+        elif op == MST:
+            out = np.zeros(2, dtype=np.uint64)
         elif op == PR:
             out = np.zeros(graph.n, dtype=np.float64)
         elif op >= 100:
@@ -401,6 +404,8 @@ class Context:
             out = np.zeros(graph.n, dtype=np.int32)
         self._chk(self._lib.irgl_read_result(self._h, graph.handle if graph else None, op,
                                              out.ctypes.data_as(C.c_void_p), out.nbytes))
+        if op == MST:
+            return int(out[0]), int(out[1])
         return int(out[0]) if op == TC else out
 
     def read_result_into(self, op, graph, out: np.ndarray):
@@ -547,6 +552,12 @@ def pagerank(ctx: Context, graph: Graph, d=0.85, tol=1e-6, max_iter=100, outline
     st = ctx.iterate(PR, graph, None, cond=COND_WHILE, reduction=RED_ANY, max_rounds=max_iter,
                      extra_comb=COMB_OR, outline=outline, pr_damping=d, pr_tol=tol)
     return ctx.read_result(PR, graph), st
+
+
+def mst(ctx: Context, graph: Graph):
+    """Boruvka (Listing 1) under Iterate While Any: returns ((forest weight, edges), Stats)."""
+    st = ctx.iterate(MST, graph, None, cond=COND_WHILE, reduction=RED_ANY)
+    return ctx.read_result(MST, graph), st
 
 
 def triangle_count(ctx: Context, graph: Graph):
