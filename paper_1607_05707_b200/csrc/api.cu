@@ -273,7 +273,7 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
     CK(cudaSetDevice(pr.dev));
     for (int k = 0; k < 4; ++k)
       if (!gp.pr[k]) CK(cudaMalloc(&gp.pr[k], std::max<int64_t>(g->n, 1) * sizeof(double)));
-    CK(launch_pr_init(gp.pr[0], gp.pr[2], gp.row_ptr, g->n, pr.st));
+    CK(launch_pr_init(gp.pr[0], reinterpret_cast<float*>(gp.pr[2]), gp.row_ptr, g->n, pr.st));
     CK(cudaStreamSynchronize(pr.st));
     gp.pr_cur = 0;
     g->lab_op = op;
@@ -893,8 +893,8 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     const double d = a && a->pr_damping > 0 ? a->pr_damping : 0.85;
     const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
     const int c = gp.pr_cur;
-    CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c], gp.pr[3 - c], d, tol, g->n,
-                       gp.ctl, 0, gm, pr.st));
+    CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
+                       reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, 0, gm, pr.st));
     stt->launches += 1;
     CK(cudaMemcpyAsync(&cell, &gp.ctl->red[0], 4, cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
@@ -950,8 +950,9 @@ static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_arg
   const int c = gp.pr_cur;
   CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
-  CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c], gp.pr[3 - c], d, tol, g->n,
-                          gp.ctl, o.max_rounds, o.cond_mode, bps * pr.sms, pr.st));
+  CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
+                          reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, o.max_rounds,
+                          o.cond_mode, bps * pr.sms, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   Ctl h;
   CK(cudaMemcpyAsync(&h, gp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));

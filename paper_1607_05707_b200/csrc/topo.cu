@@ -111,6 +111,12 @@ __device__ __forceinline__ double ld_cg_f64(const double* p) {
   return r;
 }
 
+__device__ __forceinline__ float ld_cg_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
@@ -119,9 +125,11 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 // One PR sweep over the local vertex range (tile per CTA-iteration).  Deterministic per-vertex
 // summation order (fixed by the code path chosen by degree).
+// contrib(u) = rank(u)/deg(u) is stored in fp32 (the gathered operand: half the bytes per edge
+// and an L2-resident array at RMAT-24); ranks and per-vertex sums stay fp64.
 __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
-                               double* __restrict__ rank_new, const double* __restrict__ contrib,
-                               double* __restrict__ contrib_next, double d, double tol,
+                               double* __restrict__ rank_new, const float* __restrict__ contrib,
+                               float* __restrict__ contrib_next, double d, double tol,
                                double base, int red, uint32_t* cell) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nloc = g.hi - g.lo;
@@ -148,7 +156,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       }
       __syncthreads();
       double s = 0.0;
-      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += ld_cg_f64(contrib + ld_stream(g.col + k));
+      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
       s = warp_sum(s);
       if (lane == 0) sm.red[warp] = s;
       __syncthreads();
@@ -167,7 +175,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       wm &= wm - 1;
       const int64_t b = __shfl_sync(FULL, beg, leader), e = __shfl_sync(FULL, end, leader);
       double s = 0.0;
-      for (int64_t k = b + lane; k < e; k += 32) s += ld_cg_f64(contrib + ld_stream(g.col + k));
+      for (int64_t k = b + lane; k < e; k += 32) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
       s = warp_sum(s);
       if (lane == leader) {
         mysum = s;
@@ -177,7 +185,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
     // thread level
     if (deg > 0) {
       double s = 0.0;
-      for (int64_t k = beg; k < end; ++k) s += ld_cg_f64(contrib + ld_stream(g.col + k));
+      for (int64_t k = beg; k < end; ++k) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
       mysum = s;
     }
     bool changed = false;
@@ -185,7 +193,7 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       const int64_t v = g.lo + i;
       const double r = base + d * mysum;
       rank_new[v] = r;
-      contrib_next[v] = deg0 > 0 ? r / (double)deg0 : 0.0;
+      contrib_next[v] = deg0 > 0 ? (float)(r / (double)deg0) : 0.0f;
       changed = fabs(r - ld_cg_f64(rank_old + v)) > tol;
     }
     reduce_and_return(valid, changed, red, cell);
@@ -193,28 +201,28 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
 }
 
 __global__ void __launch_bounds__(kBlock) pr_sweep_kernel(DevCSR g, const double* rank_old,
-                                                          double* rank_new, const double* contrib,
-                                                          double* contrib_next, double d,
+                                                          double* rank_new, const float* contrib,
+                                                          float* contrib_next, double d,
                                                           double tol, double base, uint32_t* cell) {
   __shared__ PrSmem sm;
   pr_sweep_tiles(sm, g, rank_old, rank_new, contrib, contrib_next, d, tol, base, IRGL_RED_ANY,
                  cell);
 }
 
-__global__ void pr_init_kernel(double* rank, double* contrib, const int64_t* row_ptr, int64_t n) {
+__global__ void pr_init_kernel(double* rank, float* contrib, const int64_t* row_ptr, int64_t n) {
   const double r0 = 1.0 / (double)n;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     rank[v] = r0;
     const int64_t deg = row_ptr[v + 1] - row_ptr[v];
-    contrib[v] = deg > 0 ? r0 / (double)deg : 0.0;
+    contrib[v] = deg > 0 ? (float)(r0 / (double)deg) : 0.0f;
   }
 }
 
 // Outlined PR: Iterate While Any PR(graph) [Or rounds >= max] as one persistent kernel.
 // Cells rotate over 3 slots: cell (r+1)%3 is reset during round r (last read at the start of r-1).
 __global__ void __launch_bounds__(kBlock) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
-                                                               double* ca, double* cb, double d,
+                                                               float* ca, float* cb, double d,
                                                                double tol, double base, Ctl* ctl,
                                                                int64_t max_rounds, int cond_mode) {
   __shared__ PrSmem sm;
@@ -222,8 +230,8 @@ __global__ void __launch_bounds__(kBlock) pr_persistent_kernel(DevCSR g, double*
   for (int64_t r = 0;; ++r) {
     double* ro = (r & 1) ? rb : ra;
     double* rn = (r & 1) ? ra : rb;
-    double* co = (r & 1) ? cb : ca;
-    double* cn = (r & 1) ? ca : cb;
+    float* co = (r & 1) ? cb : ca;
+    float* cn = (r & 1) ? ca : cb;
     uint32_t* cell = &ctl->red[r % 3];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->red[(r + 1) % 3] = 0u;
     pr_sweep_tiles(sm, g, ro, rn, co, cn, d, tol, base, IRGL_RED_ANY, cell);
@@ -338,7 +346,7 @@ cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st) {
   cc_compress_kernel<<<grid, 256, 0, st>>>(parent, n);
   return cudaGetLastError();
 }
-cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
+cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr, int64_t n,
                            cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   note_launch();
@@ -346,7 +354,7 @@ cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr
   return cudaGetLastError();
 }
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
-                            const double* contrib, double* contrib_next, double d, double tol,
+                            const float* contrib, float* contrib_next, double d, double tol,
                             int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st) {
   const double base = (1.0 - d) / (double)n_global;
   note_launch();
@@ -359,7 +367,7 @@ int pr_persistent_blocks_per_sm() {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pr_persistent_kernel, kBlock, 0);
   return nb;
 }
-cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double* ca, double* cb,
+cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float* ca, float* cb,
                                  double d, double tol, int64_t n_global, Ctl* ctl,
                                  int64_t max_rounds, int cond_mode, int grid, cudaStream_t st) {
   double base = (1.0 - d) / (double)n_global;

@@ -201,7 +201,7 @@ def test_pagerank_parity(ctx, irgl, oracle, outline):
 def test_pagerank_regular_graph_uniform(ctx, irgl, oracle):
     og = oracle.from_edges(10, list(range(10)), [(i + 1) % 10 for i in range(10)])  # cycle
     r, _ = irgl.pagerank(ctx, _upload(ctx, og))
-    np.testing.assert_allclose(r, 0.1, rtol=1e-12)
+    np.testing.assert_allclose(r, 0.1, rtol=1e-6)  # north_star PR tolerance (fp32 contrib)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -334,3 +334,15 @@ def test_bfs_direction_optimising_needs_outlined(irgl, oracle):
         with pytest.raises(irgl.IrglError) as e:
             irgl.bfs(c, g, 0, direction=1)
         assert e.value.status == 9
+
+
+def test_pagerank_parity_rmat18(ctx, irgl, oracle):
+    """fp32 contrib storage (fp64 ranks and sums): L1-relative error vs the fp64 oracle."""
+    og = oracle.rmat(18)
+    g = _upload(ctx, og)
+    ref, it = oracle.pagerank(og)
+    for outline in (0, 1):
+        r, st = irgl.pagerank(ctx, g, outline=outline)
+        err = np.abs(r - ref).sum() / np.abs(ref).sum()
+        assert err <= 1e-6, err
+        assert abs(st.rounds - it) <= 1
