@@ -116,7 +116,12 @@ typedef struct irgl_op_args {
   int32_t direction;     /* BFS: 0 = top-down worklist (Listing 2); 1 = direction-optimising
                             (bottom-up rounds when the frontier is large; outlined, 1 partition;
                             SURVEY §8f F1).  Same levels either way.                          */
-  int32_t reserved[4];
+  int32_t defer;         /* SSSP: degree-scaled deferral budget K.  A popped vertex v with
+                            (dist[v] - min dist of the frontier) * deg(v) > K is re-pushed
+                            (kept for the next round) instead of expanded, so hubs expand close
+                            to their final distance.  0 = off, <0 = runtime default.  Same
+                            distances either way (only the relaxation order changes).        */
+  int32_t reserved[3];
 } irgl_op_args;
 
 /* Iterate [While|Until Any|All] kernel(args) [ExtraCond] (ast.hpp:186-204). */

@@ -456,7 +456,15 @@ struct NearFar {
   int32_t delta = 0;
   int32_t threshold = kInf;
   int fsel = 0;  // current far pile
+  int64_t defer_k = 0;  // degree-scaled deferral budget (0 = off)
+  int dsel = 0;         // host loop: Ctl::dmin cell read by the current round
 };
+
+// Deferral budget K (irgl_op_args.defer < 0): a popped vertex is expanded only when
+// (dist - frontier min) * degree <= K.  From the RMAT-22/24 sweep (profiles/r1s2_defer_sweep.txt):
+// outlined rounds cost ~10 us, so the smaller budget (fewer re-scans, more rounds) wins; a
+// host-orchestrated round costs several times more, so it takes the larger one.
+static int64_t default_defer(bool outlined) { return outlined ? 1024 : 2048; }
 
 static int32_t default_delta(const irgl_graph* g) {
   (void)g;
@@ -497,6 +505,9 @@ static RoundBufs round_bufs(irgl_pipe* pipe, GraphPart& gp, PipePart& pp, int32_
   rb.far_cap = gp.far_cap;
   rb.threshold = nf.delta > 0 ? nf.threshold : kInf;
   rb.mf_acc = nullptr;
+  rb.defer_k = nf.defer_k;
+  rb.dmin_cur = &pp.ctl->dmin[nf.dsel];
+  rb.dmin_next = nf.defer_k > 0 ? &pp.ctl->dmin[nf.dsel ^ 1] : nullptr;
   return rb;
 }
 
@@ -601,6 +612,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       GraphPart& gp = g->parts[l];
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
+      if (nf.defer_k > 0) CK(cudaMemsetAsync(&pp.ctl->dmin[nf.dsel ^ 1], 0xff, 4, pr.st));
       rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       DistRoute dr{P, ctx->gpart(l), g->part_size, gp.send, gp.send_cnt};
       if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
@@ -645,6 +657,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       if (s2 != IRGL_OK) return s2;
     }
     stt->rounds++;
+    nf.dsel ^= 1;
     ++level;  // between_rounds { LEVEL++ }
   }
   return IRGL_OK;
@@ -683,10 +696,21 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.dir_opt = (op == IRGL_OP_BFS && dir_opt) ? 1 : 0;
   pa.n = g->n;
   pa.m = g->m;
+  pa.defer_k = op == IRGL_OP_SSSP ? nf.defer_k : 0;
+  // IRGL_ROUND_TRACE=1: the leader thread stamps %globaltimer, |in|, |out| and the edge counter
+  // after every round (the SPEC's --trace, at round granularity); printed to stderr
+  pa.trace = nullptr;
+  pa.trace_cap = 0;
+  const char* tr = getenv("IRGL_ROUND_TRACE");
+  if (tr && *tr == '1' && !pa.dir_opt) {
+    pa.trace_cap = 4096;
+    CK(cudaMallocAsync(&pa.trace, (4 * (size_t)pa.trace_cap + 1) * 8, pr.st));
+  }
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
   CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(pp.ctl->tile_ctr), pr.st));
   CK(cudaMemsetAsync(pp.ctl->far_cnt, 0, sizeof(pp.ctl->far_cnt), pr.st));
+  CK(cudaMemsetAsync(pp.ctl->dmin, 0xff, sizeof(pp.ctl->dmin), pr.st));  // round 0: no deferral
   CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(pp.ctl->mf, 0, sizeof(pp.ctl->mf) + sizeof(pp.ctl->bu_found) + 8, pr.st));
@@ -700,6 +724,19 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
     stt->kernel_ms += kms;
+  }
+  if (pa.trace) {
+    std::vector<unsigned long long> t(4 * (size_t)pa.trace_cap + 1);
+    CK(cudaMemcpy(t.data(), pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaFree(pa.trace));
+    unsigned long long prev = t[4 * (size_t)pa.trace_cap], e0 = 0;
+    for (uint64_t r = 0; r < std::min<uint64_t>(h.rounds, pa.trace_cap); ++r) {
+      fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu\n", op,
+              (unsigned long long)r, (t[4 * r] - prev) * 1e-3, t[4 * r + 1], t[4 * r + 2],
+              t[4 * r + 3] - e0);
+      prev = t[4 * r];
+      e0 = t[4 * r + 3];
+    }
   }
   if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
   const int64_t K = (int64_t)h.rounds;
@@ -1560,6 +1597,15 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     if (op == IRGL_OP_SSSP) {
       nf.delta = !args ? 0 : (args->delta < 0 ? default_delta(g) : args->delta);
       nf.threshold = nf.delta;
+      nf.defer_k = !args ? 0 : (args->defer < 0 ? default_defer(outline && ctx->ptotal() == 1) : args->defer);
+      if (nf.defer_k > 0) {
+        // the first round has no frontier minimum yet: no deferral
+        for (size_t l = 0; l < pipe->parts.size(); ++l) {
+          CK(cudaSetDevice(ctx->parts[l].dev));
+          CK(cudaMemset(pipe->parts[l].ctl->dmin, 0xff, sizeof(pipe->parts[l].ctl->dmin)));
+        }
+        CK(cudaSetDevice(pr0.dev));
+      }
       if (nf.delta > 0) {
         s = ensure_far(ctx, g);
         if (s != IRGL_OK) return s;

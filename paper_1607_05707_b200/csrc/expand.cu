@@ -59,6 +59,7 @@ struct WarpQ {
   uint32_t nf = 0;  // staged far pushes
   unsigned long long edges = 0;
   unsigned long long mf = 0;  // DO-BFS: degrees of pushed vertices
+  int32_t dmin = kInf;        // SSSP deferral: min distance this lane pushed near (per lane)
 };
 
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
@@ -78,8 +79,8 @@ __device__ __forceinline__ uint32_t ld_ctl(const uint32_t* p) {
 // CC_LP : nd = label[n];   same as SSSP.
 // Returns 0 (no push), 1 (near push) or 2 (far push: nd >= threshold).
 template <int OP>
-__device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb, int32_t cur,
-                                          int32_t sv, int32_t wt, uint32_t dst) {
+__device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb, WarpQ& q,
+                                          int32_t cur, int32_t sv, int32_t wt, uint32_t dst) {
   if (OP == IRGL_OP_BFS) {
     if (cur != kInf) return 0;
     return atomicCAS(p.lab + dst, kInf, rb.level) == kInf ? 1 : 0;
@@ -92,6 +93,8 @@ __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb,
     // first pushed far and then improved below the threshold in the same round is pushed near
     // too; its stale far entry is dropped by the split (dist < old threshold).
     const int kind = (OP == IRGL_OP_SSSP && nd >= rb.threshold) ? 2 : 1;
+    // dst now holds <= nd and sits in the near out worklist (pushed here or earlier this round)
+    if (OP == IRGL_OP_SSSP && kind == 1) q.dmin = min(q.dmin, nd);
     const int32_t code = (rb.stamp_id << 1) | (kind - 1);
     if (atomicExch(p.stamp + dst, code) == code) return 0;
     return kind;
@@ -173,6 +176,13 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
     if (lane == 0) atomicAdd(rb.mf_acc, q.mf);
     q.mf = 0;
   }
+  if (rb.dmin_next) {
+    int32_t m = q.dmin;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(FULL, m, o));
+    if (lane == 0 && m != kInf) atomicMin(rb.dmin_next, (uint32_t)m);
+    q.dmin = kInf;
+  }
   if (lane == 0) {
     sm.fl_cnt[0][warp] = q.n;
     sm.fl_cnt[1][warp] = q.nf;
@@ -236,7 +246,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       if (OP == IRGL_OP_SSSP) wt = ld_stream(w + ed);
       cur = ld_label(p.lab + dst);
     }
-    const int k = act ? relax_with<OP>(p, rb, cur, sv, wt, dst) : 0;
+    const int k = act ? relax_with<OP>(p, rb, q, cur, sv, wt, dst) : 0;
     wpush<DIST>(sm, q, p, rb, k, dst);
   }
   // aligned body: two int4 groups per lane per iteration -> 8 independent label gathers in
@@ -271,20 +281,20 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       lb3 = ld_label(p.lab + cb.w);
     }
     {
-      const int k0 = aa ? relax_with<OP>(p, rb, la0, sv, wa.x, (uint32_t)ca.x) : 0;
-      const int k1 = aa ? relax_with<OP>(p, rb, la1, sv, wa.y, (uint32_t)ca.y) : 0;
-      const int k2 = aa ? relax_with<OP>(p, rb, la2, sv, wa.z, (uint32_t)ca.z) : 0;
-      const int k3 = aa ? relax_with<OP>(p, rb, la3, sv, wa.w, (uint32_t)ca.w) : 0;
+      const int k0 = aa ? relax_with<OP>(p, rb, q, la0, sv, wa.x, (uint32_t)ca.x) : 0;
+      const int k1 = aa ? relax_with<OP>(p, rb, q, la1, sv, wa.y, (uint32_t)ca.y) : 0;
+      const int k2 = aa ? relax_with<OP>(p, rb, q, la2, sv, wa.z, (uint32_t)ca.z) : 0;
+      const int k3 = aa ? relax_with<OP>(p, rb, q, la3, sv, wa.w, (uint32_t)ca.w) : 0;
       wpush<DIST>(sm, q, p, rb, k0, (uint32_t)ca.x);
       wpush<DIST>(sm, q, p, rb, k1, (uint32_t)ca.y);
       wpush<DIST>(sm, q, p, rb, k2, (uint32_t)ca.z);
       wpush<DIST>(sm, q, p, rb, k3, (uint32_t)ca.w);
     }
     if (__any_sync(FULL, ab)) {
-      const int k0 = ab ? relax_with<OP>(p, rb, lb0, sv, wb.x, (uint32_t)cb.x) : 0;
-      const int k1 = ab ? relax_with<OP>(p, rb, lb1, sv, wb.y, (uint32_t)cb.y) : 0;
-      const int k2 = ab ? relax_with<OP>(p, rb, lb2, sv, wb.z, (uint32_t)cb.z) : 0;
-      const int k3 = ab ? relax_with<OP>(p, rb, lb3, sv, wb.w, (uint32_t)cb.w) : 0;
+      const int k0 = ab ? relax_with<OP>(p, rb, q, lb0, sv, wb.x, (uint32_t)cb.x) : 0;
+      const int k1 = ab ? relax_with<OP>(p, rb, q, lb1, sv, wb.y, (uint32_t)cb.y) : 0;
+      const int k2 = ab ? relax_with<OP>(p, rb, q, lb2, sv, wb.z, (uint32_t)cb.z) : 0;
+      const int k3 = ab ? relax_with<OP>(p, rb, q, lb3, sv, wb.w, (uint32_t)cb.w) : 0;
       wpush<DIST>(sm, q, p, rb, k0, (uint32_t)cb.x);
       wpush<DIST>(sm, q, p, rb, k1, (uint32_t)cb.y);
       wpush<DIST>(sm, q, p, rb, k2, (uint32_t)cb.z);
@@ -296,7 +306,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
 // ---- one warp tile of 32 worklist items (consecutive mapping inside the tile) --------------------
 template <int OP, bool DIST>
 __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
-                                 uint32_t base, uint32_t width) {
+                                 uint32_t base, uint32_t width, int32_t dmin) {
   const int lane = lane_id();
   const uint32_t i = base + lane;
   const bool valid = (uint32_t)lane < width && i < rb.nin;
@@ -311,6 +321,23 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     if (OP != IRGL_OP_BFS) sv = ld_label_cg(p.lab + v);
   }
   int64_t deg = end - beg;
+  // SSSP deferral: a vertex whose distance is still far above the frontier minimum, weighted by
+  // the edges a premature expansion would waste, is kept for the next round (re-pushed with the
+  // round's stamp, so at most once) instead of expanded.  The frontier's minimum vertex always
+  // has slack <= 0, so every round expands at least one vertex (progress).
+  if (OP == IRGL_OP_SSSP && rb.defer_k > 0) {
+    const bool defer = valid && deg > 0 && ((int64_t)sv - dmin) * deg > rb.defer_k;
+    if (__any_sync(FULL, defer)) {
+      int kind = 0;
+      if (defer) {
+        const int32_t code = rb.stamp_id << 1;
+        kind = atomicExch(p.stamp + v, code) != code ? 1 : 0;
+        q.dmin = min(q.dmin, sv);
+        deg = 0;
+      }
+      wpush<DIST>(sm, q, p, rb, kind, v);
+    }
+  }
   {
     unsigned long long de = (unsigned long long)deg;
 #pragma unroll
@@ -407,7 +434,7 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
 #pragma unroll
     for (int j = 0; j < kWin; ++j) {
       if (wb + 32 * j >= total) break;  // warp-uniform
-      const int kk = act[j] ? relax_with<OP>(p, rb, cur[j], s[j], wt[j], dst[j]) : 0;
+      const int kk = act[j] ? relax_with<OP>(p, rb, q, cur[j], s[j], wt[j], dst[j]) : 0;
       wpush<DIST>(sm, q, p, rb, kk, dst[j]);
     }
   }
@@ -424,9 +451,10 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   uint32_t width = 32;
   while (width > 1 && (uint64_t)(width >> 1) * nwarps >= rb.nin) width >>= 1;
   const uint32_t ntiles = (rb.nin + width - 1) / width;
+  const int32_t dmin = rb.defer_k > 0 ? (int32_t)min(ld_ctl(rb.dmin_cur), (uint32_t)kInf) : kInf;
   uint32_t t = gw;
   while (t < ntiles) {
-    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width);
+    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin);
     if (ntiles <= nwarps) break;
     uint32_t nt = 0;
     if (lane_id() == 0) nt = nwarps + atomicAdd(rb.tile_ctr, 1u);
@@ -482,6 +510,7 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
           kind = k;
           if (kind == 2) mymin = min(mymin, (uint32_t)dv);
         }
+        if (k == 1) q.dmin = min(q.dmin, dv);
       }
     }
     wpush<false>(sm, q, p, rb, kind, v);
@@ -540,6 +569,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
   uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));  // round r's in-count = round r-1's out-count
+  if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[4 * a.trace_cap]));
   for (uint32_t r = 0;; ++r) {
     uint32_t* cin = cnt + slot3(a, r);
     uint32_t* cout = cnt + slot3(a, r + 1);
@@ -547,6 +577,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
       cnt[slot3(a, r + 2)] = 0;
       p.ctl->chunk_cnt[(r + 1) % 3] = 0;
       p.ctl->tile_ctr[(r + 1) % 3] = 0;
+      p.ctl->dmin[(r + 2) % 3] = 0xffffffffu;  // last read at the start of round r-1
     }
     RoundBufs rb;
     rb.in = (r & 1) ? a.buf_b : a.buf_a;
@@ -566,6 +597,9 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     rb.far_cap = a.far_cap;
     rb.threshold = threshold;
     rb.mf_acc = nullptr;
+    rb.defer_k = (OP == IRGL_OP_SSSP) ? a.defer_k : 0;
+    rb.dmin_cur = &p.ctl->dmin[r % 3];
+    rb.dmin_next = rb.defer_k > 0 ? &p.ctl->dmin[(r + 1) % 3] : nullptr;
     item_phase<OP, false>(sm, q, p, rb);
     wflush_all(sm, q, p, rb);
     grid.sync();  // SyncRunningThreads
@@ -618,6 +652,14 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     if (leader) {
       p.ctl->popped += rb.nin;
       p.ctl->pushes += nout;
+      if (a.trace && r < a.trace_cap) {  // per-round trace: end time, |in|, |out|, edges so far
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[4 * r + 0] = t;
+        a.trace[4 * r + 1] = rb.nin;
+        a.trace[4 * r + 2] = nout;
+        a.trace[4 * r + 3] = *(volatile unsigned long long*)&p.ctl->edges;
+      }
     }
     nin_next = nout;
     // Iterate termination: in empty (next round) [Or rounds >= max_rounds]
@@ -717,6 +759,9 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
     rb.far_cap = 0;
     rb.threshold = kInf;
     rb.mf_acc = &p.ctl->mf[r % 3];
+    rb.defer_k = 0;
+    rb.dmin_cur = nullptr;
+    rb.dmin_next = nullptr;
     uint64_t nf, mf;
     if (!bottom_up) {
       item_phase<IRGL_OP_BFS, false>(sm, q, p, rb);
@@ -788,7 +833,7 @@ __global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBu
     if (i < n) {
       v = items[i];
       const int32_t cur = ld_label(p.lab + v);
-      kind = relax_with<OP>(p, rb, cur, OP == IRGL_OP_BFS ? 0 : values[i], 0, v);
+      kind = relax_with<OP>(p, rb, q, cur, OP == IRGL_OP_BFS ? 0 : values[i], 0, v);
     }
     wpush<false>(sm, q, p, rb, kind, v);
   }

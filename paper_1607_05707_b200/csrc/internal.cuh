@@ -53,6 +53,8 @@ struct Ctl {
   unsigned long long bu_scanned;   // DO-BFS: edges examined by bottom-up rounds
   unsigned long long mst_w, mst_e; // MST: forest weight / edges
   uint32_t mst_cnt[2];             // MST: internal worklist counters
+  uint32_t dmin[3];                // SSSP deferral: min distance pushed into each round's out
+                                   // worklist (0xffffffff = unknown), rotated by round
 };
 
 // ---------------------------------------------------------------------------------------------

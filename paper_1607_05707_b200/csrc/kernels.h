@@ -44,6 +44,11 @@ struct RoundBufs {
   uint32_t far_cap;
   int32_t threshold;  // INT32_MAX: near-far off
   unsigned long long* mf_acc;  // DO-BFS: sum of degrees of pushed vertices (null: off)
+  // SSSP deferral (defer_k > 0): a popped v with (dist[v] - *dmin_cur) * deg(v) > defer_k is
+  // re-pushed instead of expanded; near pushes atomicMin their distance into *dmin_next
+  int64_t defer_k;
+  const uint32_t* dmin_cur;
+  uint32_t* dmin_next;
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
@@ -80,6 +85,9 @@ struct PersistArgs {
   int32_t dir_opt;     // BFS: 1 = direction-optimising (top-down / bottom-up switching)
   int64_t n;           // vertices (bottom-up sweeps)
   int64_t m;           // directed edges
+  int64_t defer_k;     // SSSP deferral budget (0 = off); cells Ctl::dmin rotate by round
+  unsigned long long* trace;  // optional per-round trace [4 * trace_cap + 1] (IRGL_ROUND_TRACE)
+  uint32_t trace_cap;
 };
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,

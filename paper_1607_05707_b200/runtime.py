@@ -68,7 +68,7 @@ class OpArgs(C.Structure):
     _fields_ = [("round_start", C.c_int64), ("guard", C.c_int64), ("pr_damping", C.c_double),
                 ("pr_tol", C.c_double), ("values", C.POINTER(C.c_int32)), ("nvalues", C.c_int64),
                 ("mapping", C.c_int32), ("threads", C.c_int32), ("delta", C.c_int32),
-                ("direction", C.c_int32), ("reserved", C.c_int32 * 4)]
+                ("direction", C.c_int32), ("defer", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class IterateOpts(C.Structure):
@@ -212,9 +212,10 @@ def nccl_unique_id() -> bytes:
 
 
 def _op_args(round_start=0, guard=0, pr_damping=0.0, pr_tol=0.0, values=None, mapping=0,
-             threads=0, delta=-1, direction=0):
+             threads=0, delta=-1, direction=0, defer=-1):
     a = OpArgs()
     a.delta = delta
+    a.defer = defer
     a.direction = direction
     a.round_start = round_start
     a.guard = guard
@@ -527,10 +528,13 @@ def bfs(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outli
 
 
 def sssp(ctx: Context, graph: Graph, src: int, *, pipe: Pipe | None = None, outline=-1,
-         delta=-1):
+         delta=-1, defer=-1):
+    """Data-driven SSSP (IrGL form of Listing 2 with dist[n]+weight(e) and atomicMin).
+    delta > 0: near-far piles; defer > 0: degree-scaled deferral budget; -1: runtime defaults.
+    Same distances in every mode."""
     p = pipe or ctx.pipe(graph.n)
     p.init_scalars([src])
-    st = ctx.iterate(SSSP, graph, p, outline=outline, delta=delta)
+    st = ctx.iterate(SSSP, graph, p, outline=outline, delta=delta, defer=defer)
     return ctx.read_result(SSSP, graph), st
 
 

@@ -145,6 +145,39 @@ def test_sssp_near_far_parity(ctx, irgl, oracle, delta, outline):
     np.testing.assert_array_equal(d, oracle.sssp(og, s))
 
 
+@pytest.mark.parametrize("defer", [0, 1, 64, 1024, 2048, 1 << 30])
+@pytest.mark.parametrize("outline", [0, 1])
+def test_sssp_deferral_parity(ctx, irgl, oracle, defer, outline):
+    """Degree-scaled deferral re-pushes instead of expanding: distances stay bit-exact, and a
+    small budget cuts the edges scanned (hubs expand near their final distance)."""
+    og = oracle.rmat(14)
+    g = _upload(ctx, og)
+    for s in og.sources(2):
+        s = int(s)
+        d, st = irgl.sssp(ctx, g, s, outline=outline, delta=0, defer=defer)
+        np.testing.assert_array_equal(d, oracle.sssp(og, s))
+
+
+def test_sssp_deferral_cuts_rescans(ctx, irgl, oracle):
+    og = oracle.rmat(15)
+    g = _upload(ctx, og)
+    s = int(og.sources(1)[0])
+    _, plain = irgl.sssp(ctx, g, s, delta=0, defer=0)
+    d, dfr = irgl.sssp(ctx, g, s, delta=0, defer=1024)
+    np.testing.assert_array_equal(d, oracle.sssp(og, s))
+    assert dfr.edges < plain.edges
+
+
+@pytest.mark.parametrize("defer", [16, 2048])
+def test_sssp_deferral_with_near_far_and_grid(ctx, irgl, oracle, defer):
+    og = oracle.grid(64, 48, diag=True)
+    g = _upload(ctx, og)
+    for outline in (0, 1):
+        for delta in (0, 5):
+            d, _ = irgl.sssp(ctx, g, 0, outline=outline, delta=delta, defer=defer)
+            np.testing.assert_array_equal(d, oracle.sssp(og, 0))
+
+
 def test_sssp_device_generated_graph(ctx, irgl, oracle):
     og = oracle.rmat(15)
     g = ctx.generate_rmat(15)
@@ -232,8 +265,8 @@ def test_partitioned_bfs_sssp_parity(irgl, oracle, P):
             lv, st = irgl.bfs(c, g, s)
             np.testing.assert_array_equal(lv, ref)
             assert st.rounds == ecc + 1
-            for delta in (0, 64):
-                d, st = irgl.sssp(c, g, s, delta=delta)
+            for delta, defer in ((0, 0), (64, 0), (0, 1024), (0, 8)):
+                d, st = irgl.sssp(c, g, s, delta=delta, defer=defer)
                 np.testing.assert_array_equal(d, oracle.sssp(og, s))
                 assert st.remote_updates > 0
 
@@ -268,8 +301,8 @@ def test_nccl_transport_single_rank(irgl, oracle, P):
             s = int(s)
             lv, st = irgl.bfs(c, g, s)
             np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
-            for delta in (0, 8):
-                d, st = irgl.sssp(c, g, s, delta=delta)
+            for delta, defer in ((0, 0), (8, 0), (0, -1)):
+                d, st = irgl.sssp(c, g, s, delta=delta, defer=defer)
                 np.testing.assert_array_equal(d, oracle.sssp(og, s))
             if P > 1:
                 assert st.exchange_bytes > 0
