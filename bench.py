@@ -63,47 +63,76 @@ def pick_sources(n, degree_of, count=16, seed=7):
 
 # ---- clocks sampler ---------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown")
+    """SM clock and throttle reasons sampled DURING the timed region: NVML polled every 2 ms from
+    a thread (nvidia-smi's 100 ms loop misses a region of a few tens of ms); nvidia-smi fallback."""
+    NAMES = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
     def __init__(self, gpu_index):
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, reasons bitmask-decoded tuple)
+        self.stop_ev = threading.Event()
         self.proc = None
+        self.t = None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(int(gpu_index))
+            bits = (N.nvmlClocksEventReasonSwPowerCap, N.nvmlClocksEventReasonHwSlowdown,
+                    N.nvmlClocksEventReasonHwThermalSlowdown, N.nvmlClocksEventReasonSwThermalSlowdown)
+            mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, mx, tuple(n for n, b in zip(self.NAMES, bits) if r & b)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
+            self.kind = "nvml"
+            return
+        except Exception:
+            pass
+        try:
+            fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+                      "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                      "clocks_event_reasons.sw_thermal_slowdown")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={fields}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def read():
+                for line in self.proc.stdout:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                        self.rows.append((float(parts[0]), float(parts[1]),
+                                          tuple(n for n, v in zip(self.NAMES, parts[2:]) if v == "Active")))
+            self.t = threading.Thread(target=read, daemon=True)
+            self.t.start()
+            self.kind = "nvidia-smi"
         except Exception:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
-
     def stop(self):
-        if not self.proc:
-            return None
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
+        self.stop_ev.set()
+        if self.proc:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
         if not self.rows:
             return None
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted({n for r in self.rows for n in r[2]}),
+                "samples": len(self.rows), "source": self.kind}
 
 
 # ---- distributed plumbing (gloo for host-side barrier / reductions / NCCL id broadcast) ---------
@@ -377,7 +406,7 @@ def _local_row_ptr(ctx, g):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="irgl", choices=["irgl", "reference"])
     ap.add_argument("--op", default="sssp", choices=["sssp", "bfs"])

@@ -704,13 +704,16 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   const char* tr = getenv("IRGL_ROUND_TRACE");
   if (tr && *tr == '1' && !pa.dir_opt) {
     pa.trace_cap = 4096;
-    CK(cudaMallocAsync(&pa.trace, (4 * (size_t)pa.trace_cap + 1) * 8, pr.st));
+    CK(cudaMallocAsync(&pa.trace, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
+    CK(cudaMemsetAsync(pa.trace, 0, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
   }
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
   CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(pp.ctl->tile_ctr), pr.st));
   CK(cudaMemsetAsync(pp.ctl->far_cnt, 0, sizeof(pp.ctl->far_cnt), pr.st));
   CK(cudaMemsetAsync(pp.ctl->dmin, 0xff, sizeof(pp.ctl->dmin), pr.st));  // round 0: no deferral
+  CK(cudaMemsetAsync(&pp.ctl->gb_arrive, 0, sizeof(unsigned int), pr.st));  // grid_sync_bcast state
+  CK(cudaMemsetAsync(&pp.ctl->gb_release, 0, sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
   CK(cudaMemsetAsync(pp.ctl->mf, 0, sizeof(pp.ctl->mf) + sizeof(pp.ctl->bu_found) + 8, pr.st));
@@ -726,16 +729,18 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     stt->kernel_ms += kms;
   }
   if (pa.trace) {
-    std::vector<unsigned long long> t(4 * (size_t)pa.trace_cap + 1);
+    std::vector<unsigned long long> t(8 * (size_t)pa.trace_cap + 1);
     CK(cudaMemcpy(t.data(), pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
     CK(cudaFree(pa.trace));
-    unsigned long long prev = t[4 * (size_t)pa.trace_cap], e0 = 0;
+    unsigned long long prev = t[8 * (size_t)pa.trace_cap], e0 = 0;
+    auto us = [&](unsigned long long x) { return x ? (x - prev) * 1e-3 : -1.0; };
     for (uint64_t r = 0; r < std::min<uint64_t>(h.rounds, pa.trace_cap); ++r) {
-      fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu\n", op,
-              (unsigned long long)r, (t[4 * r] - prev) * 1e-3, t[4 * r + 1], t[4 * r + 2],
-              t[4 * r + 3] - e0);
-      prev = t[4 * r];
-      e0 = t[4 * r + 3];
+      const unsigned long long* q = &t[8 * r];
+      // us = whole round; item / flush / sync1 / chunk = leader-thread timestamps since round start
+      fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu item=%.2f flush=%.2f sync1=%.2f chunk=%.2f\n",
+              op, (unsigned long long)r, us(q[0]), q[1], q[2], q[3] - e0, us(q[4]), us(q[5]), us(q[6]), us(q[7]));
+      prev = q[0];
+      e0 = q[3];
     }
   }
   if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
@@ -1028,7 +1033,7 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
     g->maxdeg = std::max(g->maxdeg, gp.maxdeg);
     const ExpandCfg ec = expand_cfg(ctx);
     const int64_t nch = gp.m / ec.chunk_edges + gp.m / ec.cta_t + 1024;
-    gp.chunk_cap = (uint32_t)std::min<int64_t>(nch, 0xffffffffll);
+    gp.chunk_cap = (uint32_t)std::min<int64_t>(nch, 0xffffffll);  // 24-bit count in the barrier word
     CK(cudaMalloc(&gp.chunks, (size_t)gp.chunk_cap * sizeof(ChunkDesc)));
     if (P > 1) {
       const int64_t tot = (int64_t)P * g->part_size;

@@ -35,6 +35,10 @@ constexpr int kWBuf = 256;  // per-warp push staging entries
 #ifndef IRGL_MINB
 #define IRGL_MINB 6  // min co-resident CTAs per SM requested from ptxas: 40 registers, 48 warps/SM (tools/sweep.py)
 #endif
+#ifndef IRGL_MINB_SSSP
+#define IRGL_MINB_SSSP 4  // SSSP (weights + batched relax): 64 registers, 32 warps/SM, no spills in the hot loop
+#endif
+constexpr int minb_for(int op) { return op == IRGL_OP_SSSP ? IRGL_MINB_SSSP : IRGL_MINB; }
 
 struct Smem {
   uint32_t wbuf[kWarps][kWBuf];   // near pushes (E2)
@@ -98,6 +102,50 @@ __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb,
     const int32_t code = (rb.stamp_id << 1) | (kind - 1);
     if (atomicExch(p.stamp + dst, code) == code) return 0;
     return kind;
+  }
+}
+
+// Batched relax of one lane's K edges (same decisions as relax_with, ILP-friendly): every atomic
+// of the batch is issued before any result is consumed, so a lane pays one L2 round trip per
+// batch instead of one or two dependent round trips per edge (hub rounds are latency-bound).
+//  BFS         : CAS(INF -> LEVEL) on each candidate (cur == INF); push where the CAS won.
+//  SSSP / CC_LP: candidates nd < cur get a fire-and-forget atomic min (RED, no return) and a
+//                stamp exchange issued together; a candidate pushes where it claimed the round's
+//                stamp.  Every vertex lowered this round had a candidate, and every candidate's
+//                vertex ends in the pile exactly once (the claimer pushes), so the out worklist is
+//                the same set relax_with builds; a candidate that lost the min race still holds
+//                <= nd, which keeps the deferral minimum (q.dmin) a valid bound.  The REDs are
+//                ordered before the next round by the grid barrier / kernel boundary.
+template <int OP, int K>
+__device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& rb, WarpQ& q,
+                                            const bool (&act)[K], const int32_t (&cur)[K],
+                                            const int32_t (&sv)[K], const int32_t (&wt)[K],
+                                            const uint32_t (&dst)[K], int (&kind)[K]) {
+  if (OP == IRGL_OP_BFS) {
+    int32_t old[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      old[j] = (act[j] && cur[j] == kInf) ? atomicCAS(p.lab + dst[j], kInf, rb.level) : 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) kind[j] = (act[j] && cur[j] == kInf && old[j] == kInf) ? 1 : 0;
+  } else {
+    int32_t nd[K], code[K], prev[K];
+    bool cand[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      nd[j] = (OP == IRGL_OP_SSSP) ? sv[j] + wt[j] : sv[j];
+      cand[j] = act[j] && nd[j] < cur[j];
+      kind[j] = (OP == IRGL_OP_SSSP && nd[j] >= rb.threshold) ? 2 : 1;
+      code[j] = (rb.stamp_id << 1) | (kind[j] - 1);
+      if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) prev[j] = cand[j] ? atomicExch(p.stamp + dst[j], code[j]) : code[j];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (OP == IRGL_OP_SSSP && cand[j] && kind[j] == 1) q.dmin = min(q.dmin, nd[j]);
+      kind[j] = (cand[j] && prev[j] != code[j]) ? kind[j] : 0;
+    }
   }
 }
 
@@ -246,8 +294,12 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       if (OP == IRGL_OP_SSSP) wt = ld_stream(w + ed);
       cur = ld_label(p.lab + dst);
     }
-    const int k = act ? relax_with<OP>(p, rb, q, cur, sv, wt, dst) : 0;
-    wpush<DIST>(sm, q, p, rb, k, dst);
+    const bool a1v[1] = {act};
+    const int32_t c1[1] = {cur}, s1[1] = {sv}, w1[1] = {wt};
+    const uint32_t d1[1] = {dst};
+    int k1[1];
+    relax_batch<OP, 1>(p, rb, q, a1v, c1, s1, w1, d1, k1);
+    wpush<DIST>(sm, q, p, rb, k1[0], dst);
   }
   // aligned body: two int4 groups per lane per iteration -> 8 independent label gathers in
   // flight per lane (memory-level parallelism for the latency-bound gathers)
@@ -267,38 +319,21 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       cb = ld_stream_v4(col + 4 * qb);
       if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(w + 4 * qb);
     }
-    int32_t la0 = 0, la1 = 0, la2 = 0, la3 = 0, lb0 = 0, lb1 = 0, lb2 = 0, lb3 = 0;
-    if (aa) {
-      la0 = ld_label(p.lab + ca.x);
-      la1 = ld_label(p.lab + ca.y);
-      la2 = ld_label(p.lab + ca.z);
-      la3 = ld_label(p.lab + ca.w);
-    }
-    if (ab) {
-      lb0 = ld_label(p.lab + cb.x);
-      lb1 = ld_label(p.lab + cb.y);
-      lb2 = ld_label(p.lab + cb.z);
-      lb3 = ld_label(p.lab + cb.w);
-    }
-    {
-      const int k0 = aa ? relax_with<OP>(p, rb, q, la0, sv, wa.x, (uint32_t)ca.x) : 0;
-      const int k1 = aa ? relax_with<OP>(p, rb, q, la1, sv, wa.y, (uint32_t)ca.y) : 0;
-      const int k2 = aa ? relax_with<OP>(p, rb, q, la2, sv, wa.z, (uint32_t)ca.z) : 0;
-      const int k3 = aa ? relax_with<OP>(p, rb, q, la3, sv, wa.w, (uint32_t)ca.w) : 0;
-      wpush<DIST>(sm, q, p, rb, k0, (uint32_t)ca.x);
-      wpush<DIST>(sm, q, p, rb, k1, (uint32_t)ca.y);
-      wpush<DIST>(sm, q, p, rb, k2, (uint32_t)ca.z);
-      wpush<DIST>(sm, q, p, rb, k3, (uint32_t)ca.w);
-    }
+    const bool act8[8] = {aa, aa, aa, aa, ab, ab, ab, ab};
+    const uint32_t d8[8] = {(uint32_t)ca.x, (uint32_t)ca.y, (uint32_t)ca.z, (uint32_t)ca.w,
+                            (uint32_t)cb.x, (uint32_t)cb.y, (uint32_t)cb.z, (uint32_t)cb.w};
+    const int32_t w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+    const int32_t s8[8] = {sv, sv, sv, sv, sv, sv, sv, sv};
+    int32_t c8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c8[j] = act8[j] ? ld_label(p.lab + d8[j]) : 0;
+    int k8[8];
+    relax_batch<OP, 8>(p, rb, q, act8, c8, s8, w8, d8, k8);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wpush<DIST>(sm, q, p, rb, k8[j], d8[j]);
     if (__any_sync(FULL, ab)) {
-      const int k0 = ab ? relax_with<OP>(p, rb, q, lb0, sv, wb.x, (uint32_t)cb.x) : 0;
-      const int k1 = ab ? relax_with<OP>(p, rb, q, lb1, sv, wb.y, (uint32_t)cb.y) : 0;
-      const int k2 = ab ? relax_with<OP>(p, rb, q, lb2, sv, wb.z, (uint32_t)cb.z) : 0;
-      const int k3 = ab ? relax_with<OP>(p, rb, q, lb3, sv, wb.w, (uint32_t)cb.w) : 0;
-      wpush<DIST>(sm, q, p, rb, k0, (uint32_t)cb.x);
-      wpush<DIST>(sm, q, p, rb, k1, (uint32_t)cb.y);
-      wpush<DIST>(sm, q, p, rb, k2, (uint32_t)cb.z);
-      wpush<DIST>(sm, q, p, rb, k3, (uint32_t)cb.w);
+#pragma unroll
+      for (int j = 4; j < 8; ++j) wpush<DIST>(sm, q, p, rb, k8[j], d8[j]);
     }
   }
 }
@@ -431,11 +466,12 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     }
 #pragma unroll
     for (int j = 0; j < kWin; ++j) cur[j] = act[j] ? ld_label(p.lab + dst[j]) : 0;
+    int kk[kWin];
+    relax_batch<OP, kWin>(p, rb, q, act, cur, s, wt, dst, kk);
 #pragma unroll
     for (int j = 0; j < kWin; ++j) {
       if (wb + 32 * j >= total) break;  // warp-uniform
-      const int kk = act[j] ? relax_with<OP>(p, rb, q, cur[j], s[j], wt[j], dst[j]) : 0;
-      wpush<DIST>(sm, q, p, rb, kk, dst[j]);
+      wpush<DIST>(sm, q, p, rb, kk[j], dst[j]);
     }
   }
 }
@@ -451,7 +487,9 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   uint32_t width = 32;
   while (width > 1 && (uint64_t)(width >> 1) * nwarps >= rb.nin) width >>= 1;
   const uint32_t ntiles = (rb.nin + width - 1) / width;
-  const int32_t dmin = rb.defer_k > 0 ? (int32_t)min(ld_ctl(rb.dmin_cur), (uint32_t)kInf) : kInf;
+  const int32_t dmin = rb.defer_k <= 0 ? kInf
+                       : rb.dmin_cur ? (int32_t)min(ld_ctl(rb.dmin_cur), (uint32_t)kInf)
+                                     : rb.dmin_val;
   uint32_t t = gw;
   while (t < ntiles) {
     expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin);
@@ -521,7 +559,7 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
 }
 
 template <int OP, bool DIST>
-__global__ void __launch_bounds__(kBlock, IRGL_MINB) expand_kernel(KParams p, RoundBufs rb) {
+__global__ void __launch_bounds__(kBlock, minb_for(OP)) expand_kernel(KParams p, RoundBufs rb) {
   __shared__ Smem sm;
   WarpQ q;
   item_phase<OP, DIST>(sm, q, p, rb);
@@ -529,7 +567,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) expand_kernel(KParams p, Ro
 }
 
 template <int OP, bool DIST>
-__global__ void __launch_bounds__(kBlock, IRGL_MINB) chunk_kernel(KParams p, RoundBufs rb) {
+__global__ void __launch_bounds__(kBlock, minb_for(OP)) chunk_kernel(KParams p, RoundBufs rb) {
   __shared__ Smem sm;
   WarpQ q;
   chunk_phase<OP, DIST>(sm, q, p, rb, ld_ctl(rb.chunk_cnt));
@@ -551,13 +589,54 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) far_split_kernel(KParams p,
 // Worklist buffers alternate by round parity; counters rotate over three slots so the counter
 // cleared during round r (slot (r+2)%3, last read during round r-1) is the out-counter of round
 // r+1: no extra barrier is needed to reset it ("swap in/out and reset out").
+// SyncRunningThreads with a broadcast: every CTA arrives (bar.sync, then one
+// gpu-scope fence + atomic by thread 0); the LAST arriver evaluates `payload()` (the round's
+// counters, final once everyone has arrived) and publishes {8-bit barrier tag, 56-bit payload}
+// with one release store; the others spin on that word with acquire loads.  Compared with
+// cg::grid.sync() followed by every thread re-reading the counters, the counters cost one L2 read
+// by one thread instead of one same-address read per warp of the grid (~7,000 requests to one L2
+// slice per round), and the value arrives with the release itself.  `post(w)` runs on thread 0
+// of every CTA after the release (e.g. per-CTA reads of per-round cells into shared memory).
+// The arrival counter and tag are monotonic within a launch (both wrap consistently mod 2^32 /
+// 2^8: no CTA can be a whole barrier ahead of another), and the host zeroes them before it.
+template <class F, class G>
+__device__ __forceinline__ unsigned long long grid_sync_bcast(Ctl* ctl, uint32_t& idx,
+                                                              unsigned long long* slot,
+                                                              F&& payload, G&& post) {
+  ++idx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long tag = (unsigned long long)(idx & 0xffu) << 56;
+    __threadfence();
+    const unsigned int old = atomicAdd(&ctl->gb_arrive, 1u);
+    unsigned long long w;
+    if (old == idx * gridDim.x - 1u) {
+      __threadfence();
+      w = tag | (payload() & ((1ull << 56) - 1));
+      st_release_u64(&ctl->gb_release, w);
+    } else {
+      do {
+        w = ld_acquire_u64(&ctl->gb_release);
+      } while ((w & (0xffull << 56)) != tag);
+    }
+    w &= (1ull << 56) - 1;
+    post(w);
+    *slot = w;
+  }
+  __syncthreads();
+  return *slot;
+}
+__device__ __forceinline__ unsigned long long pack_counts(uint32_t nch, uint32_t nout) {
+  return ((unsigned long long)min(nch, 0xffffffu) << 32) | nout;
+}
+
 __device__ __forceinline__ int slot3(const PersistArgs& a, uint32_t i) {
   const uint32_t m = i % 3;
   return m == 0 ? a.slot[0] : (m == 1 ? a.slot[1] : a.slot[2]);
 }
 
 template <int OP>
-__global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p, PersistArgs a) {
+__global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
   cg::grid_group grid = cg::this_grid();
   WarpQ q;
@@ -569,7 +648,12 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
   uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));  // round r's in-count = round r-1's out-count
-  if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[4 * a.trace_cap]));
+  __shared__ unsigned long long bslot;  // barrier broadcast
+  __shared__ int32_t s_dmin;            // deferral: frontier minimum of the next round
+  uint32_t bidx = 0;
+  const bool dfr = (OP == IRGL_OP_SSSP) && a.defer_k > 0;
+  if (threadIdx.x == 0) s_dmin = dfr ? (int32_t)min(ld_ctl(&p.ctl->dmin[0]), (uint32_t)kInf) : kInf;
+  if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * a.trace_cap]));
   for (uint32_t r = 0;; ++r) {
     uint32_t* cin = cnt + slot3(a, r);
     uint32_t* cout = cnt + slot3(a, r + 1);
@@ -598,19 +682,31 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
     rb.threshold = threshold;
     rb.mf_acc = nullptr;
     rb.defer_k = (OP == IRGL_OP_SSSP) ? a.defer_k : 0;
-    rb.dmin_cur = &p.ctl->dmin[r % 3];
+    rb.dmin_cur = nullptr;
+    rb.dmin_val = s_dmin;  // written by thread 0 before the barrier that ended round r-1
     rb.dmin_next = rb.defer_k > 0 ? &p.ctl->dmin[(r + 1) % 3] : nullptr;
     item_phase<OP, false>(sm, q, p, rb);
+    if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 4]));
     wflush_all(sm, q, p, rb);
-    grid.sync();  // SyncRunningThreads
-    // both counters in flight together (one L2 round trip on the round's critical path)
-    const uint32_t nch = ld_ctl(rb.chunk_cnt);
-    uint32_t nout = ld_ctl(cout);
+    if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 5]));
+    // the deferral minimum of round r+1 is final at the round's last barrier: thread 0 of each CTA
+    // fetches it into shared memory there (no per-warp reads of one hot cell)
+    auto fetch_dmin = [&]() {
+      if (dfr) s_dmin = (int32_t)min(ld_ctl(&p.ctl->dmin[(r + 1) % 3]), (uint32_t)kInf);
+    };
+    unsigned long long w = grid_sync_bcast(
+        p.ctl, bidx, &bslot, [&]() { return pack_counts(ld_ctl(rb.chunk_cnt), ld_ctl(cout)); },
+        [&](unsigned long long v) { if ((v >> 32) == 0) fetch_dmin(); });
+    if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 6]));
+    const uint32_t nch = (uint32_t)(w >> 32);
+    uint32_t nout = (uint32_t)w;
     if (nch) {
       chunk_phase<OP, false>(sm, q, p, rb, nch);
       wflush_all(sm, q, p, rb);
-      grid.sync();
-      nout = ld_ctl(cout);
+      w = grid_sync_bcast(p.ctl, bidx, &bslot, [&]() { return pack_counts(0, ld_ctl(cout)); },
+                          [&](unsigned long long) { fetch_dmin(); });
+      nout = (uint32_t)w;
+    if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 7]));
     }
     if (nf) {
       // near frontier exhausted: advance the threshold and split the far pile; a pile past half
@@ -655,10 +751,10 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_kernel(KParams p
       if (a.trace && r < a.trace_cap) {  // per-round trace: end time, |in|, |out|, edges so far
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.trace[4 * r + 0] = t;
-        a.trace[4 * r + 1] = rb.nin;
-        a.trace[4 * r + 2] = nout;
-        a.trace[4 * r + 3] = *(volatile unsigned long long*)&p.ctl->edges;
+        a.trace[8 * r + 0] = t;
+        a.trace[8 * r + 1] = rb.nin;
+        a.trace[8 * r + 2] = nout;
+        a.trace[8 * r + 3] = *(volatile unsigned long long*)&p.ctl->edges;
       }
     }
     nin_next = nout;

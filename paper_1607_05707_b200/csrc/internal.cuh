@@ -55,6 +55,10 @@ struct Ctl {
   uint32_t mst_cnt[2];             // MST: internal worklist counters
   uint32_t dmin[3];                // SSSP deferral: min distance pushed into each round's out
                                    // worklist (0xffffffff = unknown), rotated by round
+  // grid barrier of the persistent kernels (grid_sync_bcast): monotonic arrival counter and the
+  // release word {barrier tag, payload}, on separate L2 lines; zeroed before every launch
+  alignas(256) unsigned int gb_arrive;
+  alignas(256) unsigned long long gb_release;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -93,6 +97,15 @@ __device__ __forceinline__ int32_t ld_label(const int32_t* p) {
   int32_t r;
   asm volatile("ld.global.s32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long r;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 }  // namespace irgl

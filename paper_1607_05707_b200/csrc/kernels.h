@@ -47,8 +47,9 @@ struct RoundBufs {
   // SSSP deferral (defer_k > 0): a popped v with (dist[v] - *dmin_cur) * deg(v) > defer_k is
   // re-pushed instead of expanded; near pushes atomicMin their distance into *dmin_next
   int64_t defer_k;
-  const uint32_t* dmin_cur;
+  const uint32_t* dmin_cur;  // null: use dmin_val (persistent kernel: broadcast at the barrier)
   uint32_t* dmin_next;
+  int32_t dmin_val;
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------

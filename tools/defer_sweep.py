@@ -22,6 +22,11 @@ for s in srcs:
     p.init_scalars([s])
     E += ctx.iterate(irgl.BFS, g, p).edges
 E /= len(srcs)
+tb = 0
+for s in srcs:
+    p.init_scalars([s])
+    tb += ctx.iterate(irgl.BFS, g, p).device_ms
+print(f"RMAT-{scale} BFS: {tb/len(srcs):.3f} ms GTEPS={E/2/(tb/len(srcs))/1e6:.1f}", flush=True)
 ref = None
 for K in Ks:
     for s in srcs[:2]:  # warm
