@@ -93,9 +93,12 @@ typedef struct irgl_config {
   int32_t outline;               /* default for irgl_iterate: 0 host loop, 1 outlined, -1 auto */
   int32_t blocks_per_sm;         /* FixedFromSM multiplier; 0 = occupancy    */
   int32_t retry_serialize_after; /* Retry conflict management; 0 -> 4          */
-  int32_t warp_threshold;        /* degree >= -> warp-cooperative expansion; 0 -> 128           */
-  int32_t cta_threshold;         /* degree >= -> CTA chunk list (grid edge-balanced); 0 -> 512  */
-  int32_t chunk_edges;           /* edges per CTA chunk; 0 -> 1024                              */
+  int32_t warp_threshold;        /* degree >= -> edge chunks drained by every warp of the grid
+                                    (edge-balanced); below: the warp tile's fine-grained gather;
+                                    0 -> 128                                                    */
+  int32_t cta_threshold;         /* rounds with at most one tile per warp: degrees below this are
+                                    expanded by the popping warp (no chunk phase); 0 -> 512      */
+  int32_t chunk_edges;           /* edges per chunk descriptor (<= 65535); 0 -> 512            */
   int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
   int32_t reserved[8];

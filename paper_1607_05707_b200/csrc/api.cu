@@ -128,11 +128,14 @@ static irgl_status_t fail(irgl_ctx* ctx, irgl_status_t st, const char* rule, con
 
 static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   ExpandCfg ec;
-  // degree < warp_t: warp-scan gather (4 windows / lane in flight); < cta_t: one warp per vertex
-  // (int4); >= cta_t: CTA chunks.  Defaults from the RMAT-22 sweep (profiles/r1_sweep.txt).
+  // degree < warp_t: the warp tile's fine-grained gather; >= warp_t: edge chunks of chunk_edges
+  // drained by all warps (edge-balanced), except in small rounds (one tile per warp) where degrees
+  // below cta_t are expanded by the popping warp.  Defaults from the RMAT-22 sweep
+  // (profiles/r1s2_sched_sweep.txt).
   ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 128;
-  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 512;        // RMAT-22 sweep
-  ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 1024;
+  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 512;
+  ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 512;
+  ec.chunk_edges = std::max(4, std::min(ec.chunk_edges, 65535));  // 16-bit length in ChunkDesc
   if (ec.warp_t < 1) ec.warp_t = 1;
   if (ec.cta_t < ec.warp_t) ec.cta_t = ec.warp_t;
   return ec;
@@ -1032,8 +1035,10 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
     CK(max_degree(gp.row_ptr, gp.hi - gp.lo, &gp.maxdeg, ctx->parts[l].st));
     g->maxdeg = std::max(g->maxdeg, gp.maxdeg);
     const ExpandCfg ec = expand_cfg(ctx);
-    const int64_t nch = gp.m / ec.chunk_edges + gp.m / ec.cta_t + 1024;
-    gp.chunk_cap = (uint32_t)std::min<int64_t>(nch, 0xffffffll);  // 24-bit count in the barrier word
+    // every frontier vertex with degree >= warp_t adds <= deg/chunk_edges + 1 descriptors; a
+    // vertex can be in a frontier twice (near-far split), hence the factor 2
+    const int64_t nch = 2 * (gp.m / ec.chunk_edges + std::min<int64_t>(gp.m / ec.warp_t, gp.hi - gp.lo)) + 1024;
+    gp.chunk_cap = (uint32_t)std::min<int64_t>(nch, 0x3ffffffll);  // 26-bit count in the barrier word
     CK(cudaMalloc(&gp.chunks, (size_t)gp.chunk_cap * sizeof(ChunkDesc)));
     if (P > 1) {
       const int64_t tot = (int64_t)P * g->part_size;
@@ -1243,8 +1248,8 @@ irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const i
     for (int64_t i = 0; i <= nloc; ++i) rp[i] = row_ptr[gp.lo + i] - e0;
     CK(cudaMalloc(&gp.row_ptr, (nloc + 1) * 8));
     CK(cudaMemcpy(gp.row_ptr, rp.data(), (nloc + 1) * 8, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&gp.col, std::max<int64_t>(gp.m, 4) * 4));
-    CK(cudaMalloc(&gp.w, std::max<int64_t>(gp.m, 4) * 4));
+    CK(cudaMalloc(&gp.col, (gp.m + 4) * 4));  // +4: int4 group loads of the last edges
+    CK(cudaMalloc(&gp.w, (gp.m + 4) * 4));
     if (gp.m > 0) {
       CK(cudaMemcpy(gp.col, col + e0, gp.m * 4, cudaMemcpyHostToDevice));
       if (weight) CK(cudaMemcpy(gp.w, weight + e0, gp.m * 4, cudaMemcpyHostToDevice));
@@ -1622,10 +1627,12 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
       }
     }
     const int dir_opt = args ? args->direction : 0;
-    if (dir_opt && !(outline && ctx->ptotal() == 1))
+    if (dir_opt && !(outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30)))
       return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
                   "direction-optimising BFS runs outlined on one partition");
-    if (outline && ctx->ptotal() == 1) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
+    // the outlined kernel's barrier word carries the out count in 30 bits
+    if (outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30))
+      s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s != IRGL_OK) return s;
     s = pipe_counters(ctx, pipe, &st);  // edges scanned / remote updates

@@ -1,16 +1,17 @@
 // expand.cu — the data-driven hot path: ForAll over the in-worklist x ForAll over edges(n)
 // for BFS (Listing 2), SSSP and CC_LP, lowered B200-first:
 //
-//  E1  nested-parallelism edge scheduler.  Work is handed out in warp tiles of 32 popped
+//  E1  nested-parallelism edge scheduler.  Work is handed out in warp tiles of up to 32 popped
 //      vertices (first tile static, then dynamic from a per-round counter); each vertex's edges go
 //      to
-//        - one thread          (degree < warp_t): warp-wide scan of the small degrees, each lane
-//                              finds the owner of its edge slot with a 5-step shuffle search
-//                              ("fine-grained" gather, no shared memory, no CTA barrier);
-//        - one warp            (warp_t <= degree < cta_t), 128-bit col/weight loads;
-//        - CTA chunks          (degree >= cta_t): split into chunk_edges-sized descriptors that
-//                              every CTA of the grid drains in a second phase (edge-balanced,
-//                              so super-hubs do not serialise on one CTA).
+//        - the warp's fine-grained gather (degree < warp_t): warp-wide scan of the small degrees,
+//                              each lane finds the owner of its edge slot with a 5-step shuffle
+//                              search (no shared memory, no CTA barrier);
+//        - edge chunks         (degree >= warp_t): chunk_edges-sized descriptors (one reservation
+//                              per warp tile) that every warp of the grid drains in a second,
+//                              edge-balanced phase, 128-bit col/weight loads, 8 gathers and all
+//                              atomics of a lane in flight at once (super-hubs do not serialise,
+//                              and no warp holds a long serial tail of mid-degree vertices).
 //  E2  cooperative conversion of pushes: warp __ballot_sync/__popc aggregation into a per-warp
 //      shared-memory staging queue; one global atomic reservation per 224+ staged items.
 //  E3  iteration outlining: the Iterate loop as one cooperative persistent kernel with a grid
@@ -272,43 +273,21 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
   q.edges = 0;
 }
 
-// ---- edge-range processing by a group of G lanes (G = 32 warp, G = kBlock CTA) -------------------
-// Head/tail (misaligned) edges in one predicated step, the aligned body with 128-bit loads:
-// each lane issues 4 independent label gathers before its 4 decisions (ILP).
-template <int OP, bool DIST, int G>
+// ---- edge-range processing by one warp --------------------------------------------------------
+// The range [b, e) is covered by the aligned 128-bit groups of col/weight that overlap it; each
+// lane takes two groups per iteration and masks the edges outside the range (the CSR arrays are
+// padded by 4 entries, so the last group is always in bounds).  No separate head/tail step: all 8
+// label gathers and all atomics of a lane are in flight together (relax_batch).
+template <int OP, bool DIST>
 __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams& p,
                                               const RoundBufs& rb, int64_t b, int64_t e,
                                               int32_t sv, int gl) {
   const int32_t* __restrict__ col = p.g.col;
   const int32_t* __restrict__ w = p.g.w;
-  const int64_t a0 = min((b + 3) & ~int64_t(3), e);
-  const int64_t a1 = max(e & ~int64_t(3), a0);
-  const int nh = (int)(a0 - b), nt = (int)(e - a1);
-  if (nh + nt > 0 && (G == 32 || (gl >> 5) == 0)) {  // first warp of the group (warp-uniform)
-    const bool act = gl < nh + nt;
-    const int64_t ed = gl < nh ? b + gl : a1 + (gl - nh);
-    uint32_t dst = 0;
-    int32_t wt = 0, cur = 0;
-    if (act) {
-      dst = (uint32_t)ld_stream(col + ed);
-      if (OP == IRGL_OP_SSSP) wt = ld_stream(w + ed);
-      cur = ld_label(p.lab + dst);
-    }
-    const bool a1v[1] = {act};
-    const int32_t c1[1] = {cur}, s1[1] = {sv}, w1[1] = {wt};
-    const uint32_t d1[1] = {dst};
-    int k1[1];
-    relax_batch<OP, 1>(p, rb, q, a1v, c1, s1, w1, d1, k1);
-    wpush<DIST>(sm, q, p, rb, k1[0], dst);
-  }
-  // aligned body: two int4 groups per lane per iteration -> 8 independent label gathers in
-  // flight per lane (memory-level parallelism for the latency-bound gathers)
-  const int64_t q1 = a1 >> 2;
-  for (int64_t q0 = a0 >> 2; q0 < q1; q0 += 2 * G) {
-    // a warp whose 32 lanes are all past the end skips the body (stays warp-uniform)
-    if (G > 32 && q0 + (gl & ~31) >= q1) break;
-    const int64_t qa = q0 + gl, qb = q0 + G + gl;
-    const bool aa = qa < q1, ab = qb < q1;
+  const int64_t g1 = (e + 3) >> 2;
+  for (int64_t q0 = b >> 2; q0 < g1; q0 += 64) {
+    const int64_t qa = q0 + gl, qb = q0 + 32 + gl;
+    const bool aa = qa < g1, ab = qb < g1;
     int4 ca = make_int4(0, 0, 0, 0), wa = make_int4(0, 0, 0, 0);
     int4 cb = make_int4(0, 0, 0, 0), wb = make_int4(0, 0, 0, 0);
     if (aa) {
@@ -319,7 +298,13 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       cb = ld_stream_v4(col + 4 * qb);
       if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(w + 4 * qb);
     }
-    const bool act8[8] = {aa, aa, aa, aa, ab, ab, ab, ab};
+    bool act8[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t ea = 4 * qa + k, eb = 4 * qb + k;
+      act8[k] = aa && ea >= b && ea < e;
+      act8[4 + k] = ab && eb >= b && eb < e;
+    }
     const uint32_t d8[8] = {(uint32_t)ca.x, (uint32_t)ca.y, (uint32_t)ca.z, (uint32_t)ca.w,
                             (uint32_t)cb.x, (uint32_t)cb.y, (uint32_t)cb.z, (uint32_t)cb.w};
     const int32_t w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
@@ -341,7 +326,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
 // ---- one warp tile of 32 worklist items (consecutive mapping inside the tile) --------------------
 template <int OP, bool DIST>
 __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
-                                 uint32_t base, uint32_t width, int32_t dmin) {
+                                 uint32_t base, uint32_t width, int32_t dmin, bool small_round) {
   const int lane = lane_id();
   const uint32_t i = base + lane;
   const bool valid = (uint32_t)lane < width && i < rb.nin;
@@ -380,41 +365,11 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     q.edges += de;
   }
 
-  // ---- CTA-chunk level: degree >= cta_t -> chunk descriptors (warp-cooperative emission)
-  {
-    const bool big = deg >= p.ec.cta_t;
-    uint32_t bm = __ballot_sync(FULL, big);
-    while (bm) {
-      const int leader = __ffs(bm) - 1;
-      bm &= bm - 1;
-      const int64_t b = __shfl_sync(FULL, beg, leader);
-      const int64_t e = __shfl_sync(FULL, end, leader);
-      const uint32_t vv = __shfl_sync(FULL, v, leader);
-      const int64_t ce = p.ec.chunk_edges;
-      const uint32_t nch = (uint32_t)((e - b + ce - 1) / ce);
-      uint32_t cbase = 0;
-      if (lane == 0) cbase = atomicAdd(rb.chunk_cnt, nch);
-      cbase = __shfl_sync(FULL, cbase, 0);
-      for (uint32_t k = lane; k < nch; k += 32) {
-        const uint32_t pos = cbase + k;
-        const int64_t cb = b + (int64_t)k * ce;
-        if (pos < rb.chunk_cap) {
-          ChunkDesc d;
-          d.beg = cb;
-          d.v = vv;
-          d.len = (uint32_t)min(ce, e - cb);
-          rb.chunks[pos] = d;
-        } else {
-          atomicOr(&p.ctl->overflow, 2u);
-        }
-      }
-    }
-    if (big) deg = 0;
-  }
-
-  // ---- warp level: warp_t <= degree < cta_t
-  {
-    uint32_t wm = __ballot_sync(FULL, deg >= p.ec.warp_t);
+  // ---- small rounds (every warp holds at most one tile): degrees in [warp_t, cta_t) are expanded
+  // by the popping warp itself, so a round without hubs needs no chunk phase (and no second
+  // grid barrier)
+  if (small_round) {
+    uint32_t wm = __ballot_sync(FULL, deg >= p.ec.warp_t && deg < p.ec.cta_t);
     while (wm) {
       const int leader = __ffs(wm) - 1;
       wm &= wm - 1;
@@ -422,8 +377,53 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
       const int64_t e = __shfl_sync(FULL, end, leader);
       const int32_t s = __shfl_sync(FULL, sv, leader);
       if (lane == leader) deg = 0;
-      process_range<OP, DIST, 32>(sm, q, p, rb, b, e, s, lane);
+      process_range<OP, DIST>(sm, q, p, rb, b, e, s, lane);
     }
+  }
+  // ---- edge-balanced level: degree >= warp_t -> descriptors of <= chunk_edges edges, drained
+  // by every warp of the grid in the chunk phase (one reservation per warp tile)
+  {
+    const bool big = deg >= p.ec.warp_t;
+    const int64_t ce = p.ec.chunk_edges;
+    const uint32_t nchl = big ? (uint32_t)((deg + ce - 1) / ce) : 0u;
+    uint32_t incl = nchl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    if (tot) {
+      uint32_t cbase = 0;
+      if (lane == 31) cbase = atomicAdd(rb.chunk_cnt, tot);
+      cbase = __shfl_sync(FULL, cbase, 31);
+      const uint32_t excl = cbase + incl - nchl;
+      uint32_t bm = __ballot_sync(FULL, big);
+      while (bm) {
+        const int leader = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int64_t b = __shfl_sync(FULL, beg, leader);
+        const int64_t e = __shfl_sync(FULL, end, leader);
+        const uint32_t vv = __shfl_sync(FULL, v, leader);
+        const int32_t s = __shfl_sync(FULL, sv, leader);
+        const uint32_t nch = __shfl_sync(FULL, nchl, leader);
+        const uint32_t off = __shfl_sync(FULL, excl, leader);
+        for (uint32_t k = lane; k < nch; k += 32) {
+          const uint32_t pos = off + k;
+          const int64_t cb = b + (int64_t)k * ce;
+          if (pos < rb.chunk_cap) {
+            ChunkDesc d;
+            d.beg_len = ((uint64_t)cb << 16) | (uint64_t)min(ce, e - cb);
+            d.v = vv;
+            d.sv = s;
+            rb.chunks[pos] = d;
+          } else {
+            atomicOr(&p.ctl->overflow, 2u);
+          }
+        }
+      }
+    }
+    if (big) deg = 0;
   }
 
   // ---- thread level (fine-grained): warp scan of the small degrees, shuffle owner search
@@ -492,7 +492,7 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
                                      : rb.dmin_val;
   uint32_t t = gw;
   while (t < ntiles) {
-    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin);
+    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin, ntiles <= nwarps);
     if (ntiles <= nwarps) break;
     uint32_t nt = 0;
     if (lane_id() == 0) nt = nwarps + atomicAdd(rb.tile_ctr, 1u);
@@ -500,28 +500,64 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   }
 }
 
-// ---- CTA-chunk phase: every CTA drains chunk descriptors (grid-stride); each thread reads the
-// descriptor itself (broadcast load), so no CTA barrier is needed between chunks.
+// ---- chunk phase: every warp of the grid drains edge-chunk descriptors (grid-stride by warp;
+// chunks are <= chunk_edges edges, so the phase is edge-balanced and its tail is one chunk).  The
+// next descriptor is loaded while the current one is processed.
+__device__ __forceinline__ ChunkDesc ld_desc(const ChunkDesc* p) {
+  uint32_t a0, a1, a2, a3;  // rewritten every round: L2-coherent load
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(p));
+  ChunkDesc d;
+  d.beg_len = ((uint64_t)a1 << 32) | a0;
+  d.v = a2;
+  d.sv = (int32_t)a3;
+  return d;
+}
+
+#ifdef IRGL_EXPERIMENT
+// Timing experiment only (never in the product build): replay a chunk's col/weight loads
+// (IRGL_EXPERIMENT=1) or loads + label gathers (=2) with no side effects.
+template <int OP>
+__device__ __noinline__ void probe_range(const KParams& p, int64_t b, int64_t e, int gl) {
+  const int64_t g1 = (e + 3) >> 2;
+  int acc = 0;
+  for (int64_t q0 = b >> 2; q0 < g1; q0 += 64) {
+    const int64_t qa = q0 + gl, qb = q0 + 32 + gl;
+    int4 ca = make_int4(0, 0, 0, 0), cb = ca, wa = ca, wb = ca;
+    if (qa < g1) { ca = ld_stream_v4(p.g.col + 4 * qa); if (OP == IRGL_OP_SSSP) wa = ld_stream_v4(p.g.w + 4 * qa); }
+    if (qb < g1) { cb = ld_stream_v4(p.g.col + 4 * qb); if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(p.g.w + 4 * qb); }
+    if (IRGL_EXPERIMENT == 2) {
+      const int32_t d8[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += (qa < g1 || j >= 4) && (qb < g1 || j < 4) ? ld_label(p.lab + d8[j]) : 0;
+    } else {
+      acc += ca.x ^ cb.y ^ wa.z ^ wb.w;
+    }
+  }
+  if (acc == 0x7ffffffe) p.ctl->pad = acc;  // keep the loads
+}
+#endif
+
 template <int OP, bool DIST>
 __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, uint32_t nch) {
   nch = min(nch, rb.chunk_cap);
-  // two chunks per CTA at a time (128-thread halves) -> twice the independent chains per SM
-  constexpr int kHalf = kBlock / 2;
-  const uint32_t half = threadIdx.x / kHalf;
-  const int gl = threadIdx.x % kHalf;
-  for (uint32_t c = 2 * blockIdx.x + half; c < nch; c += 2 * gridDim.x) {
-    // descriptors are rewritten every round: L2-coherent load
-    ChunkDesc dsc;
-    {
-      uint32_t a0, a1, a2, a3;
-      asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(rb.chunks + c));
-      dsc.beg = (int64_t)(((uint64_t)a1 << 32) | a0);
-      dsc.v = a2;
-      dsc.len = a3;
-    }
-    const int32_t s = (OP != IRGL_OP_BFS) ? ld_label_cg(p.lab + dsc.v) : 0;
-    process_range<OP, DIST, kHalf>(sm, q, p, rb, dsc.beg, dsc.beg + dsc.len, s, gl);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const int gl = lane_id();
+  uint32_t c = gw;
+  ChunkDesc cur{};
+  if (c < nch) cur = ld_desc(rb.chunks + c);
+  while (c < nch) {
+    const uint32_t cn = c + nw;
+    ChunkDesc nxt{};
+    if (cn < nch) nxt = ld_desc(rb.chunks + cn);
+    const int64_t b = (int64_t)(cur.beg_len >> 16);
+#ifdef IRGL_EXPERIMENT
+    probe_range<OP>(p, b, b + (int64_t)(cur.beg_len & 0xffffu), gl);
+#endif
+    process_range<OP, DIST>(sm, q, p, rb, b, b + (int64_t)(cur.beg_len & 0xffffu), cur.sv, gl);
+    c = cn;
+    cur = nxt;
   }
 }
 
@@ -626,9 +662,13 @@ __device__ __forceinline__ unsigned long long grid_sync_bcast(Ctl* ctl, uint32_t
   __syncthreads();
   return *slot;
 }
+// {chunk count: 26 bits, out count: 30 bits} (the host caps chunk_cap below 2^26 and pipe
+// capacities below 2^30)
 __device__ __forceinline__ unsigned long long pack_counts(uint32_t nch, uint32_t nout) {
-  return ((unsigned long long)min(nch, 0xffffffu) << 32) | nout;
+  return ((unsigned long long)min(nch, 0x3ffffffu) << 30) | min(nout, 0x3fffffffu);
 }
+__device__ __forceinline__ uint32_t unpack_nch(unsigned long long w) { return (uint32_t)(w >> 30); }
+__device__ __forceinline__ uint32_t unpack_nout(unsigned long long w) { return (uint32_t)(w & 0x3fffffffu); }
 
 __device__ __forceinline__ int slot3(const PersistArgs& a, uint32_t i) {
   const uint32_t m = i % 3;
@@ -696,16 +736,16 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     };
     unsigned long long w = grid_sync_bcast(
         p.ctl, bidx, &bslot, [&]() { return pack_counts(ld_ctl(rb.chunk_cnt), ld_ctl(cout)); },
-        [&](unsigned long long v) { if ((v >> 32) == 0) fetch_dmin(); });
+        [&](unsigned long long v) { if (unpack_nch(v) == 0) fetch_dmin(); });
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 6]));
-    const uint32_t nch = (uint32_t)(w >> 32);
-    uint32_t nout = (uint32_t)w;
+    const uint32_t nch = unpack_nch(w);
+    uint32_t nout = unpack_nout(w);
     if (nch) {
       chunk_phase<OP, false>(sm, q, p, rb, nch);
       wflush_all(sm, q, p, rb);
       w = grid_sync_bcast(p.ctl, bidx, &bslot, [&]() { return pack_counts(0, ld_ctl(cout)); },
                           [&](unsigned long long) { fetch_dmin(); });
-      nout = (uint32_t)w;
+      nout = unpack_nout(w);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 7]));
     }
     if (nf) {

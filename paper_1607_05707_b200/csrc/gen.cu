@@ -282,8 +282,8 @@ cudaError_t csr_from_edges_device(const EdgeRec* host_edges, int64_t ne, int64_t
   GEN_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg, rp, n + 1, st));
   int32_t* dc = nullptr;
   int32_t* dw = nullptr;
-  GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * 4, st));
-  GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * 4, st));
+  GEN_CK(cudaMallocAsync(&dc, (m + 4) * 4, st));
+  GEN_CK(cudaMallocAsync(&dw, (m + 4) * 4, st));
   if (m > 0) {
     note_launch();
     split_keys_kernel<<<fgrid, 256, 0, st>>>(uk, m, dc);
@@ -343,8 +343,8 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
     GEN_CK(cudaMemcpyAsync(&m, rp + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     GEN_CK(cudaStreamSynchronize(st));
     cudaFreeAsync(t, st);
-    GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * sizeof(int32_t), st));
-    GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * sizeof(int32_t), st));
+    GEN_CK(cudaMallocAsync(&dc, (m + 4) * sizeof(int32_t), st));
+    GEN_CK(cudaMallocAsync(&dw, (m + 4) * sizeof(int32_t), st));
     if (nloc > 0) {
       note_launch();
       grid_fill_kernel<<<grid, 256, 0, st>>>(g, lo, hi, rp, s.wseed, dc, dw);
@@ -398,8 +398,8 @@ cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t
       row_count_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, deg);
     }
     GEN_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg, rp, nloc + 1, st));
-    GEN_CK(cudaMallocAsync(&dc, (m > 0 ? m : 1) * sizeof(int32_t), st));
-    GEN_CK(cudaMallocAsync(&dw, (m > 0 ? m : 1) * sizeof(int32_t), st));
+    GEN_CK(cudaMallocAsync(&dc, (m + 4) * sizeof(int32_t), st));
+    GEN_CK(cudaMallocAsync(&dw, (m + 4) * sizeof(int32_t), st));
     if (m > 0) {
       note_launch();
       fill_csr_kernel<<<fgrid, 256, 0, st>>>(uniq, m, scale, lo, s.wseed, dc, dw);

@@ -18,12 +18,15 @@ constexpr int kWarps = kBlock / 32;
 constexpr int32_t kInf = 0x7fffffff;
 constexpr int kPushBuf = 2048;  // per-CTA shared-memory push staging (cooperative conversion)
 
-// CTA-chunk descriptor: `len` (<= chunk_edges) edges of vertex v starting at edge `beg`.
+// Edge-chunk descriptor (E1 edge-balanced level): `len` (<= chunk_edges) edges of vertex v
+// starting at edge `beg`, with the vertex's label (dist/level/label) as read when it was popped.
 struct ChunkDesc {
-  int64_t beg;
+  uint64_t beg_len;  // beg (48 bits) << 16 | len (16 bits, chunk_edges <= 65535)
   uint32_t v;
-  uint32_t len;
+  int32_t sv;        // label of v at pop time (a stale, larger value only weakens relaxations;
+                     // the improvement that made it stale re-pushes v, SPEC.md:425 epochs)
 };
+static_assert(sizeof(ChunkDesc) == 16, "one 128-bit load per descriptor");
 
 // Device-resident control block of one pipe partition.  Counter slots are addressed by index so
 // the persistent kernel can rotate them (see persistent loop in expand.cu).

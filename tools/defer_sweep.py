@@ -11,7 +11,8 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 Ks = [int(k) for k in sys.argv[2:]] or [0, 256, 512, 1024, 2048, 4096, 8192, 16384, 65536]
 outline = int(os.environ.get("OUTLINE", "1"))
 nsrc = int(os.environ.get("NSRC", "8"))
-ctx = irgl.Context()
+import json
+ctx = irgl.Context(**json.loads(os.environ.get("CTX", "{}")))
 g = ctx.generate_rmat(scale)
 rp = np.zeros(g.n + 1, dtype=np.int64)
 ctx._lib.irgl_graph_download(g.handle, rp.ctypes.data_as(C.POINTER(C.c_int64)), None, None)
@@ -26,7 +27,7 @@ tb = 0
 for s in srcs:
     p.init_scalars([s])
     tb += ctx.iterate(irgl.BFS, g, p).device_ms
-print(f"RMAT-{scale} BFS: {tb/len(srcs):.3f} ms GTEPS={E/2/(tb/len(srcs))/1e6:.1f}", flush=True)
+print(f"{os.environ.get('CTX', '')} RMAT-{scale} BFS: {tb/len(srcs):.3f} ms GTEPS={E/2/(tb/len(srcs))/1e6:.1f}", flush=True)
 ref = None
 for K in Ks:
     for s in srcs[:2]:  # warm
