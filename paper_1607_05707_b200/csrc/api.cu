@@ -772,10 +772,11 @@ static irgl_status_t pipe_counters(irgl_ctx* ctx, irgl_pipe* pipe, irgl_iter_sta
     PipePart& pp = pipe->parts[l];
     CK(cudaSetDevice(pr.dev));
     if (stt) {
-      unsigned long long hv[4] = {0, 0, 0, 0};
-      CK(cudaMemcpy(hv, &pp.ctl->edges, sizeof(hv), cudaMemcpyDeviceToHost));
-      stt->edges += (int64_t)hv[0];
-      stt->remote_updates += (int64_t)hv[3];
+      unsigned long long he = 0, hr = 0;
+      CK(cudaMemcpy(&he, &pp.ctl->edges, 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&hr, &pp.ctl->remote, 8, cudaMemcpyDeviceToHost));
+      stt->edges += (int64_t)he;
+      stt->remote_updates += (int64_t)hr;
     }
     CK(cudaMemsetAsync(&pp.ctl->edges, 0, 8, pr.st));
     CK(cudaMemsetAsync(&pp.ctl->remote, 0, 8, pr.st));

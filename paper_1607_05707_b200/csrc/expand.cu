@@ -39,7 +39,15 @@ constexpr int kWBuf = 256;  // per-warp push staging entries
 #ifndef IRGL_MINB_SSSP
 #define IRGL_MINB_SSSP 4  // SSSP (weights + batched relax): 64 registers, 32 warps/SM, no spills in the hot loop
 #endif
-constexpr int minb_for(int op) { return op == IRGL_OP_SSSP ? IRGL_MINB_SSSP : IRGL_MINB; }
+// Internal operator variants (template-level, so the common path carries no state of the others):
+// SSSP with near-far piles, and BFS accumulating the next frontier's degrees (direction-optimising).
+constexpr int kOpSsspNF = 0x101;
+constexpr int kOpBfsDO = 0x100;
+constexpr bool is_bfs(int op) { return op == IRGL_OP_BFS || op == kOpBfsDO; }
+constexpr bool is_sssp(int op) { return op == IRGL_OP_SSSP || op == kOpSsspNF; }
+constexpr bool has_far(int op) { return op == kOpSsspNF; }
+constexpr bool has_mf(int op) { return op == kOpBfsDO; }
+constexpr int minb_for(int op) { return is_sssp(op) ? IRGL_MINB_SSSP : IRGL_MINB; }
 
 struct Smem {
   uint32_t wbuf[kWarps][kWBuf];   // near pushes (E2)
@@ -58,12 +66,15 @@ struct KParams {
   ExpandCfg ec;
 };
 
+__device__ __forceinline__ void smem_init(Smem& sm) {
+  if ((threadIdx.x & 31) == 0) sm.fl_edges[threadIdx.x >> 5] = 0;  // per-warp edge counters
+}
+
 // Register-resident, warp-uniform state of a warp's staging queues.
 struct WarpQ {
   uint32_t n = 0;   // staged near pushes
   uint32_t nf = 0;  // staged far pushes
-  unsigned long long edges = 0;
-  unsigned long long mf = 0;  // DO-BFS: degrees of pushed vertices
+  unsigned long long mf = 0;  // DO-BFS: degrees of pushed vertices (kOpBfsDO only)
   int32_t dmin = kInf;        // SSSP deferral: min distance this lane pushed near (per lane)
 };
 
@@ -86,20 +97,20 @@ __device__ __forceinline__ uint32_t ld_ctl(const uint32_t* p) {
 template <int OP>
 __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb, WarpQ& q,
                                           int32_t cur, int32_t sv, int32_t wt, uint32_t dst) {
-  if (OP == IRGL_OP_BFS) {
+  if (is_bfs(OP)) {
     if (cur != kInf) return 0;
     return atomicCAS(p.lab + dst, kInf, rb.level) == kInf ? 1 : 0;
   } else {
-    const int32_t nd = (OP == IRGL_OP_SSSP) ? sv + wt : sv;
+    const int32_t nd = (is_sssp(OP)) ? sv + wt : sv;
     if (nd >= cur) return 0;
     const int32_t old = atomicMin(p.lab + dst, nd);
     if (nd >= old) return 0;
     // push dedupe per round and per pile: stamp code = 2*round_id + (far ? 1 : 0).  A vertex
     // first pushed far and then improved below the threshold in the same round is pushed near
     // too; its stale far entry is dropped by the split (dist < old threshold).
-    const int kind = (OP == IRGL_OP_SSSP && nd >= rb.threshold) ? 2 : 1;
+    const int kind = (has_far(OP) && nd >= rb.threshold) ? 2 : 1;
     // dst now holds <= nd and sits in the near out worklist (pushed here or earlier this round)
-    if (OP == IRGL_OP_SSSP && kind == 1) q.dmin = min(q.dmin, nd);
+    if (is_sssp(OP) && kind == 1) q.dmin = min(q.dmin, nd);
     const int32_t code = (rb.stamp_id << 1) | (kind - 1);
     if (atomicExch(p.stamp + dst, code) == code) return 0;
     return kind;
@@ -122,7 +133,7 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
                                             const bool (&act)[K], const int32_t (&cur)[K],
                                             const int32_t (&sv)[K], const int32_t (&wt)[K],
                                             const uint32_t (&dst)[K], int (&kind)[K]) {
-  if (OP == IRGL_OP_BFS) {
+  if (is_bfs(OP)) {
     int32_t old[K];
 #pragma unroll
     for (int j = 0; j < K; ++j)
@@ -134,9 +145,9 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
     bool cand[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      nd[j] = (OP == IRGL_OP_SSSP) ? sv[j] + wt[j] : sv[j];
+      nd[j] = (is_sssp(OP)) ? sv[j] + wt[j] : sv[j];
       cand[j] = act[j] && nd[j] < cur[j];
-      kind[j] = (OP == IRGL_OP_SSSP && nd[j] >= rb.threshold) ? 2 : 1;
+      kind[j] = (has_far(OP) && nd[j] >= rb.threshold) ? 2 : 1;
       code[j] = (rb.stamp_id << 1) | (kind[j] - 1);
       if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
     }
@@ -144,7 +155,7 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
     for (int j = 0; j < K; ++j) prev[j] = cand[j] ? atomicExch(p.stamp + dst[j], code[j]) : code[j];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      if (OP == IRGL_OP_SSSP && cand[j] && kind[j] == 1) q.dmin = min(q.dmin, nd[j]);
+      if (is_sssp(OP) && cand[j] && kind[j] == 1) q.dmin = min(q.dmin, nd[j]);
       kind[j] = (cand[j] && prev[j] != code[j]) ? kind[j] : 0;
     }
   }
@@ -168,7 +179,7 @@ __device__ __forceinline__ void wflush(uint32_t* buf, uint32_t& n, uint32_t* out
 }
 
 // Every lane of the warp must call this (converged).  kind: 0 none, 1 near, 2 far.
-template <bool DIST>
+template <int OP, bool DIST>
 __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
                                       int kind, uint32_t v) {
   uint32_t m = __ballot_sync(FULL, kind != 0);
@@ -198,7 +209,7 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
   const uint32_t mn = __ballot_sync(FULL, kind == 1);
   const uint32_t mf = m & ~mn;
   const uint32_t lt = lanemask_lt();
-  if (mn && rb.mf_acc) {  // DO-BFS: edges of the next frontier
+  if (has_mf(OP) && mn) {  // DO-BFS: edges of the next frontier
     unsigned long long dg = 0;
     if (kind == 1) dg = (unsigned long long)(__ldg(p.g.row_ptr + v - p.g.lo + 1) - __ldg(p.g.row_ptr + v - p.g.lo));
 #pragma unroll
@@ -210,7 +221,7 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
     q.n += __popc(mn);
     if (q.n > kWBuf - 32) wflush(sm.wbuf[warp], q.n, rb.out, rb.out_cnt, rb.cap, &p.ctl->overflow);
   }
-  if (mf) {
+  if (has_far(OP) && mf) {
     if (kind == 2) sm.fbuf[warp][q.nf + __popc(mf & lt)] = v;
     q.nf += __popc(mf);
     if (q.nf > kWBuf - 32) wflush(sm.fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
@@ -219,9 +230,10 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
 
 // CTA-level flush at a CTA-uniform point (every thread calls it): one global reservation per pile
 // and one stats atomic per CTA instead of one per warp (E2 at CTA granularity).
+template <int OP>
 __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  if (q.mf) {
+  if (has_mf(OP) && q.mf) {
     if (lane == 0) atomicAdd(rb.mf_acc, q.mf);
     q.mf = 0;
   }
@@ -234,11 +246,10 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
   }
   if (lane == 0) {
     sm.fl_cnt[0][warp] = q.n;
-    sm.fl_cnt[1][warp] = q.nf;
-    sm.fl_edges[warp] = q.edges;
+    sm.fl_cnt[1][warp] = has_far(OP) ? q.nf : 0u;
   }
   __syncthreads();
-  if (threadIdx.x < 2) {
+  if (threadIdx.x < (has_far(OP) ? 2 : 1)) {
     const int k = threadIdx.x;
     uint32_t tot = 0;
 #pragma unroll
@@ -263,14 +274,15 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
     if (qq < rb.cap) rb.out[qq] = sm.wbuf[warp][i];
     else atomicOr(&p.ctl->overflow, 1u);
   }
+  if (has_far(OP))
   for (uint32_t i = lane; i < q.nf; i += 32) {
     const uint32_t qq = o1 + i;
     if (qq < rb.far_cap) rb.far[qq] = sm.fbuf[warp][i];
     else atomicOr(&p.ctl->overflow, 1u);
   }
+  if (lane == 0) sm.fl_edges[warp] = 0;  // read by thread 0 before the second barrier
   __syncwarp();
   q.n = q.nf = 0;
-  q.edges = 0;
 }
 
 // ---- edge-range processing by one warp --------------------------------------------------------
@@ -278,47 +290,56 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
 // lane takes two groups per iteration and masks the edges outside the range (the CSR arrays are
 // padded by 4 entries, so the last group is always in bounds).  No separate head/tail step: all 8
 // label gathers and all atomics of a lane are in flight together (relax_batch).
+#ifndef IRGL_GROUPS
+#define IRGL_GROUPS 1  // 128-bit col/weight groups per lane per iteration (4 edges each; 1 beat 2, profiles/r1s2_variants.txt)
+#endif
 template <int OP, bool DIST>
 __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams& p,
                                               const RoundBufs& rb, int64_t b, int64_t e,
                                               int32_t sv, int gl) {
+  constexpr int NG = IRGL_GROUPS, NE = 4 * NG;
   const int32_t* __restrict__ col = p.g.col;
   const int32_t* __restrict__ w = p.g.w;
   const int64_t g1 = (e + 3) >> 2;
-  for (int64_t q0 = b >> 2; q0 < g1; q0 += 64) {
-    const int64_t qa = q0 + gl, qb = q0 + 32 + gl;
-    const bool aa = qa < g1, ab = qb < g1;
-    int4 ca = make_int4(0, 0, 0, 0), wa = make_int4(0, 0, 0, 0);
-    int4 cb = make_int4(0, 0, 0, 0), wb = make_int4(0, 0, 0, 0);
-    if (aa) {
-      ca = ld_stream_v4(col + 4 * qa);
-      if (OP == IRGL_OP_SSSP) wa = ld_stream_v4(w + 4 * qa);
+  for (int64_t q0 = b >> 2; q0 < g1; q0 += 32 * NG) {
+    int4 cg[NG], wg[NG];
+    bool ag[NG];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int64_t qk = q0 + 32 * k + gl;
+      ag[k] = qk < g1;
+      cg[k] = make_int4(0, 0, 0, 0);
+      wg[k] = make_int4(0, 0, 0, 0);
+      if (ag[k]) {
+        cg[k] = ld_stream_v4(col + 4 * qk);
+        if (is_sssp(OP)) wg[k] = ld_stream_v4(w + 4 * qk);
+      }
     }
-    if (ab) {
-      cb = ld_stream_v4(col + 4 * qb);
-      if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(w + 4 * qb);
+    bool act[NE];
+    uint32_t d[NE];
+    int32_t wt[NE], sv8[NE], cur[NE];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) {
+      const int64_t e0 = 4 * (q0 + 32 * k + gl);
+      const int32_t cc[4] = {cg[k].x, cg[k].y, cg[k].z, cg[k].w};
+      const int32_t ww[4] = {wg[k].x, wg[k].y, wg[k].z, wg[k].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        act[4 * k + t] = ag[k] && e0 + t >= b && e0 + t < e;
+        d[4 * k + t] = (uint32_t)cc[t];
+        wt[4 * k + t] = ww[t];
+        sv8[4 * k + t] = sv;
+      }
     }
-    bool act8[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t ea = 4 * qa + k, eb = 4 * qb + k;
-      act8[k] = aa && ea >= b && ea < e;
-      act8[4 + k] = ab && eb >= b && eb < e;
-    }
-    const uint32_t d8[8] = {(uint32_t)ca.x, (uint32_t)ca.y, (uint32_t)ca.z, (uint32_t)ca.w,
-                            (uint32_t)cb.x, (uint32_t)cb.y, (uint32_t)cb.z, (uint32_t)cb.w};
-    const int32_t w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
-    const int32_t s8[8] = {sv, sv, sv, sv, sv, sv, sv, sv};
-    int32_t c8[8];
+    for (int j = 0; j < NE; ++j) cur[j] = act[j] ? ld_label(p.lab + d[j]) : 0;
+    int kk[NE];
+    relax_batch<OP, NE>(p, rb, q, act, cur, sv8, wt, d, kk);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) c8[j] = act8[j] ? ld_label(p.lab + d8[j]) : 0;
-    int k8[8];
-    relax_batch<OP, 8>(p, rb, q, act8, c8, s8, w8, d8, k8);
+    for (int k = 0; k < NG; ++k) {
+      if (k > 0 && !__any_sync(FULL, ag[k])) break;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) wpush<DIST>(sm, q, p, rb, k8[j], d8[j]);
-    if (__any_sync(FULL, ab)) {
-#pragma unroll
-      for (int j = 4; j < 8; ++j) wpush<DIST>(sm, q, p, rb, k8[j], d8[j]);
+      for (int t = 0; t < 4; ++t) wpush<OP, DIST>(sm, q, p, rb, kk[4 * k + t], d[4 * k + t]);
     }
   }
 }
@@ -338,14 +359,14 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     const int64_t lv = (int64_t)v - p.g.lo;
     beg = __ldg(p.g.row_ptr + lv);
     end = __ldg(p.g.row_ptr + lv + 1);
-    if (OP != IRGL_OP_BFS) sv = ld_label_cg(p.lab + v);
+    if (!is_bfs(OP)) sv = ld_label_cg(p.lab + v);
   }
   int64_t deg = end - beg;
   // SSSP deferral: a vertex whose distance is still far above the frontier minimum, weighted by
   // the edges a premature expansion would waste, is kept for the next round (re-pushed with the
   // round's stamp, so at most once) instead of expanded.  The frontier's minimum vertex always
   // has slack <= 0, so every round expands at least one vertex (progress).
-  if (OP == IRGL_OP_SSSP && rb.defer_k > 0) {
+  if (is_sssp(OP) && rb.defer_k > 0) {
     const bool defer = valid && deg > 0 && ((int64_t)sv - dmin) * deg > rb.defer_k;
     if (__any_sync(FULL, defer)) {
       int kind = 0;
@@ -355,14 +376,14 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
         q.dmin = min(q.dmin, sv);
         deg = 0;
       }
-      wpush<DIST>(sm, q, p, rb, kind, v);
+      wpush<OP, DIST>(sm, q, p, rb, kind, v);
     }
   }
   {
     unsigned long long de = (unsigned long long)deg;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) de += __shfl_xor_sync(FULL, de, o);
-    q.edges += de;
+    if (lane == 0) sm.fl_edges[threadIdx.x >> 5] += de;
   }
 
   // ---- small rounds (every warp holds at most one tile): degrees in [warp_t, cta_t) are expanded
@@ -461,7 +482,7 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
       if (act[j]) {
         const int64_t ed = eo + k;
         dst[j] = (uint32_t)ld_stream(p.g.col + ed);
-        if (OP == IRGL_OP_SSSP) wt[j] = ld_stream(p.g.w + ed);
+        if (is_sssp(OP)) wt[j] = ld_stream(p.g.w + ed);
       }
     }
 #pragma unroll
@@ -471,7 +492,7 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
 #pragma unroll
     for (int j = 0; j < kWin; ++j) {
       if (wb + 32 * j >= total) break;  // warp-uniform
-      wpush<DIST>(sm, q, p, rb, kk[j], dst[j]);
+      wpush<OP, DIST>(sm, q, p, rb, kk[j], dst[j]);
     }
   }
 }
@@ -494,9 +515,13 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   while (t < ntiles) {
     expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin, ntiles <= nwarps);
     if (ntiles <= nwarps) break;
+#if defined(IRGL_TILE_STATIC) && IRGL_TILE_STATIC
+    t += nwarps;
+#else
     uint32_t nt = 0;
     if (lane_id() == 0) nt = nwarps + atomicAdd(rb.tile_ctr, 1u);
     t = __shfl_sync(FULL, nt, 0);
+#endif
   }
 }
 
@@ -524,8 +549,8 @@ __device__ __noinline__ void probe_range(const KParams& p, int64_t b, int64_t e,
   for (int64_t q0 = b >> 2; q0 < g1; q0 += 64) {
     const int64_t qa = q0 + gl, qb = q0 + 32 + gl;
     int4 ca = make_int4(0, 0, 0, 0), cb = ca, wa = ca, wb = ca;
-    if (qa < g1) { ca = ld_stream_v4(p.g.col + 4 * qa); if (OP == IRGL_OP_SSSP) wa = ld_stream_v4(p.g.w + 4 * qa); }
-    if (qb < g1) { cb = ld_stream_v4(p.g.col + 4 * qb); if (OP == IRGL_OP_SSSP) wb = ld_stream_v4(p.g.w + 4 * qb); }
+    if (qa < g1) { ca = ld_stream_v4(p.g.col + 4 * qa); if (is_sssp(OP)) wa = ld_stream_v4(p.g.w + 4 * qa); }
+    if (qb < g1) { cb = ld_stream_v4(p.g.col + 4 * qb); if (is_sssp(OP)) wb = ld_stream_v4(p.g.w + 4 * qb); }
     if (IRGL_EXPERIMENT == 2) {
       const int32_t d8[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
 #pragma unroll
@@ -587,7 +612,7 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
         if (k == 1) q.dmin = min(q.dmin, dv);
       }
     }
-    wpush<false>(sm, q, p, rb, kind, v);
+    wpush<kOpSsspNF, false>(sm, q, p, rb, kind, v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mymin = min(mymin, __shfl_xor_sync(FULL, mymin, o));
@@ -597,17 +622,19 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
 template <int OP, bool DIST>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) expand_kernel(KParams p, RoundBufs rb) {
   __shared__ Smem sm;
+  smem_init(sm);
   WarpQ q;
   item_phase<OP, DIST>(sm, q, p, rb);
-  wflush_all(sm, q, p, rb);
+  wflush_all<OP>(sm, q, p, rb);
 }
 
 template <int OP, bool DIST>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) chunk_kernel(KParams p, RoundBufs rb) {
   __shared__ Smem sm;
+  smem_init(sm);
   WarpQ q;
   chunk_phase<OP, DIST>(sm, q, p, rb, ld_ctl(rb.chunk_cnt));
-  wflush_all(sm, q, p, rb);
+  wflush_all<OP>(sm, q, p, rb);
 }
 
 __global__ void __launch_bounds__(kBlock, IRGL_MINB) far_split_kernel(KParams p, RoundBufs rb,
@@ -616,9 +643,10 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) far_split_kernel(KParams p,
                                                               int32_t t_old,
                                                               unsigned int* minkeep) {
   __shared__ Smem sm;
+  smem_init(sm);
   WarpQ q;
   far_split(sm, q, p, rb, far_in, ld_ctl(nfar_ptr), t_old, minkeep);
-  wflush_all(sm, q, p, rb);
+  wflush_all<kOpSsspNF>(sm, q, p, rb);
 }
 
 // ---- E3: outlined Iterate.  One cooperative launch; rounds separated by grid.sync() --------------
@@ -678,10 +706,11 @@ __device__ __forceinline__ int slot3(const PersistArgs& a, uint32_t i) {
 template <int OP>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
+  smem_init(sm);
   cg::grid_group grid = cg::this_grid();
   WarpQ q;
   uint32_t* cnt = p.ctl->cnt;
-  const bool nf = (OP == IRGL_OP_SSSP) && a.delta > 0;
+  const bool nf = has_far(OP) && a.delta > 0;
   int32_t threshold = nf ? a.delta : kInf;
   int32_t sid = a.stamp0;       // unique stamp ids: rounds and splits
   uint32_t fsel = 0;            // which far buffer is current
@@ -689,9 +718,10 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));  // round r's in-count = round r-1's out-count
   __shared__ unsigned long long bslot;  // barrier broadcast
+  __shared__ RoundBufs srb;             // this round's view (no near-far)
   __shared__ int32_t s_dmin;            // deferral: frontier minimum of the next round
   uint32_t bidx = 0;
-  const bool dfr = (OP == IRGL_OP_SSSP) && a.defer_k > 0;
+  const bool dfr = (is_sssp(OP)) && a.defer_k > 0;
   if (threadIdx.x == 0) s_dmin = dfr ? (int32_t)min(ld_ctl(&p.ctl->dmin[0]), (uint32_t)kInf) : kInf;
   if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * a.trace_cap]));
   for (uint32_t r = 0;; ++r) {
@@ -721,13 +751,24 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     rb.far_cap = a.far_cap;
     rb.threshold = threshold;
     rb.mf_acc = nullptr;
-    rb.defer_k = (OP == IRGL_OP_SSSP) ? a.defer_k : 0;
+    rb.defer_k = (is_sssp(OP)) ? a.defer_k : 0;
     rb.dmin_cur = nullptr;
     rb.dmin_val = s_dmin;  // written by thread 0 before the barrier that ended round r-1
     rb.dmin_next = rb.defer_k > 0 ? &p.ctl->dmin[(r + 1) % 3] : nullptr;
-    item_phase<OP, false>(sm, q, p, rb);
+    // Without near-far the round's view lives in shared memory (written by thread 0 between two
+    // CTA barriers): the expansion then reads its pointers from smem at the use sites instead of
+    // holding ~20 registers of per-round state live across the hot loops.
+    const RoundBufs* rp = &rb;
+    if constexpr (!has_far(OP)) {
+      __syncthreads();  // readers of the previous round's view are done
+      if (threadIdx.x == 0) srb = rb;
+      __syncthreads();
+      rp = &srb;
+    }
+    const RoundBufs& rr = *rp;
+    item_phase<OP, false>(sm, q, p, rr);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 4]));
-    wflush_all(sm, q, p, rb);
+    wflush_all<OP>(sm, q, p, rr);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 5]));
     // the deferral minimum of round r+1 is final at the round's last barrier: thread 0 of each CTA
     // fetches it into shared memory there (no per-warp reads of one hot cell)
@@ -741,14 +782,14 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     const uint32_t nch = unpack_nch(w);
     uint32_t nout = unpack_nout(w);
     if (nch) {
-      chunk_phase<OP, false>(sm, q, p, rb, nch);
-      wflush_all(sm, q, p, rb);
+      chunk_phase<OP, false>(sm, q, p, rr, nch);
+      wflush_all<OP>(sm, q, p, rr);
       w = grid_sync_bcast(p.ctl, bidx, &bslot, [&]() { return pack_counts(0, ld_ctl(cout)); },
                           [&](unsigned long long) { fetch_dmin(); });
       nout = unpack_nout(w);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 7]));
     }
-    if (nf) {
+    if constexpr (has_far(OP)) if (nf) {
       // near frontier exhausted: advance the threshold and split the far pile; a pile past half
       // its capacity is compacted (split at the unchanged threshold) even when near is not empty
       uint32_t nfar = ld_ctl(rb.far_cnt);
@@ -772,7 +813,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
           sb.threshold = threshold;
           sb.stamp_id = sid++;
           far_split(sm, q, p, sb, rb.far, nfar, t_old, mk);
-          wflush_all(sm, q, p, sb);
+          wflush_all<OP>(sm, q, p, sb);
           grid.sync();
           fsel ^= 1;
           rb.far = sb.far;
@@ -854,12 +895,13 @@ __device__ void bu_compact(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   for (int64_t v0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); v0 < n; v0 += T) {
     const int64_t v = v0 + lane_id();
     const int kind = (v < n && ld_label(p.lab + v) == L) ? 1 : 0;
-    wpush<false>(sm, q, p, rb, kind, (uint32_t)v);
+    wpush<IRGL_OP_BFS, false>(sm, q, p, rb, kind, (uint32_t)v);
   }
 }
 
 __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
+  smem_init(sm);
   cg::grid_group grid = cg::this_grid();
   WarpQ q;
   uint32_t* cnt = p.ctl->cnt;
@@ -900,14 +942,14 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
     rb.dmin_next = nullptr;
     uint64_t nf, mf;
     if (!bottom_up) {
-      item_phase<IRGL_OP_BFS, false>(sm, q, p, rb);
-      wflush_all(sm, q, p, rb);
+      item_phase<kOpBfsDO, false>(sm, q, p, rb);
+      wflush_all<kOpBfsDO>(sm, q, p, rb);
       grid.sync();
       const uint32_t nch = ld_ctl(rb.chunk_cnt);
       nf = ld_ctl(cout);
       if (nch) {
-        chunk_phase<IRGL_OP_BFS, false>(sm, q, p, rb, nch);
-        wflush_all(sm, q, p, rb);
+        chunk_phase<kOpBfsDO, false>(sm, q, p, rb, nch);
+        wflush_all<kOpBfsDO>(sm, q, p, rb);
         grid.sync();
         nf = ld_ctl(cout);
       }
@@ -936,7 +978,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
         RoundBufs cb = rb;
         cb.mf_acc = nullptr;
         bu_compact(sm, q, p, cb, a.n, rb.level);
-        wflush_all(sm, q, p, cb);
+        wflush_all<IRGL_OP_BFS>(sm, q, p, cb);
         grid.sync();
         nf = ld_ctl(cout);
       }
@@ -961,6 +1003,7 @@ __global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBu
                                                            const uint32_t* items,
                                                            const int32_t* values, uint32_t n) {
   __shared__ Smem sm;
+  smem_init(sm);
   WarpQ q;
   for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < n; i0 += gridDim.x * kBlock) {
     const uint32_t i = i0 + lane_id();
@@ -969,11 +1012,11 @@ __global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBu
     if (i < n) {
       v = items[i];
       const int32_t cur = ld_label(p.lab + v);
-      kind = relax_with<OP>(p, rb, q, cur, OP == IRGL_OP_BFS ? 0 : values[i], 0, v);
+      kind = relax_with<OP>(p, rb, q, cur, is_bfs(OP) ? 0 : values[i], 0, v);
     }
-    wpush<false>(sm, q, p, rb, kind, v);
+    wpush<OP, false>(sm, q, p, rb, kind, v);
   }
-  wflush_all(sm, q, p, rb);
+  wflush_all<OP>(sm, q, p, rb);
 }
 
 __global__ void pack_values_kernel(const int32_t* lab, const uint32_t* items, int32_t* values,
@@ -1007,6 +1050,9 @@ cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* 
       return dist ? round_impl<IRGL_OP_BFS, true>(kp, rb, grid_max, st)
                   : round_impl<IRGL_OP_BFS, false>(kp, rb, grid_max, st);
     case IRGL_OP_SSSP:
+      if (rb.threshold != kInf)  // near-far piles
+        return dist ? round_impl<kOpSsspNF, true>(kp, rb, grid_max, st)
+                    : round_impl<kOpSsspNF, false>(kp, rb, grid_max, st);
       return dist ? round_impl<IRGL_OP_SSSP, true>(kp, rb, grid_max, st)
                   : round_impl<IRGL_OP_SSSP, false>(kp, rb, grid_max, st);
     case IRGL_OP_CC_LP:
@@ -1038,7 +1084,10 @@ cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, 
       apply_remote_kernel<IRGL_OP_BFS><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
       break;
     case IRGL_OP_SSSP:
-      apply_remote_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+      if (rb.threshold != kInf)
+        apply_remote_kernel<kOpSsspNF><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+      else
+        apply_remote_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
       break;
     case IRGL_OP_CC_LP:
       apply_remote_kernel<IRGL_OP_CC_LP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
@@ -1066,9 +1115,12 @@ int persistent_blocks_per_sm(int op) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nd, persistent_bfs_do_kernel, kBlock, 0);
       nb = min(nb, nd);
     } break;
-    case IRGL_OP_SSSP:
+    case IRGL_OP_SSSP: {
+      int nn = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
-      break;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nn, persistent_kernel<kOpSsspNF>, kBlock, 0);
+      nb = min(nb, nn);
+    } break;
     case IRGL_OP_CC_LP:
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_CC_LP>, kBlock, 0);
       break;
@@ -1105,6 +1157,8 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
         return cudaLaunchCooperativeKernel((void*)persistent_bfs_do_kernel, grid, kBlock, args, 0, st);
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_BFS>, grid, kBlock, args, 0, st);
     case IRGL_OP_SSSP:
+      if (a.delta > 0)
+        return cudaLaunchCooperativeKernel((void*)persistent_kernel<kOpSsspNF>, grid, kBlock, args, 0, st);
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_SSSP>, grid, kBlock, args, 0, st);
     case IRGL_OP_CC_LP:
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_CC_LP>, grid, kBlock, args, 0, st);

@@ -30,33 +30,36 @@ static_assert(sizeof(ChunkDesc) == 16, "one 128-bit load per descriptor");
 
 // Device-resident control block of one pipe partition.  Counter slots are addressed by index so
 // the persistent kernel can rotate them (see persistent loop in expand.cu).
+// The counters every warp hits during an expansion (out count, chunk reservations, tile fetches,
+// edge totals, deferral minimum) each sit on their own 256-byte line, so their atomics spread
+// over different L2 slices instead of queueing at one.
 struct Ctl {
-  uint32_t cnt[4];        // worklist counters: in / out / retry / spare (slots named by the host)
-  uint32_t chunk_cnt[3];  // CTA-chunk list counters, rotated by round
-  uint32_t red[3];        // ReduceAndReturn cells, rotated by round
+  alignas(256) uint32_t cnt[4];        // worklist counters: in / out / retry / spare (slots named by the host)
+  alignas(256) uint32_t chunk_cnt[3];  // edge-chunk list counters, rotated by round
+  alignas(256) uint32_t red[3];        // ReduceAndReturn cells, rotated by round
   uint32_t overflow;      // push beyond capacity (IRGL_E_WL_OVERFLOW)
   uint32_t pad;
-  unsigned long long edges;    // directed edges scanned
-  unsigned long long popped;   // items popped (persistent mode)
+  alignas(256) unsigned long long edges;    // directed edges scanned
+  alignas(256) unsigned long long popped;   // items popped (persistent mode)
   unsigned long long pushes;   // items pushed (persistent mode)
   unsigned long long remote;   // remote updates emitted
   unsigned long long rounds;   // persistent: rounds executed
   int32_t last_red;            // persistent: last round's reduced value
   int32_t exit_in_slot;        // persistent: buffer parity at exit
   unsigned long long tc_count; // TC: Sum reduction (extension)
-  uint32_t tile_ctr[3];        // dynamic warp-tile counters, rotated by round
+  alignas(256) uint32_t tile_ctr[3];        // dynamic warp-tile counters, rotated by round
   uint32_t far_cnt[2];         // SSSP near-far pile counters (double-buffered)
   uint32_t minkeep[2];         // min dist kept in the far pile by a split (double-buffered: the
                                // persistent kernel resets one slot while CTAs may still read the other)
   uint32_t stamp_used;         // persistent: stamp ids consumed (rounds + splits)
   uint32_t far_sel;            // persistent: current far pile at exit
   uint32_t bu_rounds;          // direction-optimising BFS: bottom-up rounds executed
-  unsigned long long mf[3];    // DO-BFS: edges of the next frontier (rotated by round)
+  alignas(256) unsigned long long mf[3];    // DO-BFS: edges of the next frontier (rotated by round)
   unsigned long long bu_found[3];  // DO-BFS: vertices discovered by a bottom-up round
   unsigned long long bu_scanned;   // DO-BFS: edges examined by bottom-up rounds
   unsigned long long mst_w, mst_e; // MST: forest weight / edges
   uint32_t mst_cnt[2];             // MST: internal worklist counters
-  uint32_t dmin[3];                // SSSP deferral: min distance pushed into each round's out
+  alignas(256) uint32_t dmin[3];                // SSSP deferral: min distance pushed into each round's out
                                    // worklist (0xffffffff = unknown), rotated by round
   // grid barrier of the persistent kernels (grid_sync_bcast): monotonic arrival counter and the
   // release word {barrier tag, payload}, on separate L2 lines; zeroed before every launch
