@@ -97,7 +97,7 @@ typedef struct irgl_config {
                                     (edge-balanced); below: the warp tile's fine-grained gather;
                                     0 -> 128                                                    */
   int32_t cta_threshold;         /* rounds with at most one tile per warp: degrees below this are
-                                    expanded by the popping warp (no chunk phase); 0 -> 512      */
+                                    expanded by the popping warp (no chunk phase); 0 -> 256      */
   int32_t chunk_edges;           /* edges per chunk descriptor (<= 65535); 0 -> 512            */
   int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */

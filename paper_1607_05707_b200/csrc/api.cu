@@ -133,7 +133,7 @@ static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   // below cta_t are expanded by the popping warp.  Defaults from the RMAT-22 sweep
   // (profiles/r1s2_sched_sweep.txt).
   ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 128;
-  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 512;
+  ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 256;
   ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 512;
   ec.chunk_edges = std::max(4, std::min(ec.chunk_edges, 65535));  // 16-bit length in ChunkDesc
   if (ec.warp_t < 1) ec.warp_t = 1;
@@ -740,8 +740,9 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     for (uint64_t r = 0; r < std::min<uint64_t>(h.rounds, pa.trace_cap); ++r) {
       const unsigned long long* q = &t[8 * r];
       // us = whole round; item / flush / sync1 / chunk = leader-thread timestamps since round start
-      fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu item=%.2f flush=%.2f sync1=%.2f chunk=%.2f\n",
-              op, (unsigned long long)r, us(q[0]), q[1], q[2], q[3] - e0, us(q[4]), us(q[5]), us(q[6]), us(q[7]));
+      fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu item=%.2f flush=%.2f sync1=%.2f chunk=%.2f nch=%llu\n",
+              op, (unsigned long long)r, us(q[0]), q[1] & 0xffffffffull, q[2], q[3] - e0, us(q[4]), us(q[5]), us(q[6]),
+              us(q[7]), q[1] >> 32);
       prev = q[0];
       e0 = q[3];
     }

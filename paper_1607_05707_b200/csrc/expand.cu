@@ -539,29 +539,6 @@ __device__ __forceinline__ ChunkDesc ld_desc(const ChunkDesc* p) {
   return d;
 }
 
-#ifdef IRGL_EXPERIMENT
-// Timing experiment only (never in the product build): replay a chunk's col/weight loads
-// (IRGL_EXPERIMENT=1) or loads + label gathers (=2) with no side effects.
-template <int OP>
-__device__ __noinline__ void probe_range(const KParams& p, int64_t b, int64_t e, int gl) {
-  const int64_t g1 = (e + 3) >> 2;
-  int acc = 0;
-  for (int64_t q0 = b >> 2; q0 < g1; q0 += 64) {
-    const int64_t qa = q0 + gl, qb = q0 + 32 + gl;
-    int4 ca = make_int4(0, 0, 0, 0), cb = ca, wa = ca, wb = ca;
-    if (qa < g1) { ca = ld_stream_v4(p.g.col + 4 * qa); if (is_sssp(OP)) wa = ld_stream_v4(p.g.w + 4 * qa); }
-    if (qb < g1) { cb = ld_stream_v4(p.g.col + 4 * qb); if (is_sssp(OP)) wb = ld_stream_v4(p.g.w + 4 * qb); }
-    if (IRGL_EXPERIMENT == 2) {
-      const int32_t d8[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc += (qa < g1 || j >= 4) && (qb < g1 || j < 4) ? ld_label(p.lab + d8[j]) : 0;
-    } else {
-      acc += ca.x ^ cb.y ^ wa.z ^ wb.w;
-    }
-  }
-  if (acc == 0x7ffffffe) p.ctl->pad = acc;  // keep the loads
-}
-#endif
 
 template <int OP, bool DIST>
 __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, uint32_t nch) {
@@ -569,20 +546,96 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const int gl = lane_id();
+  if (nch * 2 <= nw) {
+    // few chunks (latency-bound round): every chunk is split over P warps, so the phase costs one
+    // or two 128-edge iterations per warp instead of chunk_edges / 128 sequential ones
+    if (nch == 0) return;
+    const uint32_t P = min(nw / nch, 16u);
+    if (gw >= nch * P) return;
+    const ChunkDesc d = ld_desc(rb.chunks + gw / P);
+    const uint32_t part = gw % P;
+    const int64_t b = (int64_t)(d.beg_len >> 16), len = (int64_t)(d.beg_len & 0xffffu);
+    const int64_t per = (((len + P - 1) / P) + 3) & ~int64_t(3);
+    const int64_t b0 = b + part * per, e0 = min(b0 + per, b + len);
+    if (b0 < e0) process_range<OP, DIST>(sm, q, p, rb, b0, e0, d.sv, gl);
+    return;
+  }
+  // Software-pipelined drain: each iteration is one int4 group per lane (128 edges per warp);
+  // the NEXT iteration's col/weight group (possibly the first group of the warp's next chunk) is
+  // loaded before this iteration's gathers and atomics are waited on, so the DRAM latency of the
+  // CSR stream is off the per-iteration dependency chain.
   uint32_t c = gw;
-  ChunkDesc cur{};
-  if (c < nch) cur = ld_desc(rb.chunks + c);
-  while (c < nch) {
-    const uint32_t cn = c + nw;
-    ChunkDesc nxt{};
-    if (cn < nch) nxt = ld_desc(rb.chunks + cn);
-    const int64_t b = (int64_t)(cur.beg_len >> 16);
-#ifdef IRGL_EXPERIMENT
-    probe_range<OP>(p, b, b + (int64_t)(cur.beg_len & 0xffffu), gl);
-#endif
-    process_range<OP, DIST>(sm, q, p, rb, b, b + (int64_t)(cur.beg_len & 0xffffu), cur.sv, gl);
-    c = cn;
-    cur = nxt;
+  if (c >= nch) return;
+  const int32_t* __restrict__ col = p.g.col;
+  const int32_t* __restrict__ wgt = p.g.w;
+  ChunkDesc nx = (c + nw < nch) ? ld_desc(rb.chunks + c + nw) : ChunkDesc{};
+  ChunkDesc cd = ld_desc(rb.chunks + c);
+  int64_t b = (int64_t)(cd.beg_len >> 16);
+  int64_t e = b + (int64_t)(cd.beg_len & 0xffffu);
+  int32_t sv = cd.sv;
+  int64_t q0 = b >> 2;
+  int4 cc = make_int4(0, 0, 0, 0), ww = cc;
+  {
+    const int64_t qk = q0 + gl;
+    if (qk < ((e + 3) >> 2)) {
+      cc = ld_stream_v4(col + 4 * qk);
+      if (is_sssp(OP)) ww = ld_stream_v4(wgt + 4 * qk);
+    }
+  }
+  for (;;) {
+    // position of the next iteration
+    int64_t nq0 = q0 + 32, nb = b, ne = e;
+    int32_t nsv = sv;
+    bool more = true;
+    if (nq0 >= ((e + 3) >> 2)) {
+      c += nw;
+      if (c >= nch) {
+        more = false;
+      } else {
+        nb = (int64_t)(nx.beg_len >> 16);
+        ne = nb + (int64_t)(nx.beg_len & 0xffffu);
+        nsv = nx.sv;
+        nq0 = nb >> 2;
+        if (c + nw < nch) nx = ld_desc(rb.chunks + c + nw);
+      }
+    }
+    int4 ncc = make_int4(0, 0, 0, 0), nww = ncc;
+    if (more) {
+      const int64_t qk = nq0 + gl;
+      if (qk < ((ne + 3) >> 2)) {
+        ncc = ld_stream_v4(col + 4 * qk);
+        if (is_sssp(OP)) nww = ld_stream_v4(wgt + 4 * qk);
+      }
+    }
+    // this iteration: 4 edges per lane
+    const int64_t e0 = 4 * (q0 + gl);
+    bool act[4];
+    uint32_t d[4];
+    int32_t wt[4], s4[4], cur[4];
+    {
+      const int32_t c4[4] = {cc.x, cc.y, cc.z, cc.w};
+      const int32_t w4[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        act[t] = e0 + t >= b && e0 + t < e;
+        d[t] = (uint32_t)c4[t];
+        wt[t] = w4[t];
+        s4[t] = sv;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) cur[t] = act[t] ? ld_label(p.lab + d[t]) : 0;
+    int kk[4];
+    relax_batch<OP, 4>(p, rb, q, act, cur, s4, wt, d, kk);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) wpush<OP, DIST>(sm, q, p, rb, kk[t], d[t]);
+    if (!more) break;
+    q0 = nq0;
+    b = nb;
+    e = ne;
+    sv = nsv;
+    cc = ncc;
+    ww = nww;
   }
 }
 
@@ -833,7 +886,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[8 * r + 0] = t;
-        a.trace[8 * r + 1] = rb.nin;
+        a.trace[8 * r + 1] = rb.nin | ((unsigned long long)nch << 32);
         a.trace[8 * r + 2] = nout;
         a.trace[8 * r + 3] = *(volatile unsigned long long*)&p.ctl->edges;
       }
