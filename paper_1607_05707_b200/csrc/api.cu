@@ -181,7 +181,7 @@ static irgl_status_t pipe_set_in(irgl_ctx* ctx, irgl_pipe* p, int l, const std::
   CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->overflow, 0, sizeof(uint32_t), pr.st));
-  CK(cudaStreamSynchronize(pr.st));
+  // pageable sources are staged before cudaMemcpyAsync returns: no host sync needed (stream order)
   pp.n_in = (uint32_t)items.size();
   return IRGL_OK;
 }
@@ -255,18 +255,19 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
         // label[v] = v (iota over int32 as uint32)
         CK(launch_iota_u32(reinterpret_cast<uint32_t*>(gp.lab), 0u, (uint32_t)g->n, pr.st));
       }
-      if (gp.stamp) CK(cudaMemsetAsync(gp.stamp, 0, g->n * sizeof(int32_t), pr.st));
+      // push-dedupe stamps: ids keep increasing across traversals, so old stamps never match a new
+      // round's code; the array is cleared only when the id space (codes 2*id+1 < 2^31) wraps
+      if (gp.stamp && g->stamp_epoch > (1ll << 29)) CK(cudaMemsetAsync(gp.stamp, 0, g->n * sizeof(int32_t), pr.st));
       if ((op == IRGL_OP_BFS || op == IRGL_OP_SSSP) && pipe) {
         // level/dist[src] = 0 for the initial items (App. B2); items were routed to owners
         PipePart& pp = pipe->parts[l];
         CK(launch_scatter_zero(gp.lab, pp.buf[pp.b_in], pp.n_in, pr.st));
       }
-      CK(cudaStreamSynchronize(pr.st));
     }
     // NCCL mode: every rank's ghost copy must also see the sources as 0 (they are owned elsewhere
     // but never pushed back) — handled because the owner applies; remote ghosts stay INF.
     g->lab_op = op;
-    g->stamp_epoch = 0;
+    if (g->stamp_epoch > (1ll << 29)) g->stamp_epoch = 0;
     return IRGL_OK;
   }
   if (op == IRGL_OP_PR) {
@@ -711,21 +712,16 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     CK(cudaMemsetAsync(pa.trace, 0, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
   }
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
-  CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
-  CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(pp.ctl->tile_ctr), pr.st));
-  CK(cudaMemsetAsync(pp.ctl->far_cnt, 0, sizeof(pp.ctl->far_cnt), pr.st));
-  CK(cudaMemsetAsync(pp.ctl->dmin, 0xff, sizeof(pp.ctl->dmin), pr.st));  // round 0: no deferral
-  CK(cudaMemsetAsync(&pp.ctl->gb_arrive, 0, sizeof(unsigned int), pr.st));  // grid_sync_bcast state
-  CK(cudaMemsetAsync(&pp.ctl->gb_release, 0, sizeof(unsigned long long), pr.st));
-  CK(cudaMemsetAsync(&pp.ctl->popped, 0, 2 * sizeof(unsigned long long), pr.st));
-  CK(cudaMemsetAsync(&pp.ctl->rounds, 0, sizeof(unsigned long long), pr.st));
-  CK(cudaMemsetAsync(pp.ctl->mf, 0, sizeof(pp.ctl->mf) + sizeof(pp.ctl->bu_found) + 8, pr.st));
+  // one launch resets the control block for the outlined loop (chunk / tile / far counters, deferral
+  // minima = unknown so round 0 defers nothing, barrier state, statistics)
+  CK(launch_ctl_prepare(pp.ctl, pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
-  Ctl h;
-  CK(cudaMemcpyAsync(&h, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
-  CK(cudaStreamSynchronize(pr.st));
+  static_assert(sizeof(Ctl) <= 4096, "control block readback goes through the 4 KB pinned scratch");
+  CK(cudaMemcpyAsync(pr.h_pin, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaStreamSynchronize(pr.st));  // the iterate's one host synchronisation
+  const Ctl& h = *reinterpret_cast<const Ctl*>(pr.h_pin);
   {
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
@@ -757,7 +753,8 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pp.c_spare = slots[(K + 2) % 3];
   pp.n_in = h.cnt[pp.c_in];
   g->stamp_epoch += h.stamp_used;
-  stt->edges += (int64_t)h.bu_scanned;  // pipe_counters adds the top-down scans
+  stt->edges += (int64_t)(h.bu_scanned + h.edges);  // bottom-up + top-down scans
+  stt->remote_updates += (int64_t)h.remote;
   stt->rounds += K;
   stt->launches += 1;
   stt->popped += (int64_t)h.popped;
@@ -767,21 +764,23 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
 }
 
 // Read (stt != null) and zero the edges / remote counters of the pipe's control blocks.
+// stt == nullptr: zero the edge / remote counters (stream-ordered, no host sync).  Otherwise add
+// them to the stats (one pinned readback + sync) and zero them.
 static irgl_status_t pipe_counters(irgl_ctx* ctx, irgl_pipe* pipe, irgl_iter_stats* stt) {
   for (size_t l = 0; l < pipe->parts.size(); ++l) {
     PartRT& pr = ctx->parts[l];
     PipePart& pp = pipe->parts[l];
     CK(cudaSetDevice(pr.dev));
     if (stt) {
-      unsigned long long he = 0, hr = 0;
-      CK(cudaMemcpy(&he, &pp.ctl->edges, 8, cudaMemcpyDeviceToHost));
-      CK(cudaMemcpy(&hr, &pp.ctl->remote, 8, cudaMemcpyDeviceToHost));
-      stt->edges += (int64_t)he;
-      stt->remote_updates += (int64_t)hr;
+      unsigned long long* hv = reinterpret_cast<unsigned long long*>(pr.h_pin);
+      CK(cudaMemcpyAsync(hv, &pp.ctl->edges, 8, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaMemcpyAsync(hv + 1, &pp.ctl->remote, 8, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+      stt->edges += (int64_t)hv[0];
+      stt->remote_updates += (int64_t)hv[1];
     }
     CK(cudaMemsetAsync(&pp.ctl->edges, 0, 8, pr.st));
     CK(cudaMemsetAsync(&pp.ctl->remote, 0, 8, pr.st));
-    CK(cudaStreamSynchronize(pr.st));
   }
   return IRGL_OK;
 }
@@ -1614,7 +1613,7 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
         // the first round has no frontier minimum yet: no deferral
         for (size_t l = 0; l < pipe->parts.size(); ++l) {
           CK(cudaSetDevice(ctx->parts[l].dev));
-          CK(cudaMemset(pipe->parts[l].ctl->dmin, 0xff, sizeof(pipe->parts[l].ctl->dmin)));
+          CK(cudaMemsetAsync(pipe->parts[l].ctl->dmin, 0xff, sizeof(pipe->parts[l].ctl->dmin), ctx->parts[l].st));
         }
         CK(cudaSetDevice(pr0.dev));
       }
@@ -1633,11 +1632,12 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
       return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
                   "direction-optimising BFS runs outlined on one partition");
     // the outlined kernel's barrier word carries the out count in 30 bits
-    if (outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30))
-      s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
+    const bool outlined = outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30);
+    if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s != IRGL_OK) return s;
-    s = pipe_counters(ctx, pipe, &st);  // edges scanned / remote updates
+    // edges scanned / remote updates (the outlined path read them with its control block)
+    s = pipe_counters(ctx, pipe, outlined ? nullptr : &st);
     if (s != IRGL_OK) return s;
   } else if (op == IRGL_OP_PR && outline && ctx->ptotal() == 1 &&
              (o.cond_mode != IRGL_COND_NONE || o.max_rounds > 0)) {

@@ -1159,6 +1159,31 @@ cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_
   return cudaGetLastError();
 }
 
+__global__ void ctl_prepare_kernel(Ctl* c) {
+  const int t = threadIdx.x;
+  if (t < 3) {
+    c->chunk_cnt[t] = 0;
+    c->tile_ctr[t] = 0;
+    c->dmin[t] = 0xffffffffu;  // round 0: no frontier minimum yet (no deferral)
+    c->mf[t] = 0;
+    c->bu_found[t] = 0;
+  }
+  if (t < 2) c->far_cnt[t] = 0;
+  if (t == 0) {
+    c->gb_arrive = 0;
+    c->gb_release = 0;
+    c->popped = c->pushes = 0;
+    c->rounds = 0;
+    c->bu_scanned = 0;
+  }
+}
+
+cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st) {
+  note_launch();
+  ctl_prepare_kernel<<<1, 32, 0, st>>>(ctl);
+  return cudaGetLastError();
+}
+
 int persistent_blocks_per_sm(int op) {
   int nb = 0;
   switch (op) {

@@ -131,6 +131,9 @@ cudaError_t launch_exclusive_test(const uint32_t* in, uint32_t nin, const int32_
                                   int32_t* owner, int32_t* won, int32_t* log, int grid,
                                   cudaStream_t st);
 
+// Reset of the control block before an outlined (persistent) launch, in one kernel.
+cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st);
+
 // ---- misc (util.cu) ---------------------------------------------------------------------------
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);
 cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st);
