@@ -101,7 +101,10 @@ typedef struct irgl_config {
   int32_t chunk_edges;           /* edges per chunk descriptor (<= 65535); 0 -> 512            */
   int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
-  int32_t reserved[8];
+  int32_t dense_div;             /* outlined rounds whose frontier has >= n/dense_div vertices run
+                                    dense: relaxations mark (fire-and-forget stores / REDs) and a
+                                    compaction sweep builds the out worklist; 0 -> 16, <0 off    */
+  int32_t reserved[7];
 } irgl_config;
 
 /* Kernel arguments (the Invoke/Iterate `args`). */

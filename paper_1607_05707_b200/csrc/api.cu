@@ -509,6 +509,7 @@ static RoundBufs round_bufs(irgl_pipe* pipe, GraphPart& gp, PipePart& pp, int32_
   rb.far_cap = gp.far_cap;
   rb.threshold = nf.delta > 0 ? nf.threshold : kInf;
   rb.mf_acc = nullptr;
+  rb.dense = 0;
   rb.defer_k = nf.defer_k;
   rb.dmin_cur = &pp.ctl->dmin[nf.dsel];
   rb.dmin_next = nf.defer_k > 0 ? &pp.ctl->dmin[nf.dsel ^ 1] : nullptr;
@@ -701,6 +702,11 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.n = g->n;
   pa.m = g->m;
   pa.defer_k = op == IRGL_OP_SSSP ? nf.defer_k : 0;
+  // dense rounds (mark + compaction sweep) once the frontier reaches n / dense_div
+  {
+    const int32_t dd = ctx->cfg.dense_div == 0 ? 16 : ctx->cfg.dense_div;
+    pa.dense_min = (dd > 0 && nf.delta <= 0) ? std::max<int64_t>(g->n / dd, 1) : 0;
+  }
   // IRGL_ROUND_TRACE=1: the leader thread stamps %globaltimer, |in|, |out| and the edge counter
   // after every round (the SPEC's --trace, at round granularity); printed to stderr
   pa.trace = nullptr;

@@ -133,6 +133,29 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
                                             const bool (&act)[K], const int32_t (&cur)[K],
                                             const int32_t (&sv)[K], const int32_t (&wt)[K],
                                             const uint32_t (&dst)[K], int (&kind)[K]) {
+  if (!has_far(OP) && rb.dense) {
+    // dense round: mark instead of push, every write fire-and-forget (no result waited on); the
+    // compaction phase after the barrier builds the out worklist from the marks
+    if (is_bfs(OP)) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (act[j] && cur[j] == kInf) p.lab[dst[j]] = rb.level;  // every writer stores LEVEL
+    } else {
+      const int32_t code = rb.stamp_id << 1;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int32_t nd = is_sssp(OP) ? sv[j] + wt[j] : sv[j];
+        if (act[j] && nd < cur[j]) {
+          atomicMin(p.lab + dst[j], nd);    // RED.MIN
+          atomicMax(p.stamp + dst[j], code);  // RED.MAX: stamp ids only grow
+          if (is_sssp(OP)) q.dmin = min(q.dmin, nd);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) kind[j] = 0;
+    return;
+  }
   if (is_bfs(OP)) {
     int32_t old[K];
 #pragma unroll
@@ -372,11 +395,12 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
       int kind = 0;
       if (defer) {
         const int32_t code = rb.stamp_id << 1;
-        kind = atomicExch(p.stamp + v, code) != code ? 1 : 0;
+        if (!has_far(OP) && rb.dense) atomicMax(p.stamp + v, code);  // mark (compaction pushes)
+        else kind = atomicExch(p.stamp + v, code) != code ? 1 : 0;
         q.dmin = min(q.dmin, sv);
         deg = 0;
       }
-      wpush<OP, DIST>(sm, q, p, rb, kind, v);
+      if (has_far(OP) || !rb.dense) wpush<OP, DIST>(sm, q, p, rb, kind, v);
     }
   }
   {
@@ -639,6 +663,23 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
   }
 }
 
+// ---- dense-round compaction: the out worklist = the vertices marked this round (BFS: level ==
+// LEVEL; SSSP / CC: stamp == the round's code), in vertex order; coalesced sweep over the
+// partition's label (or stamp) array, pushes through the usual warp staging.
+template <int OP>
+__device__ void compact_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
+  const int64_t n = p.g.hi - p.g.lo;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int32_t* mark = is_bfs(OP) ? p.lab : p.stamp;
+  const int32_t want = is_bfs(OP) ? rb.level : (rb.stamp_id << 1);
+  for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); i0 < n; i0 += T) {
+    const int64_t i = i0 + lane_id();
+    const uint32_t v = (uint32_t)(p.g.lo + i);
+    const int kind = (i < n && ld_label_cg(mark + v) == want) ? 1 : 0;
+    wpush<OP, false>(sm, q, p, rb, kind, v);
+  }
+}
+
 // ---- near-far split: far pile -> near worklist / next far pile / dropped --------------------------
 //   dist <  t_old            : already expanded when it dropped below the old threshold -> drop
 //   t_old <= dist < threshold: near worklist
@@ -807,6 +848,9 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     rb.defer_k = (is_sssp(OP)) ? a.defer_k : 0;
     rb.dmin_cur = nullptr;
     rb.dmin_val = s_dmin;  // written by thread 0 before the barrier that ended round r-1
+    // dense round: relaxations mark (fire-and-forget stores / REDs) instead of pushing, and a
+    // compaction sweep builds the out worklist after the expansion barrier
+    rb.dense = (!has_far(OP) && a.dense_min > 0 && (int64_t)nin_next >= a.dense_min) ? 1 : 0;
     rb.dmin_next = rb.defer_k > 0 ? &p.ctl->dmin[(r + 1) % 3] : nullptr;
     // Without near-far the round's view lives in shared memory (written by thread 0 between two
     // CTA barriers): the expansion then reads its pointers from smem at the use sites instead of
@@ -841,6 +885,15 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
                           [&](unsigned long long) { fetch_dmin(); });
       nout = unpack_nout(w);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 7]));
+    }
+    if constexpr (!has_far(OP)) {
+      if (rr.dense) {
+        compact_phase<OP>(sm, q, p, rr);
+        wflush_all<OP>(sm, q, p, rr);
+        w = grid_sync_bcast(p.ctl, bidx, &bslot, [&]() { return pack_counts(0, ld_ctl(cout)); },
+                            [&](unsigned long long) {});
+        nout = unpack_nout(w);
+      }
     }
     if constexpr (has_far(OP)) if (nf) {
       // near frontier exhausted: advance the threshold and split the far pile; a pile past half
@@ -990,6 +1043,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
     rb.far_cap = 0;
     rb.threshold = kInf;
     rb.mf_acc = &p.ctl->mf[r % 3];
+    rb.dense = 0;
     rb.defer_k = 0;
     rb.dmin_cur = nullptr;
     rb.dmin_next = nullptr;

@@ -50,6 +50,7 @@ struct RoundBufs {
   const uint32_t* dmin_cur;  // null: use dmin_val (persistent kernel: broadcast at the barrier)
   uint32_t* dmin_next;
   int32_t dmin_val;
+  int32_t dense;  // 1: mark-instead-of-push round (outlined, one partition, no near-far)
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
@@ -87,6 +88,7 @@ struct PersistArgs {
   int64_t n;           // vertices (bottom-up sweeps)
   int64_t m;           // directed edges
   int64_t defer_k;     // SSSP deferral budget (0 = off); cells Ctl::dmin rotate by round
+  int64_t dense_min;   // rounds with |in| >= dense_min run dense (0 = never)
   unsigned long long* trace;  // optional per-round trace [4 * trace_cap + 1] (IRGL_ROUND_TRACE)
   uint32_t trace_cap;
 };

@@ -178,6 +178,34 @@ def test_sssp_deferral_with_near_far_and_grid(ctx, irgl, oracle, defer):
             np.testing.assert_array_equal(d, oracle.sssp(og, 0))
 
 
+@pytest.mark.parametrize("dense_div", [-1, 1, 4, 32, 100000])
+def test_dense_rounds_parity(irgl, oracle, dense_div):
+    """Dense rounds (mark + compaction sweep instead of pushes) build the same frontiers: BFS
+    levels / invocation counts, SSSP distances and CC_LP labels stay bit-exact whether no round,
+    every round or only the large ones run dense."""
+    og = oracle.rmat(14)
+    with irgl.Context(dense_div=dense_div) as c:
+        g = _upload(c, og)
+        for s in og.sources(2):
+            s = int(s)
+            ref, ecc = oracle.bfs(og, s)
+            lv, st = irgl.bfs(c, g, s, outline=1)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1
+            for defer in (0, 1024):
+                d, _ = irgl.sssp(c, g, s, outline=1, delta=0, defer=defer)
+                np.testing.assert_array_equal(d, oracle.sssp(og, s))
+        lab, _ = irgl.cc_lp(c, g, outline=1)
+        np.testing.assert_array_equal(lab, oracle.cc(og))
+    og = oracle.grid(40, 30, diag=True)
+    with irgl.Context(dense_div=dense_div) as c:
+        g = _upload(c, og)
+        lv, st = irgl.bfs(c, g, 0, outline=1)
+        np.testing.assert_array_equal(lv, oracle.bfs(og, 0)[0])
+        d, _ = irgl.sssp(c, g, 0, outline=1)
+        np.testing.assert_array_equal(d, oracle.sssp(og, 0))
+
+
 def test_sssp_device_generated_graph(ctx, irgl, oracle):
     og = oracle.rmat(15)
     g = ctx.generate_rmat(15)
