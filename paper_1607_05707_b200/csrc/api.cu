@@ -19,6 +19,7 @@ struct PartRT {  // one vertex partition hosted by this process
   cudaStream_t st = nullptr;
   int sms = 0;
   uint32_t* h_pin = nullptr;  // pinned scratch (counts readback)
+  uint32_t* hdr = nullptr;    // multi-partition round header {send counts [P], in-count, overflow}
 };
 }  // namespace irgl
 
@@ -30,6 +31,7 @@ struct irgl_ctx {
   const irgl::NcclApi* nccl = nullptr;
   int64_t route_size = INT64_MAX;   // partition size of the last graph (pipe routing)
   uint32_t* cnt_dev = nullptr;      // NCCL count exchange scratch [L*P + P*P]
+  uint32_t* hdr_all = nullptr;      // NCCL round-header gather [(L + P) * (P + 2)]
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // hot-kernel timing (iter_stats.kernel_ms)
@@ -495,6 +497,7 @@ static RoundBufs round_bufs(irgl_pipe* pipe, GraphPart& gp, PipePart& pp, int32_
   RoundBufs rb;
   rb.in = pp.buf[pp.b_in];
   rb.nin = pp.n_in;
+  rb.nin_dev = nullptr;
   rb.out = pp.buf[pp.b_out];
   rb.out_cnt = &pp.ctl->cnt[pp.c_out];
   rb.cap = (uint32_t)pipe->cap;
@@ -664,6 +667,180 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
     stt->rounds++;
     nf.dsel ^= 1;
     ++level;  // between_rounds { LEVEL++ }
+  }
+  return IRGL_OK;
+}
+
+// ---- multi-partition rounds with one host synchronisation each -----------------------------------
+// Per round: expand every local partition (the in-count is read on the device), pack the remote
+// updates' ghost labels (counts read on the device), write a round header {send counts, in-count,
+// overflow} per partition and gather all headers (NCCL AllGather across ranks, D2H copies within a
+// process) -> the ONE sync.  The headers give the payload sizes of the grouped send/recv and the
+// global in-count: an all-empty round is the Iterate termination and did no work.
+// Owner-side applies are stream-ordered after the receives; the in/out swap needs no counts.
+static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                                          int64_t level0, const irgl_iterate_opts& o, NearFar& nf,
+                                          irgl_iter_stats* stt) {
+  const int L = (int)ctx->parts.size();
+  const int P = ctx->ptotal();
+  const int H = P + 2;  // header words per partition
+  const int64_t ps = g->part_size;
+  const bool vals = op != IRGL_OP_BFS;
+  const ExpandCfg ec = expand_cfg(ctx);
+  int64_t level = level0;
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    if (!pr.hdr) CK(cudaMalloc(&pr.hdr, (size_t)H * 4));
+  }
+  if (ctx->comm && !ctx->hdr_all) {
+    CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaMalloc(&ctx->hdr_all, (size_t)(L + P) * H * 4));
+  }
+  std::vector<uint32_t> hdr((size_t)P * H, 0);
+  for (;;) {
+    if (o.max_rounds > 0 && stt->rounds >= o.max_rounds) break;  // ExtraCond (Or)
+    const int32_t stamp_id = (int32_t)(++g->stamp_epoch);
+    std::vector<RoundBufs> rbs(L);
+    // 1. local expansion + remote-update pack + round header (all stream-ordered)
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      if (nf.defer_k > 0) CK(cudaMemsetAsync(&pp.ctl->dmin[nf.dsel ^ 1], 0xff, 4, pr.st));
+      rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
+      rbs[l].nin_dev = &pp.ctl->cnt[pp.c_in];
+      DistRoute dr{P, ctx->gpart(l), ps, gp.send, gp.send_cnt};
+      if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
+      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
+      if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
+      stt->launches += 2;
+      if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
+      CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow, pr.st));
+      CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(uint32_t), pr.st));
+      CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(uint32_t), pr.st));
+    }
+    // 2. gather the headers: the round's one host synchronisation
+    if (ctx->comm) {
+      PartRT& pr = ctx->parts[0];
+      CK(cudaSetDevice(pr.dev));
+      for (int l = 1; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // same device
+      for (int l = 0; l < L; ++l)
+        CK(cudaMemcpyAsync(ctx->hdr_all + (size_t)l * H, ctx->parts[l].hdr, (size_t)H * 4,
+                           cudaMemcpyDeviceToDevice, pr.st));
+      NCK(ctx->nccl->AllGather(ctx->hdr_all, ctx->hdr_all + (size_t)L * H, (size_t)L * H, ncclUint32,
+                               ctx->comm, pr.st));
+      CK(cudaMemcpyAsync(pr.h_pin, ctx->hdr_all + (size_t)L * H, (size_t)P * H * 4,
+                         cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+      std::memcpy(hdr.data(), pr.h_pin, (size_t)P * H * 4);
+    } else {
+      for (int l = 0; l < L; ++l) {
+        PartRT& pr = ctx->parts[l];
+        CK(cudaSetDevice(pr.dev));
+        CK(cudaMemcpyAsync(pr.h_pin, pr.hdr, (size_t)H * 4, cudaMemcpyDeviceToHost, pr.st));
+      }
+      for (int l = 0; l < L; ++l) {
+        PartRT& pr = ctx->parts[l];
+        CK(cudaSetDevice(pr.dev));
+        CK(cudaStreamSynchronize(pr.st));
+        std::memcpy(&hdr[(size_t)ctx->gpart(l) * H], pr.h_pin, (size_t)H * 4);
+      }
+    }
+    {
+      float kms = 0.f;
+      CK(cudaSetDevice(ctx->parts[0].dev));
+      CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
+      stt->kernel_ms += kms;
+    }
+    uint64_t total_in = 0, local_in = 0;
+    for (int p = 0; p < P; ++p) {
+      total_in += hdr[(size_t)p * H + P];
+      if (hdr[(size_t)p * H + P + 1]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+    }
+    for (int l = 0; l < L; ++l) local_in += hdr[(size_t)ctx->gpart(l) * H + P];
+    if (stt->rounds > 0) stt->pushes += (int64_t)local_in;  // last round's out = this round's in
+    if (total_in == 0) break;  // every in worklist was empty: Iterate ends (no sends queued)
+    stt->popped += (int64_t)local_in;
+    // 3. payloads: grouped send/recv (NCCL) or peer copies (one process), then owner-side applies
+    auto count = [&](int p, int q) { return hdr[(size_t)p * H + q]; };
+    if (ctx->comm) {
+      PartRT& pr = ctx->parts[0];
+      CK(cudaSetDevice(pr.dev));
+      for (int l = 1; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // packs done
+      const int lo_part = ctx->gpart(0);
+      NCK(ctx->nccl->GroupStart());
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < P; ++q) {
+          if (p == q) continue;
+          const uint32_t c = count(p, q);
+          if (!c) continue;
+          const bool src_local = p >= lo_part && p < lo_part + L;
+          const bool dst_local = q >= lo_part && q < lo_part + L;
+          if (src_local) {
+            GraphPart& sp = g->parts[p - lo_part];
+            NCK(ctx->nccl->Send(sp.send + (int64_t)q * ps, c, ncclUint32, q / L, ctx->comm, pr.st));
+            if (vals) NCK(ctx->nccl->Send(sp.send_val + (int64_t)q * ps, c, ncclInt32, q / L, ctx->comm, pr.st));
+            stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
+          }
+          if (dst_local) {
+            GraphPart& dp = g->parts[q - lo_part];
+            NCK(ctx->nccl->Recv(dp.recv + (int64_t)p * ps, c, ncclUint32, p / L, ctx->comm, pr.st));
+            if (vals) NCK(ctx->nccl->Recv(dp.recv_val + (int64_t)p * ps, c, ncclInt32, p / L, ctx->comm, pr.st));
+          }
+        }
+      NCK(ctx->nccl->GroupEnd());
+      if (L > 1) CK(cudaStreamSynchronize(pr.st));  // other local partitions apply on their streams
+    } else {
+      for (int q = 0; q < L; ++q) {
+        PartRT& dst = ctx->parts[q];
+        CK(cudaSetDevice(dst.dev));
+        for (int p = 0; p < L; ++p) {
+          if (p == q) continue;
+          const uint32_t c = count(p, q);
+          if (!c) continue;
+          CK(cudaMemcpyPeerAsync(g->parts[q].recv + (int64_t)p * ps, dst.dev,
+                                 g->parts[p].send + (int64_t)q * ps, ctx->parts[p].dev, (size_t)c * 4, dst.st));
+          if (vals)
+            CK(cudaMemcpyPeerAsync(g->parts[q].recv_val + (int64_t)p * ps, dst.dev,
+                                   g->parts[p].send_val + (int64_t)q * ps, ctx->parts[p].dev,
+                                   (size_t)c * 4, dst.st));
+          stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
+        }
+      }
+    }
+    for (int l = 0; l < L; ++l) {
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      const int q = ctx->gpart(l);
+      for (int p = 0; p < P; ++p) {
+        if (p == q) continue;
+        const uint32_t c = count(p, q);
+        if (!c) continue;
+        CK(launch_apply_remote(op, gp.lab, gp.stamp, pp.ctl, gp.recv + (int64_t)p * ps,
+                               vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
+      }
+      CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
+      // 4. swap in/out; the new out counter is cleared in stream order
+      std::swap(pp.b_in, pp.b_out);
+      std::swap(pp.c_in, pp.c_out);
+      CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_out], 0, 4, pr.st));
+    }
+    stt->rounds++;
+    nf.dsel ^= 1;
+    ++level;  // between_rounds { LEVEL++ }
+  }
+  // host mirror of the in-counts (pipe_size, the next Iterate): read back once per Iterate
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    PipePart& pp = pipe->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaMemcpyAsync(pr.h_pin, &pp.ctl->cnt[pp.c_in], 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    pp.n_in = pr.h_pin[0];
   }
   return IRGL_OK;
 }
@@ -1034,6 +1211,10 @@ static irgl_status_t upload_values(irgl_ctx* ctx, const irgl_op_args* a, int32_t
 
 static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
   const int P = ctx->ptotal();
+  // remote pushes are staged as (owner << 28 | vertex): at most 16 partitions, ids below 2^28
+  if (P > 16 || (P > 1 && g->n >= (1ll << 28)))
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID",
+                "vertex-partitioned graphs need <= 16 partitions and n < 2^28");
   for (size_t l = 0; l < g->parts.size(); ++l) {
     GraphPart& gp = g->parts[l];
     CK(cudaSetDevice(ctx->parts[l].dev));
@@ -1207,6 +1388,9 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
   if (ctx->test_ctl) cudaFree(ctx->test_ctl);
   if (ctx->test_lock) cudaFree(ctx->test_lock);
   if (ctx->cnt_dev) cudaFree(ctx->cnt_dev);
+  if (ctx->hdr_all) cudaFree(ctx->hdr_all);
+  for (auto& pr : ctx->parts)
+    if (pr.hdr) cudaFree(pr.hdr);
   for (cudaEvent_t e : {ctx->ev0, ctx->ev1, ctx->kev0, ctx->kev1})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->user_ev)
@@ -1639,7 +1823,10 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
                   "direction-optimising BFS runs outlined on one partition");
     // the outlined kernel's barrier word carries the out count in 30 bits
     const bool outlined = outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30);
+    const bool dist_loop = !outlined && ctx->ptotal() > 1 && nf.delta <= 0 &&
+                           !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
+    else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s != IRGL_OK) return s;
     // edges scanned / remote updates (the outlined path read them with its control block)

@@ -23,6 +23,7 @@
 // Reference semantics (SPEC.md:317-322 ForAll lowering; :425 bulk-synchronous worklists: pops
 // read `in`, pushes append to `out`, never visible in the same launch).
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -66,6 +67,13 @@ struct KParams {
   ExpandCfg ec;
 };
 
+// Multi-partition kernels also stage remote pushes per warp: entries (owner << 28 | v), flushed
+// to the per-owner send buckets with one reservation per owner per flush (the owner counters are
+// a handful of addresses every warp of the grid would otherwise hit once per push).
+struct SmemDist : Smem {
+  uint32_t rbuf[kWarps][kWBuf];
+};
+
 __device__ __forceinline__ void smem_init(Smem& sm) {
   if ((threadIdx.x & 31) == 0) sm.fl_edges[threadIdx.x >> 5] = 0;  // per-warp edge counters
 }
@@ -76,6 +84,8 @@ struct WarpQ {
   uint32_t nf = 0;  // staged far pushes
   unsigned long long mf = 0;  // DO-BFS: degrees of pushed vertices (kOpBfsDO only)
   int32_t dmin = kInf;        // SSSP deferral: min distance this lane pushed near (per lane)
+  uint32_t nr = 0;            // multi-partition: staged remote pushes
+  uint32_t remote = 0;        // multi-partition: remote pushes emitted (stats)
 };
 
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
@@ -201,6 +211,48 @@ __device__ __forceinline__ void wflush(uint32_t* buf, uint32_t& n, uint32_t* out
   n = 0;
 }
 
+// Flush of the warp's staged remote pushes: per owner, count the warp's entries, reserve once,
+// write in staging order.  Warp-collective.
+__device__ __noinline__ void wflush_remote(SmemDist& sd, WarpQ& q, const KParams& p) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t n = q.nr;
+  __syncwarp();
+  for (int o = 0; o < p.dr.nparts; ++o) {
+    if (o == p.dr.me) continue;
+    uint32_t c = 0;
+    for (uint32_t i = lane; i < n; i += 32) c += (sd.rbuf[warp][i] >> 28) == (uint32_t)o;
+    uint32_t incl = c;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, incl, k);
+      if (lane >= k) incl += t;
+    }
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    if (tot == 0) continue;
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(p.dr.send_cnt + o, tot);
+    base = __shfl_sync(FULL, base, 31);
+    uint32_t pos = base + incl - c;
+    uint32_t* bucket = p.dr.send + (int64_t)o * p.dr.part_size;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t e = sd.rbuf[warp][i];
+      if ((e >> 28) == (uint32_t)o) {
+        if (pos < (uint32_t)p.dr.part_size) bucket[pos] = e & 0x0fffffffu;
+        else atomicOr(&p.ctl->overflow, 1u);
+        ++pos;
+      }
+    }
+  }
+  __syncwarp();
+  q.nr = 0;
+}
+// Phase end of a multi-partition kernel: remaining staged remote pushes and the remote counter.
+__device__ __forceinline__ void wflush_remote_all(SmemDist& sd, WarpQ& q, const KParams& p) {
+  if (q.nr) wflush_remote(sd, q, p);
+  if (lane_id() == 0 && q.remote) atomicAdd(&p.ctl->remote, (unsigned long long)q.remote);
+  q.remote = 0;
+}
+
 // Every lane of the warp must call this (converged).  kind: 0 none, 1 near, 2 far.
 template <int OP, bool DIST>
 __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
@@ -213,17 +265,13 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
     const bool remote = kind && owner != p.dr.me;
     const uint32_t rm = __ballot_sync(FULL, remote);
     if (rm) {
-      if (remote) {
-        const uint32_t grp = __match_any_sync(rm, owner);
-        const uint32_t leader = __ffs(grp) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(p.dr.send_cnt + owner, __popc(grp));
-        base = __shfl_sync(grp, base, leader);
-        const uint32_t pos = base + __popc(grp & lanemask_lt());
-        if (pos < (uint32_t)p.dr.part_size) p.dr.send[(int64_t)owner * p.dr.part_size + pos] = v;
-        else atomicOr(&p.ctl->overflow, 1u);
+      if constexpr (DIST) {
+        SmemDist& sd = static_cast<SmemDist&>(sm);
+        if (remote) sd.rbuf[warp][q.nr + __popc(rm & lanemask_lt())] = ((uint32_t)owner << 28) | v;
+        q.nr += __popc(rm);
+        q.remote += __popc(rm);
+        if (q.nr > kWBuf - 32) wflush_remote(sd, q, p);
       }
-      if (lane == __ffs(rm) - 1) atomicAdd(&p.ctl->remote, (unsigned long long)__popc(rm));
       if (remote) kind = 0;
       m = __ballot_sync(FULL, kind != 0);
       if (m == 0) return;
@@ -370,10 +418,11 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
 // ---- one warp tile of 32 worklist items (consecutive mapping inside the tile) --------------------
 template <int OP, bool DIST>
 __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
-                                 uint32_t base, uint32_t width, int32_t dmin, bool small_round) {
+                                 uint32_t base, uint32_t width, int32_t dmin, bool small_round,
+                                 uint32_t nin) {
   const int lane = lane_id();
   const uint32_t i = base + lane;
-  const bool valid = (uint32_t)lane < width && i < rb.nin;
+  const bool valid = (uint32_t)lane < width && i < nin;
   uint32_t v = 0;
   int64_t beg = 0, end = 0;
   int32_t sv = 0;
@@ -530,14 +579,16 @@ __device__ void item_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   uint32_t width = 32;
-  while (width > 1 && (uint64_t)(width >> 1) * nwarps >= rb.nin) width >>= 1;
-  const uint32_t ntiles = (rb.nin + width - 1) / width;
+  // host-orchestrated multi-partition rounds leave the in-count on the device (no host sync)
+  const uint32_t nin = rb.nin_dev ? ld_ctl(rb.nin_dev) : rb.nin;
+  while (width > 1 && (uint64_t)(width >> 1) * nwarps >= nin) width >>= 1;
+  const uint32_t ntiles = (nin + width - 1) / width;
   const int32_t dmin = rb.defer_k <= 0 ? kInf
                        : rb.dmin_cur ? (int32_t)min(ld_ctl(rb.dmin_cur), (uint32_t)kInf)
                                      : rb.dmin_val;
   uint32_t t = gw;
   while (t < ntiles) {
-    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin, ntiles <= nwarps);
+    expand_warp_tile<OP, DIST>(sm, q, p, rb, t * width, width, dmin, ntiles <= nwarps, nin);
     if (ntiles <= nwarps) break;
 #if defined(IRGL_TILE_STATIC) && IRGL_TILE_STATIC
     t += nwarps;
@@ -715,19 +766,21 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
 
 template <int OP, bool DIST>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) expand_kernel(KParams p, RoundBufs rb) {
-  __shared__ Smem sm;
+  __shared__ std::conditional_t<DIST, SmemDist, Smem> sm;
   smem_init(sm);
   WarpQ q;
   item_phase<OP, DIST>(sm, q, p, rb);
+  if constexpr (DIST) wflush_remote_all(sm, q, p);
   wflush_all<OP>(sm, q, p, rb);
 }
 
 template <int OP, bool DIST>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) chunk_kernel(KParams p, RoundBufs rb) {
-  __shared__ Smem sm;
+  __shared__ std::conditional_t<DIST, SmemDist, Smem> sm;
   smem_init(sm);
   WarpQ q;
   chunk_phase<OP, DIST>(sm, q, p, rb, ld_ctl(rb.chunk_cnt));
+  if constexpr (DIST) wflush_remote_all(sm, q, p);
   wflush_all<OP>(sm, q, p, rb);
 }
 
@@ -830,6 +883,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     RoundBufs rb;
     rb.in = (r & 1) ? a.buf_b : a.buf_a;
     rb.nin = nin_next;
+    rb.nin_dev = nullptr;
     (void)cin;
     rb.out = (r & 1) ? a.buf_a : a.buf_b;
     rb.out_cnt = cout;
@@ -1029,6 +1083,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
     RoundBufs rb;
     rb.in = (r & 1) ? a.buf_b : a.buf_a;
     rb.nin = nin_next;
+    rb.nin_dev = nullptr;
     rb.out = (r & 1) ? a.buf_a : a.buf_b;
     rb.out_cnt = cout;
     rb.cap = a.cap;
@@ -1126,6 +1181,27 @@ __global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBu
   wflush_all<OP>(sm, q, p, rb);
 }
 
+// Multi-partition round, one launch: ghost label of every queued remote update (all owners).
+__global__ void pack_all_kernel(const int32_t* lab, const uint32_t* send, int32_t* send_val,
+                                const uint32_t* send_cnt, int P, int me, int64_t ps) {
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const uint32_t c = ld_ctl(send_cnt + q);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x)
+      send_val[(int64_t)q * ps + i] = ld_label(lab + send[(int64_t)q * ps + i]);
+  }
+}
+// Round header of one partition: {send counts [P], in-count, overflow flag}.
+__global__ void round_header_kernel(uint32_t* hdr, const uint32_t* send_cnt, int P,
+                                    const uint32_t* in_cnt, const uint32_t* overflow) {
+  const int t = threadIdx.x;
+  if (t < P) hdr[t] = send_cnt ? ld_ctl(send_cnt + t) : 0u;
+  if (t == 0) {
+    hdr[P] = ld_ctl(in_cnt);
+    hdr[P + 1] = ld_ctl(overflow);
+  }
+}
+
 __global__ void pack_values_kernel(const int32_t* lab, const uint32_t* items, int32_t* values,
                                    uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -1134,7 +1210,10 @@ __global__ void pack_values_kernel(const int32_t* lab, const uint32_t* items, in
 
 template <int OP, bool DIST>
 cudaError_t round_impl(const KParams& kp, const RoundBufs& rb, int grid_max, cudaStream_t st) {
-  if (rb.nin > 0) {
+  if (rb.nin_dev) {
+    note_launch();
+    expand_kernel<OP, DIST><<<grid_max, kBlock, 0, st>>>(kp, rb);
+  } else if (rb.nin > 0) {
     const int wtiles = (int)((rb.nin + 31) / 32);
     const int blocks = min((wtiles + kWarps - 1) / kWarps, grid_max);
     note_launch();
@@ -1202,6 +1281,20 @@ cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, 
     default:
       return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* send_val,
+                            const uint32_t* send_cnt, int P, int me, int64_t ps, cudaStream_t st) {
+  note_launch();
+  pack_all_kernel<<<148 * 4, 256, 0, st>>>(lab, send, send_val, send_cnt, P, me, ps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
+                                const uint32_t* overflow, cudaStream_t st) {
+  note_launch();
+  round_header_kernel<<<1, 32, 0, st>>>(hdr, send_cnt, P, in_cnt, overflow);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,7 @@ struct RoundBufs {
   uint32_t* dmin_next;
   int32_t dmin_val;
   int32_t dense;  // 1: mark-instead-of-push round (outlined, one partition, no near-far)
+  const uint32_t* nin_dev;  // non-null: the in-count lives on the device (multi-partition rounds)
 };
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
@@ -66,6 +67,12 @@ cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, 
 cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
                              const RoundBufs& rb, const uint32_t* far_in, const uint32_t* nfar_ptr,
                              int32_t t_old, unsigned int* minkeep, int grid, cudaStream_t st);
+// Multi-partition round helpers: pack every owner's bucket values in one launch (counts read on
+// the device), and write the partition's round header {send counts [P], in-count, overflow}.
+cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* send_val,
+                            const uint32_t* send_cnt, int P, int me, int64_t ps, cudaStream_t st);
+cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
+                                const uint32_t* overflow, cudaStream_t st);
 // Gather current label values of the send buckets (SSSP / CC_LP pack step).
 cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
                                uint32_t n, cudaStream_t st);
