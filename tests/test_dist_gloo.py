@@ -1,10 +1,11 @@
 """World-size-2 CPU tests (gloo) of the multi-GPU path's host logic.
 
 1. The 1D vertex-partition exchange protocol the runtime implements in api.cu
-   (exchange_and_apply) and expand.cu (owner routing in wpush<DIST>), restated over
-   torch.distributed/gloo: ghost-label send filter, per-owner buckets deduped per round,
-   counts-then-payload all-to-all, owner-side min-reduce, sum-allreduce termination.  Checked
-   against the serial oracle on RMAT and grid graphs.
+   (wl_graph_rounds_dist) and expand.cu (owner routing in wpush<DIST>), restated over
+   torch.distributed/gloo: ghost-label send filter, per-owner buckets deduped per round, round
+   headers {send counts, |in|} all-gathered (payload sizes + termination in one collective),
+   payload all-to-all, owner-side min-reduce.  Checked against the serial oracle on RMAT and grid
+   graphs.
 2. bench.py's own multi-process plumbing (torchrun launch, rank-0-only reference arm).
 """
 import json
@@ -48,11 +49,6 @@ def _partitioned_traversal(rank, world, port, op, graph_spec, src, out_q):
         lab[src] = 0
     level, rnd = 1, 0
     while True:
-        tot = torch.tensor([len(wl)], dtype=torch.int64)
-        dist.all_reduce(tot)                # termination: sum-allreduce of |in|
-        if tot.item() == 0:
-            break
-        rnd += 1
         out, buckets = [], [[] for _ in range(world)]
         for u in wl:                        # expand: relax on the ghost array, route by owner
             for e in range(rp[u - 0], rp[u + 1]):
@@ -61,16 +57,26 @@ def _partitioned_traversal(rank, world, port, op, graph_spec, src, out_q):
                 better = lab[v] == INF if op == "bfs" else nd < lab[v]
                 if better:
                     lab[v] = nd
-                    if stamp[v] != rnd:     # per-round push dedupe
-                        stamp[v] = rnd
+                    if stamp[v] != rnd + 1:  # per-round push dedupe
+                        stamp[v] = rnd + 1
                         (out if v // ps == rank else buckets[v // ps]).append(v)
-        # counts then payload (ids, and for SSSP the ghost value at pack time)
+        # round header {send counts [world], |in|} all-gathered: the sizes of the payload
+        # exchange and, folded in, the termination test (wl_graph_rounds_dist: an all-empty round
+        # did no work and ends the Iterate)
+        hdr = torch.tensor([len(b) for b in buckets] + [len(wl)], dtype=torch.int64)
+        hdrs = [torch.zeros_like(hdr) for _ in range(world)]
+        dist.all_gather(hdrs, hdr)
+        if sum(int(h[world]) for h in hdrs) == 0:
+            break
+        rnd += 1
+        # payload: ids, and for SSSP the ghost value packed after the expansion
         payload = [[(v, int(lab[v])) for v in b] for b in buckets]
         recv = [None] * world
         dist.all_gather_object(recv, payload)
         for p in range(world):              # owner-side min-reduce
             if p == rank:
                 continue
+            assert len(recv[p][rank]) == int(hdrs[p][rank])
             for v, val in recv[p][rank]:
                 nd = level if op == "bfs" else val
                 if (op == "bfs" and lab[v] == INF) or (op != "bfs" and nd < lab[v]):
