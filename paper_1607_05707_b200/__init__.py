@@ -9,7 +9,7 @@ from .runtime import (  # noqa: F401
     MAP_CONSECUTIVE, PR, RED_ALL, RED_ANY, RED_NONE, SSSP, TC, TEST_COUNTDOWN, TEST_FORALL_MAP,
     TEST_NOPUSH, TEST_PUSHPOP, TEST_REDUCE, TEST_RESPAWN_ODD, TEST_RETRY_ODD, WL_IN, WL_OUT, WL_RETRY,
     BLOCK_ELASTIC, BLOCK_FIXED, BLOCK_SHRINKABLE, EXPORTS, LIB_PATH, Context, Graph, IrglError,
-    Pipe, Stats, bfs, cc, cc_lp, launch_count, load_library, mst, nccl_unique_id, pagerank, sssp, t_control,
+    Module, Pipe, Stats, bfs, cc, cc_lp, launch_count, load_library, mst, nccl_unique_id, pagerank, sssp, t_control,
     triangle_count,
 )
 

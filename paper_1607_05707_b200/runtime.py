@@ -116,7 +116,18 @@ EXPORTS = [
     "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
 ]
 
+# every symbol include/irgl/frontend.h declares
+FRONTEND_EXPORTS = [
+    "irgl_module_parse", "irgl_module_destroy", "irgl_module_kernel_count", "irgl_module_kernel_info",
+    "irgl_module_print", "irgl_run_host", "irgl_module_scalar",
+]
+
 _lib = None
+
+
+class RunInfo(C.Structure):
+    _fields_ = [("last_op", C.c_int32), ("last_reduced", C.c_int32), ("invocations", C.c_int64),
+                ("orchestrations", C.c_int64), ("reserved", C.c_int64 * 4)]
 
 
 def load_library(path: str | None = None):
@@ -165,6 +176,16 @@ def load_library(path: str | None = None):
         "irgl_event_record": ([P, C.c_int], i32),
         "irgl_event_elapsed": ([P, C.c_int, C.c_int, C.POINTER(C.c_double)], i32),
         "irgl_launch_count": ([], i64),
+        # IrGL source front end (include/irgl/frontend.h)
+        "irgl_module_parse": ([C.c_char_p, C.c_char_p, pp, C.c_char_p, C.c_size_t], i32),
+        "irgl_module_destroy": ([P], i32),
+        "irgl_module_kernel_count": ([P], C.c_int),
+        "irgl_module_kernel_info": ([P, C.c_int, C.c_char_p, C.c_size_t, i32p, C.c_char_p, C.c_size_t,
+                                    i32p], i32),
+        "irgl_module_print": ([P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], i32),
+        "irgl_run_host": ([P, P, C.c_char_p, P, C.POINTER(C.c_char_p), C.POINTER(C.c_double), C.c_int,
+                           C.POINTER(RunInfo), C.c_char_p, C.c_size_t], i32),
+        "irgl_module_scalar": ([P, C.c_char_p, C.POINTER(C.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -568,3 +589,72 @@ def mst(ctx: Context, graph: Graph):
 def triangle_count(ctx: Context, graph: Graph):
     _, st = ctx.invoke(TC, graph)
     return ctx.read_result(TC, graph), st
+
+
+# ---- IrGL source front end ----------------------------------------------------
+class Module:
+    """An IrGL program parsed by the runtime's front end (frontend.h): parse_source
+    plus the recognition of each plain kernel as one of the runtime's operators."""
+
+    def __init__(self, text: str, filename: str = "<input>"):
+        L = load_library()
+        self._lib = L
+        h = C.c_void_p()
+        diag = C.create_string_buffer(8192)
+        st = L.irgl_module_parse(text.encode(), filename.encode(), C.byref(h), diag, len(diag))
+        if st != OK:
+            raise IrglError(st, diag.value.decode())
+        self._h = h
+
+    @classmethod
+    def from_file(cls, path):
+        with open(path) as f:
+            return cls(f.read(), os.path.basename(path))
+
+    def kernels(self):
+        """[(name, op or -1, written field, is_host)]"""
+        out = []
+        for i in range(self._lib.irgl_module_kernel_count(self._h)):
+            name, field = C.create_string_buffer(256), C.create_string_buffer(256)
+            op, host = C.c_int32(), C.c_int32()
+            _check(self._lib.irgl_module_kernel_info(self._h, i, name, 256, C.byref(op), field, 256,
+                                                     C.byref(host)))
+            out.append((name.value.decode(), op.value, field.value.decode(), bool(host.value)))
+        return out
+
+    def pretty(self) -> str:
+        need = C.c_size_t(0)
+        self._lib.irgl_module_print(self._h, None, 0, C.byref(need))
+        buf = C.create_string_buffer(need.value)
+        _check(self._lib.irgl_module_print(self._h, buf, need.value, None))
+        return buf.value.decode()
+
+    def run_host(self, ctx: "Context", graph: "Graph", entry: str | None = None, **bindings):
+        """run_host: execute the host code; returns the RunInfo as a dict."""
+        names = (C.c_char_p * max(len(bindings), 1))(*[k.encode() for k in bindings])
+        vals = (C.c_double * max(len(bindings), 1))(*[float(v) for v in bindings.values()])
+        info = RunInfo()
+        diag = C.create_string_buffer(8192)
+        st = self._lib.irgl_run_host(ctx.handle, self._h, entry.encode() if entry else None,
+                                     graph.handle if graph else None, names, vals, len(bindings),
+                                     C.byref(info), diag, len(diag))
+        if st != OK:
+            raise IrglError(st, diag.value.decode() or _err(ctx.handle))
+        return {"last_op": info.last_op, "last_reduced": info.last_reduced,
+                "invocations": info.invocations, "orchestrations": info.orchestrations}
+
+    def scalar(self, name: str) -> float:
+        v = C.c_double()
+        _check(self._lib.irgl_module_scalar(self._h, name.encode(), C.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.irgl_module_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
