@@ -117,6 +117,27 @@ __device__ __forceinline__ float ld_cg_f32(const float* p) {
   return r;
 }
 
+// Sum of contrib[col[k]] for k = k0, k0+S, k0+2S, ... < e, U gathers in flight per step; the
+// summation order is fixed (deterministic per vertex for a given launch shape).
+template <int S, int U = 8>
+__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ col, const float* contrib,
+                                             int64_t k0, int64_t e) {
+  double s = 0.0;
+  int64_t k = k0;
+  for (; k + (U - 1) * S < e; k += U * S) {
+    int32_t c[U];
+    float v[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) c[j] = ld_stream(col + k + j * S);
+#pragma unroll
+    for (int j = 0; j < U; ++j) v[j] = ld_cg_f32(contrib + c[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) s += (double)v[j];
+  }
+  for (; k < e; k += S) s += (double)ld_cg_f32(contrib + ld_stream(col + k));
+  return s;
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
@@ -155,9 +176,8 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
         deg = 0;
       }
       __syncthreads();
-      double s = 0.0;
-      for (int64_t k = sm.b + tid; k < sm.e; k += kBlock) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
-      s = warp_sum(s);
+      const double s0 = gather_sum<kBlock>(g.col, contrib, sm.b + tid, sm.e);
+      const double s = warp_sum(s0);
       if (lane == 0) sm.red[warp] = s;
       __syncthreads();
       if (tid == own) {
@@ -174,20 +194,14 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       const int leader = __ffs(wm) - 1;
       wm &= wm - 1;
       const int64_t b = __shfl_sync(FULL, beg, leader), e = __shfl_sync(FULL, end, leader);
-      double s = 0.0;
-      for (int64_t k = b + lane; k < e; k += 32) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
-      s = warp_sum(s);
+      const double s = warp_sum(gather_sum<32>(g.col, contrib, b + lane, e));
       if (lane == leader) {
         mysum = s;
         deg = 0;
       }
     }
     // thread level
-    if (deg > 0) {
-      double s = 0.0;
-      for (int64_t k = beg; k < end; ++k) s += (double)ld_cg_f32(contrib + ld_stream(g.col + k));
-      mysum = s;
-    }
+    if (deg > 0) mysum = gather_sum<1>(g.col, contrib, beg, end);
     bool changed = false;
     if (valid) {
       const int64_t v = g.lo + i;
