@@ -60,6 +60,7 @@ struct GraphPart {
   int pr_cur = 0;
   int64_t* tc_rp = nullptr;
   int32_t* tc_cl = nullptr;
+  int32_t* tc_src = nullptr;  // source vertex of every oriented edge (edge-parallel count)
   int64_t tc_m = -1;
   ChunkDesc* chunks = nullptr;
   uint32_t chunk_cap = 0;
@@ -1147,8 +1148,8 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     gp.mst_sel = sel ^ 1;
     if (red == IRGL_RED_ALL) cell = cell ? 1u : 0u;
   } else if (op == IRGL_OP_TC) {
-    if (gp.tc_m < 0) CK(tc_orient(gp.csr(), g->n, &gp.tc_rp, &gp.tc_cl, &gp.tc_m, pr.st));
-    CK(launch_tc_count(gp.tc_rp, gp.tc_cl, g->n, gp.ctl, pr.st));
+    if (gp.tc_m < 0) CK(tc_orient(gp.csr(), g->n, &gp.tc_rp, &gp.tc_cl, &gp.tc_src, &gp.tc_m, pr.st));
+    CK(launch_tc_count(gp.tc_rp, gp.tc_cl, gp.tc_src, gp.tc_m, gp.ctl, pr.st));
     unsigned long long c = 0;
     CK(cudaMemcpyAsync(&c, &gp.ctl->tc_count, 8, cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
@@ -1602,7 +1603,7 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     cudaSetDevice(ctx->parts[l].dev);
     cudaStreamSynchronize(ctx->parts[l].st);
     void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
-                  gp.tc_rp, gp.tc_cl, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
+                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
     for (void* p : ps)
@@ -1744,6 +1745,9 @@ irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op
   if (s != IRGL_OK) return s;
   irgl_iter_stats st{};
   st.last_reduced = -1;
+  const PartRT& pr0 = ctx->parts[0];
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaEventRecord(ctx->ev0, pr0.st));
   if (is_test_op(op)) {
     int32_t* dv = nullptr;
     s = upload_values(ctx, args, &dv);
@@ -1763,6 +1767,14 @@ irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op
     if (reduced) *reduced = red == IRGL_RED_ALL ? 1 : red == IRGL_RED_ANY ? 0 : -1;  // identity
   } else {
     s = topo_invoke(ctx, g, op, args, red, reduced, &st);
+  }
+  if (s == IRGL_OK) {  // device time of the invocation (CUDA events on the ctx stream)
+    CK(cudaSetDevice(pr0.dev));
+    CK(cudaEventRecord(ctx->ev1, pr0.st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    st.device_ms = ms;
   }
   if (stats) *stats = st;
   return s;

@@ -120,10 +120,10 @@ cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float*
                                  double d, double tol, int64_t n_global, Ctl* ctl,
                                  int64_t max_rounds, int cond_mode, int grid, cudaStream_t st);
 int pr_persistent_blocks_per_sm();
-cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out, int64_t* m_out,
-                      cudaStream_t st);
-cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl* ctl,
-                            cudaStream_t st);
+cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out,
+                      int32_t** src_out, int64_t* m_out, cudaStream_t st);
+cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, const int32_t* src, int64_t mo,
+                            Ctl* ctl, cudaStream_t st);
 
 // ---- Atomic / Exclusive constructs and Boruvka MST (mst.cu) -----------------------------------
 cudaError_t launch_mst_init(int32_t* parent, int32_t* comp, int32_t* lock, int32_t* bw, int32_t* ba,

@@ -36,9 +36,25 @@ __device__ __forceinline__ int32_t cc_find(const int32_t* par, int32_t x) {
   return x;
 }
 
+// Root of x with intermediate pointer jumping (each visited node is re-pointed to its grandparent;
+// benign races: hooks only ever lower a parent, par[x] <= x holds throughout), so the trees a hook
+// round builds stay shallow and later finds are short (ECL-CC's find).
+__device__ __forceinline__ int32_t cc_find_jump(int32_t* par, int32_t x) {
+  int32_t cur = ld_label(par + x);
+  if (cur != x) {
+    int32_t prev = x, next;
+    while (cur > (next = ld_label(par + cur))) {
+      par[prev] = next;
+      prev = cur;
+      cur = next;
+    }
+  }
+  return cur;
+}
+
 // Hook edge (u, v): ECL-CC style CAS retry so each edge needs one visit.
 __device__ __forceinline__ bool cc_hook_edge(int32_t* par, int32_t u, int32_t v) {
-  int32_t a = cc_find(par, u), b = cc_find(par, v);
+  int32_t a = cc_find_jump(par, u), b = cc_find_jump(par, v);
   bool changed = false;
   while (a != b) {
     const int32_t hi = max(a, b), lo = min(a, b);
@@ -47,8 +63,8 @@ __device__ __forceinline__ bool cc_hook_edge(int32_t* par, int32_t u, int32_t v)
       changed = true;
       break;
     }
-    a = cc_find(par, old);
-    b = cc_find(par, lo);
+    a = cc_find_jump(par, old);
+    b = cc_find_jump(par, lo);
   }
   return changed;
 }
@@ -274,38 +290,83 @@ __device__ __forceinline__ bool tc_less(const int64_t* rp, int64_t u, int64_t v)
   return du < dv || (du == dv && u < v);
 }
 
+// Orientation, pass 1: out-degree d+(u).  Thread per vertex for degree < 32 (meshes, road
+// graphs), warp-cooperative above (hubs).
 __global__ void tc_count_out_kernel(const int64_t* rp, const int32_t* col, int64_t n,
                                     int64_t* dout) {
   const int lane = threadIdx.x & 31;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
-       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    int64_t c = 0;
-    for (int64_t k0 = rp[u]; k0 < rp[u + 1]; k0 += 32) {
-      const int64_t k = k0 + lane;
-      const bool p = k < rp[u + 1] && tc_less(rp, u, col[k]);
-      c += __popc(__ballot_sync(FULL, p));
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); u0 < n; u0 += T) {
+    const int64_t u = u0 + lane;
+    int64_t b = 0, e = 0;
+    if (u < n) {
+      b = rp[u];
+      e = rp[u + 1];
     }
-    if (lane == 0) dout[u] = c;
+    int64_t c = 0;
+    if (e - b < 32)
+      for (int64_t k = b; k < e; ++k) c += tc_less(rp, u, col[k]);
+    uint32_t wm = __ballot_sync(FULL, e - b >= 32);
+    while (wm) {
+      const int ld = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const int64_t uu = __shfl_sync(FULL, u, ld), bb = __shfl_sync(FULL, b, ld), ee = __shfl_sync(FULL, e, ld);
+      int64_t cc = 0;
+      for (int64_t k0 = bb; k0 < ee; k0 += 32) {
+        const int64_t k = k0 + lane;
+        cc += __popc(__ballot_sync(FULL, k < ee && tc_less(rp, uu, col[k])));
+      }
+      if (lane == ld) c = cc;
+    }
+    if (u < n) dout[u] = c;
   }
 }
 
+// Pass 2: N+(u) in col order (sorted), plus the source of every oriented edge (edge-parallel
+// counting).  Same thread / warp split.
 __global__ void tc_fill_kernel(const int64_t* rp, const int32_t* col, int64_t n, const int64_t* orp,
-                               int32_t* ocl) {
+                               int32_t* ocl, int32_t* osrc) {
   const int lane = threadIdx.x & 31;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
-       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    int64_t o = orp[u];
-    for (int64_t k0 = rp[u]; k0 < rp[u + 1]; k0 += 32) {
-      const int64_t k = k0 + lane;
-      int32_t v = 0;
-      bool p = false;
-      if (k < rp[u + 1]) {
-        v = col[k];
-        p = tc_less(rp, u, v);
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); u0 < n; u0 += T) {
+    const int64_t u = u0 + lane;
+    int64_t b = 0, e = 0;
+    if (u < n) {
+      b = rp[u];
+      e = rp[u + 1];
+    }
+    if (e - b < 32) {
+      int64_t o = u < n ? orp[u] : 0;
+      for (int64_t k = b; k < e; ++k) {
+        const int32_t v = col[k];
+        if (tc_less(rp, u, v)) {
+          ocl[o] = v;
+          osrc[o] = (int32_t)u;
+          ++o;
+        }
       }
-      const uint32_t m = __ballot_sync(FULL, p);
-      if (p) ocl[o + __popc(m & lanemask_lt())] = v;
-      o += __popc(m);
+    }
+    uint32_t wm = __ballot_sync(FULL, e - b >= 32);
+    while (wm) {
+      const int ld = __ffs(wm) - 1;
+      wm &= wm - 1;
+      const int64_t uu = __shfl_sync(FULL, u, ld), bb = __shfl_sync(FULL, b, ld), ee = __shfl_sync(FULL, e, ld);
+      int64_t o = orp[uu];
+      for (int64_t k0 = bb; k0 < ee; k0 += 32) {
+        const int64_t k = k0 + lane;
+        int32_t v = 0;
+        bool p = false;
+        if (k < ee) {
+          v = col[k];
+          p = tc_less(rp, uu, v);
+        }
+        const uint32_t m = __ballot_sync(FULL, p);
+        if (p) {
+          ocl[o + __popc(m & lanemask_lt())] = v;
+          osrc[o + __popc(m & lanemask_lt())] = (int32_t)uu;
+        }
+        o += __popc(m);
+      }
     }
   }
 }
@@ -322,23 +383,72 @@ __device__ __forceinline__ bool bsearch_i32(const int32_t* a, int64_t n, int32_t
   return false;
 }
 
-// warp per vertex u; for each v in N+(u): lanes stride the shorter of N+(u), N+(v) and binary
-// search the longer.  Warp-reduced 64-bit count, one atomic per warp.
-__global__ void tc_count_kernel(const int64_t* orp, const int32_t* ocl, int64_t n,
+// |N+(u) ∩ N+(v)| for one oriented edge, by one thread: sorted merge when the lists are of similar
+// length, binary search of the shorter in the longer when they are not.
+__device__ __forceinline__ unsigned long long tc_intersect(const int32_t* __restrict__ ocl,
+                                                           int64_t ub, int64_t ue, int64_t vb, int64_t ve) {
+  int64_t du = ue - ub, dv = ve - vb;
+  if (du > dv) {
+    int64_t t = ub; ub = vb; vb = t;
+    t = ue; ue = ve; ve = t;
+    t = du; du = dv; dv = t;
+  }
+  unsigned long long c = 0;
+  if (du == 0) return 0;
+  if (du * 8 < dv) {
+    for (int64_t j = ub; j < ue; ++j) c += bsearch_i32(ocl + vb, dv, ocl[j]);
+    return c;
+  }
+  int64_t i = ub, j = vb;
+  int32_t a = ocl[i], b = ocl[j];
+  for (;;) {
+    if (a == b) {
+      ++c;
+      if (++i == ue || ++j == ve) break;
+      a = ocl[i];
+      b = ocl[j];
+    } else if (a < b) {
+      if (++i == ue) break;
+      a = ocl[i];
+    } else {
+      if (++j == ve) break;
+      b = ocl[j];
+    }
+  }
+  return c;
+}
+
+// Edge-parallel count over the oriented edges: thread per edge (u, v) for short lists; an edge
+// whose shorter list has >= 64 entries is intersected by its warp (lanes stride the shorter list
+// and binary-search the longer).  Warp-reduced 64-bit count, one atomic per warp.
+__global__ void tc_count_kernel(const int64_t* orp, const int32_t* ocl, const int32_t* osrc, int64_t mo,
                                 unsigned long long* total) {
   const int lane = threadIdx.x & 31;
   unsigned long long cnt = 0;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n;
-       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t ub = orp[u], ue = orp[u + 1];
-    for (int64_t k = ub; k < ue; ++k) {
-      const int32_t v = ocl[k];
-      const int64_t vb = orp[v], ve = orp[v + 1];
-      const int64_t du = ue - ub, dv = ve - vb;
-      const int32_t* S = du <= dv ? ocl + ub : ocl + vb;
-      const int32_t* L = du <= dv ? ocl + vb : ocl + ub;
-      const int64_t ns = du <= dv ? du : dv, nl = du <= dv ? dv : du;
-      for (int64_t j = lane; j < ns; j += 32) cnt += bsearch_i32(L, nl, S[j]) ? 1 : 0;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); k0 < mo; k0 += T) {
+    const int64_t k = k0 + lane;
+    int64_t ub = 0, ue = 0, vb = 0, ve = 0;
+    if (k < mo) {
+      const int32_t u = osrc[k], v = ocl[k];
+      ub = orp[u];
+      ue = orp[u + 1];
+      vb = orp[v];
+      ve = orp[v + 1];
+    }
+    const bool wide = min(ue - ub, ve - vb) >= 64;
+    if (k < mo && !wide) cnt += tc_intersect(ocl, ub, ue, vb, ve);
+    uint32_t wm = __ballot_sync(FULL, k < mo && wide);
+    while (wm) {
+      const int ld = __ffs(wm) - 1;
+      wm &= wm - 1;
+      int64_t sb = __shfl_sync(FULL, ub, ld), se = __shfl_sync(FULL, ue, ld);
+      int64_t lb = __shfl_sync(FULL, vb, ld), le = __shfl_sync(FULL, ve, ld);
+      if (se - sb > le - lb) {
+        int64_t t = sb; sb = lb; lb = t;
+        t = se; se = le; le = t;
+      }
+      for (int64_t j = sb + lane; j < se; j += 32) cnt += bsearch_i32(ocl + lb, le - lb, ocl[j]);
     }
   }
 #pragma unroll
@@ -392,14 +502,15 @@ cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float*
 }
 
 cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out,
-                      int64_t* m_out, cudaStream_t st) {
+                      int32_t** src_out, int64_t* m_out, cudaStream_t st) {
   int64_t* dout = nullptr;
   int64_t* orp = nullptr;
   int32_t* ocl = nullptr;
+  int32_t* osrc = nullptr;
   cudaError_t e;
   if ((e = cudaMallocAsync(&dout, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&orp, (n + 1) * sizeof(int64_t), st)) != cudaSuccess) return e;
-  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   note_launch();
   tc_count_out_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, dout);
   cudaMemsetAsync(dout + n, 0, sizeof(int64_t), st);
@@ -412,22 +523,24 @@ cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl
   cudaMemcpyAsync(&mo, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
   if ((e = cudaMallocAsync(&ocl, (mo > 0 ? mo : 1) * sizeof(int32_t), st)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&osrc, (mo > 0 ? mo : 1) * sizeof(int32_t), st)) != cudaSuccess) return e;
   note_launch();
-  tc_fill_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, orp, ocl);
+  tc_fill_kernel<<<grid, 256, 0, st>>>(g.row_ptr, g.col, n, orp, ocl, osrc);
   cudaFreeAsync(t, st);
   cudaFreeAsync(dout, st);
   *rp_out = orp;
   *cl_out = ocl;
+  *src_out = osrc;
   *m_out = mo;
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, int64_t n, Ctl* ctl,
-                            cudaStream_t st) {
+cudaError_t launch_tc_count(const int64_t* rp, const int32_t* cl, const int32_t* src, int64_t mo,
+                            Ctl* ctl, cudaStream_t st) {
   cudaMemsetAsync(&ctl->tc_count, 0, sizeof(unsigned long long), st);
-  const int grid = (int)std::min<int64_t>((n * 32 + 255) / 256, 148 * 32);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((mo + 255) / 256, 148 * 16));
   note_launch();
-  tc_count_kernel<<<grid, 256, 0, st>>>(rp, cl, n, &ctl->tc_count);
+  tc_count_kernel<<<grid, 256, 0, st>>>(rp, cl, src, mo, &ctl->tc_count);
   return cudaGetLastError();
 }
 

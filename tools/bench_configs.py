@@ -78,7 +78,8 @@ def grids(ctx):
     t0 = time.time()
     c, st = irgl.triangle_count(ctx, g)
     emit({"config": "TC triangulated grid 4096^2", "n": g.n, "m": g.m, "triangles": c,
-          "known_answer_ok": c == 2 * (W - 1) * (H - 1), "ms_incl_orientation": round((time.time() - t0) * 1e3, 3)})
+          "known_answer_ok": c == 2 * (W - 1) * (H - 1),
+          "ms_incl_orientation": round(st.device_ms, 3), "wall_ms_first_call": round((time.time() - t0) * 1e3, 3)})
     c2, st2 = irgl.triangle_count(ctx, g)
     emit({"config": "TC triangulated grid 4096^2 (oriented CSR cached)", "ms": round(st2.device_ms, 3) if st2.device_ms else None})
     g.close()
