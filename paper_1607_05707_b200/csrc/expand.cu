@@ -532,7 +532,10 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   const int64_t off = beg - (int64_t)(incl - d);  // edge of slot k (owned here) = off + k
   // 4 windows of 32 edge slots per iteration: each lane has 4 independent col/label chains in
   // flight (memory-level parallelism); owner of slot k = #lanes with inclusive prefix <= k
-  constexpr int kWin = 4;
+#ifndef IRGL_KWIN
+#define IRGL_KWIN 4
+#endif
+  constexpr int kWin = IRGL_KWIN;
   for (uint32_t wb = 0; wb < total; wb += 32 * kWin) {
     uint32_t dst[kWin];
     int32_t wt[kWin], s[kWin], cur[kWin];
