@@ -61,6 +61,12 @@ struct GraphPart {
   int64_t* tc_rp = nullptr;
   int32_t* tc_cl = nullptr;
   int32_t* tc_src = nullptr;  // source vertex of every oriented edge (edge-parallel count)
+  uint32_t* vis = nullptr;    // BFS visited bitmap, n bits (valid while lab_op == BFS)
+  // The kernels see the bitmap only when the level array would not stay L2-resident: below that
+  // the level CAS is cheaper than bitmap atomics shared by 32 vertices (RMAT-22: 87 vs 78 GTEPS;
+  // RMAT-25: 66 vs 96; RMAT-27: 34 vs 95, profiles/r1s2_bfs_bitmap.txt)
+  uint32_t* vis_k() const { return vis_on ? vis : nullptr; }
+  bool vis_on = false;
   int64_t tc_m = -1;
   ChunkDesc* chunks = nullptr;
   uint32_t chunk_cap = 0;
@@ -229,6 +235,12 @@ static irgl_status_t ensure_lab(irgl_ctx* ctx, irgl_graph* g, bool need_stamp) {
     GraphPart& gp = g->parts[l];
     CK(cudaSetDevice(ctx->parts[l].dev));
     if (!gp.lab) CK(cudaMalloc(&gp.lab, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
+    {
+      const int32_t c = ctx->cfg.bfs_bitmap_min_n;
+      const int64_t min_n = c == 0 ? (12ll << 20) : c;
+      gp.vis_on = c >= 0 && g->n >= min_n;
+    }
+    if (gp.vis_on && !gp.vis) CK(cudaMalloc(&gp.vis, ((std::max<int64_t>(g->n, 1) + 31) / 32) * sizeof(uint32_t)));
     if (need_stamp && !gp.stamp) {
       CK(cudaMalloc(&gp.stamp, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
       CK(cudaMemset(gp.stamp, 0, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
@@ -254,6 +266,7 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
       CK(cudaSetDevice(pr.dev));
       if (op == IRGL_OP_BFS || op == IRGL_OP_SSSP) {
         CK(launch_fill_i32(gp.lab, kInf, g->n, pr.st));
+        if (op == IRGL_OP_BFS && gp.vis_k()) CK(cudaMemsetAsync(gp.vis, 0, ((g->n + 31) / 32) * sizeof(uint32_t), pr.st));
       } else {
         // label[v] = v (iota over int32 as uint32)
         CK(launch_iota_u32(reinterpret_cast<uint32_t*>(gp.lab), 0u, (uint32_t)g->n, pr.st));
@@ -264,7 +277,7 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
       if ((op == IRGL_OP_BFS || op == IRGL_OP_SSSP) && pipe) {
         // level/dist[src] = 0 for the initial items (App. B2); items were routed to owners
         PipePart& pp = pipe->parts[l];
-        CK(launch_scatter_zero(gp.lab, pp.buf[pp.b_in], pp.n_in, pr.st));
+        CK(launch_scatter_zero(gp.lab, pp.buf[pp.b_in], pp.n_in, pr.st, op == IRGL_OP_BFS ? gp.vis_k() : nullptr));
       }
     }
     // NCCL mode: every rank's ghost copy must also see the sources as 0 (they are owned elsewhere
@@ -421,7 +434,7 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       if (p == q) continue;
       const uint32_t c = cnt[(size_t)p * P + q];
       if (!c) continue;
-      CK(launch_apply_remote(op, gp.lab, gp.stamp, pp.ctl, gp.recv + (int64_t)p * ps,
+      CK(launch_apply_remote(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv + (int64_t)p * ps,
                              vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
     }
     CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
@@ -625,7 +638,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       DistRoute dr{P, ctx->gpart(l), g->part_size, gp.send, gp.send_cnt};
       if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
-      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
+      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
       if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
     }
@@ -714,7 +727,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       rbs[l].nin_dev = &pp.ctl->cnt[pp.c_in];
       DistRoute dr{P, ctx->gpart(l), ps, gp.send, gp.send_cnt};
       if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
-      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
+      CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
       if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
       if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
@@ -821,7 +834,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         if (p == q) continue;
         const uint32_t c = count(p, q);
         if (!c) continue;
-        CK(launch_apply_remote(op, gp.lab, gp.stamp, pp.ctl, gp.recv + (int64_t)p * ps,
+        CK(launch_apply_remote(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv + (int64_t)p * ps,
                                vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
       }
       CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
@@ -900,7 +913,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   // minima = unknown so round 0 defers nothing, barrier state, statistics)
   CK(launch_ctl_prepare(pp.ctl, pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
-  CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
+  CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   static_assert(sizeof(Ctl) <= 4096, "control block readback goes through the 4 KB pinned scratch");
   CK(cudaMemcpyAsync(pr.h_pin, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
@@ -1603,7 +1616,7 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     cudaSetDevice(ctx->parts[l].dev);
     cudaStreamSynchronize(ctx->parts[l].st);
     void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
-                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
+                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
     for (void* p : ps)

@@ -62,6 +62,8 @@ struct KParams {
   DevCSR g;
   int32_t* lab;
   int32_t* stamp;
+  uint32_t* vis;  // BFS: visited bitmap over all n vertices (L2-resident where the level array is
+                  // not: 16.8 MB at RMAT-27 vs 537 MB); null for the other operators
   Ctl* ctl;
   DistRoute dr;
   ExpandCfg ec;
@@ -99,6 +101,19 @@ __device__ __forceinline__ uint32_t ld_ctl(const uint32_t* p) {
   return r;
 }
 
+// Per-edge gather of the destination's state.  BFS reads one bit of the visited bitmap and returns
+// it in the level encoding the relax code tests (INF = unvisited; a stale 0 bit is benign: the
+// atomicOr that follows decides).  Other operators read the label.
+template <int OP>
+__device__ __forceinline__ int32_t gather_cur(const KParams& p, uint32_t dst) {
+  if (is_bfs(OP) && p.vis) {
+    uint32_t w;
+    asm volatile("ld.global.u32 %0, [%1];" : "=r"(w) : "l"(p.vis + (dst >> 5)));
+    return ((w >> (dst & 31)) & 1u) ? 0 : kInf;
+  }
+  return ld_label(p.lab + dst);
+}
+
 // ---- relax: the operator body for one edge (n -> dst) ----------------------------------------
 // BFS   : if level[dst]==INF { level[dst]=LEVEL; push(dst) }   CAS dedupes the push.
 // SSSP  : nd = dist[n]+w;  if atomicMin(dist[dst],nd) > nd and stamp[dst] != round: push(dst)
@@ -109,6 +124,12 @@ __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb,
                                           int32_t cur, int32_t sv, int32_t wt, uint32_t dst) {
   if (is_bfs(OP)) {
     if (cur != kInf) return 0;
+    if (p.vis) {  // claim the vertex in the bitmap; the winner writes its level
+      const uint32_t bit = 1u << (dst & 31);
+      if (atomicOr(p.vis + (dst >> 5), bit) & bit) return 0;
+      p.lab[dst] = rb.level;
+      return 1;
+    }
     return atomicCAS(p.lab + dst, kInf, rb.level) == kInf ? 1 : 0;
   } else {
     const int32_t nd = (is_sssp(OP)) ? sv + wt : sv;
@@ -149,7 +170,10 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
     if (is_bfs(OP)) {
 #pragma unroll
       for (int j = 0; j < K; ++j)
-        if (act[j] && cur[j] == kInf) p.lab[dst[j]] = rb.level;  // every writer stores LEVEL
+        if (act[j] && cur[j] == kInf) {
+          p.lab[dst[j]] = rb.level;  // every writer stores LEVEL
+          if (p.vis) atomicOr(p.vis + (dst[j] >> 5), 1u << (dst[j] & 31));  // RED.OR
+        }
     } else {
       const int32_t code = rb.stamp_id << 1;
 #pragma unroll
@@ -167,6 +191,18 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
     return;
   }
   if (is_bfs(OP)) {
+    if (p.vis) {
+      uint32_t old[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        old[j] = (act[j] && cur[j] == kInf) ? atomicOr(p.vis + (dst[j] >> 5), 1u << (dst[j] & 31)) : ~0u;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        kind[j] = (old[j] & (1u << (dst[j] & 31))) ? 0 : 1;
+        if (kind[j]) p.lab[dst[j]] = rb.level;
+      }
+      return;
+    }
     int32_t old[K];
 #pragma unroll
     for (int j = 0; j < K; ++j)
@@ -403,7 +439,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       }
     }
 #pragma unroll
-    for (int j = 0; j < NE; ++j) cur[j] = act[j] ? ld_label(p.lab + d[j]) : 0;
+    for (int j = 0; j < NE; ++j) cur[j] = act[j] ? gather_cur<OP>(p, d[j]) : 0;
     int kk[NE];
     relax_batch<OP, NE>(p, rb, q, act, cur, sv8, wt, d, kk);
 #pragma unroll
@@ -562,7 +598,7 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
       }
     }
 #pragma unroll
-    for (int j = 0; j < kWin; ++j) cur[j] = act[j] ? ld_label(p.lab + dst[j]) : 0;
+    for (int j = 0; j < kWin; ++j) cur[j] = act[j] ? gather_cur<OP>(p, dst[j]) : 0;
     int kk[kWin];
     relax_batch<OP, kWin>(p, rb, q, act, cur, s, wt, dst, kk);
 #pragma unroll
@@ -702,7 +738,7 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
       }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) cur[t] = act[t] ? ld_label(p.lab + d[t]) : 0;
+    for (int t = 0; t < 4; ++t) cur[t] = act[t] ? gather_cur<OP>(p, d[t]) : 0;
     int kk[4];
     relax_batch<OP, 4>(p, rb, q, act, cur, s4, wt, d, kk);
 #pragma unroll
@@ -1030,6 +1066,7 @@ __device__ void bu_phase(const KParams& p, int64_t n, int32_t L, unsigned long l
       const int32_t u = ld_stream(p.g.col + k);
       if (ld_label(p.lab + u) == L - 1) {
         p.lab[v] = L;
+        if (p.vis) atomicOr(p.vis + (v >> 5), 1u << (v & 31));  // keep the bitmap exact
         ++f;
         fd += (unsigned long long)(e - b);
         sc += (unsigned long long)(k - b + 1);
@@ -1176,7 +1213,7 @@ __global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBu
     uint32_t v = 0;
     if (i < n) {
       v = items[i];
-      const int32_t cur = ld_label(p.lab + v);
+      const int32_t cur = gather_cur<OP>(p, v);
       kind = relax_with<OP>(p, rb, q, cur, is_bfs(OP) ? 0 : values[i], 0, v);
     }
     wpush<OP, false>(sm, q, p, rb, kind, v);
@@ -1229,10 +1266,10 @@ cudaError_t round_impl(const KParams& kp, const RoundBufs& rb, int grid_max, cud
 
 }  // namespace
 
-cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                 const RoundBufs& rb, const DistRoute& dr, const ExpandCfg& ec,
                                 int grid_max, cudaStream_t st) {
-  KParams kp{g, lab, stamp, ctl, dr, ec};
+  KParams kp{g, lab, stamp, vis, ctl, dr, ec};
   const bool dist = dr.nparts > 1;
   switch (op) {
     case IRGL_OP_BFS:
@@ -1254,18 +1291,18 @@ cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* 
 cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
                              const RoundBufs& rb, const uint32_t* far_in, const uint32_t* nfar_ptr,
                              int32_t t_old, unsigned int* minkeep, int grid, cudaStream_t st) {
-  KParams kp{g, lab, stamp, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
+  KParams kp{g, lab, stamp, nullptr, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
   note_launch();
   far_split_kernel<<<grid, kBlock, 0, st>>>(kp, rb, far_in, nfar_ptr, t_old, minkeep);
   return cudaGetLastError();
 }
 
-cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, const uint32_t* items,
+cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl, const uint32_t* items,
                                 const int32_t* values, uint32_t n, const RoundBufs& rb,
                                 cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   const int grid = (int)min((n + kBlock - 1) / kBlock, 148u * 8u);
-  KParams kp{DevCSR{nullptr, nullptr, nullptr, 0, 0}, lab, stamp, ctl,
+  KParams kp{DevCSR{nullptr, nullptr, nullptr, 0, 0}, lab, stamp, vis, ctl,
              DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
   note_launch();
   switch (op) {
@@ -1372,10 +1409,10 @@ int expand_blocks_per_sm(int op) {
   return nb;
 }
 
-cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                               const PersistArgs& pa, const ExpandCfg& ec, int grid,
                               cudaStream_t st) {
-  KParams kp{g, lab, stamp, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ec};
+  KParams kp{g, lab, stamp, vis, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ec};
   PersistArgs a = pa;
   void* args[] = {&kp, &a};
   note_launch();

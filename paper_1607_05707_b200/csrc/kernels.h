@@ -56,11 +56,11 @@ struct RoundBufs {
 
 // ---- data-driven operators: BFS / SSSP / CC_LP (expand.cu) ----------------------------------
 // One host-orchestrated round: expansion of `in` plus the CTA-chunk (hub) phase.
-cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                 const RoundBufs& rb, const DistRoute& dr, const ExpandCfg& ec,
                                 int grid_max, cudaStream_t st);
 // Apply received remote updates (owner side min-reduce): items[i] with values[i] (BFS: level).
-cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, Ctl* ctl, const uint32_t* items,
+cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl, const uint32_t* items,
                                 const int32_t* values, uint32_t n, const RoundBufs& rb,
                                 cudaStream_t st);
 // Near-far split of a far pile into rb.out (dist < rb.threshold) / rb.far (the next pile).
@@ -100,7 +100,7 @@ struct PersistArgs {
   uint32_t trace_cap;
 };
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
-cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
+cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                               const PersistArgs& pa, const ExpandCfg& ec, int grid,
                               cudaStream_t st);
 // Co-resident CTAs/SM of the persistent kernel for `op` (occupancy API).
@@ -145,7 +145,8 @@ cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st);
 
 // ---- misc (util.cu) ---------------------------------------------------------------------------
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);
-cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st);
+cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st,
+                                uint32_t* vis = nullptr);
 cudaError_t launch_iota_u32(uint32_t* p, uint32_t begin, uint32_t n, cudaStream_t st);
 cudaError_t launch_set_red(Ctl* ctl, int slot, uint32_t v, cudaStream_t st);
 

@@ -88,9 +88,12 @@ __global__ void fill_i32_kernel(int32_t* p, int32_t v, int64_t n) {
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
 }
-__global__ void scatter_zero_kernel(int32_t* lab, const uint32_t* items, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    lab[items[i]] = 0;
+__global__ void scatter_zero_kernel(int32_t* lab, const uint32_t* items, uint32_t n, uint32_t* vis) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = items[i];
+    lab[v] = 0;
+    if (vis) atomicOr(vis + (v >> 5), 1u << (v & 31));  // BFS visited bitmap
+  }
 }
 __global__ void iota_kernel(uint32_t* p, uint32_t begin, uint32_t n) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -114,10 +117,11 @@ cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st) {
   fill_i32_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(p, v, n);
   return cudaGetLastError();
 }
-cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st) {
+cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st,
+                                uint32_t* vis) {
   if (n == 0) return cudaSuccess;
   note_launch();
-  scatter_zero_kernel<<<(int)std::min<uint32_t>((n + 255) / 256, 1024), 256, 0, st>>>(lab, items, n);
+  scatter_zero_kernel<<<(int)std::min<uint32_t>((n + 255) / 256, 1024), 256, 0, st>>>(lab, items, n, vis);
   return cudaGetLastError();
 }
 cudaError_t launch_iota_u32(uint32_t* p, uint32_t begin, uint32_t n, cudaStream_t st) {

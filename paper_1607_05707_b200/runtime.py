@@ -61,7 +61,7 @@ class Config(C.Structure):
                 ("retry_serialize_after", C.c_int32), ("warp_threshold", C.c_int32),
                 ("cta_threshold", C.c_int32), ("chunk_edges", C.c_int32),
                 ("l2_persist", C.c_int32), ("logical_partitions", C.c_int32),
-                ("dense_div", C.c_int32), ("reserved", C.c_int32 * 7)]
+                ("dense_div", C.c_int32), ("bfs_bitmap_min_n", C.c_int32), ("reserved", C.c_int32 * 6)]
 
 
 class OpArgs(C.Structure):
@@ -274,7 +274,7 @@ class Context:
 
     def __init__(self, devices=(0,), *, outline=-1, blocks_per_sm=0, retry_serialize_after=0,
                  warp_threshold=0, cta_threshold=0, chunk_edges=0, logical_partitions=0,
-                 dense_div=0, nccl=None):
+                 dense_div=0, bfs_bitmap_min_n=0, nccl=None):
         L = load_library()
         cfg = Config()
         cfg.outline = outline
@@ -285,6 +285,7 @@ class Context:
         cfg.chunk_edges = chunk_edges
         cfg.logical_partitions = logical_partitions
         cfg.dense_div = dense_div
+        cfg.bfs_bitmap_min_n = bfs_bitmap_min_n
         h = C.c_void_p()
         if nccl is not None:  # (device, rank, nranks, uid)
             dev, rank, nranks, uid = nccl

@@ -206,6 +206,31 @@ def test_dense_rounds_parity(irgl, oracle, dense_div):
         np.testing.assert_array_equal(d, oracle.sssp(og, 0))
 
 
+@pytest.mark.parametrize("P", [1, 3])
+@pytest.mark.parametrize("dense_div", [-1, 16])
+def test_bfs_visited_bitmap_parity(irgl, oracle, P, dense_div):
+    """The visited-bitmap BFS (large graphs) gives the same levels and invocation counts: top-down
+    sparse and dense rounds, direction-optimising, multi-partition."""
+    og = oracle.rmat(14)
+    with irgl.Context(bfs_bitmap_min_n=1, dense_div=dense_div, logical_partitions=P) as c:
+        g = _upload(c, og)
+        for s in og.sources(3):
+            s = int(s)
+            ref, ecc = oracle.bfs(og, s)
+            for outline in (0, 1):
+                lv, st = irgl.bfs(c, g, s, outline=outline)
+                np.testing.assert_array_equal(lv, ref)
+                assert st.rounds == ecc + 1
+            if P == 1:
+                lv, _ = irgl.bfs(c, g, s, direction=1)
+                np.testing.assert_array_equal(lv, ref)
+    og = oracle.grid(50, 37, diag=True)
+    with irgl.Context(bfs_bitmap_min_n=1, dense_div=dense_div) as c:
+        g = _upload(c, og)
+        lv, _ = irgl.bfs(c, g, 0)
+        np.testing.assert_array_equal(lv, oracle.bfs(og, 0)[0])
+
+
 def test_sssp_device_generated_graph(ctx, irgl, oracle):
     og = oracle.rmat(15)
     g = ctx.generate_rmat(15)
