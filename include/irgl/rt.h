@@ -249,6 +249,15 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
 irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out,
                                size_t bytes);
 
+/* Asynchronous variant for pipelined queries: the copy of the node result (BFS/SSSP/CC/CC_LP
+ * int32[n]) into host_out (pinned memory to overlap) is queued on a copy stream behind the work
+ * already issued and the call returns at once; the next traversal on the graph writes a second
+ * label buffer, so it overlaps the copy.  host_out is valid after irgl_results_wait.  Other
+ * operators fall back to irgl_read_result. */
+irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out,
+                                     size_t bytes);
+irgl_status_t irgl_results_wait(irgl_ctx* ctx);
+
 /* ---- measurement --------------------------------------------------------------------------- */
 /* CUDA events on the stream of the ctx's first partition (the stream every kernel of this ctx is
  * ordered on), slots 0..7; elapsed time between two recorded slots in ms. */

@@ -20,6 +20,11 @@ struct PartRT {  // one vertex partition hosted by this process
   int sms = 0;
   uint32_t* h_pin = nullptr;  // pinned scratch (counts readback)
   uint32_t* hdr = nullptr;    // multi-partition round header {send counts [P], in-count, overflow}
+  cudaStream_t copy_st = nullptr;  // asynchronous result readback (irgl_read_result_async)
+  uint32_t* h_stage = nullptr;     // pinned staging for small worklist initialisers
+  Ctl* h_ctl = nullptr;            // host-mapped control-block mirror: written by a kernel (no copy
+                                   // engine, so it never queues behind an async result readback)
+  cudaEvent_t stage_ev = nullptr;  // last copy out of h_stage (reuse waits on it)
 };
 }  // namespace irgl
 
@@ -62,6 +67,13 @@ struct GraphPart {
   int32_t* tc_cl = nullptr;
   int32_t* tc_src = nullptr;  // source vertex of every oriented edge (edge-parallel count)
   uint32_t* vis = nullptr;    // BFS visited bitmap, n bits (valid while lab_op == BFS)
+  // Label double buffer, created by the first irgl_read_result_async: every operator reset then
+  // alternates buffers, so a traversal never overwrites the labels an asynchronous readback is
+  // still copying (it waits on that buffer's copy event only when it comes round again).
+  int32_t* lab_buf[2] = {nullptr, nullptr};
+  int lab_sel = 0;
+  cudaEvent_t lab_copied[2] = {nullptr, nullptr};
+  bool copy_pending[2] = {false, false};
   // The kernels see the bitmap only when the level array would not stay L2-resident: below that
   // the level CAS is cheaper than bitmap atomics shared by 32 vertices (RMAT-22: 87 vs 78 GTEPS;
   // RMAT-25: 66 vs 96; RMAT-27: 34 vs 95, profiles/r1s2_bfs_bitmap.txt)
@@ -183,11 +195,24 @@ static irgl_status_t pipe_set_in(irgl_ctx* ctx, irgl_pipe* p, int l, const std::
   PipePart& pp = p->parts[l];
   PartRT& pr = ctx->parts[l];
   CK(cudaSetDevice(pr.dev));
-  if (!items.empty())
-    CK(cudaMemcpyAsync(pp.buf[pp.b_in], items.data(), items.size() * 4, cudaMemcpyHostToDevice, pr.st));
   uint32_t zeros[4] = {0, 0, 0, 0};
   zeros[pp.c_in] = (uint32_t)items.size();
-  CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+  if (items.size() <= 1000) {
+    // small initialisers (Initial [src]) go through pinned staging: a truly asynchronous copy that
+    // does not wait for other streams (a pageable copy would serialise with an in-flight
+    // asynchronous result readback)
+    CK(cudaEventSynchronize(pr.stage_ev));  // the previous staged copy has been consumed
+    std::memcpy(pr.h_stage, zeros, sizeof(zeros));
+    if (!items.empty()) std::memcpy(pr.h_stage + 4, items.data(), items.size() * 4);
+    if (!items.empty())
+      CK(cudaMemcpyAsync(pp.buf[pp.b_in], pr.h_stage + 4, items.size() * 4, cudaMemcpyHostToDevice, pr.st));
+    CK(cudaMemcpyAsync(pp.ctl->cnt, pr.h_stage, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+    CK(cudaEventRecord(pr.stage_ev, pr.st));
+  } else {
+    if (!items.empty())
+      CK(cudaMemcpyAsync(pp.buf[pp.b_in], items.data(), items.size() * 4, cudaMemcpyHostToDevice, pr.st));
+    CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+  }
   CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
   CK(cudaMemsetAsync(&pp.ctl->overflow, 0, sizeof(uint32_t), pr.st));
   // pageable sources are staged before cudaMemcpyAsync returns: no host sync needed (stream order)
@@ -264,6 +289,14 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
       GraphPart& gp = g->parts[l];
       PartRT& pr = ctx->parts[l];
       CK(cudaSetDevice(pr.dev));
+      if (gp.lab_buf[1]) {  // double-buffered: write the other buffer, after its readback
+        gp.lab_sel ^= 1;
+        gp.lab = gp.lab_buf[gp.lab_sel];
+        if (gp.copy_pending[gp.lab_sel]) {
+          CK(cudaStreamWaitEvent(pr.st, gp.lab_copied[gp.lab_sel], 0));
+          gp.copy_pending[gp.lab_sel] = false;
+        }
+      }
       if (op == IRGL_OP_BFS || op == IRGL_OP_SSSP) {
         CK(launch_fill_i32(gp.lab, kInf, g->n, pr.st));
         if (op == IRGL_OP_BFS && gp.vis_k()) CK(cudaMemsetAsync(gp.vis, 0, ((g->n + 31) / 32) * sizeof(uint32_t), pr.st));
@@ -915,10 +948,11 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
-  static_assert(sizeof(Ctl) <= 4096, "control block readback goes through the 4 KB pinned scratch");
-  CK(cudaMemcpyAsync(pr.h_pin, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+  // (a kernel writing host-mapped memory instead was slower with an async readback in flight:
+  // its PCIe writes queue behind the bulk copy, profiles/r1s2_e2e.txt)
+  CK(cudaMemcpyAsync(pr.h_ctl, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
   CK(cudaStreamSynchronize(pr.st));  // the iterate's one host synchronisation
-  const Ctl& h = *reinterpret_cast<const Ctl*>(pr.h_pin);
+  const Ctl& h = *pr.h_ctl;
   {
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
@@ -1279,8 +1313,12 @@ static irgl_status_t ctx_init_parts(irgl_ctx* c, const int* devices, int ndev, i
     pr.dev = devices ? devices[l % ndev] : 0;
     CK(cudaSetDevice(pr.dev));
     CK(cudaStreamCreateWithFlags(&pr.st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&pr.copy_st, cudaStreamNonBlocking));
     CK(cudaDeviceGetAttribute(&pr.sms, cudaDevAttrMultiProcessorCount, pr.dev));
     CK(cudaMallocHost(&pr.h_pin, 4096));
+    CK(cudaMallocHost(&pr.h_stage, 4096));
+    CK(cudaHostAlloc(&pr.h_ctl, sizeof(Ctl), cudaHostAllocMapped));
+    CK(cudaEventCreateWithFlags(&pr.stage_ev, cudaEventDisableTiming));
   }
   CK(cudaSetDevice(c->parts[0].dev));
   CK(cudaEventCreate(&c->ev0));
@@ -1412,7 +1450,11 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
   for (auto& p : ctx->parts) {
     cudaSetDevice(p.dev);
     if (p.st) cudaStreamDestroy(p.st);
+    if (p.copy_st) cudaStreamDestroy(p.copy_st);
     if (p.h_pin) cudaFreeHost(p.h_pin);
+    if (p.h_stage) cudaFreeHost(p.h_stage);
+    if (p.h_ctl) cudaFreeHost(p.h_ctl);
+    if (p.stage_ev) cudaEventDestroy(p.stage_ev);
   }
   delete ctx;
   return IRGL_OK;
@@ -1615,8 +1657,13 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     GraphPart& gp = g->parts[l];
     cudaSetDevice(ctx->parts[l].dev);
     cudaStreamSynchronize(ctx->parts[l].st);
-    void* ps[] = {gp.row_ptr, gp.col, gp.w, gp.lab, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
-                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
+    cudaStreamSynchronize(ctx->parts[l].copy_st);
+    for (auto& e : gp.lab_copied)
+      if (e) cudaEventDestroy(e);
+    // double-buffered labels: both buffers (gp.lab is one of them)
+    int32_t* lab0 = gp.lab_buf[1] ? gp.lab_buf[0] : gp.lab;
+    void* ps[] = {gp.row_ptr, gp.col, gp.w, lab0, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
+                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.lab_buf[1], gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
     for (void* p : ps)
@@ -1946,6 +1993,45 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
     } else {
       CK(cudaMemcpy((int32_t*)host_out + gp.lo, gp.lab + gp.lo, nloc * 4, cudaMemcpyDeviceToHost));
     }
+  }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out,
+                                     size_t bytes) {
+  if (!ctx || !host_out) return IRGL_E_INVALID;
+  if (!g || !(op == IRGL_OP_BFS || op == IRGL_OP_SSSP || op == IRGL_OP_CC || op == IRGL_OP_CC_LP))
+    return irgl_read_result(ctx, g, op, host_out, bytes);  // small or host-side results: synchronous
+  if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
+  if (bytes < (size_t)g->n * 4) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  for (size_t l = 0; l < g->parts.size(); ++l) {
+    GraphPart& gp = g->parts[l];
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    if (!gp.lab_buf[1]) {  // switch this graph to double-buffered labels
+      gp.lab_buf[0] = gp.lab;
+      gp.lab_sel = 0;
+      CK(cudaMalloc(&gp.lab_buf[1], std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
+      for (auto& e : gp.lab_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t nloc = gp.hi - gp.lo;
+    if (nloc <= 0) continue;
+    // the copy follows everything already queued on the compute stream
+    CK(cudaEventRecord(gp.lab_copied[gp.lab_sel], pr.st));
+    CK(cudaStreamWaitEvent(pr.copy_st, gp.lab_copied[gp.lab_sel], 0));
+    CK(cudaMemcpyAsync((int32_t*)host_out + gp.lo, gp.lab + gp.lo, nloc * 4, cudaMemcpyDeviceToHost,
+                       pr.copy_st));
+    CK(cudaEventRecord(gp.lab_copied[gp.lab_sel], pr.copy_st));
+    gp.copy_pending[gp.lab_sel] = true;
+  }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_results_wait(irgl_ctx* ctx) {
+  if (!ctx) return IRGL_E_INVALID;
+  for (PartRT& pr : ctx->parts) {
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaStreamSynchronize(pr.copy_st));
   }
   return IRGL_OK;
 }

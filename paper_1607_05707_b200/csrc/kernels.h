@@ -142,6 +142,8 @@ cudaError_t launch_exclusive_test(const uint32_t* in, uint32_t nin, const int32_
 
 // Reset of the control block before an outlined (persistent) launch, in one kernel.
 cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st);
+// Copies the control block into host-mapped pinned memory (the post-iterate readback).
+cudaError_t launch_ctl_export(const Ctl* ctl, Ctl* host_mapped, cudaStream_t st);
 
 // ---- misc (util.cu) ---------------------------------------------------------------------------
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);

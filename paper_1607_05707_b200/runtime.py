@@ -114,6 +114,7 @@ EXPORTS = [
     "irgl_pipe_init_range", "irgl_pipe_size", "irgl_pipe_read", "irgl_pipe_destroy",
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
     "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
+    "irgl_read_result_async", "irgl_results_wait",
 ]
 
 # every symbol include/irgl/frontend.h declares
@@ -171,6 +172,8 @@ def load_library(path: str | None = None):
         "irgl_iterate": ([P, P, P, C.c_int, C.POINTER(OpArgs), C.POINTER(IterateOpts),
                           C.POINTER(IterStats)], i32),
         "irgl_read_result": ([P, P, C.c_int, P, C.c_size_t], i32),
+        "irgl_read_result_async": ([P, P, C.c_int, P, C.c_size_t], i32),
+        "irgl_results_wait": ([P], i32),
         "irgl_t_control": ([C.POINTER(BlockConstraint), C.c_int, i32p], i32),
         "irgl_op_plan": ([P, C.c_int, C.POINTER(BlockConstraint), i32p, i32p], i32),
         "irgl_event_record": ([P, C.c_int], i32),
@@ -436,6 +439,16 @@ class Context:
         self._chk(self._lib.irgl_read_result(self._h, graph.handle, op,
                                              out.ctypes.data_as(C.c_void_p), out.nbytes))
         return out
+
+    def read_result_async(self, op, graph, out: np.ndarray):
+        """Queue the node result's copy into `out` (pinned to overlap) and return at once; the
+        next traversal writes the graph's other label buffer.  Valid after results_wait()."""
+        self._chk(self._lib.irgl_read_result_async(self._h, graph.handle, op,
+                                                   out.ctypes.data_as(C.c_void_p), out.nbytes))
+        return out
+
+    def results_wait(self):
+        self._chk(self._lib.irgl_results_wait(self._h))
 
     def event_record(self, slot):
         self._chk(self._lib.irgl_event_record(self._h, slot))
