@@ -2019,8 +2019,12 @@ irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, v
     // the copy follows everything already queued on the compute stream
     CK(cudaEventRecord(gp.lab_copied[gp.lab_sel], pr.st));
     CK(cudaStreamWaitEvent(pr.copy_st, gp.lab_copied[gp.lab_sel], 0));
-    CK(cudaMemcpyAsync((int32_t*)host_out + gp.lo, gp.lab + gp.lo, nloc * 4, cudaMemcpyDeviceToHost,
-                       pr.copy_st));
+    // 1 MiB pieces: a copy engine switches channels between commands, so the iterate's own small
+    // readback (control block) waits for at most one piece instead of the whole result
+    const int64_t piece = (1 << 20) / 4;
+    for (int64_t o = 0; o < nloc; o += piece)
+      CK(cudaMemcpyAsync((int32_t*)host_out + gp.lo + o, gp.lab + gp.lo + o,
+                         std::min<int64_t>(piece, nloc - o) * 4, cudaMemcpyDeviceToHost, pr.copy_st));
     CK(cudaEventRecord(gp.lab_copied[gp.lab_sel], pr.copy_st));
     gp.copy_pending[gp.lab_sel] = true;
   }
