@@ -9,16 +9,22 @@
 //                              search (no shared memory, no CTA barrier);
 //        - edge chunks         (degree >= warp_t): chunk_edges-sized descriptors (one reservation
 //                              per warp tile) that every warp of the grid drains in a second,
-//                              edge-balanced phase, 128-bit col/weight loads, 8 gathers and all
-//                              atomics of a lane in flight at once (super-hubs do not serialise,
-//                              and no warp holds a long serial tail of mid-degree vertices).
+//                              edge-balanced phase: one 128-bit col/weight group per lane per
+//                              iteration, the next group loaded before the current gathers and
+//                              atomics are waited on; few chunks are split over several warps.
+//      relax_batch issues every atomic of a lane's batch before consuming any result (BFS CAS or
+//      visited-bitmap OR; SSSP/CC RED.MIN + stamp exchange); large frontiers run "dense" rounds
+//      that mark instead of push and compact the marks into the next worklist.
 //  E2  cooperative conversion of pushes: warp __ballot_sync/__popc aggregation into a per-warp
-//      shared-memory staging queue; one global atomic reservation per 224+ staged items.
-//  E3  iteration outlining: the Iterate loop as one cooperative persistent kernel with a grid
-//      barrier (SyncRunningThreads) instead of per-round host launches.
-//  SSSP near-far (delta > 0): pushes with dist >= threshold go to a far pile that is split back
-//      into the worklist when the near frontier empties (same fixed point as Bellman-Ford, less
-//      re-relaxation).
+//      shared-memory staging queue; one global atomic reservation per 224+ staged items, per CTA
+//      at phase end; remote pushes (multi-partition) staged per owner the same way.
+//  E3  iteration outlining: the Iterate loop as one cooperative persistent kernel; rounds are
+//      separated by grid_sync_bcast (SyncRunningThreads) whose release word
+//      carries the round's counters, so no thread re-reads hot counters after the barrier.
+//  SSSP degree-scaled deferral (defer > 0): a popped vertex whose (dist - frontier min) * degree
+//      exceeds the budget is re-pushed instead of expanded (hubs expand near their final
+//      distance); near-far piles (delta > 0) are the bucketed alternative.  Both leave the fixed
+//      point of Bellman-Ford, i.e. the distances, unchanged.
 //
 // Reference semantics (SPEC.md:317-322 ForAll lowering; :425 bulk-synchronous worklists: pops
 // read `in`, pushes append to `out`, never visible in the same launch).
