@@ -254,7 +254,9 @@ def workload_config(args, g):
                        f"one traversal per step over 16 sources",
            "op": args.op, "graph": "rmat", "scale": args.scale, "edge_factor": 16,
            "sources": 16, "partitions": args.gpus, "outline": args.outline,
-           "l2": "inputs larger than L2 (CSR col+weight >> 126 MB); no flush"}
+           "l2": "inputs larger than L2 (CSR col+weight >> 126 MB); no flush",
+           "layout": ("degree-ordered vertex relabelling (untimed preprocessing; API ids unchanged)"
+                      if args.relabel and args.gpus == 1 else "generator ids")}
     if g is not None:
         cfg["n"] = int(g.n)
         cfg["m_directed"] = int(g.m)
@@ -273,10 +275,21 @@ def run_irgl(args, d):
     t0 = time.time()
     g = ctx.generate_rmat(args.scale)
     gen_s = time.time() - t0
+    relabel_s = None
+    if args.relabel and d.world == 1:
+        # data layout: degree-ordered vertex ids (preprocessing, like the CSR build: untimed);
+        # every id crossing the API stays the generator's
+        t0 = time.time()
+        g.relabel()
+        relabel_s = time.time() - t0
     info = g.info
     # local degrees -> sources (Philox stream of the oracle), agreed across ranks
     rp = _local_row_ptr(ctx, g)
     lo, hi = info.lo, info.hi
+    if relabel_s is not None:  # degrees in the caller's ids for the source pick
+        dg = np.diff(rp)[g.perm()]
+        rp = np.zeros(g.n + 1, dtype=np.int64)
+        rp[1:] = np.cumsum(dg)
 
     def local_deg(x):
         return int(rp[x - lo + 1] - rp[x - lo]) if lo <= x < hi else 0
@@ -370,7 +383,7 @@ def run_irgl(args, d):
                 "d2h_bytes_per_step": 4 * int(g.n)},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "detail": {"gen_s": round(gen_s, 3), "rounds_per_step": float(np.mean([s.rounds for s in stats])),
+        "detail": {"gen_s": round(gen_s, 3), "relabel_s": round(relabel_s, 3) if relabel_s else None, "rounds_per_step": float(np.mean([s.rounds for s in stats])),
                    "edges_scanned_per_step": float(np.mean([s.edges for s in stats])),
                    "E_r_mean": float(np.mean(er)), "V_r_mean": float(np.mean(vr)),
                    "outlined": int(stats[-1].outlined) if stats else None,
@@ -417,6 +430,8 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--relabel", type=int, default=1,
+                    help="1 = degree-ordered vertex relabelling before timing (one GPU only)")
     ap.add_argument("--direction", type=int, default=0,
                     help="BFS: 1 = direction-optimising (SURVEY §8f F1), 0 = Listing-2 top-down")
     args = ap.parse_args()

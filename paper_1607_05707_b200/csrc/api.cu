@@ -109,6 +109,17 @@ struct irgl_graph {
   irgl_ctx* ctx = nullptr;
   int64_t n = 0, m = 0;
   bool has_w = false;
+  // degree-ordered relabelling (irgl_graph_relabel; one partition): device perm[old] = new,
+  // inv[new] = old, host inv for worklist reads, result staging (two buffers for async reads)
+  bool relabeled = false;
+  int32_t* perm = nullptr;
+  int32_t* inv = nullptr;
+  std::vector<int32_t> inv_host;
+  void* res_buf[2] = {nullptr, nullptr};
+  int32_t* res_cmin = nullptr;
+  int res_sel = 0;
+  cudaEvent_t res_copied[2] = {nullptr, nullptr};
+  bool res_pending[2] = {false, false};
   int64_t part_size = 1;
   std::vector<irgl::GraphPart> parts;
   int lab_op = -1;
@@ -121,6 +132,7 @@ struct irgl_pipe {
   irgl_ctx* ctx = nullptr;
   int64_t cap = 0;
   std::vector<irgl::PipePart> parts;
+  const irgl_graph* mapped_for = nullptr;  // relabelled graph whose ids the items now carry
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -222,6 +234,7 @@ static irgl_status_t pipe_set_in(irgl_ctx* ctx, irgl_pipe* p, int l, const std::
 
 static irgl_status_t pipe_init_items(irgl_pipe* p, const int64_t* items, int64_t count) {
   irgl_ctx* ctx = p->ctx;
+  p->mapped_for = nullptr;  // caller ids; mapped at the first Iterate / Invoke on a relabelled graph
   if (count < 0 || (count > 0 && !items)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "bad init array");
   const int L = (int)ctx->parts.size();
   std::vector<std::vector<uint32_t>> per(L);
@@ -1669,6 +1682,13 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     for (void* p : ps)
       if (p) cudaFree(p);
   }
+  if (g->relabeled) {
+    cudaSetDevice(ctx->parts[0].dev);
+    for (void* p : {(void*)g->perm, (void*)g->inv, g->res_buf[0], g->res_buf[1], (void*)g->res_cmin})
+      if (p) cudaFree(p);
+    for (auto& e : g->res_copied)
+      if (e) cudaEventDestroy(e);
+  }
   delete g;
   return IRGL_OK;
 }
@@ -1718,6 +1738,7 @@ irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end) {
     PartRT& pr = ctx->parts[l];
     CK(cudaSetDevice(pr.dev));
     CK(launch_iota_u32(pp.buf[pp.b_in], (uint32_t)b, (uint32_t)(e - b), pr.st));
+    p->mapped_for = nullptr;
     uint32_t zeros[4] = {0, 0, 0, 0};
     zeros[pp.c_in] = (uint32_t)(e - b);
     CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
@@ -1755,8 +1776,9 @@ irgl_status_t irgl_pipe_read(irgl_pipe* p, irgl_wl which, int64_t* items, int64_
     c = (uint32_t)std::min<int64_t>(c, p->cap);
     std::vector<uint32_t> h(c);
     if (c) CK(cudaMemcpy(h.data(), pp.buf[buf], c * 4, cudaMemcpyDeviceToHost));
+    const std::vector<int32_t>* inv = p->mapped_for ? &p->mapped_for->inv_host : nullptr;
     for (uint32_t i = 0; i < c; ++i)
-      if (tot + i < cap && items) items[tot + i] = h[i];
+      if (tot + i < cap && items) items[tot + i] = inv ? (*inv)[h[i]] : h[i];
     tot += c;
   }
   *count = tot;
@@ -1776,11 +1798,15 @@ irgl_status_t irgl_pipe_destroy(irgl_pipe* p) {
 }
 
 // ---- operators ---------------------------------------------------------------------------------
+static irgl_status_t map_pipe(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g);
+
 irgl_status_t irgl_op_reset(irgl_ctx* ctx, irgl_graph* g, irgl_op op, const irgl_op_args* args,
                             irgl_pipe* pipe) {
   (void)args;
   if (!ctx || !is_known_op(op)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown operator");
   if (g && g->ctx != ctx) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph belongs to another ctx");
+  irgl_status_t s = map_pipe(ctx, pipe, g);
+  if (s != IRGL_OK) return s;
   return op_reset(ctx, g, op, pipe);
 }
 
@@ -1798,11 +1824,26 @@ static irgl_status_t check_call(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, i
   return IRGL_OK;
 }
 
+// A pipe initialised with caller ids meets a relabelled graph: map its items once (in, out and
+// retry; only `in` can be non-empty after an init).
+static irgl_status_t map_pipe(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g) {
+  if (!pipe || !g || !g->relabeled || pipe->mapped_for == g) return IRGL_OK;
+  if (pipe->mapped_for)
+    return fail(ctx, IRGL_E_USAGE, "E_USAGE", "pipe items carry another relabelled graph's ids; re-initialise it");
+  PipePart& pp = pipe->parts[0];
+  PartRT& pr = ctx->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  CK(launch_map_items(pp.buf[pp.b_in], pp.n_in, g->perm, pr.st));
+  pipe->mapped_for = g;
+  return IRGL_OK;
+}
+
 irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
                           const irgl_op_args* args, irgl_reduction red, int32_t* reduced,
                           irgl_iter_stats* stats) {
   irgl_status_t s = check_call(ctx, pipe, g, op);
   if (s != IRGL_OK) return s;
+  if (!is_test_op(op) && (s = map_pipe(ctx, pipe, g)) != IRGL_OK) return s;
   irgl_iter_stats st{};
   st.last_reduced = -1;
   const PartRT& pr0 = ctx->parts[0];
@@ -1845,6 +1886,7 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
                            irgl_iter_stats* stats) {
   irgl_status_t s = check_call(ctx, pipe, g, op);
   if (s != IRGL_OK) return s;
+  if (!is_test_op(op) && (s = map_pipe(ctx, pipe, g)) != IRGL_OK) return s;
   irgl_iterate_opts o{};
   o.outline = -1;
   o.reset = 1;
@@ -1957,6 +1999,67 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
   return IRGL_OK;
 }
 
+// Result of a relabelled graph in the caller's ids, into res_buf[k] (ordered on the compute stream):
+// per-vertex values are gathered through perm; CC labels (a component's smallest id) are
+// re-expressed as the component's smallest original id.
+static irgl_status_t stage_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, int k) {
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  if (!g->res_buf[k]) CK(cudaMalloc(&g->res_buf[k], std::max<int64_t>(g->n, 1) * 8));
+  if (op == IRGL_OP_PR) {
+    CK(launch_gather_f64((double*)g->res_buf[k], gp.pr[gp.pr_cur], g->perm, g->n, pr.st));
+  } else if (op == IRGL_OP_CC || op == IRGL_OP_CC_LP) {
+    if (!g->res_cmin) CK(cudaMalloc(&g->res_cmin, std::max<int64_t>(g->n, 1) * 4));
+    CK(launch_cc_labels_original((int32_t*)g->res_buf[k], gp.lab, g->perm, g->inv, g->res_cmin, g->n, pr.st));
+  } else {
+    CK(launch_gather_i32((int32_t*)g->res_buf[k], gp.lab, g->perm, g->n, pr.st));
+  }
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_relabel(irgl_ctx* ctx, irgl_graph* g) {
+  if (!ctx || !g || g->ctx != ctx) return IRGL_E_INVALID;
+  if (g->parts.size() != 1 || ctx->ptotal() != 1)
+    return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED", "relabelling needs a one-partition graph");
+  if (g->relabeled) return IRGL_OK;
+  if (g->n >= (1ll << 31)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "relabelling needs n < 2^31");
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  CK(cudaStreamSynchronize(pr.st));
+  int64_t* rp_new = nullptr;
+  CK(relabel_degree(g->n, gp.m, g->maxdeg, gp.row_ptr, &gp.col, &gp.w, &rp_new, &g->perm, &g->inv, pr.st));
+  CK(cudaFree(gp.row_ptr));
+  gp.row_ptr = rp_new;
+  g->inv_host.resize(g->n);
+  CK(cudaMemcpy(g->inv_host.data(), g->inv, g->n * 4, cudaMemcpyDeviceToHost));
+  // state derived from the old numbering
+  if (gp.tc_rp) cudaFree(gp.tc_rp);
+  if (gp.tc_cl) cudaFree(gp.tc_cl);
+  if (gp.tc_src) cudaFree(gp.tc_src);
+  gp.tc_rp = nullptr;
+  gp.tc_cl = nullptr;
+  gp.tc_src = nullptr;
+  gp.tc_m = -1;
+  g->lab_op = -1;
+  for (auto& e : g->res_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  g->relabeled = true;
+  return IRGL_OK;
+}
+
+irgl_status_t irgl_graph_perm(irgl_graph* g, int32_t* new_of_old) {
+  if (!g || !new_of_old) return IRGL_E_INVALID;
+  irgl_ctx* ctx = g->ctx;
+  if (!g->relabeled) {
+    for (int64_t v = 0; v < g->n; ++v) new_of_old[v] = (int32_t)v;
+    return IRGL_OK;
+  }
+  CK(cudaSetDevice(ctx->parts[0].dev));
+  CK(cudaMemcpy(new_of_old, g->perm, g->n * 4, cudaMemcpyDeviceToHost));
+  return IRGL_OK;
+}
+
 irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* host_out, size_t bytes) {
   if (!ctx || !host_out) return IRGL_E_INVALID;
   if (is_test_op(op)) {
@@ -1982,6 +2085,18 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
   if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
   const size_t esz = op == IRGL_OP_PR ? 8 : 4;
   if (bytes < (size_t)g->n * esz) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  if (g->relabeled) {  // back to the caller's vertex ids on the device, then one copy
+    const int k = g->res_sel;
+    if (g->res_pending[k]) {
+      CK(cudaEventSynchronize(g->res_copied[k]));
+      g->res_pending[k] = false;
+    }
+    irgl_status_t s = stage_result(ctx, g, op, k);
+    if (s != IRGL_OK) return s;
+    CK(cudaMemcpyAsync(host_out, g->res_buf[k], g->n * esz, cudaMemcpyDeviceToHost, ctx->parts[0].st));
+    CK(cudaStreamSynchronize(ctx->parts[0].st));
+    return IRGL_OK;
+  }
   for (size_t l = 0; l < g->parts.size(); ++l) {
     GraphPart& gp = g->parts[l];
     CK(cudaSetDevice(ctx->parts[l].dev));
@@ -2004,6 +2119,23 @@ irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, v
     return irgl_read_result(ctx, g, op, host_out, bytes);  // small or host-side results: synchronous
   if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
   if (bytes < (size_t)g->n * 4) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  if (g->relabeled) {  // stage into one of two result buffers, copy from it in pieces
+    PartRT& pr = ctx->parts[0];
+    const int k = g->res_sel;
+    g->res_sel ^= 1;
+    if (g->res_pending[k]) CK(cudaStreamWaitEvent(pr.st, g->res_copied[k], 0));
+    irgl_status_t s = stage_result(ctx, g, op, k);
+    if (s != IRGL_OK) return s;
+    CK(cudaEventRecord(g->res_copied[k], pr.st));
+    CK(cudaStreamWaitEvent(pr.copy_st, g->res_copied[k], 0));
+    const int64_t piece = (1 << 20) / 4;
+    for (int64_t o = 0; o < g->n; o += piece)
+      CK(cudaMemcpyAsync((int32_t*)host_out + o, (int32_t*)g->res_buf[k] + o, std::min<int64_t>(piece, g->n - o) * 4,
+                         cudaMemcpyDeviceToHost, pr.copy_st));
+    CK(cudaEventRecord(g->res_copied[k], pr.copy_st));
+    g->res_pending[k] = true;
+    return IRGL_OK;
+  }
   for (size_t l = 0; l < g->parts.size(); ++l) {
     GraphPart& gp = g->parts[l];
     PartRT& pr = ctx->parts[l];

@@ -145,6 +145,18 @@ cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st);
 // Copies the control block into host-mapped pinned memory (the post-iterate readback).
 cudaError_t launch_ctl_export(const Ctl* ctl, Ctl* host_mapped, cudaStream_t st);
 
+// ---- degree-ordered relabelling (relabel.cu) ---------------------------------------------------
+// Replaces *col_io / *w_io (freed) with the relabelled arrays, returns new row offsets, perm
+// (new id of each old vertex) and inv (old vertex of each new id); the caller frees rp_old.
+cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* rp_old, int32_t** col_io,
+                           int32_t** w_io, int64_t** rp_new, int32_t** perm_out, int32_t** inv_out,
+                           cudaStream_t st);
+cudaError_t launch_map_items(uint32_t* items, uint32_t n, const int32_t* table, cudaStream_t st);
+cudaError_t launch_gather_i32(int32_t* out, const int32_t* src, const int32_t* perm, int64_t n, cudaStream_t st);
+cudaError_t launch_gather_f64(double* out, const double* src, const int32_t* perm, int64_t n, cudaStream_t st);
+cudaError_t launch_cc_labels_original(int32_t* out, const int32_t* lab, const int32_t* perm, const int32_t* inv,
+                                      int32_t* cmin, int64_t n, cudaStream_t st);
+
 // ---- misc (util.cu) ---------------------------------------------------------------------------
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t st);
 cudaError_t launch_scatter_zero(int32_t* lab, const uint32_t* items, uint32_t n, cudaStream_t st,

@@ -114,7 +114,7 @@ EXPORTS = [
     "irgl_pipe_init_range", "irgl_pipe_size", "irgl_pipe_read", "irgl_pipe_destroy",
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
     "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
-    "irgl_read_result_async", "irgl_results_wait",
+    "irgl_read_result_async", "irgl_results_wait", "irgl_graph_relabel", "irgl_graph_perm",
 ]
 
 # every symbol include/irgl/frontend.h declares
@@ -174,6 +174,8 @@ def load_library(path: str | None = None):
         "irgl_read_result": ([P, P, C.c_int, P, C.c_size_t], i32),
         "irgl_read_result_async": ([P, P, C.c_int, P, C.c_size_t], i32),
         "irgl_results_wait": ([P], i32),
+        "irgl_graph_relabel": ([P, P], i32),
+        "irgl_graph_perm": ([P, i32p], i32),
         "irgl_t_control": ([C.POINTER(BlockConstraint), C.c_int, i32p], i32),
         "irgl_op_plan": ([P, C.c_int, C.POINTER(BlockConstraint), i32p, i32p], i32),
         "irgl_event_record": ([P, C.c_int], i32),
@@ -480,6 +482,18 @@ class Graph:
     @property
     def handle(self):
         return self._h
+
+    def relabel(self):
+        """Degree-ordered relabelling (irgl_graph_relabel): faster traversals on graphs whose
+        per-vertex state leaves L2; ids seen through this API are unchanged."""
+        _check(self.ctx._lib.irgl_graph_relabel(self.ctx.handle, self._h), self.ctx.handle)
+        return self
+
+    def perm(self):
+        out = np.empty(self.n, dtype=np.int32)
+        _check(self.ctx._lib.irgl_graph_perm(self._h, out.ctypes.data_as(C.POINTER(C.c_int32))),
+               self.ctx.handle)
+        return out
 
     def download(self):
         rp = np.zeros(self.info.local_n + 1, dtype=np.int64) if self.info.partitions > 1 and \

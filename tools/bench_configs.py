@@ -27,10 +27,15 @@ def rowptr(ctx, g):
     return rp
 
 
-def rmat_traversals(ctx, scale, nsrc=4):
+def rmat_traversals(ctx, scale, nsrc=4, relabel=False):
     g = ctx.generate_rmat(scale)
     rp = rowptr(ctx, g)
     srcs = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=nsrc)
+    tag = ""
+    if relabel:
+        t0 = time.time()
+        g.relabel()
+        tag = f" (degree-ordered ids, relabel {time.time() - t0:.2f} s untimed)"
     p = ctx.pipe(g.n)
     for op, name in ((irgl.BFS, "bfs"), (irgl.SSSP, "sssp")):
         tms = kms = E = V = 0.0
@@ -41,7 +46,7 @@ def rmat_traversals(ctx, scale, nsrc=4):
             tms += st.device_ms; kms += st.kernel_ms; E += b.edges; V += b.popped
             rounds.append(st.rounds)
         byts = bench.algorithmic_bytes(name, V, E)
-        emit({"config": f"{name.upper()} RMAT-{scale}", "n": g.n, "m": g.m, "sources": nsrc,
+        emit({"config": f"{name.upper()} RMAT-{scale}{tag}", "n": g.n, "m": g.m, "sources": nsrc,
               "GTEPS": round(E / 2 / (tms * 1e-3) / 1e9, 2), "ms_per_traversal": round(tms / nsrc, 3),
               "rounds": rounds, "roofline_frac": round(byts / (kms * 1e-3) / 1e9 / PEAK, 4),
               "achieved_GBps": round(byts / (kms * 1e-3) / 1e9, 1)})
@@ -95,7 +100,8 @@ def grids(ctx):
 def main():
     ctx = irgl.Context()
     scale = int(os.environ.get("IRGL_CFG_SCALE", "24"))
-    g = rmat_traversals(ctx, scale)
+    rmat_traversals(ctx, scale).close()
+    g = rmat_traversals(ctx, scale, relabel=True)
     pagerank(ctx, g, scale)
     g.close()
     grids(ctx)
