@@ -17,6 +17,8 @@ g = ctx.generate_rmat(scale)
 rp = np.zeros(g.n + 1, dtype=np.int64)
 ctx._lib.irgl_graph_download(g.handle, rp.ctypes.data_as(C.POINTER(C.c_int64)), None, None)
 srcs = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=nsrc)
+if os.environ.get("RELABEL", "0") == "1":
+    g.relabel()
 p = ctx.pipe(g.n)
 E = 0
 for s in srcs:
