@@ -66,6 +66,13 @@ struct GraphPart {
   int64_t* tc_rp = nullptr;
   int32_t* tc_cl = nullptr;
   int32_t* tc_src = nullptr;  // source vertex of every oriented edge (edge-parallel count)
+  // PageRank hub split (built on first use; see PrHubs in kernels.h)
+  int32_t* pr_hub_of = nullptr;
+  int64_t* pr_hfirst = nullptr;
+  int64_t* pr_cbeg = nullptr;
+  int32_t* pr_clen = nullptr;
+  double* pr_partial = nullptr;
+  int64_t pr_nchunks = -1;
   uint32_t* vis = nullptr;    // BFS visited bitmap, n bits (valid while lab_op == BFS)
   // Label double buffer, created by the first irgl_read_result_async: every operator reset then
   // alternates buffers, so a traversal never overwrites the labels an asynchronous readback is
@@ -1152,6 +1159,55 @@ static irgl_status_t test_invoke(irgl_ctx* ctx, irgl_pipe* pipe, int op, const i
 }
 
 // ---- topology-driven invocations ---------------------------------------------------------------
+// PageRank hubs: vertices of degree >= kPrHubT (the CTA-level path is then unused), cut into chunks of <= kPrChunk edges.  Built once
+// per graph on the host from the row offsets (the hub set never changes between sweeps).
+constexpr int64_t kPrHubT = 1024, kPrChunk = 2048;
+static void free_pr_hubs(GraphPart& gp) {
+  for (void* p : {(void*)gp.pr_hub_of, (void*)gp.pr_hfirst, (void*)gp.pr_cbeg, (void*)gp.pr_clen, (void*)gp.pr_partial})
+    if (p) cudaFree(p);
+  gp.pr_hub_of = nullptr;
+  gp.pr_hfirst = nullptr;
+  gp.pr_cbeg = nullptr;
+  gp.pr_clen = nullptr;
+  gp.pr_partial = nullptr;
+  gp.pr_nchunks = -1;
+}
+static irgl_status_t ensure_pr_hubs(irgl_ctx* ctx, GraphPart& gp, PrHubs* out) {
+  if (gp.pr_nchunks < 0) {
+    const int64_t nloc = gp.hi - gp.lo;
+    std::vector<int64_t> rp(nloc + 1);
+    CK(cudaMemcpy(rp.data(), gp.row_ptr, (nloc + 1) * 8, cudaMemcpyDeviceToHost));
+    std::vector<int32_t> hub_of(std::max<int64_t>(nloc, 1), 0);
+    std::vector<int64_t> hfirst(1, 0), cbeg;
+    std::vector<int32_t> clen;
+    for (int64_t v = 0; v < nloc; ++v) {
+      const int64_t b = rp[v], e = rp[v + 1];
+      if (e - b < kPrHubT) continue;
+      hub_of[v] = (int32_t)(hfirst.size() - 1);
+      for (int64_t c = b; c < e; c += kPrChunk) {
+        cbeg.push_back(c);
+        clen.push_back((int32_t)std::min<int64_t>(kPrChunk, e - c));
+      }
+      hfirst.push_back((int64_t)cbeg.size());
+    }
+    gp.pr_nchunks = (int64_t)cbeg.size();
+    if (gp.pr_nchunks > 0) {
+      CK(cudaMalloc(&gp.pr_hub_of, hub_of.size() * 4));
+      CK(cudaMalloc(&gp.pr_hfirst, hfirst.size() * 8));
+      CK(cudaMalloc(&gp.pr_cbeg, cbeg.size() * 8));
+      CK(cudaMalloc(&gp.pr_clen, clen.size() * 4));
+      CK(cudaMalloc(&gp.pr_partial, cbeg.size() * 8));
+      CK(cudaMemcpy(gp.pr_hub_of, hub_of.data(), hub_of.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(gp.pr_hfirst, hfirst.data(), hfirst.size() * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(gp.pr_cbeg, cbeg.data(), cbeg.size() * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(gp.pr_clen, clen.data(), clen.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  *out = PrHubs{gp.pr_hub_of, gp.pr_hfirst, gp.pr_cbeg, gp.pr_clen, gp.pr_partial,
+                std::max<int64_t>(gp.pr_nchunks, 0), kPrHubT};
+  return IRGL_OK;
+}
+
 static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irgl_op_args* a,
                                  int red, int32_t* reduced, irgl_iter_stats* stt) {
   if (ctx->ptotal() > 1)
@@ -1183,8 +1239,11 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     const double d = a && a->pr_damping > 0 ? a->pr_damping : 0.85;
     const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
     const int c = gp.pr_cur;
+    PrHubs hubs;
+    irgl_status_t hs = ensure_pr_hubs(ctx, gp, &hubs);
+    if (hs != IRGL_OK) return hs;
     CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
-                       reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, 0, gm, pr.st));
+                       reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, 0, gm, hubs, pr.st));
     stt->launches += 1;
     CK(cudaMemcpyAsync(&cell, &gp.ctl->red[0], 4, cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
@@ -1233,16 +1292,21 @@ static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_arg
     irgl_status_t s = op_reset(ctx, g, IRGL_OP_PR, nullptr);
     if (s != IRGL_OK) return s;
   }
-  const int bps = pr_persistent_blocks_per_sm();
+  int bps = pr_persistent_blocks_per_sm();
   if (bps <= 0) return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "PR control kernel not co-resident");
+  if (ctx->cfg.blocks_per_sm > 0) bps = std::min(bps, (int)ctx->cfg.blocks_per_sm);
   const double d = a && a->pr_damping > 0 ? a->pr_damping : 0.85;
   const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
   const int c = gp.pr_cur;
+  PrHubs hubs;
+  irgl_status_t hs = ensure_pr_hubs(ctx, gp, &hubs);
+  if (hs != IRGL_OK) return hs;
   CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
+  CK(cudaMemsetAsync(gp.ctl->tile_ctr, 0, sizeof(gp.ctl->tile_ctr), pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
   CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
                           reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, o.max_rounds,
-                          o.cond_mode, bps * pr.sms, pr.st));
+                          o.cond_mode, bps * pr.sms, hubs, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   Ctl h;
   CK(cudaMemcpyAsync(&h, gp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
@@ -1676,7 +1740,8 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
     // double-buffered labels: both buffers (gp.lab is one of them)
     int32_t* lab0 = gp.lab_buf[1] ? gp.lab_buf[0] : gp.lab;
     void* ps[] = {gp.row_ptr, gp.col, gp.w, lab0, gp.stamp, gp.pr[0], gp.pr[1], gp.pr[2], gp.pr[3],
-                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.lab_buf[1], gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
+                  gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.lab_buf[1], gp.pr_hub_of, gp.pr_hfirst, gp.pr_cbeg,
+                  gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
     for (void* p : ps)
@@ -2042,6 +2107,7 @@ irgl_status_t irgl_graph_relabel(irgl_ctx* ctx, irgl_graph* g) {
   gp.tc_cl = nullptr;
   gp.tc_src = nullptr;
   gp.tc_m = -1;
+  free_pr_hubs(gp);
   g->lab_op = -1;
   for (auto& e : g->res_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   g->relabeled = true;

@@ -113,12 +113,26 @@ cudaError_t launch_cc_hook(const DevCSR& g, int32_t* parent, Ctl* ctl, int red_s
 cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st);
 cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr, int64_t n,
                            cudaStream_t st);
+// PageRank hub split (built once per graph): hub_of[v] = hub index of vertex v (valid when
+// deg(v) >= hub_t), hub k's chunks are [hfirst[k], hfirst[k+1]), chunk c = edges
+// [cbeg[c], cbeg[c] + clen[c]); partial[c] receives the chunk's sum every sweep.
+struct PrHubs {
+  const int32_t* hub_of;
+  const int64_t* hfirst;
+  const int64_t* cbeg;
+  const int32_t* clen;
+  double* partial;
+  int64_t nchunks;  // 0: no hub split
+  int64_t hub_t;
+};
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
                             const float* contrib, float* contrib_next, double d, double tol,
-                            int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st);
+                            int64_t n_global, Ctl* ctl, int red_slot, int grid, const PrHubs& h,
+                            cudaStream_t st);
 cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float* ca, float* cb,
                                  double d, double tol, int64_t n_global, Ctl* ctl,
-                                 int64_t max_rounds, int cond_mode, int grid, cudaStream_t st);
+                                 int64_t max_rounds, int cond_mode, int grid, const PrHubs& h,
+                                 cudaStream_t st);
 int pr_persistent_blocks_per_sm();
 cudaError_t tc_orient(const DevCSR& g, int64_t n, int64_t** rp_out, int32_t** cl_out,
                       int32_t** src_out, int64_t* m_out, cudaStream_t st);

@@ -117,6 +117,8 @@ struct PrSmem {
   double red[kWarps];
   int32_t owner;
   int64_t b, e;
+  int64_t tile;
+  int64_t round;
 };
 
 // contrib / rank arrays are rewritten every sweep; in the persistent kernel a plain load could hit
@@ -160,17 +162,42 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// Hub vertices (degree >= hub_t) are summed edge-balanced: their edge ranges are cut once per
+// graph into chunks of <= chunk edges; every warp of the grid sums whole chunks into partial[c]
+// (phase A), and the vertex's sweep adds its partials in chunk order (phase B) — deterministic,
+// and no CTA walks a run of hubs alone: with degree-ordered ids every hub sits in the first
+// vertex tiles (without the split PR on relabelled RMAT-24 took 18.5 ms per sweep instead of 2.8).
+__device__ void pr_hub_chunks(const DevCSR& g, const float* contrib, const PrHubs& h) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < h.nchunks; c += nw) {
+    const int64_t b = h.cbeg[c], e = b + h.clen[c];
+    const double s = warp_sum(gather_sum<32>(g.col, contrib, b + lane, e));
+    if (lane == 0) h.partial[c] = s;
+  }
+}
+
 // One PR sweep over the local vertex range (tile per CTA-iteration).  Deterministic per-vertex
 // summation order (fixed by the code path chosen by degree).
 // contrib(u) = rank(u)/deg(u) is stored in fp32 (the gathered operand: half the bytes per edge
 // and an L2-resident array at RMAT-24); ranks and per-vertex sums stay fp64.
+// Round slot of the persistent kernel's rotating cells, read from shared memory at each use so
+// that neither the slot nor the derived cell pointers occupy registers across the sweep.
+__shared__ int32_t s_pr_slot;
+
+// kSmemSlot: cells ctl->red[s], ctl->tile_ctr[s] with s = s_pr_slot (persistent kernel) or
+// s = slot (host-loop kernel, a constant-bank parameter).
+template <bool kSmemSlot>
 __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
                                double* __restrict__ rank_new, const float* __restrict__ contrib,
                                float* __restrict__ contrib_next, double d, double tol,
-                               double base, int red, uint32_t* cell) {
+                               double base, int red, Ctl* ctl, int slot, const PrHubs& h) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nloc = g.hi - g.lo;
-  for (int64_t t0 = (int64_t)blockIdx.x * kBlock; t0 < nloc; t0 += (int64_t)gridDim.x * kBlock) {
+  // tiles: the first one static, then dynamic (tctr counts from 0; tile = gridDim + count), so
+  // with degree-ordered ids the expensive front tiles are taken first and the tail stays short
+  for (int64_t t0 = (int64_t)blockIdx.x * kBlock;;) {
+    if (t0 >= nloc) break;
     const int64_t i = t0 + tid;
     const bool valid = i < nloc;
     int64_t beg = 0, end = 0;
@@ -181,6 +208,12 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
     const int64_t deg0 = end - beg;
     int64_t deg = deg0;
     double mysum = 0.0;
+    if (h.nchunks > 0 && deg >= h.hub_t) {  // hub: its chunks' partial sums, in order
+      const int32_t k = __ldg(h.hub_of + i);
+      const int64_t c0 = h.hfirst[k], c1 = h.hfirst[k + 1];
+      for (int64_t c = c0; c < c1; ++c) mysum += ld_cg_f64(h.partial + c);
+      deg = 0;
+    }
     // CTA level (deg >= 1024): whole CTA sums one vertex at a time
     while (__syncthreads_or(deg >= 1024)) {
       if (deg >= 1024) sm.owner = tid;  // any winner
@@ -226,17 +259,27 @@ __device__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __rest
       contrib_next[v] = deg0 > 0 ? (float)(r / (double)deg0) : 0.0f;
       changed = fabs(r - ld_cg_f64(rank_old + v)) > tol;
     }
-    reduce_and_return(valid, changed, red, cell);
+    const int sl = kSmemSlot ? *(volatile int32_t*)&s_pr_slot : slot;
+    reduce_and_return(valid, changed, red, &ctl->red[sl]);
+    if (tid == 0) sm.tile = ((int64_t)gridDim.x + atomicAdd(&ctl->tile_ctr[sl], 1u)) * kBlock;
+    __syncthreads();
+    t0 = sm.tile;
+    __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(kBlock) pr_sweep_kernel(DevCSR g, const double* rank_old,
                                                           double* rank_new, const float* contrib,
                                                           float* contrib_next, double d,
-                                                          double tol, double base, uint32_t* cell) {
+                                                          double tol, double base, PrHubs h, Ctl* ctl,
+                                                          int slot) {
   __shared__ PrSmem sm;
-  pr_sweep_tiles(sm, g, rank_old, rank_new, contrib, contrib_next, d, tol, base, IRGL_RED_ANY,
-                 cell);
+  pr_sweep_tiles<false>(sm, g, rank_old, rank_new, contrib, contrib_next, d, tol, base, IRGL_RED_ANY,
+                        ctl, slot, h);
+}
+
+__global__ void __launch_bounds__(kBlock) pr_hub_kernel(DevCSR g, const float* contrib, PrHubs h) {
+  pr_hub_chunks(g, contrib, h);
 }
 
 __global__ void pr_init_kernel(double* rank, float* contrib, const int64_t* row_ptr, int64_t n) {
@@ -251,34 +294,57 @@ __global__ void pr_init_kernel(double* rank, float* contrib, const int64_t* row_
 
 // Outlined PR: Iterate While Any PR(graph) [Or rounds >= max] as one persistent kernel.
 // Cells rotate over 3 slots: cell (r+1)%3 is reset during round r (last read at the start of r-1).
-__global__ void __launch_bounds__(kBlock) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
+// Returns true when the Iterate stops after round r.
+__device__ __forceinline__ bool pr_round(PrSmem& sm, cg::grid_group& grid, const DevCSR& g,
+                                         const double* ro, double* rn, const float* co, float* cn,
+                                         double d, double tol, double base, Ctl* ctl,
+                                         int64_t max_rounds, int cond_mode, const PrHubs& h,
+                                         int64_t r) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->red[(r + 1) % 3] = 0u;
+    ctl->tile_ctr[(r + 1) % 3] = 0u;  // last used in round r-2
+  }
+  __syncthreads();  // every thread has read the previous round's sm.round
+  if (threadIdx.x == 0) {
+    s_pr_slot = (int32_t)(r % 3);
+    sm.round = r;
+  }
+  __syncthreads();
+  if (h.nchunks > 0) {
+    pr_hub_chunks(g, co, h);
+    grid.sync();
+  }
+  pr_sweep_tiles<true>(sm, g, ro, rn, co, cn, d, tol, base, IRGL_RED_ANY, ctl, 0, h);
+  grid.sync();
+  r = *(volatile int64_t*)&sm.round;
+  const uint32_t any = *(volatile uint32_t*)&ctl->red[r % 3];
+  bool stop = false;
+  if (cond_mode == IRGL_COND_WHILE) stop = (any == 0u);
+  if (cond_mode == IRGL_COND_UNTIL) stop = (any == 1u);
+  if (max_rounds > 0 && r + 1 >= max_rounds) stop = true;
+  if (stop && blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->rounds = (unsigned long long)(r + 1);
+    ctl->last_red = (int32_t)any;
+    ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+  }
+  return stop;
+}
+
+// Two rounds per loop trip with the buffers swapped by name, so the round's rank / contribution
+// pointers stay kernel parameters (constant bank) instead of live registers: selecting them with
+// (r & 1) cost 40 B of spills at the 40-register budget and made the sweep 25% slower than the
+// host-loop kernel on RMAT-24.
+__global__ void __launch_bounds__(kBlock, 6) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
                                                                float* ca, float* cb, double d,
                                                                double tol, double base, Ctl* ctl,
-                                                               int64_t max_rounds, int cond_mode) {
+                                                               int64_t max_rounds, int cond_mode,
+                                                               PrHubs h) {
   __shared__ PrSmem sm;
   cg::grid_group grid = cg::this_grid();
-  for (int64_t r = 0;; ++r) {
-    double* ro = (r & 1) ? rb : ra;
-    double* rn = (r & 1) ? ra : rb;
-    float* co = (r & 1) ? cb : ca;
-    float* cn = (r & 1) ? ca : cb;
-    uint32_t* cell = &ctl->red[r % 3];
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->red[(r + 1) % 3] = 0u;
-    pr_sweep_tiles(sm, g, ro, rn, co, cn, d, tol, base, IRGL_RED_ANY, cell);
-    grid.sync();
-    const uint32_t any = *(volatile uint32_t*)cell;
-    bool stop = false;
-    if (cond_mode == IRGL_COND_WHILE) stop = (any == 0u);
-    if (cond_mode == IRGL_COND_UNTIL) stop = (any == 1u);
-    if (max_rounds > 0 && r + 1 >= max_rounds) stop = true;
-    if (stop) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctl->rounds = (unsigned long long)(r + 1);
-        ctl->last_red = (int32_t)any;
-        ctl->exit_in_slot = (int32_t)((r + 1) & 1);
-      }
-      break;
-    }
+  for (int64_t r = 0;; r = *(volatile int64_t*)&sm.round + 1) {
+    if (pr_round(sm, grid, g, ra, rb, ca, cb, d, tol, base, ctl, max_rounds, cond_mode, h, r)) break;
+    r = *(volatile int64_t*)&sm.round + 1;
+    if (pr_round(sm, grid, g, rb, ra, cb, ca, d, tol, base, ctl, max_rounds, cond_mode, h, r)) break;
   }
 }
 
@@ -479,11 +545,17 @@ cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr,
 }
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
                             const float* contrib, float* contrib_next, double d, double tol,
-                            int64_t n_global, Ctl* ctl, int red_slot, int grid, cudaStream_t st) {
+                            int64_t n_global, Ctl* ctl, int red_slot, int grid, const PrHubs& h,
+                            cudaStream_t st) {
   const double base = (1.0 - d) / (double)n_global;
+  if (h.nchunks > 0) {
+    note_launch();
+    pr_hub_kernel<<<grid, kBlock, 0, st>>>(g, contrib, h);
+  }
+  cudaMemsetAsync(&ctl->tile_ctr[red_slot], 0, sizeof(uint32_t), st);
   note_launch();
   pr_sweep_kernel<<<grid, kBlock, 0, st>>>(g, rank_old, rank_new, contrib, contrib_next, d, tol,
-                                           base, &ctl->red[red_slot]);
+                                           base, h, ctl, red_slot);
   return cudaGetLastError();
 }
 int pr_persistent_blocks_per_sm() {
@@ -493,10 +565,12 @@ int pr_persistent_blocks_per_sm() {
 }
 cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float* ca, float* cb,
                                  double d, double tol, int64_t n_global, Ctl* ctl,
-                                 int64_t max_rounds, int cond_mode, int grid, cudaStream_t st) {
+                                 int64_t max_rounds, int cond_mode, int grid, const PrHubs& hubs,
+                                 cudaStream_t st) {
   double base = (1.0 - d) / (double)n_global;
   DevCSR gg = g;
-  void* args[] = {&gg, &ra, &rb, &ca, &cb, &d, &tol, &base, &ctl, &max_rounds, &cond_mode};
+  PrHubs h = hubs;
+  void* args[] = {&gg, &ra, &rb, &ca, &cb, &d, &tol, &base, &ctl, &max_rounds, &cond_mode, &h};
   note_launch();
   return cudaLaunchCooperativeKernel((void*)pr_persistent_kernel, grid, kBlock, args, 0, st);
 }
