@@ -2,7 +2,7 @@
 python tools/bench_configs.py > profiles/<round>_configs.jsonl   (one JSON object per line)
 
   - BFS / SSSP on RMAT-24 (north-star 1-GPU target), 4 sources
-  - PageRank on RMAT-24 (configs[3]), tol 1e-6, <= 100 iterations, outlined
+  - PageRank on RMAT-24 (configs[3]), tol 1e-6, <= 100 iterations, outlined, both id orders
   - CC on the 4096^2 grid cut into 8 stripes (known answer: labels k*2^21) and its p=0.5
     percolation; TC on the triangulated 4096^2 grid (known answer 2*4095^2)
   - BFS on the 4096^2 grid from a corner: 8191 rounds, outlined vs host-orchestrated
@@ -53,11 +53,12 @@ def rmat_traversals(ctx, scale, nsrc=4, relabel=False):
     return g
 
 
-def pagerank(ctx, g, scale):
+def pagerank(ctx, g, scale, tag=""):
+    irgl.pagerank(ctx, g, outline=1)  # first call builds the hub chunk table
     r, st = irgl.pagerank(ctx, g, outline=1)
     it = st.rounds
     byts = (12 * g.m + 36 * g.n) * it
-    emit({"config": f"PR RMAT-{scale}", "iterations": it, "ms_total": round(st.kernel_ms, 3),
+    emit({"config": f"PR RMAT-{scale}{tag}", "iterations": it, "ms_total": round(st.kernel_ms, 3),
           "ms_per_iter": round(st.kernel_ms / it, 4), "sum_rank": float(r.sum()),
           "achieved_GBps": round(byts / (st.kernel_ms * 1e-3) / 1e9, 1),
           "roofline_frac": round(byts / (st.kernel_ms * 1e-3) / 1e9 / PEAK, 4),
@@ -67,6 +68,7 @@ def pagerank(ctx, g, scale):
 def grids(ctx):
     W = H = 4096
     g = ctx.generate_grid(W, H, cut_period=512)
+    irgl.cc(ctx, g)  # first call allocates the per-graph label state
     lab, st = irgl.cc(ctx, g)
     ok = sorted(set(lab[::4097].tolist())) == [k * 512 * W for k in range(8)] and \
         len(np.unique(lab)) == 8
@@ -75,6 +77,7 @@ def grids(ctx):
           "edges_per_s": round(g.m * st.rounds / (st.device_ms * 1e-3), 1)})
     g.close()
     g = ctx.generate_grid(W, H, perc_keep=0.5, perc_seed=5)
+    irgl.cc(ctx, g)
     lab, st = irgl.cc(ctx, g)
     emit({"config": "CC percolated grid 4096^2 p=0.5", "n": g.n, "m": g.m, "rounds": st.rounds,
           "ms": round(st.device_ms, 3), "components": int(len(np.unique(lab)))})
@@ -100,9 +103,11 @@ def grids(ctx):
 def main():
     ctx = irgl.Context()
     scale = int(os.environ.get("IRGL_CFG_SCALE", "24"))
-    rmat_traversals(ctx, scale).close()
-    g = rmat_traversals(ctx, scale, relabel=True)
+    g = rmat_traversals(ctx, scale)
     pagerank(ctx, g, scale)
+    g.close()
+    g = rmat_traversals(ctx, scale, relabel=True)
+    pagerank(ctx, g, scale, " (degree-ordered ids)")
     g.close()
     grids(ctx)
     ctx.close()
