@@ -18,12 +18,13 @@ for rl in (0, 1):
         g.relabel()
     p = ctx.pipe(g.n)
     out = []
-    for op, name in ((irgl.BFS, "BFS"), (irgl.SSSP, "SSSP")):
+    for op, name, kw in ((irgl.BFS, "BFS", {}), (irgl.BFS, "BFS-DO", {"direction": 1}),
+                         (irgl.SSSP, "SSSP", {})):
         t = []
         for rep in range(2):
             for s in srcs:
                 p.init_scalars([s])
-                st = ctx.iterate(op, g, p)
+                st = ctx.iterate(op, g, p, **kw)
                 if rep:
                     t.append(st.kernel_ms)
         out.append(f"{name} {np.mean(t):.3f} ms")

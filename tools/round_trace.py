@@ -1,5 +1,5 @@
 """Per-round trace of one outlined traversal: IRGL_ROUND_TRACE=1 python tools/round_trace.py
-[scale] [op] [defer]   (op: bfs|sssp).  The runtime prints one line per round to stderr."""
+[scale] [op] [defer]   (op: bfs|sssp; RELABEL=1: degree-ordered ids).  The runtime prints one line per round to stderr."""
 import ctypes as C, os, sys
 os.environ["IRGL_ROUND_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,6 +15,8 @@ g = ctx.generate_rmat(scale)
 rp = np.zeros(g.n + 1, dtype=np.int64)
 ctx._lib.irgl_graph_download(g.handle, rp.ctypes.data_as(C.POINTER(C.c_int64)), None, None)
 srcs = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=2)
+if os.environ.get("RELABEL") == "1":  # degree-ordered ids (API ids unchanged)
+    g.relabel()
 p = ctx.pipe(g.n)
 kw = dict(defer=defer, delta=0) if op == irgl.SSSP else {}
 for s in srcs:
