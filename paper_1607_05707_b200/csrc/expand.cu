@@ -915,6 +915,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
   uint32_t bidx = 0;
   const bool dfr = (is_sssp(OP)) && a.defer_k > 0;
   if (threadIdx.x == 0) s_dmin = dfr ? (int32_t)min(ld_ctl(&p.ctl->dmin[0]), (uint32_t)kInf) : kInf;
+  __syncthreads();  // round 0 reads s_dmin in every thread
   if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * a.trace_cap]));
   for (uint32_t r = 0;; ++r) {
     uint32_t* cin = cnt + slot3(a, r);
