@@ -921,7 +921,8 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   PipePart& pp = pipe->parts[0];
   CK(cudaSetDevice(pr.dev));
   if (pp.n_in == 0) return IRGL_OK;
-  const int bps = persistent_blocks_per_sm(op);
+  const int bps = persistent_blocks_per_sm(
+      op, (op == IRGL_OP_BFS && dir_opt) || (op == IRGL_OP_SSSP && nf.delta > 0) ? 1 : 0);
   if (bps <= 0)
     return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY",
                 "outlined kernel cannot be co-resident (SyncRunningThreads would deadlock, PAPER.md:248)");
@@ -956,7 +957,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.trace = nullptr;
   pa.trace_cap = 0;
   const char* tr = getenv("IRGL_ROUND_TRACE");
-  if (tr && *tr == '1' && !pa.dir_opt) {
+  if (tr && *tr == '1') {
     pa.trace_cap = 4096;
     CK(cudaMallocAsync(&pa.trace, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
     CK(cudaMemsetAsync(pa.trace, 0, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));

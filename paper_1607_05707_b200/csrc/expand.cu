@@ -1062,25 +1062,46 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
 // Bottom-up round at level L: every unvisited vertex scans its neighbours for a parent at level
 // L-1 and stops at the first one (Beamer et al.).  Only the owning thread writes level[v], so a
 // plain store suffices; a neighbour already set to L in this round is not a parent.
-__device__ void bu_phase(const KParams& p, int64_t n, int32_t L, unsigned long long* found,
-                         unsigned long long* found_deg, unsigned long long* scanned) {
+// Bottom-up round: every unvisited vertex scans its neighbours for a parent on level L-1, 4 at a
+// time (the 4 column loads, then the 4 level gathers, in flight together: one dependent round trip
+// per 4 candidates); the first parent in CSR order wins.  Found vertices are pushed, so the out
+// worklist is the level-L frontier if the next round runs top-down (no compaction sweep).  `sc`
+// counts the edges actually loaded.
+__device__ void bu_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, int64_t n,
+                         int32_t L, unsigned long long* found, unsigned long long* found_deg,
+                         unsigned long long* scanned) {
   unsigned long long f = 0, fd = 0, sc = 0;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += T) {
-    if (ld_label(p.lab + v) != kInf) continue;
-    const int64_t b = __ldg(p.g.row_ptr + v), e = __ldg(p.g.row_ptr + v + 1);
-    for (int64_t k = b; k < e; ++k) {
-      const int32_t u = ld_stream(p.g.col + k);
-      if (ld_label(p.lab + u) == L - 1) {
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); v0 < n; v0 += T) {
+    const int64_t v = v0 + lane_id();
+    bool hit = false;
+    // unvisited?  the visited bitmap (exact in DO-BFS) is one word per 32 lanes; else the level
+    bool open = v < n;
+    if (open) {
+      if (p.vis) open = !((ld_label(reinterpret_cast<const int32_t*>(p.vis) + (v >> 5)) >> (v & 31)) & 1);
+      else open = ld_label(p.lab + v) == kInf;
+    }
+    if (open) {
+      const int64_t b = __ldg(p.g.row_ptr + v), e = __ldg(p.g.row_ptr + v + 1);
+      for (int64_t k = b; k < e; k += 4) {
+        int32_t u[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) u[j] = k + j < e ? ld_stream(p.g.col + k + j) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) l[j] = u[j] >= 0 ? ld_label(p.lab + u[j]) : kInf;
+        sc += (unsigned long long)(e - k < 4 ? e - k : 4);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) hit |= l[j] == L - 1;
+        if (hit) break;
+      }
+      if (hit) {
         p.lab[v] = L;
         if (p.vis) atomicOr(p.vis + (v >> 5), 1u << (v & 31));  // keep the bitmap exact
         ++f;
         fd += (unsigned long long)(e - b);
-        sc += (unsigned long long)(k - b + 1);
-        break;
       }
-      if (k + 1 == e) sc += (unsigned long long)(e - b);
     }
+    wpush<IRGL_OP_BFS, false>(sm, q, p, rb, hit ? 1 : 0, (uint32_t)v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1095,24 +1116,17 @@ __device__ void bu_phase(const KParams& p, int64_t n, int32_t L, unsigned long l
   }
 }
 
-// Bottom-up -> top-down: materialise the frontier (level == L) as the out worklist.
-__device__ void bu_compact(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, int64_t n,
-                           int32_t L) {
-  const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); v0 < n; v0 += T) {
-    const int64_t v = v0 + lane_id();
-    const int kind = (v < n && ld_label(p.lab + v) == L) ? 1 : 0;
-    wpush<IRGL_OP_BFS, false>(sm, q, p, rb, kind, (uint32_t)v);
-  }
-}
-
-__global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KParams p, PersistArgs a) {
+#ifndef IRGL_DO_MINB
+#define IRGL_DO_MINB IRGL_MINB
+#endif
+__global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
   smem_init(sm);
   cg::grid_group grid = cg::this_grid();
   WarpQ q;
   uint32_t* cnt = p.ctl->cnt;
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  if (leader && a.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * a.trace_cap]));
   constexpr double kAlpha = 14.0, kBeta = 24.0;  // Beamer's switching constants
   bool bottom_up = false;
   uint32_t nbu = 0;
@@ -1164,7 +1178,13 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
       }
       mf = *(volatile unsigned long long*)&p.ctl->mf[r % 3];
     } else {
-      bu_phase(p, a.n, rb.level, &p.ctl->bu_found[r % 3], &p.ctl->mf[r % 3], &p.ctl->bu_scanned);
+      bu_phase(sm, q, p, rb, a.n, rb.level, &p.ctl->bu_found[r % 3], &p.ctl->mf[r % 3],
+               &p.ctl->bu_scanned);
+      {
+        RoundBufs cb = rb;
+        cb.mf_acc = nullptr;
+        wflush_all<IRGL_OP_BFS>(sm, q, p, cb);
+      }
       grid.sync();
       nf = *(volatile unsigned long long*)&p.ctl->bu_found[r % 3];
       mf = *(volatile unsigned long long*)&p.ctl->mf[r % 3];
@@ -1174,6 +1194,15 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
     if (leader) {
       p.ctl->popped += rb.nin;
       p.ctl->pushes += nf;
+      if (a.trace && r < a.trace_cap) {  // per-round trace (nch field = 1 for a bottom-up round)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[8 * r + 0] = t;
+        a.trace[8 * r + 1] = rb.nin | ((unsigned long long)(bottom_up ? 1 : 0) << 32);
+        a.trace[8 * r + 2] = nf;
+        a.trace[8 * r + 3] = *(volatile unsigned long long*)&p.ctl->edges +
+                             *(volatile unsigned long long*)&p.ctl->bu_scanned;
+      }
     }
     const bool done = nf == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
     if (!done) {
@@ -1182,15 +1211,8 @@ __global__ void __launch_bounds__(kBlock, IRGL_MINB) persistent_bfs_do_kernel(KP
       bool next_bu = bottom_up;
       if (!bottom_up && (double)mf > mu / kAlpha) next_bu = true;
       else if (bottom_up && (double)nf < (double)a.n / kBeta) next_bu = false;
-      if (bottom_up && !next_bu) {
-        // materialise the level-L frontier as the next round's worklist
-        RoundBufs cb = rb;
-        cb.mf_acc = nullptr;
-        bu_compact(sm, q, p, cb, a.n, rb.level);
-        wflush_all<IRGL_OP_BFS>(sm, q, p, cb);
-        grid.sync();
-        nf = ld_ctl(cout);
-      }
+      // bottom-up -> top-down: the bottom-up round pushed its finds, so the out worklist is
+      // already the level-L frontier
       bottom_up = next_bu;
     }
     nin_next = (uint32_t)nf;
@@ -1391,20 +1413,20 @@ cudaError_t launch_ctl_export(const Ctl* ctl, Ctl* host_mapped, cudaStream_t st)
   return cudaGetLastError();
 }
 
-int persistent_blocks_per_sm(int op) {
+int persistent_blocks_per_sm(int op, int variant) {
   int nb = 0;
   switch (op) {
     case IRGL_OP_BFS: {
       int nd = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_BFS>, kBlock, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nd, persistent_bfs_do_kernel, kBlock, 0);
-      nb = min(nb, nd);
+      nb = variant < 0 ? min(nb, nd) : variant ? nd : nb;
     } break;
     case IRGL_OP_SSSP: {
       int nn = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nn, persistent_kernel<kOpSsspNF>, kBlock, 0);
-      nb = min(nb, nn);
+      nb = variant < 0 ? min(nb, nn) : variant ? nn : nb;
     } break;
     case IRGL_OP_CC_LP:
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_CC_LP>, kBlock, 0);

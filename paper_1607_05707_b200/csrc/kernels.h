@@ -104,7 +104,9 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
                               const PersistArgs& pa, const ExpandCfg& ec, int grid,
                               cudaStream_t st);
 // Co-resident CTAs/SM of the persistent kernel for `op` (occupancy API).
-int persistent_blocks_per_sm(int op);
+// variant: 0 the operator's base kernel, 1 its direction-optimising (BFS) / near-far (SSSP)
+// kernel, -1 the minimum over both (a grid valid for either)
+int persistent_blocks_per_sm(int op, int variant = -1);
 int expand_blocks_per_sm(int op);
 
 // ---- topology-driven operators (topo.cu) ----------------------------------------------------
