@@ -762,12 +762,45 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
 // ---- dense-round compaction: the out worklist = the vertices marked this round (BFS: level ==
 // LEVEL; SSSP / CC: stamp == the round's code), in vertex order; coalesced sweep over the
 // partition's label (or stamp) array, pushes through the usual warp staging.
+#ifndef IRGL_COMPACT_U
+#define IRGL_COMPACT_U 1  // 1, 2, 4 within 1% on RMAT-22/24
+#endif
 template <int OP>
 __device__ void compact_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb) {
   const int64_t n = p.g.hi - p.g.lo;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   const int32_t* mark = is_bfs(OP) ? p.lab : p.stamp;
   const int32_t want = is_bfs(OP) ? rb.level : (rb.stamp_id << 1);
+  if ((p.g.lo & 3) == 0) {
+    // 4 consecutive marks per lane (one 16-byte load; 512 B per warp per step): a quarter of the
+    // dependent load steps of the 1-mark loop, which left the sweep latency-bound (~70 us for
+    // 16.7M marks)
+    const int32_t* mb = mark + p.g.lo;
+    constexpr int kU = IRGL_COMPACT_U;  // 16-byte groups per lane per step
+    for (int64_t i0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31)) * 4 * kU; i0 < n;
+         i0 += 4 * kU * T) {
+      int32_t m[kU][4];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + 128 * u + 4 * lane_id();
+        if (i + 3 < n) {
+          asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(m[u][0]), "=r"(m[u][1]), "=r"(m[u][2]), "=r"(m[u][3]) : "l"(mb + i));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) m[u][j] = i + j < n ? ld_label_cg(mb + i + j) : 0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + 128 * u + 4 * lane_id();
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          wpush<OP, false>(sm, q, p, rb, (i + j < n && m[u][j] == want) ? 1 : 0, (uint32_t)(p.g.lo + i + j));
+      }
+    }
+    return;
+  }
   for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~int64_t(31); i0 < n; i0 += T) {
     const int64_t i = i0 + lane_id();
     const uint32_t v = (uint32_t)(p.g.lo + i);
