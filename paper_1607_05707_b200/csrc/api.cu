@@ -1173,7 +1173,7 @@ static void free_pr_hubs(GraphPart& gp) {
   gp.pr_partial = nullptr;
   gp.pr_nchunks = -1;
 }
-static irgl_status_t ensure_pr_hubs(irgl_ctx* ctx, GraphPart& gp, PrHubs* out) {
+static irgl_status_t ensure_pr_hubs(irgl_ctx* ctx, GraphPart& gp, bool relabeled, PrHubs* out) {
   if (gp.pr_nchunks < 0) {
     const int64_t nloc = gp.hi - gp.lo;
     std::vector<int64_t> rp(nloc + 1);
@@ -1205,7 +1205,7 @@ static irgl_status_t ensure_pr_hubs(irgl_ctx* ctx, GraphPart& gp, PrHubs* out) {
     }
   }
   *out = PrHubs{gp.pr_hub_of, gp.pr_hfirst, gp.pr_cbeg, gp.pr_clen, gp.pr_partial,
-                std::max<int64_t>(gp.pr_nchunks, 0), kPrHubT};
+                std::max<int64_t>(gp.pr_nchunks, 0), kPrHubT, relabeled ? 1 : 0};
   return IRGL_OK;
 }
 
@@ -1241,7 +1241,7 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
     const int c = gp.pr_cur;
     PrHubs hubs;
-    irgl_status_t hs = ensure_pr_hubs(ctx, gp, &hubs);
+    irgl_status_t hs = ensure_pr_hubs(ctx, gp, g->relabeled, &hubs);
     if (hs != IRGL_OK) return hs;
     CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
                        reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, 0, gm, hubs, pr.st));
@@ -1300,7 +1300,7 @@ static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_arg
   const double tol = a && a->pr_tol > 0 ? a->pr_tol : 1e-6;
   const int c = gp.pr_cur;
   PrHubs hubs;
-  irgl_status_t hs = ensure_pr_hubs(ctx, gp, &hubs);
+  irgl_status_t hs = ensure_pr_hubs(ctx, gp, g->relabeled, &hubs);
   if (hs != IRGL_OK) return hs;
   CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
   CK(cudaMemsetAsync(gp.ctl->tile_ctr, 0, sizeof(gp.ctl->tile_ctr), pr.st));

@@ -126,6 +126,7 @@ struct PrHubs {
   double* partial;
   int64_t nchunks;  // 0: no hub split
   int64_t hub_t;
+  int32_t cta_tiles;  // sweep layout: 1 CTA tiles (degree-ordered ids), 0 warp tiles
 };
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
                             const float* contrib, float* contrib_next, double d, double tol,
