@@ -59,6 +59,8 @@ struct GraphPart {
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
   int32_t* w = nullptr;
+  uint8_t* w8 = nullptr;  // byte copy of w for the outlined SSSP (all weights in [0, 255])
+  int w8_state = 0;       // 0 unknown, 1 built, -1 weights do not fit a byte
   int32_t* lab = nullptr;     // level / dist / label [N]
   int32_t* stamp = nullptr;   // push dedupe [N]
   double* pr[4] = {nullptr, nullptr, nullptr, nullptr};  // rank a, rank b, contrib a, contrib b
@@ -101,7 +103,7 @@ struct GraphPart {
   int32_t* send_val = nullptr;
   uint32_t* recv = nullptr;
   int32_t* recv_val = nullptr;
-  DevCSR csr() const { return DevCSR{row_ptr, col, w, lo, hi}; }
+  DevCSR csr() const { return DevCSR{row_ptr, col, w, lo, hi, w8}; }
 };
 struct PipePart {
   uint32_t* buf[3] = {nullptr, nullptr, nullptr};
@@ -921,6 +923,22 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   PipePart& pp = pipe->parts[0];
   CK(cudaSetDevice(pr.dev));
   if (pp.n_in == 0) return IRGL_OK;
+  if (op == IRGL_OP_SSSP && nf.delta == 0 && gp.w && gp.w8_state == 0) {
+    // byte weight copy (once per graph; weights never change after upload / relabelling)
+    CK(cudaMalloc(&gp.w8, gp.m + 16));
+    CK(cudaMemsetAsync(gp.w8, 0, gp.m + 16, pr.st));
+    CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));
+    CK(launch_weights_u8(gp.w, gp.m, gp.w8, &gp.ctl->overflow, pr.st));
+    uint32_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, &gp.ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));  // scratch flag: leave it clear
+    CK(cudaStreamSynchronize(pr.st));
+    gp.w8_state = bad ? -1 : 1;
+    if (bad) {
+      CK(cudaFree(gp.w8));
+      gp.w8 = nullptr;
+    }
+  }
   const int bps = persistent_blocks_per_sm(
       op, (op == IRGL_OP_BFS && dir_opt) || (op == IRGL_OP_SSSP && nf.delta > 0) ? 1 : 0);
   if (bps <= 0)
@@ -1744,7 +1762,7 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
                   gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.lab_buf[1], gp.pr_hub_of, gp.pr_hfirst, gp.pr_cbeg,
                   gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
-                  gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1]};
+                  gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8};
     for (void* p : ps)
       if (p) cudaFree(p);
   }
@@ -2109,6 +2127,9 @@ irgl_status_t irgl_graph_relabel(irgl_ctx* ctx, irgl_graph* g) {
   gp.tc_src = nullptr;
   gp.tc_m = -1;
   free_pr_hubs(gp);
+  if (gp.w8) cudaFree(gp.w8);  // the weights were permuted
+  gp.w8 = nullptr;
+  gp.w8_state = 0;
   g->lab_op = -1;
   for (auto& e : g->res_copied) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   g->relabeled = true;

@@ -49,9 +49,11 @@ constexpr int kWBuf = 256;  // per-warp push staging entries
 // Internal operator variants (template-level, so the common path carries no state of the others):
 // SSSP with near-far piles, and BFS accumulating the next frontier's degrees (direction-optimising).
 constexpr int kOpSsspNF = 0x101;
+constexpr int kOpSssp8 = 0x102;  // outlined SSSP over the byte weight copy (DevCSR::w8)
 constexpr int kOpBfsDO = 0x100;
 constexpr bool is_bfs(int op) { return op == IRGL_OP_BFS || op == kOpBfsDO; }
-constexpr bool is_sssp(int op) { return op == IRGL_OP_SSSP || op == kOpSsspNF; }
+constexpr bool is_sssp(int op) { return op == IRGL_OP_SSSP || op == kOpSsspNF || op == kOpSssp8; }
+constexpr bool w8_op(int op) { return op == kOpSssp8; }
 constexpr bool has_far(int op) { return op == kOpSsspNF; }
 constexpr bool has_mf(int op) { return op == kOpBfsDO; }
 constexpr int minb_for(int op) { return is_sssp(op) ? IRGL_MINB_SSSP : IRGL_MINB; }
@@ -95,6 +97,18 @@ struct WarpQ {
   uint32_t nr = 0;            // multi-partition: staged remote pushes
   uint32_t remote = 0;        // multi-partition: remote pushes emitted (stats)
 };
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint8_t* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int32_t ld_stream_u8(const uint8_t* p) {
+  uint16_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(r) : "l"(p));
+  return (int32_t)r;
+}
+__device__ __forceinline__ int32_t w8_at(uint32_t x, int t) { return (int32_t)((x >> (8 * t)) & 255u); }
 
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
   uint32_t r;
@@ -416,6 +430,7 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
   const int64_t g1 = (e + 3) >> 2;
   for (int64_t q0 = b >> 2; q0 < g1; q0 += 32 * NG) {
     int4 cg[NG], wg[NG];
+    uint32_t w8g[NG];
     bool ag[NG];
 #pragma unroll
     for (int k = 0; k < NG; ++k) {
@@ -423,9 +438,11 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
       ag[k] = qk < g1;
       cg[k] = make_int4(0, 0, 0, 0);
       wg[k] = make_int4(0, 0, 0, 0);
+      w8g[k] = 0;
       if (ag[k]) {
         cg[k] = ld_stream_v4(col + 4 * qk);
-        if (is_sssp(OP)) wg[k] = ld_stream_v4(w + 4 * qk);
+        if (w8_op(OP)) w8g[k] = ld_stream_u32(p.g.w8 + 4 * qk);
+        else if (is_sssp(OP)) wg[k] = ld_stream_v4(w + 4 * qk);
       }
     }
     bool act[NE];
@@ -435,7 +452,8 @@ __device__ __forceinline__ void process_range(Smem& sm, WarpQ& q, const KParams&
     for (int k = 0; k < NG; ++k) {
       const int64_t e0 = 4 * (q0 + 32 * k + gl);
       const int32_t cc[4] = {cg[k].x, cg[k].y, cg[k].z, cg[k].w};
-      const int32_t ww[4] = {wg[k].x, wg[k].y, wg[k].z, wg[k].w};
+      const int32_t ww[4] = {w8_op(OP) ? w8_at(w8g[k], 0) : wg[k].x, w8_op(OP) ? w8_at(w8g[k], 1) : wg[k].y,
+                             w8_op(OP) ? w8_at(w8g[k], 2) : wg[k].z, w8_op(OP) ? w8_at(w8g[k], 3) : wg[k].w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         act[4 * k + t] = ag[k] && e0 + t >= b && e0 + t < e;
@@ -600,7 +618,8 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
       if (act[j]) {
         const int64_t ed = eo + k;
         dst[j] = (uint32_t)ld_stream(p.g.col + ed);
-        if (is_sssp(OP)) wt[j] = ld_stream(p.g.w + ed);
+        if (w8_op(OP)) wt[j] = ld_stream_u8(p.g.w8 + ed);
+        else if (is_sssp(OP)) wt[j] = ld_stream(p.g.w + ed);
       }
     }
 #pragma unroll
@@ -695,11 +714,13 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
   int32_t sv = cd.sv;
   int64_t q0 = b >> 2;
   int4 cc = make_int4(0, 0, 0, 0), ww = cc;
+  uint32_t w8c = 0;
   {
     const int64_t qk = q0 + gl;
     if (qk < ((e + 3) >> 2)) {
       cc = ld_stream_v4(col + 4 * qk);
-      if (is_sssp(OP)) ww = ld_stream_v4(wgt + 4 * qk);
+      if (w8_op(OP)) w8c = ld_stream_u32(p.g.w8 + 4 * qk);
+      else if (is_sssp(OP)) ww = ld_stream_v4(wgt + 4 * qk);
     }
   }
   for (;;) {
@@ -720,11 +741,13 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
       }
     }
     int4 ncc = make_int4(0, 0, 0, 0), nww = ncc;
+    uint32_t nw8 = 0;
     if (more) {
       const int64_t qk = nq0 + gl;
       if (qk < ((ne + 3) >> 2)) {
         ncc = ld_stream_v4(col + 4 * qk);
-        if (is_sssp(OP)) nww = ld_stream_v4(wgt + 4 * qk);
+        if (w8_op(OP)) nw8 = ld_stream_u32(p.g.w8 + 4 * qk);
+        else if (is_sssp(OP)) nww = ld_stream_v4(wgt + 4 * qk);
       }
     }
     // this iteration: 4 edges per lane
@@ -734,7 +757,8 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
     int32_t wt[4], s4[4], cur[4];
     {
       const int32_t c4[4] = {cc.x, cc.y, cc.z, cc.w};
-      const int32_t w4[4] = {ww.x, ww.y, ww.z, ww.w};
+      const int32_t w4[4] = {w8_op(OP) ? w8_at(w8c, 0) : ww.x, w8_op(OP) ? w8_at(w8c, 1) : ww.y,
+                             w8_op(OP) ? w8_at(w8c, 2) : ww.z, w8_op(OP) ? w8_at(w8c, 3) : ww.w};
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         act[t] = e0 + t >= b && e0 + t < e;
@@ -756,6 +780,7 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
     sv = nsv;
     cc = ncc;
     ww = nww;
+    w8c = nw8;
   }
 }
 
@@ -1456,9 +1481,11 @@ int persistent_blocks_per_sm(int op, int variant) {
       nb = variant < 0 ? min(nb, nd) : variant ? nd : nb;
     } break;
     case IRGL_OP_SSSP: {
-      int nn = 0;
+      int nn = 0, n8 = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nn, persistent_kernel<kOpSsspNF>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n8, persistent_kernel<kOpSssp8>, kBlock, 0);
+      nb = min(nb, n8);  // int32 or byte weights
       nb = variant < 0 ? min(nb, nn) : variant ? nn : nb;
     } break;
     case IRGL_OP_CC_LP:
@@ -1499,6 +1526,8 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
     case IRGL_OP_SSSP:
       if (a.delta > 0)
         return cudaLaunchCooperativeKernel((void*)persistent_kernel<kOpSsspNF>, grid, kBlock, args, 0, st);
+      if (g.w8)
+        return cudaLaunchCooperativeKernel((void*)persistent_kernel<kOpSssp8>, grid, kBlock, args, 0, st);
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_SSSP>, grid, kBlock, args, 0, st);
     case IRGL_OP_CC_LP:
       return cudaLaunchCooperativeKernel((void*)persistent_kernel<IRGL_OP_CC_LP>, grid, kBlock, args, 0, st);

@@ -10,6 +10,9 @@ struct DevCSR {
   const int32_t* col;      // [m_local]
   const int32_t* w;        // [m_local] or nullptr
   int64_t lo, hi;
+  // byte copy of w when every weight is in [0, 255] (the RMAT weights): the outlined SSSP reads
+  // 1 B per edge of weight stream instead of 4 (padded by 16 B); nullptr otherwise
+  const uint8_t* w8 = nullptr;
 };
 
 // Routing of pushes whose destination is owned by another partition (1D vertex partition).
@@ -107,6 +110,8 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
 // variant: 0 the operator's base kernel, 1 its direction-optimising (BFS) / near-far (SSSP)
 // kernel, -1 the minimum over both (a grid valid for either)
 int persistent_blocks_per_sm(int op, int variant = -1);
+// w8[k] = w[k] for k < m; *bad = 1 if some weight is outside [0, 255]
+cudaError_t launch_weights_u8(const int32_t* w, int64_t m, uint8_t* w8, uint32_t* bad, cudaStream_t st);
 int expand_blocks_per_sm(int op);
 
 // ---- topology-driven operators (topo.cu) ----------------------------------------------------

@@ -71,6 +71,14 @@ __global__ void cc_out_kernel(int32_t* out, const int32_t* lab, const int32_t* p
     out[v] = cmin[lab[perm[v]]];
 }
 
+__global__ void weights_u8_kernel(const int32_t* w, int64_t m, uint8_t* w8, uint32_t* bad) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = w[k];
+    if (x < 0 || x > 255) *bad = 1u;
+    w8[k] = (uint8_t)x;
+  }
+}
+
 inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 }  // namespace
@@ -170,6 +178,13 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
   *perm_out = perm;
   *inv_out = inv;
   return cudaStreamSynchronize(st);
+}
+
+cudaError_t launch_weights_u8(const int32_t* w, int64_t m, uint8_t* w8, uint32_t* bad, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  note_launch();
+  weights_u8_kernel<<<grid_for(m), 256, 0, st>>>(w, m, w8, bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_map_items(uint32_t* items, uint32_t n, const int32_t* table, cudaStream_t st) {

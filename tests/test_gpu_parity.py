@@ -273,6 +273,31 @@ def test_sssp_path_known_answer(ctx, irgl, oracle):
     assert d.tolist() == [7 * i for i in range(n)]  # App. C
 
 
+@pytest.mark.parametrize("wmax", [255, 256, 100000])
+def test_sssp_byte_weight_layout(irgl, oracle, wmax):
+    # outlined SSSP reads a byte copy of the weights when all of them fit [0, 255] and the int32
+    # array otherwise; both layouts (and the boundary 255 / 256) must give the oracle's distances,
+    # before and after degree-ordered relabelling (which rebuilds the byte copy)
+    rng = np.random.default_rng(wmax)
+    n, m = 3000, 24000
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    w = rng.integers(1, wmax + 1, m)
+    w[0] = wmax
+    og = oracle.from_edges(n, u.tolist(), v.tolist(), w=w.tolist())
+    with irgl.Context() as c:
+        g = _upload(c, og)
+        for relabel in (False, True):
+            if relabel:
+                g.relabel()
+            for s in og.sources(3):
+                s = int(s)
+                ref = oracle.sssp(og, s)
+                for outline in (1, 0):
+                    d, _ = irgl.sssp(c, g, s, outline=outline)
+                    np.testing.assert_array_equal(d, ref)
+
+
 # ---------------------------------------------------------------------------------------------
 # CC
 def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):
