@@ -663,6 +663,29 @@ static irgl_status_t near_far_split(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pip
   return IRGL_OK;
 }
 
+// Byte copy of partition l's weights (DevCSR::w8) for the SSSP kernels, built once per graph
+// (weights never change after upload; relabelling drops it); skipped when a weight exceeds 255.
+static irgl_status_t ensure_w8(irgl_ctx* ctx, irgl_graph* g, int l) {
+  GraphPart& gp = g->parts[l];
+  if (!gp.w || gp.w8_state != 0) return IRGL_OK;
+  PartRT& pr = ctx->parts[l];
+  CK(cudaSetDevice(pr.dev));
+  CK(cudaMalloc(&gp.w8, gp.m + 16));
+  CK(cudaMemsetAsync(gp.w8, 0, gp.m + 16, pr.st));
+  CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));
+  CK(launch_weights_u8(gp.w, gp.m, gp.w8, &gp.ctl->overflow, pr.st));
+  uint32_t bad = 0;
+  CK(cudaMemcpyAsync(&bad, &gp.ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));  // scratch flag: leave it clear
+  CK(cudaStreamSynchronize(pr.st));
+  gp.w8_state = bad ? -1 : 1;
+  if (bad) {
+    CK(cudaFree(gp.w8));
+    gp.w8 = nullptr;
+  }
+  return IRGL_OK;
+}
+
 static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                      int64_t level0, const irgl_iterate_opts& o, bool once,
                                      NearFar& nf, irgl_iter_stats* stt) {
@@ -671,6 +694,11 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
   const ExpandCfg ec = expand_cfg(ctx);
   int64_t level = level0;
   std::vector<uint32_t> nout(L, 0);
+  if (op == IRGL_OP_SSSP)
+    for (int l = 0; l < L; ++l) {
+      irgl_status_t ws = ensure_w8(ctx, g, l);
+      if (ws != IRGL_OK) return ws;
+    }
   for (;;) {
     uint64_t total_in = 0;
     for (int l = 0; l < L; ++l) total_in += pipe->parts[l].n_in;
@@ -757,6 +785,11 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
   const bool vals = op != IRGL_OP_BFS;
   const ExpandCfg ec = expand_cfg(ctx);
   int64_t level = level0;
+  if (op == IRGL_OP_SSSP)
+    for (int l = 0; l < L; ++l) {
+      irgl_status_t ws = ensure_w8(ctx, g, l);
+      if (ws != IRGL_OK) return ws;
+    }
   for (int l = 0; l < L; ++l) {
     PartRT& pr = ctx->parts[l];
     CK(cudaSetDevice(pr.dev));
@@ -923,21 +956,9 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   PipePart& pp = pipe->parts[0];
   CK(cudaSetDevice(pr.dev));
   if (pp.n_in == 0) return IRGL_OK;
-  if (op == IRGL_OP_SSSP && nf.delta == 0 && gp.w && gp.w8_state == 0) {
-    // byte weight copy (once per graph; weights never change after upload / relabelling)
-    CK(cudaMalloc(&gp.w8, gp.m + 16));
-    CK(cudaMemsetAsync(gp.w8, 0, gp.m + 16, pr.st));
-    CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));
-    CK(launch_weights_u8(gp.w, gp.m, gp.w8, &gp.ctl->overflow, pr.st));
-    uint32_t bad = 0;
-    CK(cudaMemcpyAsync(&bad, &gp.ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
-    CK(cudaMemsetAsync(&gp.ctl->overflow, 0, 4, pr.st));  // scratch flag: leave it clear
-    CK(cudaStreamSynchronize(pr.st));
-    gp.w8_state = bad ? -1 : 1;
-    if (bad) {
-      CK(cudaFree(gp.w8));
-      gp.w8 = nullptr;
-    }
+  if (op == IRGL_OP_SSSP && nf.delta == 0) {
+    irgl_status_t ws = ensure_w8(ctx, g, 0);
+    if (ws != IRGL_OK) return ws;
   }
   const int bps = persistent_blocks_per_sm(
       op, (op == IRGL_OP_BFS && dir_opt) || (op == IRGL_OP_SSSP && nf.delta > 0) ? 1 : 0);

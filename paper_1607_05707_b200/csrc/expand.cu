@@ -1366,6 +1366,9 @@ cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* 
       if (rb.threshold != kInf)  // near-far piles
         return dist ? round_impl<kOpSsspNF, true>(kp, rb, grid_max, st)
                     : round_impl<kOpSsspNF, false>(kp, rb, grid_max, st);
+      if (g.w8)  // byte weights
+        return dist ? round_impl<kOpSssp8, true>(kp, rb, grid_max, st)
+                    : round_impl<kOpSssp8, false>(kp, rb, grid_max, st);
       return dist ? round_impl<IRGL_OP_SSSP, true>(kp, rb, grid_max, st)
                   : round_impl<IRGL_OP_SSSP, false>(kp, rb, grid_max, st);
     case IRGL_OP_CC_LP:
