@@ -7,6 +7,8 @@ g = ctx.generate_rmat(22)
 rp = np.zeros(g.n + 1, dtype=np.int64)
 ctx._lib.irgl_graph_download(g.handle, rp.ctypes.data_as(C.POINTER(C.c_int64)), None, None)
 srcs = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=16)
+if os.environ.get("RELABEL", "1") == "1":
+    g.relabel()
 p = ctx.pipe(g.n)
 bufs = [torch.empty(g.n, dtype=torch.int32, pin_memory=True).numpy() for _ in range(2)]
 def run(mode, K=32):
@@ -24,6 +26,6 @@ def run(mode, K=32):
             ctx.read_result_into(irgl.SSSP, g, bufs[i % 2])
     ctx.results_wait(); ctx.sync()
     return (time.perf_counter() - t0) / K * 1e3, km / K
-for m in ("iter", "sync", "async", "copy", "iter", "async"):
+for m in ("iter", "sync", "async", "copy", "iter", "async", "async", "copy"):
     w, k = run(m)
     print(m, f"{w:.3f} ms/step wall, persistent kernel {k:.3f} ms", flush=True)
