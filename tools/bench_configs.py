@@ -82,6 +82,14 @@ def grids(ctx):
     emit({"config": "CC cut grid 4096^2 (8 stripes)", "n": g.n, "m": g.m, "rounds": st.rounds,
           "ms": round(st.device_ms, 3), "known_answer_ok": bool(ok),
           "edges_per_s": round(g.m * st.rounds / (st.device_ms * 1e-3), 1)})
+    # CC as data-driven label propagation: ~diameter rounds on the cut grid, the
+    # iteration-outlining showcase of configs[2]
+    for outline in (1, 0):
+        irgl.cc_lp(ctx, g, outline=outline)
+        lab2, st = irgl.cc_lp(ctx, g, outline=outline)
+        emit({"config": f"CC-LP cut grid 4096^2, outline={outline}", "rounds": st.rounds,
+              "ms": round(st.device_ms, 3), "us_per_round": round(st.device_ms * 1e3 / st.rounds, 2),
+              "same_labels_as_hooking": bool(np.array_equal(lab2, lab))})
     g.close()
     g = ctx.generate_grid(W, H, perc_keep=0.5, perc_seed=5)
     irgl.cc(ctx, g)
