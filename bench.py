@@ -350,6 +350,12 @@ def run_irgl(args, d):
         host_out = [torch.empty(g.n, dtype=torch.int32, pin_memory=True).numpy() for _ in range(2)]
     except Exception:
         host_out = [np.empty(g.n, dtype=np.int32) for _ in range(2)]
+    # untimed warm-up of the serving loop: the first asynchronous read allocates the graph's second
+    # label buffer and the copy events (a cudaMalloc inside the timed loop cost 1-100+ ms)
+    for i in range(max(2, args.warmup)):
+        step(i)
+        ctx.read_result_async(op_id, g, host_out[i % 2])
+    ctx.results_wait()
     d.barrier()
     t0 = time.perf_counter()
     for i in range(args.steps):
@@ -358,6 +364,14 @@ def run_irgl(args, d):
     ctx.results_wait()
     wall = d.reduce(time.perf_counter() - t0, "max")
     e2e = tot_e / 2 / wall / 1e9
+    # the host link's speed on this box right now: one result copy alone (the e2e copies are
+    # PCIe-bound; the same build measured 14-44 GTEPS e2e on different boxes at equal device time)
+    ctx.sync()
+    t1 = time.perf_counter()
+    for _ in range(4):
+        ctx.read_result_async(op_id, g, host_out[0])
+        ctx.results_wait()
+    d2h_gbps = 4 * 4 * int(g.n) / (time.perf_counter() - t1) / 1e9
 
     peak, peak_kind = load_peaks()
     achieved = tot_b / (kms * 1e-3) / 1e9 if kms > 0 else None
@@ -380,7 +394,7 @@ def run_irgl(args, d):
                      "algorithmic_bytes_per_step": round(tot_b / args.steps),
                      "kernel_ms_per_step": round(kms / args.steps, 4)},
         "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": 8,
-                "d2h_bytes_per_step": 4 * int(g.n)},
+                "d2h_bytes_per_step": 4 * int(g.n), "d2h_GBps_alone": round(d2h_gbps, 1)},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "detail": {"gen_s": round(gen_s, 3), "relabel_s": round(relabel_s, 3) if relabel_s else None, "rounds_per_step": float(np.mean([s.rounds for s in stats])),
