@@ -1,0 +1,28 @@
+"""Scheduler thresholds on the current kernels: python tools/sched_probe.py SCALE
+warp_t (fine-grained vs descriptor split) x chunk_edges, degree-ordered ids, 8 sources."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import bench
+import paper_1607_05707_b200 as irgl
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
+for wt, ce in ((128, 512), (64, 512), (96, 512), (192, 512), (128, 256), (128, 1024)):
+    ctx = irgl.Context(warp_threshold=wt, chunk_edges=ce, cta_threshold=max(256, wt))
+    g = ctx.generate_rmat(scale)
+    deg = np.diff(g.download()[0])
+    srcs = bench.pick_sources(g.n, lambda x: int(deg[x]), count=8)
+    g.relabel()
+    p = ctx.pipe(g.n)
+    out = []
+    for op, name in ((irgl.BFS, "BFS"), (irgl.SSSP, "SSSP")):
+        t = []
+        for rep in range(2):
+            for s in srcs:
+                p.init_scalars([s])
+                st = ctx.iterate(op, g, p)
+                if rep:
+                    t.append(st.kernel_ms)
+        out.append(f"{name} {np.mean(t):.3f} ms")
+    print(f"RMAT-{scale} warp_t={wt} chunk={ce}: " + ", ".join(out), flush=True)
+    p.close(); g.close(); ctx.close()
