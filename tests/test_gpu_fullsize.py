@@ -11,7 +11,8 @@ exactly:
          root label is the smallest id of its component (BFS-level check via the edge test
          plus the root count matching the component count of the label graph).
   PR   : ranks within the Jacobi fixed point: |rank - ((1-d)/N + d * sum contrib)| <= tol.
-Sizes: RMAT-22 (4.19M vertices, 128M directed edges), grid 4096^2 (16.8M vertices)."""
+Sizes: RMAT-22 (4.19M vertices, 128M directed edges) in generator and in degree-ordered ids,
+grid 4096^2 (16.8M vertices)."""
 import numpy as np
 import pytest
 
@@ -117,3 +118,34 @@ def test_pagerank_fixed_point_rmat22(irgl, rmat22):
     # (fp32 contrib storage adds ~1e-8 relative)
     assert np.abs(nxt - r).max() <= 2 * tol
     assert r.sum() <= 1.0 + 1e-9
+
+
+# ---- the same certificates with degree-ordered ids (irgl_graph_relabel): the bench's layout, the
+# byte-weight SSSP kernel, the direction-optimising BFS and both PR sweep layouts.  Results come
+# back in the caller's ids, so they are checked against the CSR downloaded before relabelling.
+@pytest.fixture(scope="module")
+def rmat22_relabelled(irgl):
+    c = irgl.Context()
+    g = c.generate_rmat(22)
+    rp, col, w = g.download()
+    deg = np.diff(rp)
+    src = np.repeat(np.arange(g.n, dtype=np.int64), deg)
+    g.relabel()
+    yield c, g, rp, col.astype(np.int64), w.astype(np.int64), src, deg
+    c.close()
+
+
+def test_bfs_certificate_rmat22_relabelled(irgl, rmat22_relabelled):
+    test_bfs_certificate_rmat22(irgl, rmat22_relabelled)
+
+
+def test_sssp_certificate_rmat22_relabelled(irgl, rmat22_relabelled):
+    test_sssp_certificate_rmat22(irgl, rmat22_relabelled)
+
+
+def test_cc_certificate_rmat22_relabelled(irgl, rmat22_relabelled):
+    test_cc_certificate_rmat22(irgl, rmat22_relabelled)
+
+
+def test_pagerank_fixed_point_rmat22_relabelled(irgl, rmat22_relabelled):
+    test_pagerank_fixed_point_rmat22(irgl, rmat22_relabelled)
