@@ -105,7 +105,8 @@ typedef struct irgl_config {
                                     dense: relaxations mark (fire-and-forget stores / REDs) and a
                                     compaction sweep builds the out worklist; 0 -> 16, <0 off    */
   int32_t bfs_bitmap_min_n;      /* BFS tracks visited vertices in an n-bit bitmap (L2-resident)
-                                    when n >= this: 0 -> 12M (level array > 48 MB), <0 never    */
+                                    when n >= this: 0 -> 12M (level array > 48 MB), or always
+                                    for a relabelled graph; <0 never                             */
   int32_t reserved[6];
 } irgl_config;
 

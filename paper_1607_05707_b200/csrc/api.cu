@@ -83,9 +83,10 @@ struct GraphPart {
   int lab_sel = 0;
   cudaEvent_t lab_copied[2] = {nullptr, nullptr};
   bool copy_pending[2] = {false, false};
-  // The kernels see the bitmap only when the level array would not stay L2-resident: below that
-  // the level CAS is cheaper than bitmap atomics shared by 32 vertices (RMAT-22: 87 vs 78 GTEPS;
-  // RMAT-25: 66 vs 96; RMAT-27: 34 vs 95, profiles/r1s2_bfs_bitmap.txt)
+  // The kernels see the bitmap when the level array would not stay L2-resident or the ids are
+  // degree-ordered; otherwise the level CAS is cheaper than bitmap atomics shared by 32 vertices
+  // (RMAT-22 generator ids: 0.72 vs 0.76 ms; RMAT-25: 66 vs 96 GTEPS; RMAT-27: 34 vs 95,
+  // profiles/r1s2_bfs_bitmap.txt)
   uint32_t* vis_k() const { return vis_on ? vis : nullptr; }
   bool vis_on = false;
   int64_t tc_m = -1;
@@ -283,8 +284,10 @@ static irgl_status_t ensure_lab(irgl_ctx* ctx, irgl_graph* g, bool need_stamp) {
     CK(cudaSetDevice(ctx->parts[l].dev));
     if (!gp.lab) CK(cudaMalloc(&gp.lab, std::max<int64_t>(g->n, 1) * sizeof(int32_t)));
     {
+      // default: always with degree-ordered ids (the hubs' bits share a few L1-resident lines:
+      // RMAT-22 0.753 -> 0.653 ms), else once the level array leaves L2 (>= 12M vertices)
       const int32_t c = ctx->cfg.bfs_bitmap_min_n;
-      const int64_t min_n = c == 0 ? (12ll << 20) : c;
+      const int64_t min_n = c == 0 ? (g->relabeled ? 0 : (12ll << 20)) : c;
       gp.vis_on = c >= 0 && g->n >= min_n;
     }
     if (gp.vis_on && !gp.vis) CK(cudaMalloc(&gp.vis, ((std::max<int64_t>(g->n, 1) + 31) / 32) * sizeof(uint32_t)));
