@@ -1009,7 +1009,11 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   // minima = unknown so round 0 defers nothing, barrier state, statistics)
   CK(launch_ctl_prepare(pp.ctl, pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
-  CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
+  // DO-BFS keeps the level array below 12M vertices even with degree-ordered ids (its bottom-up
+  // reads levels anyway: RMAT-22 0.193 vs 0.204 ms with the bitmap)
+  uint32_t* visk = gp.vis_k();
+  if (pa.dir_opt && ctx->cfg.bfs_bitmap_min_n == 0 && g->n < (12ll << 20)) visk = nullptr;
+  CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, visk, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   // (a kernel writing host-mapped memory instead was slower with an async readback in flight:
   // its PCIe writes queue behind the bulk copy, profiles/r1s2_e2e.txt)
