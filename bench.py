@@ -320,9 +320,15 @@ def run_irgl(args, d):
     sampler = ClockSampler(d.local_rank) if d.rank == 0 else None
     l0 = irgl.launch_count()
     ctx.event_record(0)
-    kms, tot_e, tot_b, stats = 0.0, 0.0, 0.0, []
-    for i in range(args.steps):
-        st = step(args.warmup + i)
+    kms, tot_e, tot_b = 0.0, 0.0, 0.0
+    if args.batch:  # the K steps as one irgl_traverse_batch call (no per-step Python overhead)
+        stats = ctx.traverse_batch(op_id, g, p, [cand[(args.warmup + i) % 16] for i in range(args.steps)],
+                                   **kw)
+    else:
+        stats = [step(args.warmup + i) for i in range(args.steps)]
+    ctx.event_record(1)
+    ctx.sync()
+    for i, st in enumerate(stats):
         k = (args.warmup + i) % 16
         kms += st.kernel_ms
         tot_e += er[k]
@@ -330,9 +336,6 @@ def run_irgl(args, d):
         # (SURVEY §8f F1); otherwise the fixed work-efficient formula of §8d
         e_bytes = d.reduce(st.edges, "sum") if kw else er[k]
         tot_b += algorithmic_bytes(args.op, vr[k], e_bytes)
-        stats.append(st)
-    ctx.event_record(1)
-    ctx.sync()
     dev_ms = ctx.event_elapsed(0, 1)
     launches = irgl.launch_count() - l0
     d.barrier()
@@ -358,10 +361,14 @@ def run_irgl(args, d):
     ctx.results_wait()
     d.barrier()
     t0 = time.perf_counter()
-    for i in range(args.steps):
-        step(args.warmup + i)
-        ctx.read_result_async(op_id, g, host_out[i % 2])
-    ctx.results_wait()
+    if args.batch:
+        ctx.traverse_batch(op_id, g, p, [cand[(args.warmup + i) % 16] for i in range(args.steps)],
+                           host_out, **kw)
+    else:
+        for i in range(args.steps):
+            step(args.warmup + i)
+            ctx.read_result_async(op_id, g, host_out[i % 2])
+        ctx.results_wait()
     wall = d.reduce(time.perf_counter() - t0, "max")
     e2e = tot_e / 2 / wall / 1e9
     # the host link's speed on this box right now: one result copy alone (the e2e copies are
@@ -444,6 +451,9 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="1: the K steps as one irgl_traverse_batch call; 0: one Python-level "
+                         "init/iterate/read per step")
     ap.add_argument("--relabel", type=int, default=1,
                     help="1 = degree-ordered vertex relabelling before timing (one GPU only)")
     ap.add_argument("--direction", type=int, default=0,

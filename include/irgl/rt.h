@@ -266,6 +266,16 @@ irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, v
                                      size_t bytes);
 irgl_status_t irgl_results_wait(irgl_ctx* ctx);
 
+/* A batch of single-source queries in one call (the serving loop without per-query host-language
+ * overhead): for each i < k, Initial [sources[i]] -> irgl_iterate(op, args, opts) -> stats[i]
+ * (may be NULL), and when host_out is non-NULL the node result is queued into host_out[i] with
+ * irgl_read_result_async (pointers may repeat; copies land in issue order) and the call returns
+ * after irgl_results_wait.  Same results as the k separate calls. */
+irgl_status_t irgl_traverse_batch(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
+                                  const int64_t* sources, int32_t k, const irgl_op_args* args,
+                                  const irgl_iterate_opts* opts, void* const* host_out,
+                                  size_t bytes, irgl_iter_stats* stats);
+
 /* ---- measurement --------------------------------------------------------------------------- */
 /* CUDA events on the stream of the ctx's first partition (the stream every kernel of this ctx is
  * ordered on), slots 0..7; elapsed time between two recorded slots in ms. */

@@ -2288,6 +2288,25 @@ irgl_status_t irgl_results_wait(irgl_ctx* ctx) {
   return IRGL_OK;
 }
 
+irgl_status_t irgl_traverse_batch(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
+                                  const int64_t* sources, int32_t k, const irgl_op_args* args,
+                                  const irgl_iterate_opts* opts, void* const* host_out,
+                                  size_t bytes, irgl_iter_stats* stats) {
+  if (!ctx || !pipe || !g || (k > 0 && !sources) || k < 0) return IRGL_E_INVALID;
+  for (int32_t i = 0; i < k; ++i) {
+    irgl_status_t s = irgl_pipe_init_scalars(pipe, sources + i, 1);
+    if (s != IRGL_OK) return s;
+    irgl_iter_stats local;
+    s = irgl_iterate(ctx, pipe, g, op, args, opts, stats ? stats + i : &local);
+    if (s != IRGL_OK) return s;
+    if (host_out && host_out[i]) {
+      s = irgl_read_result_async(ctx, g, op, host_out[i], bytes);
+      if (s != IRGL_OK) return s;
+    }
+  }
+  return host_out ? irgl_results_wait(ctx) : IRGL_OK;
+}
+
 // ---- measurement --------------------------------------------------------------------------------
 irgl_status_t irgl_event_record(irgl_ctx* ctx, int slot) {
   if (!ctx || slot < 0 || slot >= 8) return IRGL_E_INVALID;

@@ -115,6 +115,7 @@ EXPORTS = [
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
     "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
     "irgl_read_result_async", "irgl_results_wait", "irgl_graph_relabel", "irgl_graph_perm",
+    "irgl_traverse_batch",
 ]
 
 # every symbol include/irgl/frontend.h declares
@@ -174,6 +175,9 @@ def load_library(path: str | None = None):
         "irgl_read_result": ([P, P, C.c_int, P, C.c_size_t], i32),
         "irgl_read_result_async": ([P, P, C.c_int, P, C.c_size_t], i32),
         "irgl_results_wait": ([P], i32),
+        "irgl_traverse_batch": ([P, P, P, C.c_int, i64p, C.c_int32, C.POINTER(OpArgs),
+                                 C.POINTER(IterateOpts), C.POINTER(C.c_void_p), C.c_size_t,
+                                 C.POINTER(IterStats)], i32),
         "irgl_graph_relabel": ([P, P], i32),
         "irgl_graph_perm": ([P, i32p], i32),
         "irgl_t_control": ([C.POINTER(BlockConstraint), C.c_int, i32p], i32),
@@ -451,6 +455,25 @@ class Context:
 
     def results_wait(self):
         self._chk(self._lib.irgl_results_wait(self._h))
+
+    def traverse_batch(self, op, graph, pipe, sources, outs=None, *, outline=-1, **args):
+        """irgl_traverse_batch: one single-source Iterate per source (Initial [s]); with `outs`
+        (numpy arrays, may repeat) each node result is copied asynchronously into outs[i % len]
+        and the call returns after the copies landed.  Returns one Stats per source."""
+        src = _i64(sources)
+        k = len(src)
+        a, _keep = _op_args(**args)
+        o = IterateOpts()
+        o.cond_mode, o.reduction, o.extra_comb = COND_NONE, RED_NONE, COMB_OR
+        o.outline, o.max_rounds, o.reset = int(outline), 0, 1
+        st = (IterStats * max(k, 1))()
+        ptrs = None
+        if outs:
+            ptrs = (C.c_void_p * k)(*[outs[i % len(outs)].ctypes.data for i in range(k)])
+            nbytes = outs[0].nbytes
+        self._chk(self._lib.irgl_traverse_batch(self._h, pipe.handle, graph.handle, op, _p64(src), k,
+                                                C.byref(a), C.byref(o), ptrs, nbytes if outs else 0, st))
+        return [Stats(**st[i].as_dict()) for i in range(k)]
 
     def event_record(self, slot):
         self._chk(self._lib.irgl_event_record(self._h, slot))

@@ -298,6 +298,27 @@ def test_sssp_byte_weight_layout(irgl, oracle, wmax):
                     np.testing.assert_array_equal(d, ref)
 
 
+def test_traverse_batch_matches_single_calls(irgl, oracle):
+    # irgl_traverse_batch = k x (Initial [s] -> Iterate -> async read) in one call; results land
+    # in the (reused) host buffers in issue order, stats per source
+    og = oracle.rmat(14)
+    with irgl.Context() as c:
+        g = _upload(c, og)
+        p = c.pipe(og.n)
+        srcs = [int(s) for s in og.sources(5)]
+        for op, ref_fn in ((irgl.SSSP, oracle.sssp), (irgl.BFS, lambda gr, s: oracle.bfs(gr, s)[0])):
+            outs = [np.zeros(og.n, dtype=np.int32) for _ in range(len(srcs))]
+            stats = c.traverse_batch(op, g, p, srcs, outs)
+            assert len(stats) == len(srcs)
+            for s, o, st in zip(srcs, outs, stats):
+                np.testing.assert_array_equal(o, ref_fn(og, s))
+                assert st.rounds > 0
+            two = [np.zeros(og.n, dtype=np.int32) for _ in range(2)]  # reused buffers
+            c.traverse_batch(op, g, p, srcs, two)
+            np.testing.assert_array_equal(two[(len(srcs) - 1) % 2], ref_fn(og, srcs[-1]))
+            np.testing.assert_array_equal(two[(len(srcs) - 2) % 2], ref_fn(og, srcs[-2]))
+
+
 # ---------------------------------------------------------------------------------------------
 # CC
 def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):
