@@ -25,6 +25,11 @@ struct PartRT {  // one vertex partition hosted by this process
   Ctl* h_ctl = nullptr;            // host-mapped control-block mirror: written by a kernel (no copy
                                    // engine, so it never queues behind an async result readback)
   cudaEvent_t stage_ev = nullptr;  // last copy out of h_stage (reuse waits on it)
+  // pipelined batches (irgl_traverse_batch): two control-block snapshots and their events
+  // {iterate start, kernel start, kernel end, snapshot landed}, so traversal i+1 is queued before
+  // traversal i's results are read on the host
+  Ctl* h_snap[2] = {nullptr, nullptr};
+  cudaEvent_t bev[2][4] = {};
 };
 }  // namespace irgl
 
@@ -950,6 +955,39 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
   return IRGL_OK;
 }
 
+// Arguments of the outlined kernel for the pipe's current worklist slots (wl_graph_outlined and
+// the pipelined batch of irgl_traverse_batch).
+static void fill_persist_args(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op, int64_t level0,
+                              const irgl_iterate_opts& o, const NearFar& nf, int dir_opt,
+                              int64_t rounds_done, PersistArgs* pa) {
+  GraphPart& gp = g->parts[0];
+  PipePart& pp = pipe->parts[0];
+  pa->buf_a = pp.buf[pp.b_in];
+  pa->buf_b = pp.buf[pp.b_out];
+  pa->slot[0] = pp.c_in;
+  pa->slot[1] = pp.c_out;
+  pa->slot[2] = pp.c_spare;
+  pa->cap = (uint32_t)pipe->cap;
+  pa->chunks = gp.chunks;
+  pa->chunk_cap = gp.chunk_cap;
+  pa->level0 = (int32_t)level0;
+  pa->stamp0 = (int32_t)(g->stamp_epoch + 1);
+  pa->max_rounds = o.max_rounds > 0 ? std::max<int64_t>(o.max_rounds - rounds_done, 0) : 0;
+  pa->far_a = gp.far[0];
+  pa->far_b = gp.far[1];
+  pa->far_cap = gp.far_cap;
+  pa->delta = nf.delta;
+  pa->dir_opt = (op == IRGL_OP_BFS && dir_opt) ? 1 : 0;
+  pa->n = g->n;
+  pa->m = g->m;
+  pa->defer_k = op == IRGL_OP_SSSP ? nf.defer_k : 0;
+  // dense rounds (mark + compaction sweep) once the frontier reaches n / dense_div
+  {
+    const int32_t dd = ctx->cfg.dense_div == 0 ? 16 : ctx->cfg.dense_div;
+    pa->dense_min = (dd > 0 && nf.delta <= 0) ? std::max<int64_t>(g->n / dd, 1) : 0;
+  }
+}
+
 // ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
 static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                        int64_t level0, const irgl_iterate_opts& o,
@@ -970,30 +1008,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
                 "outlined kernel cannot be co-resident (SyncRunningThreads would deadlock, PAPER.md:248)");
   const int grid = bps * pr.sms;
   PersistArgs pa;
-  pa.buf_a = pp.buf[pp.b_in];
-  pa.buf_b = pp.buf[pp.b_out];
-  pa.slot[0] = pp.c_in;
-  pa.slot[1] = pp.c_out;
-  pa.slot[2] = pp.c_spare;
-  pa.cap = (uint32_t)pipe->cap;
-  pa.chunks = gp.chunks;
-  pa.chunk_cap = gp.chunk_cap;
-  pa.level0 = (int32_t)level0;
-  pa.stamp0 = (int32_t)(g->stamp_epoch + 1);
-  pa.max_rounds = o.max_rounds > 0 ? std::max<int64_t>(o.max_rounds - stt->rounds, 0) : 0;
-  pa.far_a = gp.far[0];
-  pa.far_b = gp.far[1];
-  pa.far_cap = gp.far_cap;
-  pa.delta = nf.delta;
-  pa.dir_opt = (op == IRGL_OP_BFS && dir_opt) ? 1 : 0;
-  pa.n = g->n;
-  pa.m = g->m;
-  pa.defer_k = op == IRGL_OP_SSSP ? nf.defer_k : 0;
-  // dense rounds (mark + compaction sweep) once the frontier reaches n / dense_div
-  {
-    const int32_t dd = ctx->cfg.dense_div == 0 ? 16 : ctx->cfg.dense_div;
-    pa.dense_min = (dd > 0 && nf.delta <= 0) ? std::max<int64_t>(g->n / dd, 1) : 0;
-  }
+  fill_persist_args(ctx, pipe, g, op, level0, o, nf, dir_opt, stt->rounds, &pa);
   // IRGL_ROUND_TRACE=1: the leader thread stamps %globaltimer, |in|, |out| and the edge counter
   // after every round (the SPEC's --trace, at round granularity); printed to stderr
   pa.trace = nullptr;
@@ -1579,6 +1594,11 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
     if (p.h_stage) cudaFreeHost(p.h_stage);
     if (p.h_ctl) cudaFreeHost(p.h_ctl);
     if (p.stage_ev) cudaEventDestroy(p.stage_ev);
+    for (int k = 0; k < 2; ++k) {
+      if (p.h_snap[k]) cudaFreeHost(p.h_snap[k]);
+      for (cudaEvent_t e : p.bev[k])
+        if (e) cudaEventDestroy(e);
+    }
   }
   delete ctx;
   return IRGL_OK;
@@ -2288,11 +2308,159 @@ irgl_status_t irgl_results_wait(irgl_ctx* ctx) {
   return IRGL_OK;
 }
 
+// Pipelined batch (one partition, outlined BFS / SSSP without near-far piles): traversal i+1 is
+// queued — worklist init, node-state reset, control-block reset, persistent launch, result copy —
+// before the host waits for traversal i's control-block snapshot, so the GPU runs the traversals
+// back to back instead of idling for a host round trip between them.  The worklist slots are reset
+// to their canonical assignment before each init (the init defines the whole pipe state), the
+// stamp epoch lives on the device for the batch (PersistArgs::stamp_base), and the host
+// bookkeeping of traversal i (stats, stamp epoch, overflow) runs while i+1 executes.
+static bool batch_pipelinable(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                              const irgl_op_args* args, const irgl_iterate_opts& o) {
+  if (ctx->ptotal() != 1 || !(op == IRGL_OP_BFS || op == IRGL_OP_SSSP)) return false;
+  const int outline = o.outline >= 0 ? o.outline : (ctx->cfg.outline < 0 ? 1 : ctx->cfg.outline);
+  if (!outline || pipe->cap >= (1ll << 30) || !o.reset || o.max_rounds > 0) return false;
+  if (op == IRGL_OP_SSSP && (args ? (args->delta < 0 ? default_delta(g) : args->delta) : 0) > 0)
+    return false;
+  const char* tr = getenv("IRGL_ROUND_TRACE");
+  if (tr && *tr == '1') return false;
+  return g->stamp_epoch < (1ll << 28);  // headroom: no stamp wrap inside the batch
+}
+
+static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                                              const int64_t* sources, int32_t k,
+                                              const irgl_op_args* args, const irgl_iterate_opts& o,
+                                              void* const* host_out, size_t bytes,
+                                              irgl_iter_stats* stats) {
+  PartRT& pr = ctx->parts[0];
+  GraphPart& gp = g->parts[0];
+  PipePart& pp = pipe->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  for (int b = 0; b < 2; ++b) {
+    if (!pr.h_snap[b]) CK(cudaHostAlloc(&pr.h_snap[b], sizeof(Ctl), cudaHostAllocDefault));
+    for (cudaEvent_t& e : pr.bev[b])
+      if (!e) CK(cudaEventCreate(&e));
+  }
+  const int64_t level = args && args->round_start > 0 ? args->round_start : 1;
+  NearFar nf;
+  if (op == IRGL_OP_SSSP) nf.defer_k = !args ? 0 : (args->defer < 0 ? default_defer(true) : args->defer);
+  const int dir_opt = args ? args->direction : 0;
+  const int bps = persistent_blocks_per_sm(op, op == IRGL_OP_BFS && dir_opt ? 1 : 0);
+  if (bps <= 0)
+    return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY",
+                "outlined kernel cannot be co-resident (SyncRunningThreads would deadlock, PAPER.md:248)");
+  const int grid = bps * pr.sms;
+  if (op == IRGL_OP_SSSP) {
+    irgl_status_t ws = ensure_w8(ctx, g, 0);
+    if (ws != IRGL_OK) return ws;
+  }
+  {  // the device copy of the stamp epoch for this batch
+    const int32_t e = (int32_t)g->stamp_epoch;
+    CK(cudaMemcpy(&gp.ctl->stamp_base, &e, sizeof(e), cudaMemcpyHostToDevice));
+  }
+  uint32_t last_rounds = 0;
+  auto finish = [&](int32_t j) -> irgl_status_t {
+    const int b = j & 1;
+    CK(cudaEventSynchronize(pr.bev[b][3]));
+    const Ctl& h = *pr.h_snap[b];
+    if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+    g->stamp_epoch += h.stamp_used;
+    last_rounds = h.rounds;
+    if (stats) {
+      irgl_iter_stats& st = stats[j];
+      st = irgl_iter_stats{};
+      st.last_reduced = -1;
+      st.rounds = (int64_t)h.rounds;
+      st.launches = 1;
+      st.popped = (int64_t)h.popped;
+      st.pushes = (int64_t)h.pushes;
+      st.edges = (int64_t)(h.bu_scanned + h.edges);
+      st.remote_updates = (int64_t)h.remote;
+      st.outlined = 1;
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pr.bev[b][1], pr.bev[b][2]));
+      st.kernel_ms = ms;
+      CK(cudaEventElapsedTime(&ms, pr.bev[b][0], pr.bev[b][3]));
+      st.device_ms = ms;
+    }
+    return IRGL_OK;
+  };
+  for (int32_t i = 0; i < k; ++i) {
+    const int b = i & 1;
+    if (g->stamp_epoch >= (1ll << 28)) {
+      // stamp ids running out (the host epoch trails the device by one traversal): drain the
+      // pipeline and let the plain path (which clears the stamps at 2^29) take the rest
+      irgl_status_t s = i > 0 ? finish(i - 1) : IRGL_OK;
+      if (s != IRGL_OK) return s;
+      for (int32_t r = i; r < k; ++r) {
+        irgl_iter_stats local;
+        if ((s = irgl_pipe_init_scalars(pipe, sources + r, 1)) != IRGL_OK) return s;
+        if ((s = irgl_iterate(ctx, pipe, g, (irgl_op)op, args, &o, stats ? stats + r : &local)) != IRGL_OK)
+          return s;
+        if (host_out && host_out[r] &&
+            (s = irgl_read_result_async(ctx, g, (irgl_op)op, host_out[r], bytes)) != IRGL_OK)
+          return s;
+      }
+      return host_out ? irgl_results_wait(ctx) : IRGL_OK;
+    }
+    // canonical slots, then Initial [source] (defines the whole worklist state)
+    pp.b_in = 0, pp.b_out = 1, pp.b_retry = 2;
+    pp.c_in = 0, pp.c_out = 1, pp.c_retry = 2, pp.c_spare = 3;
+    irgl_status_t s = irgl_pipe_init_scalars(pipe, sources + i, 1);
+    if (s != IRGL_OK) return s;
+    if ((s = map_pipe(ctx, pipe, g)) != IRGL_OK) return s;
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaEventRecord(pr.bev[b][0], pr.st));
+    if ((s = op_reset(ctx, g, op, pipe)) != IRGL_OK) return s;
+    if ((s = pipe_counters(ctx, pipe, nullptr)) != IRGL_OK) return s;
+    if (nf.defer_k > 0) CK(cudaMemsetAsync(pp.ctl->dmin, 0xff, sizeof(pp.ctl->dmin), pr.st));
+    PersistArgs pa;
+    fill_persist_args(ctx, pipe, g, op, level, o, nf, dir_opt, 0, &pa);
+    pa.trace = nullptr;
+    pa.trace_cap = 0;
+    pa.stamp_base = &gp.ctl->stamp_base;
+    uint32_t* visk = gp.vis_k();
+    if (pa.dir_opt && ctx->cfg.bfs_bitmap_min_n == 0 && g->n < (12ll << 20)) visk = nullptr;
+    CK(launch_ctl_prepare(pp.ctl, pr.st));
+    CK(cudaEventRecord(pr.bev[b][1], pr.st));
+    CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, visk, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
+    CK(cudaEventRecord(pr.bev[b][2], pr.st));
+    CK(cudaMemcpyAsync(pr.h_snap[b], pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaEventRecord(pr.bev[b][3], pr.st));
+    if (host_out && host_out[i] && (s = irgl_read_result_async(ctx, g, (irgl_op)op, host_out[i], bytes)) != IRGL_OK)
+      return s;
+    if (i > 0 && (s = finish(i - 1)) != IRGL_OK) return s;
+  }
+  if (k > 0) {
+    irgl_status_t s = finish(k - 1);
+    if (s != IRGL_OK) return s;
+    // host view of the pipe after the last traversal (as wl_graph_outlined leaves it)
+    const int64_t K = last_rounds;
+    const int slots[3] = {pp.c_in, pp.c_out, pp.c_spare};
+    if (K & 1) std::swap(pp.b_in, pp.b_out);
+    pp.c_in = slots[K % 3];
+    pp.c_out = slots[(K + 1) % 3];
+    pp.c_spare = slots[(K + 2) % 3];
+    pp.n_in = pr.h_snap[(k - 1) & 1]->cnt[pp.c_in];
+  }
+  return host_out ? irgl_results_wait(ctx) : IRGL_OK;
+}
+
 irgl_status_t irgl_traverse_batch(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op op,
                                   const int64_t* sources, int32_t k, const irgl_op_args* args,
                                   const irgl_iterate_opts* opts, void* const* host_out,
                                   size_t bytes, irgl_iter_stats* stats) {
   if (!ctx || !pipe || !g || (k > 0 && !sources) || k < 0) return IRGL_E_INVALID;
+  {
+    irgl_status_t s = check_call(ctx, pipe, g, op);
+    if (s != IRGL_OK) return s;
+    irgl_iterate_opts o{};
+    o.outline = -1;
+    o.reset = 1;
+    if (opts) o = *opts;
+    if (o.cond_mode == IRGL_COND_NONE && batch_pipelinable(ctx, pipe, g, op, args, o))
+      return traverse_batch_pipelined(ctx, pipe, g, op, sources, k, args, o, host_out, bytes, stats);
+  }
   for (int32_t i = 0; i < k; ++i) {
     irgl_status_t s = irgl_pipe_init_scalars(pipe, sources + i, 1);
     if (s != IRGL_OK) return s;

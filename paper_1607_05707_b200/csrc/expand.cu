@@ -962,7 +962,8 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
   uint32_t* cnt = p.ctl->cnt;
   const bool nf = has_far(OP) && a.delta > 0;
   int32_t threshold = nf ? a.delta : kInf;
-  int32_t sid = a.stamp0;       // unique stamp ids: rounds and splits
+  const int32_t s0 = a.stamp_base ? *(volatile int32_t*)a.stamp_base + 1 : a.stamp0;
+  int32_t sid = s0;             // unique stamp ids: rounds and splits
   uint32_t fsel = 0;            // which far buffer is current
   uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
@@ -1108,7 +1109,8 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
       if (leader) {
         p.ctl->rounds = r + 1;
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
-        p.ctl->stamp_used = (uint32_t)(sid - a.stamp0);
+        p.ctl->stamp_used = (uint32_t)(sid - s0);
+        if (a.stamp_base) *a.stamp_base = sid - 1;  // every thread read it before the 1st barrier
         p.ctl->far_sel = fsel;
       }
       break;
@@ -1189,6 +1191,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
   bool bottom_up = false;
   uint32_t nbu = 0;
   unsigned long long explored = 0;               // edges of vertices already discovered
+  const int32_t s0 = a.stamp_base ? *(volatile int32_t*)a.stamp_base + 1 : a.stamp0;
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));
   for (uint32_t r = 0;; ++r) {
     uint32_t* cout = cnt + slot3(a, r + 1);
@@ -1211,7 +1214,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
     rb.chunk_cap = a.chunk_cap;
     rb.tile_ctr = &p.ctl->tile_ctr[r % 3];
     rb.level = a.level0 + (int32_t)r;
-    rb.stamp_id = a.stamp0 + (int32_t)r;
+    rb.stamp_id = s0 + (int32_t)r;
     rb.far = nullptr;
     rb.far_cnt = nullptr;
     rb.far_cap = 0;
@@ -1279,6 +1282,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
         p.ctl->rounds = r + 1;
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
         p.ctl->stamp_used = r + 1;
+        if (a.stamp_base) *a.stamp_base = s0 + (int32_t)r;
         p.ctl->bu_rounds = nbu;
       }
       break;

@@ -52,6 +52,7 @@ struct Ctl {
   uint32_t minkeep[2];         // min dist kept in the far pile by a split (double-buffered: the
                                // persistent kernel resets one slot while CTAs may still read the other)
   uint32_t stamp_used;         // persistent: stamp ids consumed (rounds + splits)
+  int32_t stamp_base;          // graph part: last stamp id used (pipelined batches, PersistArgs)
   uint32_t far_sel;            // persistent: current far pile at exit
   uint32_t bu_rounds;          // direction-optimising BFS: bottom-up rounds executed
   alignas(256) unsigned long long mf[3];    // DO-BFS: edges of the next frontier (rotated by round)

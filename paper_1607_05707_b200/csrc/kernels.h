@@ -101,6 +101,10 @@ struct PersistArgs {
   int64_t dense_min;   // rounds with |in| >= dense_min run dense (0 = never)
   unsigned long long* trace;  // optional per-round trace [4 * trace_cap + 1] (IRGL_ROUND_TRACE)
   uint32_t trace_cap;
+  // device-resident stamp epoch (pipelined batches): when set, the kernel takes its first stamp
+  // id from *stamp_base + 1 instead of stamp0 and leaves its last used id there, so a traversal
+  // can be launched before the previous one's stamp count reached the host
+  int32_t* stamp_base = nullptr;
 };
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,

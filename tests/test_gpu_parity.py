@@ -298,25 +298,37 @@ def test_sssp_byte_weight_layout(irgl, oracle, wmax):
                     np.testing.assert_array_equal(d, ref)
 
 
-def test_traverse_batch_matches_single_calls(irgl, oracle):
-    # irgl_traverse_batch = k x (Initial [s] -> Iterate -> async read) in one call; results land
-    # in the (reused) host buffers in issue order, stats per source
+@pytest.mark.parametrize("relabel", [False, True])
+def test_traverse_batch_matches_single_calls(irgl, oracle, relabel):
+    # irgl_traverse_batch = k x (Initial [s] -> Iterate -> async read) in one call (pipelined:
+    # traversal i+1 is queued before traversal i's stats reach the host); results land in the
+    # (reused) host buffers in issue order, and the stats equal those of separate iterate calls
     og = oracle.rmat(14)
     with irgl.Context() as c:
         g = _upload(c, og)
+        if relabel:
+            g.relabel()
         p = c.pipe(og.n)
         srcs = [int(s) for s in og.sources(5)]
-        for op, ref_fn in ((irgl.SSSP, oracle.sssp), (irgl.BFS, lambda gr, s: oracle.bfs(gr, s)[0])):
+        cases = ((irgl.SSSP, {}, oracle.sssp), (irgl.BFS, {}, lambda gr, s: oracle.bfs(gr, s)[0]),
+                 (irgl.BFS, {"direction": 1}, lambda gr, s: oracle.bfs(gr, s)[0]))
+        for op, kw, ref_fn in cases:
             outs = [np.zeros(og.n, dtype=np.int32) for _ in range(len(srcs))]
-            stats = c.traverse_batch(op, g, p, srcs, outs)
+            stats = c.traverse_batch(op, g, p, srcs, outs, **kw)
             assert len(stats) == len(srcs)
             for s, o, st in zip(srcs, outs, stats):
                 np.testing.assert_array_equal(o, ref_fn(og, s))
-                assert st.rounds > 0
+                p.init_scalars([s])
+                one = c.iterate(op, g, p, **kw)
+                assert (st.rounds, st.edges, st.pushes, st.popped) == (one.rounds, one.edges, one.pushes, one.popped)
+                np.testing.assert_array_equal(c.read_result(op, g), o)
             two = [np.zeros(og.n, dtype=np.int32) for _ in range(2)]  # reused buffers
-            c.traverse_batch(op, g, p, srcs, two)
+            c.traverse_batch(op, g, p, srcs, two, **kw)
             np.testing.assert_array_equal(two[(len(srcs) - 1) % 2], ref_fn(og, srcs[-1]))
             np.testing.assert_array_equal(two[(len(srcs) - 2) % 2], ref_fn(og, srcs[-2]))
+            # no host buffers: node state of the last traversal stays readable
+            c.traverse_batch(op, g, p, srcs[:3], None, **kw)
+            np.testing.assert_array_equal(c.read_result(op, g), ref_fn(og, srcs[2]))
 
 
 # ---------------------------------------------------------------------------------------------
