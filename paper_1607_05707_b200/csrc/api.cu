@@ -493,13 +493,12 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
     PipePart& pp = pipe->parts[l];
     CK(cudaSetDevice(pr.dev));
     const int q = ctx->gpart(l);
-    for (int p = 0; p < P; ++p) {
-      if (p == q) continue;
-      const uint32_t c = cnt[(size_t)p * P + q];
-      if (!c) continue;
-      CK(launch_apply_remote(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv + (int64_t)p * ps,
-                             vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
-    }
+    ApplySegs sg{};
+    sg.P = P;
+    sg.stride = ps;
+    for (int p = 0; p < P; ++p) sg.off[p + 1] = sg.off[p] + (p == q ? 0u : cnt[(size_t)p * P + q]);
+    CK(launch_apply_remote_segs(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv,
+                                vals ? gp.recv_val : nullptr, sg, rbs[l], pr.st));
     CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
   }
   return IRGL_OK;
@@ -926,13 +925,12 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
       const int q = ctx->gpart(l);
-      for (int p = 0; p < P; ++p) {
-        if (p == q) continue;
-        const uint32_t c = count(p, q);
-        if (!c) continue;
-        CK(launch_apply_remote(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv + (int64_t)p * ps,
-                               vals ? gp.recv_val + (int64_t)p * ps : nullptr, c, rbs[l], pr.st));
-      }
+      ApplySegs sg{};  // every peer's segment in one launch
+      sg.P = P;
+      sg.stride = ps;
+      for (int p = 0; p < P; ++p) sg.off[p + 1] = sg.off[p] + (p == q ? 0u : count(p, q));
+      CK(launch_apply_remote_segs(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv,
+                                  vals ? gp.recv_val : nullptr, sg, rbs[l], pr.st));
       CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
       // 4. swap in/out; the new out counter is cleared in stream order
       std::swap(pp.b_in, pp.b_out);

@@ -1291,21 +1291,26 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
 }
 
 // ---- owner-side application of remote updates (E5 min-reduce) ---------------------------------
+// Owner-side apply of every peer's segment in one launch (ApplySegs): global index i belongs to
+// segment p with off[p] <= i < off[p+1].
 template <int OP>
-__global__ void __launch_bounds__(kBlock) apply_remote_kernel(KParams p, RoundBufs rb,
-                                                           const uint32_t* items,
-                                                           const int32_t* values, uint32_t n) {
+__global__ void __launch_bounds__(kBlock) apply_segs_kernel(KParams p, RoundBufs rb, const uint32_t* items,
+                                                          const int32_t* values, ApplySegs sg) {
   __shared__ Smem sm;
   smem_init(sm);
   WarpQ q;
+  const uint32_t n = sg.off[sg.P];
   for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < n; i0 += gridDim.x * kBlock) {
     const uint32_t i = i0 + lane_id();
     int kind = 0;
     uint32_t v = 0;
     if (i < n) {
-      v = items[i];
+      int s = 0;
+      while (s + 1 < sg.P && sg.off[s + 1] <= i) ++s;
+      const int64_t at = (int64_t)s * sg.stride + (i - sg.off[s]);
+      v = items[at];
       const int32_t cur = gather_cur<OP>(p, v);
-      kind = relax_with<OP>(p, rb, q, cur, is_bfs(OP) ? 0 : values[i], 0, v);
+      kind = relax_with<OP>(p, rb, q, cur, is_bfs(OP) ? 0 : values[at], 0, v);
     }
     wpush<OP, false>(sm, q, p, rb, kind, v);
   }
@@ -1391,9 +1396,10 @@ cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl*
   return cudaGetLastError();
 }
 
-cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl, const uint32_t* items,
-                                const int32_t* values, uint32_t n, const RoundBufs& rb,
-                                cudaStream_t st) {
+cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
+                                     const uint32_t* items, const int32_t* values,
+                                     const ApplySegs& segs, const RoundBufs& rb, cudaStream_t st) {
+  const uint32_t n = segs.off[segs.P];
   if (n == 0) return cudaSuccess;
   const int grid = (int)min((n + kBlock - 1) / kBlock, 148u * 8u);
   KParams kp{DevCSR{nullptr, nullptr, nullptr, 0, 0}, lab, stamp, vis, ctl,
@@ -1401,16 +1407,16 @@ cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, uint32_t* 
   note_launch();
   switch (op) {
     case IRGL_OP_BFS:
-      apply_remote_kernel<IRGL_OP_BFS><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+      apply_segs_kernel<IRGL_OP_BFS><<<grid, kBlock, 0, st>>>(kp, rb, items, values, segs);
       break;
     case IRGL_OP_SSSP:
       if (rb.threshold != kInf)
-        apply_remote_kernel<kOpSsspNF><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+        apply_segs_kernel<kOpSsspNF><<<grid, kBlock, 0, st>>>(kp, rb, items, values, segs);
       else
-        apply_remote_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+        apply_segs_kernel<IRGL_OP_SSSP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, segs);
       break;
     case IRGL_OP_CC_LP:
-      apply_remote_kernel<IRGL_OP_CC_LP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, n);
+      apply_segs_kernel<IRGL_OP_CC_LP><<<grid, kBlock, 0, st>>>(kp, rb, items, values, segs);
       break;
     default:
       return cudaErrorInvalidValue;

@@ -62,10 +62,17 @@ struct RoundBufs {
 cudaError_t launch_expand_round(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                 const RoundBufs& rb, const DistRoute& dr, const ExpandCfg& ec,
                                 int grid_max, cudaStream_t st);
-// Apply received remote updates (owner side min-reduce): items[i] with values[i] (BFS: level).
-cudaError_t launch_apply_remote(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl, const uint32_t* items,
-                                const int32_t* values, uint32_t n, const RoundBufs& rb,
-                                cudaStream_t st);
+// Apply received remote updates (owner side min-reduce), all of one owner's received segments in
+// one launch: segment p (peer p's updates) holds counts[p] items at items + p * stride, values
+// likewise (BFS: none); P <= 16.
+struct ApplySegs {
+  uint32_t off[17];  // off[p] = first global index of segment p, off[P] = total
+  int P;
+  int64_t stride;
+};
+cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
+                                     const uint32_t* items, const int32_t* values,
+                                     const ApplySegs& segs, const RoundBufs& rb, cudaStream_t st);
 // Near-far split of a far pile into rb.out (dist < rb.threshold) / rb.far (the next pile).
 cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl* ctl,
                              const RoundBufs& rb, const uint32_t* far_in, const uint32_t* nfar_ptr,
