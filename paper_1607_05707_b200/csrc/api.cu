@@ -2,6 +2,7 @@
 // constructs Invoke / Iterate / Pipe with the in/out/retry swap protocol (PAPER.md:358-381,
 // SPEC.md:359-381, :459-467) over the device kernels of expand.cu / topo.cu / testops.cu.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstring>
 #include <memory>
@@ -807,6 +808,13 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     CK(cudaMalloc(&ctx->hdr_all, (size_t)(L + P) * H * 4));
   }
   std::vector<uint32_t> hdr((size_t)P * H, 0);
+  // IRGL_DIST_TRACE=1: host-side phase times per round (us) to stderr
+  const char* dtr = getenv("IRGL_DIST_TRACE");
+  const bool dtrace = dtr && *dtr == '1';
+  auto now_us = []() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  double t_a = 0, t_b = 0, t_c = 0, t_d = 0;
   for (;;) {
     if (o.max_rounds > 0 && stt->rounds >= o.max_rounds) break;  // ExtraCond (Or)
     const int32_t stamp_id = (int32_t)(++g->stamp_epoch);
@@ -826,10 +834,10 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
       if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
-      CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow, pr.st));
-      CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(uint32_t), pr.st));
-      CK(cudaMemsetAsync(pp.ctl->tile_ctr, 0, sizeof(uint32_t), pr.st));
+      CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow,
+                             pp.ctl->chunk_cnt, pp.ctl->tile_ctr, pr.st));
     }
+    if (dtrace) t_a = now_us();
     // 2. gather the headers: the round's one host synchronisation
     if (ctx->comm) {
       PartRT& pr = ctx->parts[0];
@@ -863,6 +871,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
       stt->kernel_ms += kms;
     }
+    if (dtrace) t_b = now_us();
     uint64_t total_in = 0, local_in = 0;
     for (int p = 0; p < P; ++p) {
       total_in += hdr[(size_t)p * H + P];
@@ -872,6 +881,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     if (stt->rounds > 0) stt->pushes += (int64_t)local_in;  // last round's out = this round's in
     if (total_in == 0) break;  // every in worklist was empty: Iterate ends (no sends queued)
     stt->popped += (int64_t)local_in;
+    if (dtrace) t_c = now_us();
     // 3. payloads: grouped send/recv (NCCL) or peer copies (one process), then owner-side applies
     auto count = [&](int p, int q) { return hdr[(size_t)p * H + q]; };
     if (ctx->comm) {
@@ -929,13 +939,23 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       sg.P = P;
       sg.stride = ps;
       for (int p = 0; p < P; ++p) sg.off[p + 1] = sg.off[p] + (p == q ? 0u : count(p, q));
+      // 4. swap in/out: the launch also clears the send counts and the consumed in-count (the new
+      // out counter) in stream order
+      sg.zero_send = gp.send_cnt;
+      sg.zero_cnt = &pp.ctl->cnt[pp.c_in];
       CK(launch_apply_remote_segs(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv,
                                   vals ? gp.recv_val : nullptr, sg, rbs[l], pr.st));
-      CK(cudaMemsetAsync(gp.send_cnt, 0, P * 4, pr.st));
-      // 4. swap in/out; the new out counter is cleared in stream order
       std::swap(pp.b_in, pp.b_out);
       std::swap(pp.c_in, pp.c_out);
-      CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_out], 0, 4, pr.st));
+    }
+    if (dtrace) {
+      t_d = now_us();
+      static double t_prev = 0;
+      // enqueue: host time to issue the round's expansion (from the previous round's end);
+      // hdr_wait: header gather incl. waiting for the expansion; send_apply: payload exchange
+      fprintf(stderr, "irgl-dist round=%lld enqueue=%.1f hdr_wait=%.1f counts=%.1f send_apply=%.1f us\n",
+              (long long)stt->rounds, t_a - (t_prev ? t_prev : t_a), t_b - t_a, t_c - t_b, t_d - t_c);
+      t_prev = t_d;
     }
     stt->rounds++;
     nf.dsel ^= 1;

@@ -1299,6 +1299,10 @@ __global__ void __launch_bounds__(kBlock) apply_segs_kernel(KParams p, RoundBufs
   __shared__ Smem sm;
   smem_init(sm);
   WarpQ q;
+  if (blockIdx.x == 0) {
+    if (sg.zero_send && (int)threadIdx.x < sg.P) sg.zero_send[threadIdx.x] = 0u;
+    if (sg.zero_cnt && threadIdx.x == 0) *sg.zero_cnt = 0u;
+  }
   const uint32_t n = sg.off[sg.P];
   for (uint32_t i0 = blockIdx.x * kBlock + (threadIdx.x & ~31u); i0 < n; i0 += gridDim.x * kBlock) {
     const uint32_t i = i0 + lane_id();
@@ -1328,13 +1332,18 @@ __global__ void pack_all_kernel(const int32_t* lab, const uint32_t* send, int32_
   }
 }
 // Round header of one partition: {send counts [P], in-count, overflow flag}.
+// It also clears the round's chunk / tile counters (their users, the expansion launches, precede
+// it in stream order) so the next round needs no separate memsets.
 __global__ void round_header_kernel(uint32_t* hdr, const uint32_t* send_cnt, int P,
-                                    const uint32_t* in_cnt, const uint32_t* overflow) {
+                                    const uint32_t* in_cnt, const uint32_t* overflow,
+                                    uint32_t* chunk_cnt, uint32_t* tile_ctr) {
   const int t = threadIdx.x;
   if (t < P) hdr[t] = send_cnt ? ld_ctl(send_cnt + t) : 0u;
   if (t == 0) {
     hdr[P] = ld_ctl(in_cnt);
     hdr[P + 1] = ld_ctl(overflow);
+    if (chunk_cnt) *chunk_cnt = 0u;
+    if (tile_ctr) *tile_ctr = 0u;
   }
 }
 
@@ -1400,8 +1409,8 @@ cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint3
                                      const uint32_t* items, const int32_t* values,
                                      const ApplySegs& segs, const RoundBufs& rb, cudaStream_t st) {
   const uint32_t n = segs.off[segs.P];
-  if (n == 0) return cudaSuccess;
-  const int grid = (int)min((n + kBlock - 1) / kBlock, 148u * 8u);
+  if (n == 0 && !segs.zero_send && !segs.zero_cnt) return cudaSuccess;
+  const int grid = (int)max(1u, min((n + kBlock - 1) / kBlock, 148u * 8u));
   KParams kp{DevCSR{nullptr, nullptr, nullptr, 0, 0}, lab, stamp, vis, ctl,
              DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{32, 1024, 2048}};
   note_launch();
@@ -1432,9 +1441,10 @@ cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* s
 }
 
 cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
-                                const uint32_t* overflow, cudaStream_t st) {
+                                const uint32_t* overflow, uint32_t* chunk_cnt, uint32_t* tile_ctr,
+                                cudaStream_t st) {
   note_launch();
-  round_header_kernel<<<1, 32, 0, st>>>(hdr, send_cnt, P, in_cnt, overflow);
+  round_header_kernel<<<1, 32, 0, st>>>(hdr, send_cnt, P, in_cnt, overflow, chunk_cnt, tile_ctr);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,10 @@ struct ApplySegs {
   uint32_t off[17];  // off[p] = first global index of segment p, off[P] = total
   int P;
   int64_t stride;
+  // cleared by the launch (always issued, also with nothing to apply): the round's send counts
+  // [P] and the consumed in-count — the next round's out counter after the swap
+  uint32_t* zero_send = nullptr;
+  uint32_t* zero_cnt = nullptr;
 };
 cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                      const uint32_t* items, const int32_t* values,
@@ -82,7 +86,8 @@ cudaError_t launch_far_split(const DevCSR& g, int32_t* lab, int32_t* stamp, Ctl*
 cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* send_val,
                             const uint32_t* send_cnt, int P, int me, int64_t ps, cudaStream_t st);
 cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
-                                const uint32_t* overflow, cudaStream_t st);
+                                const uint32_t* overflow, uint32_t* chunk_cnt, uint32_t* tile_ctr,
+                                cudaStream_t st);
 // Gather current label values of the send buckets (SSSP / CC_LP pack step).
 cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
                                uint32_t n, cudaStream_t st);
