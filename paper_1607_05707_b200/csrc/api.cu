@@ -149,6 +149,7 @@ struct irgl_pipe {
   int64_t cap = 0;
   std::vector<irgl::PipePart> parts;
   const irgl_graph* mapped_for = nullptr;  // relabelled graph whose ids the items now carry
+  int64_t id_bound = 0;  // every item id is < id_bound (host inits: max + 1; after a graph op: n)
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -254,9 +255,11 @@ static irgl_status_t pipe_init_items(irgl_pipe* p, const int64_t* items, int64_t
   if (count < 0 || (count > 0 && !items)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "bad init array");
   const int L = (int)ctx->parts.size();
   std::vector<std::vector<uint32_t>> per(L);
+  p->id_bound = 0;
   for (int64_t i = 0; i < count; ++i) {
     if (items[i] < 0 || items[i] > 0xffffffffll)
       return fail(ctx, IRGL_E_INVALID, "E_INVALID", "work item id out of uint32 range (App. B5)");
+    p->id_bound = std::max(p->id_bound, items[i] + 1);
     // one partition: no routing.  P > 1: the owner of vertex id x is x / part_size.
     const bool route = ctx->ptotal() > 1 && ctx->route_size != INT64_MAX;
     const int64_t owner = route ? items[i] / ctx->route_size : 0;
@@ -1889,6 +1892,7 @@ irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end) {
     CK(cudaSetDevice(pr.dev));
     CK(launch_iota_u32(pp.buf[pp.b_in], (uint32_t)b, (uint32_t)(e - b), pr.st));
     p->mapped_for = nullptr;
+    p->id_bound = end;
     uint32_t zeros[4] = {0, 0, 0, 0};
     zeros[pp.c_in] = (uint32_t)(e - b);
     CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
@@ -1971,6 +1975,10 @@ static irgl_status_t check_call(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, i
   if (!is_test_op(op) && !g) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "graph operator needs a graph");
   if (op == IRGL_OP_SSSP && g && !g->has_w)
     return fail(ctx, IRGL_E_USAGE, "E_USAGE", "SSSP needs edge weights");
+  if (pipe && g && is_wl_graph_op(op) && pipe->id_bound > g->n)
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID",
+                "work item id >= the graph's vertex count (Value arrays are bounds-checked, SPEC.md:421)");
+  if (pipe && g && is_wl_graph_op(op)) pipe->id_bound = g->n;  // the op pushes ids < n only
   return IRGL_OK;
 }
 
@@ -2476,6 +2484,10 @@ irgl_status_t irgl_traverse_batch(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g,
     o.outline = -1;
     o.reset = 1;
     if (opts) o = *opts;
+    for (int32_t i = 0; i < k; ++i)
+      if (sources[i] < 0 || sources[i] >= g->n)
+        return fail(ctx, IRGL_E_INVALID, "E_INVALID",
+                    "source id >= the graph's vertex count (Value arrays are bounds-checked, SPEC.md:421)");
     if (o.cond_mode == IRGL_COND_NONE && batch_pipelinable(ctx, pipe, g, op, args, o))
       return traverse_batch_pipelined(ctx, pipe, g, op, sources, k, args, o, host_out, bytes, stats);
   }

@@ -331,6 +331,28 @@ def test_traverse_batch_matches_single_calls(irgl, oracle, relabel):
             np.testing.assert_array_equal(c.read_result(op, g), ref_fn(og, srcs[2]))
 
 
+def test_traverse_batch_edge_cases(irgl, oracle):
+    og = oracle.rmat(10)
+    with irgl.Context() as c:
+        g = _upload(c, og)
+        p = c.pipe(og.n)
+        assert c.traverse_batch(irgl.SSSP, g, p, []) == []          # k = 0: nothing to do
+        s = int(og.sources(1)[0])
+        # a host-orchestrated batch (outline=0) takes the plain per-query path, same results
+        out = [np.zeros(og.n, dtype=np.int32)]
+        st = c.traverse_batch(irgl.SSSP, g, p, [s], out, outline=0)
+        np.testing.assert_array_equal(out[0], oracle.sssp(og, s))
+        assert st[0].outlined == 0
+        with pytest.raises(Exception):                               # out-of-range source
+            c.traverse_batch(irgl.BFS, g, p, [og.n + 5], None)
+        p.init_scalars([og.n])                                       # item id == n: rejected
+        with pytest.raises(Exception):
+            c.iterate(irgl.BFS, g, p)
+        # the context stays usable after the error
+        lv, _ = irgl.bfs(c, g, s)
+        np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
+
+
 # ---------------------------------------------------------------------------------------------
 # CC
 def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):
