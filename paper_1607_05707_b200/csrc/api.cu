@@ -1637,6 +1637,9 @@ irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const i
     if (row_ptr[i + 1] < row_ptr[i]) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "row_ptr not monotone");
   for (int64_t e = 0; e < m; ++e)
     if (col[e] < 0 || col[e] >= n) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "column id out of range");
+  if (weight)  // a negative weight on a symmetric graph is a negative cycle: SSSP would not end
+    for (int64_t e = 0; e < m; ++e)
+      if (weight[e] < 0) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "negative edge weight");
   auto g = std::make_unique<irgl_graph>();
   g->ctx = ctx;
   g->n = n;
@@ -1747,6 +1750,11 @@ irgl_status_t irgl_graph_read_edgelist(irgl_ctx* ctx, const char* path, int symm
       std::fclose(f);
       return fail(ctx, IRGL_E_INVALID, "E_INVALID",
                   "bad edge at line " + std::to_string(lineno) + " (ids must be in [0, N))");
+    }
+    if (c < 0 || c > 0x7fffffffll) {
+      std::fclose(f);
+      return fail(ctx, IRGL_E_INVALID, "E_INVALID",
+                  "bad weight at line " + std::to_string(lineno) + " (must be in [0, 2^31))");
     }
     if (a == b) continue;
     edges.push_back({(uint32_t)a, (uint32_t)b, (int32_t)c});

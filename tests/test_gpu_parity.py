@@ -497,6 +497,14 @@ def test_edgelist_reader(ctx, irgl, oracle, tmp_path):
     with pytest.raises(irgl.IrglError) as e:
         ctx.read_edgelist(f4)
     assert e.value.status == 1
+    f5 = tmp_path / "negw.txt"  # a negative weight on a symmetric graph is a negative cycle
+    f5.write_text("3 2\n0 1 5\n1 2 -1\n")
+    with pytest.raises(irgl.IrglError) as e:
+        ctx.read_edgelist(f5)
+    assert e.value.status == 1
+    with pytest.raises(irgl.IrglError):
+        ctx.graph_from_csr(np.array([0, 1, 2], dtype=np.int64), np.array([1, 0], dtype=np.int32),
+                           np.array([3, -2], dtype=np.int32))
 
 
 # ---------------------------------------------------------------------------------------------
