@@ -199,12 +199,14 @@ const char* irgl_last_error(const irgl_ctx* ctx); /* ctx may be NULL: last globa
 int irgl_abi_version(void);
 
 /* ---- graph (reference Value::Graph; builtins edges/dst/weight) ----- */
+/* Column ids must be in [0, n) and weights >= 0 (IRGL_E_INVALID otherwise); distances are int32,
+ * so a path's weight sum must stay below INT32_MAX (= INF). */
 irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const int64_t* row_ptr,
                                     const int32_t* col, const int32_t* weight /*nullable*/,
                                     irgl_graph** out);
 irgl_status_t irgl_graph_generate(irgl_ctx* ctx, const irgl_gen_spec* spec, irgl_graph** out);
-/* Text edge list: first line "N M", then M lines "u v [w]" (0-based ids, '#' and
- * blank lines ignored).  symmetrise=1 adds reverse edges; self loops dropped, duplicates merged
+/* Text edge list: first line "N M", then M lines "u v [w]" (0-based ids, w >= 0;
+ * '#' and blank lines ignored).  symmetrise=1 adds reverse edges; self loops dropped, duplicates merged
  * (minimum weight); missing weights = 1.  The CSR is built on the device (sort + unique). */
 irgl_status_t irgl_graph_read_edgelist(irgl_ctx* ctx, const char* path, int symmetrise,
                                        irgl_graph** out);
