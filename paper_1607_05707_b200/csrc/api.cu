@@ -828,7 +828,6 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       GraphPart& gp = g->parts[l];
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
-      if (nf.defer_k > 0) CK(cudaMemsetAsync(&pp.ctl->dmin[nf.dsel ^ 1], 0xff, 4, pr.st));
       rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       rbs[l].nin_dev = &pp.ctl->cnt[pp.c_in];
       DistRoute dr{P, ctx->gpart(l), ps, gp.send, gp.send_cnt};
@@ -837,8 +836,11 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
       if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
+      // the header launch also resets the counters this round used (chunk / tile) and its
+      // deferral minimum, which accumulates the next round's (irgl_iterate reset both cells)
       CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow,
-                             pp.ctl->chunk_cnt, pp.ctl->tile_ctr, pr.st));
+                             pp.ctl->chunk_cnt, pp.ctl->tile_ctr,
+                             nf.defer_k > 0 ? &pp.ctl->dmin[nf.dsel] : nullptr, pr.st));
     }
     if (dtrace) t_a = now_us();
     // 2. gather the headers: the round's one host synchronisation

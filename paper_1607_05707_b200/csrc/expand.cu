@@ -1336,7 +1336,7 @@ __global__ void pack_all_kernel(const int32_t* lab, const uint32_t* send, int32_
 // it in stream order) so the next round needs no separate memsets.
 __global__ void round_header_kernel(uint32_t* hdr, const uint32_t* send_cnt, int P,
                                     const uint32_t* in_cnt, const uint32_t* overflow,
-                                    uint32_t* chunk_cnt, uint32_t* tile_ctr) {
+                                    uint32_t* chunk_cnt, uint32_t* tile_ctr, uint32_t* dmin_done) {
   const int t = threadIdx.x;
   if (t < P) hdr[t] = send_cnt ? ld_ctl(send_cnt + t) : 0u;
   if (t == 0) {
@@ -1344,6 +1344,7 @@ __global__ void round_header_kernel(uint32_t* hdr, const uint32_t* send_cnt, int
     hdr[P + 1] = ld_ctl(overflow);
     if (chunk_cnt) *chunk_cnt = 0u;
     if (tile_ctr) *tile_ctr = 0u;
+    if (dmin_done) *dmin_done = 0xffffffffu;  // this round's deferral minimum: next round's accumulator
   }
 }
 
@@ -1442,9 +1443,9 @@ cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* s
 
 cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
                                 const uint32_t* overflow, uint32_t* chunk_cnt, uint32_t* tile_ctr,
-                                cudaStream_t st) {
+                                uint32_t* dmin_done, cudaStream_t st) {
   note_launch();
-  round_header_kernel<<<1, 32, 0, st>>>(hdr, send_cnt, P, in_cnt, overflow, chunk_cnt, tile_ctr);
+  round_header_kernel<<<1, 32, 0, st>>>(hdr, send_cnt, P, in_cnt, overflow, chunk_cnt, tile_ctr, dmin_done);
   return cudaGetLastError();
 }
 

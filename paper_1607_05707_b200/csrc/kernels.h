@@ -87,7 +87,7 @@ cudaError_t launch_pack_all(const int32_t* lab, const uint32_t* send, int32_t* s
                             const uint32_t* send_cnt, int P, int me, int64_t ps, cudaStream_t st);
 cudaError_t launch_round_header(uint32_t* hdr, const uint32_t* send_cnt, int P, const uint32_t* in_cnt,
                                 const uint32_t* overflow, uint32_t* chunk_cnt, uint32_t* tile_ctr,
-                                cudaStream_t st);
+                                uint32_t* dmin_done, cudaStream_t st);
 // Gather current label values of the send buckets (SSSP / CC_LP pack step).
 cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_t* values,
                                uint32_t n, cudaStream_t st);
