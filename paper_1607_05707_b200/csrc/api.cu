@@ -23,8 +23,7 @@ struct PartRT {  // one vertex partition hosted by this process
   uint32_t* hdr = nullptr;    // multi-partition round header {send counts [P], in-count, overflow}
   cudaStream_t copy_st = nullptr;  // asynchronous result readback (irgl_read_result_async)
   uint32_t* h_stage = nullptr;     // pinned staging for small worklist initialisers
-  Ctl* h_ctl = nullptr;            // host-mapped control-block mirror: written by a kernel (no copy
-                                   // engine, so it never queues behind an async result readback)
+  Ctl* h_ctl = nullptr;            // pinned control-block mirror (the outlined iterate's readback)
   cudaEvent_t stage_ev = nullptr;  // last copy out of h_stage (reuse waits on it)
   // pipelined batches (irgl_traverse_batch): two control-block snapshots and their events
   // {iterate start, kernel start, kernel end, snapshot landed}, so traversal i+1 is queued before
@@ -1479,7 +1478,7 @@ static irgl_status_t ctx_init_parts(irgl_ctx* c, const int* devices, int ndev, i
     CK(cudaDeviceGetAttribute(&pr.sms, cudaDevAttrMultiProcessorCount, pr.dev));
     CK(cudaMallocHost(&pr.h_pin, 4096));
     CK(cudaMallocHost(&pr.h_stage, 4096));
-    CK(cudaHostAlloc(&pr.h_ctl, sizeof(Ctl), cudaHostAllocMapped));
+    CK(cudaHostAlloc(&pr.h_ctl, sizeof(Ctl), cudaHostAllocDefault));
     CK(cudaEventCreateWithFlags(&pr.stage_ev, cudaEventDisableTiming));
   }
   CK(cudaSetDevice(c->parts[0].dev));

@@ -1482,19 +1482,6 @@ cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-__global__ void ctl_export_kernel(const uint32_t* src, volatile uint32_t* dst, int nwords) {
-  for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
-  __threadfence_system();
-}
-
-cudaError_t launch_ctl_export(const Ctl* ctl, Ctl* host_mapped, cudaStream_t st) {
-  note_launch();
-  ctl_export_kernel<<<1, 256, 0, st>>>(reinterpret_cast<const uint32_t*>(ctl),
-                                       reinterpret_cast<volatile uint32_t*>(host_mapped),
-                                       (int)(sizeof(Ctl) / 4));
-  return cudaGetLastError();
-}
-
 int persistent_blocks_per_sm(int op, int variant) {
   int nb = 0;
   switch (op) {

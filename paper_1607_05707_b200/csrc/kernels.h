@@ -180,8 +180,6 @@ cudaError_t launch_exclusive_test(const uint32_t* in, uint32_t nin, const int32_
 
 // Reset of the control block before an outlined (persistent) launch, in one kernel.
 cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st);
-// Copies the control block into host-mapped pinned memory (the post-iterate readback).
-cudaError_t launch_ctl_export(const Ctl* ctl, Ctl* host_mapped, cudaStream_t st);
 
 // ---- degree-ordered relabelling (relabel.cu) ---------------------------------------------------
 // Replaces *col_io / *w_io (freed) with the relabelled arrays, returns new row offsets, perm
