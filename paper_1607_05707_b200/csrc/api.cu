@@ -2497,8 +2497,19 @@ irgl_status_t irgl_traverse_batch(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g,
       if (sources[i] < 0 || sources[i] >= g->n)
         return fail(ctx, IRGL_E_INVALID, "E_INVALID",
                     "source id >= the graph's vertex count (Value arrays are bounds-checked, SPEC.md:421)");
-    if (o.cond_mode == IRGL_COND_NONE && batch_pipelinable(ctx, pipe, g, op, args, o))
-      return traverse_batch_pipelined(ctx, pipe, g, op, sources, k, args, o, host_out, bytes, stats);
+    if (o.cond_mode == IRGL_COND_NONE && batch_pipelinable(ctx, pipe, g, op, args, o)) {
+      s = traverse_batch_pipelined(ctx, pipe, g, op, sources, k, args, o, host_out, bytes, stats);
+      if (s != IRGL_OK) {
+        // an error left later traversals queued: drain them and take the stamp epoch the device
+        // reached, so no later traversal reuses a stamp id that is still in the array
+        PartRT& pr = ctx->parts[0];
+        int32_t e = 0;
+        if (cudaSetDevice(pr.dev) == cudaSuccess && cudaStreamSynchronize(pr.st) == cudaSuccess &&
+            cudaMemcpy(&e, &g->parts[0].ctl->stamp_base, sizeof(e), cudaMemcpyDeviceToHost) == cudaSuccess)
+          g->stamp_epoch = std::max<int64_t>(g->stamp_epoch, e);
+      }
+      return s;
+    }
   }
   for (int32_t i = 0; i < k; ++i) {
     irgl_status_t s = irgl_pipe_init_scalars(pipe, sources + i, 1);

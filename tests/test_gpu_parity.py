@@ -351,6 +351,15 @@ def test_traverse_batch_edge_cases(irgl, oracle):
         # the context stays usable after the error
         lv, _ = irgl.bfs(c, g, s)
         np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
+        # a worklist overflow inside a pipelined batch: the error surfaces, the queued traversals
+        # drain, and later traversals (fresh stamp ids) are exact
+        tiny = c.pipe(8)
+        srcs = [int(x) for x in og.sources(4)]
+        with pytest.raises(Exception):
+            c.traverse_batch(irgl.SSSP, g, tiny, srcs, None)
+        for x in srcs:
+            d, _ = irgl.sssp(c, g, x)
+            np.testing.assert_array_equal(d, oracle.sssp(og, x))
 
 
 # ---------------------------------------------------------------------------------------------
