@@ -1245,7 +1245,10 @@ static irgl_status_t test_invoke(irgl_ctx* ctx, irgl_pipe* pipe, int op, const i
 // ---- topology-driven invocations ---------------------------------------------------------------
 // PageRank hubs: vertices of degree >= kPrHubT (the CTA-level path is then unused), cut into chunks of <= kPrChunk edges.  Built once
 // per graph on the host from the row offsets (the hub set never changes between sweeps).
-constexpr int64_t kPrHubT = 1024, kPrChunk = 2048;
+#ifndef IRGL_PR_HUB_T
+#define IRGL_PR_HUB_T 1024
+#endif
+constexpr int64_t kPrHubT = IRGL_PR_HUB_T, kPrChunk = 2048;
 static void free_pr_hubs(GraphPart& gp) {
   for (void* p : {(void*)gp.pr_hub_of, (void*)gp.pr_hfirst, (void*)gp.pr_cbeg, (void*)gp.pr_clen, (void*)gp.pr_partial})
     if (p) cudaFree(p);
