@@ -1078,7 +1078,14 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
       e0 = q[3];
     }
   }
-  if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+  g->stamp_epoch += h.stamp_used;  // also on failure: the ids are in the stamp array
+  if (h.overflow)
+    return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
+                std::string(h.overflow & 2 ? "edge-chunk descriptors beyond capacity" : "push beyond worklist capacity") +
+                    " (rounds " + std::to_string(h.rounds) + ", far piles " + std::to_string(h.far_cnt[0]) + "/" +
+                    std::to_string(h.far_cnt[1]) + " of " + std::to_string(gp.far_cap) + ", counts " +
+                    std::to_string(h.cnt[0]) + "/" + std::to_string(h.cnt[1]) + "/" + std::to_string(h.cnt[2]) +
+                    "/" + std::to_string(h.cnt[3]) + " of " + std::to_string(pipe->cap) + ")");
   const int64_t K = (int64_t)h.rounds;
   // rotate the host view: buffers by parity, counters by K mod 3 (see persistent_kernel)
   const int slots[3] = {pp.c_in, pp.c_out, pp.c_spare};
@@ -1087,7 +1094,6 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pp.c_out = slots[(K + 1) % 3];
   pp.c_spare = slots[(K + 2) % 3];
   pp.n_in = h.cnt[pp.c_in];
-  g->stamp_epoch += h.stamp_used;
   stt->edges += (int64_t)(h.bu_scanned + h.edges);  // bottom-up + top-down scans
   stt->remote_updates += (int64_t)h.remote;
   stt->rounds += K;
@@ -2401,8 +2407,8 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
     const int b = j & 1;
     CK(cudaEventSynchronize(pr.bev[b][3]));
     const Ctl& h = *pr.h_snap[b];
+    g->stamp_epoch += h.stamp_used;  // also on failure: the ids are in the stamp array
     if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
-    g->stamp_epoch += h.stamp_used;
     last_rounds = h.rounds;
     if (stats) {
       irgl_iter_stats& st = stats[j];

@@ -232,13 +232,23 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
   } else {
     int32_t nd[K], code[K], prev[K];
     bool cand[K];
+    int32_t old[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       nd[j] = (is_sssp(OP)) ? sv[j] + wt[j] : sv[j];
       cand[j] = act[j] && nd[j] < cur[j];
       kind[j] = (has_far(OP) && nd[j] >= rb.threshold) ? 2 : 1;
       code[j] = (rb.stamp_id << 1) | (kind[j] - 1);
-      if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
+      if (has_far(OP)) old[j] = cand[j] ? atomicMin(p.lab + dst[j], nd[j]) : 0;
+      else if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
+    }
+    // Near-far: only a candidate that lowered the distance may claim the stamp.  A far candidate
+    // working from a stale label that arrives after the vertex was pushed near would otherwise
+    // flip the stamp to the far code, and the next near candidate would push the vertex near a
+    // second time (more than n pushes in a round: worklist overflow, found by tools/stress.py).
+    if (has_far(OP)) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) cand[j] = cand[j] && nd[j] < old[j];
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) prev[j] = cand[j] ? atomicExch(p.stamp + dst[j], code[j]) : code[j];

@@ -363,6 +363,24 @@ def test_traverse_batch_edge_cases(irgl, oracle):
             np.testing.assert_array_equal(d, oracle.sssp(og, x))
 
 
+def test_sssp_near_far_no_duplicate_pushes(irgl, oracle):
+    # bucket width just above the largest weight on small RMAT graphs: far candidates working from
+    # a stale label used to flip a vertex's stamp after its near push and let it be pushed near
+    # again (more than n pushes in a round -> E_WL_OVERFLOW; the failed run's stamp ids were then
+    # reused -> wrong distances).  Found by tools/stress.py.
+    with irgl.Context() as c:
+        for seed, wseed in ((3, 3), (4, 1), (4, 2), (10, 3), (11, 1), (13, 1)):
+            og = oracle.rmat(8, seed=seed, wseed=wseed)
+            g = _upload(c, og)
+            for s in [int(x) for x in og.sources(3)]:
+                ref = oracle.sssp(og, s)
+                for delta in (64, 264, 1000):
+                    for outline in (1, 0):
+                        d, _ = irgl.sssp(c, g, s, delta=delta, defer=0, outline=outline)
+                        np.testing.assert_array_equal(d, ref)
+            g.close()
+
+
 # ---------------------------------------------------------------------------------------------
 # CC
 def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):
