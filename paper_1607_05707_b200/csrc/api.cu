@@ -413,6 +413,9 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
     CK(cudaSetDevice(pr.dev));
     CK(cudaStreamSynchronize(pr.st));
     std::memcpy(&cnt[(size_t)ctx->gpart(l) * P], pr.h_pin, P * 4);
+    for (int q = 0; q < P; ++q)  // a bucket holds part_size ids: more means dropped pushes
+      if (cnt[(size_t)ctx->gpart(l) * P + q] > (uint64_t)ps)
+        return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
   }
   // 2. pack values (SSSP / CC_LP): current ghost label of each bucket entry
   if (vals)

@@ -238,7 +238,10 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
       nd[j] = (is_sssp(OP)) ? sv[j] + wt[j] : sv[j];
       cand[j] = act[j] && nd[j] < cur[j];
       kind[j] = (has_far(OP) && nd[j] >= rb.threshold) ? 2 : 1;
-      code[j] = (rb.stamp_id << 1) | (kind[j] - 1);
+      // a vertex another partition owns is sent once per round whatever its pile (the owner
+      // decides near / far): one code for both kinds
+      const bool remote = has_far(OP) && p.dr.nparts > 1 && (int64_t)dst[j] / p.dr.part_size != p.dr.me;
+      code[j] = (rb.stamp_id << 1) | (remote ? 0 : kind[j] - 1);
       if (has_far(OP)) old[j] = cand[j] ? atomicMin(p.lab + dst[j], nd[j]) : 0;
       else if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
     }

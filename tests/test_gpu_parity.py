@@ -381,6 +381,22 @@ def test_sssp_near_far_no_duplicate_pushes(irgl, oracle):
             g.close()
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_sssp_near_far_partitioned_single_send(irgl, oracle, P):
+    # near-far with logical partitions: a remote vertex claimed near and far in one round was sent
+    # twice, so a bucket could exceed part_size (the peer copy then read past it: invalid argument)
+    with irgl.Context(logical_partitions=P) as c:
+        for seed in (3, 7, 11):
+            og = oracle.rmat(8 + seed % 3, seed=seed, wseed=seed)
+            g = _upload(c, og)
+            for s in [int(x) for x in og.sources(3)]:
+                ref = oracle.sssp(og, s)
+                for delta in (244, 290):
+                    d, _ = irgl.sssp(c, g, s, delta=delta, defer=0)
+                    np.testing.assert_array_equal(d, ref)
+            g.close()
+
+
 # ---------------------------------------------------------------------------------------------
 # CC
 def test_cc_rmat_and_cut_grid(ctx, irgl, oracle):

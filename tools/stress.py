@@ -10,7 +10,8 @@ secs = float(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 t_end = time.time() + secs
 n_checks = 0
-ctx = irgl.Context()
+P = int(os.environ.get("STRESS_P", "1"))  # logical partitions (P > 1: BFS / SSSP only)
+ctx = irgl.Context(logical_partitions=P) if P > 1 else irgl.Context()
 while time.time() < t_end:
     kind = rng.integers(0, 3)
     if kind == 0:
@@ -24,12 +25,12 @@ while time.time() < t_end:
         og = O.from_edges(n, rng.integers(0, n, m).tolist(), rng.integers(0, n, m).tolist(),
                           w=rng.integers(1, int(rng.choice([2, 16, 256, 100000])), m).tolist())
     g = ctx.graph_from_csr(og.row_ptr, og.col, og.weight)
-    if rng.random() < 0.5:
+    if P == 1 and rng.random() < 0.5:
         g.relabel()
     srcs = [int(s) for s in og.sources(3, seed=int(rng.integers(1, 1000)))] or [0]
     for s in srcs:
         ref_l = O.bfs(og, s)[0]
-        for direction in (0, 1):
+        for direction in ((0, 1) if P == 1 else (0,)):
             lv, _ = irgl.bfs(ctx, g, s, direction=direction, outline=int(rng.integers(0, 2)) if not direction else 1)
             assert np.array_equal(lv, ref_l), ("bfs", kind, og.n, s, direction)
         ref_d = O.sssp(og, s)
@@ -43,6 +44,9 @@ while time.time() < t_end:
                 raise
             assert np.array_equal(d, ref_d), ("sssp", kind, og.n, s, delta, defer)
         n_checks += 6
+    if P > 1:
+        g.close()
+        continue
     p = ctx.pipe(og.n)
     outs = [np.zeros(og.n, dtype=np.int32) for _ in range(2)]
     ctx.traverse_batch(irgl.SSSP, g, p, srcs, outs)
