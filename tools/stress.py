@@ -15,7 +15,7 @@ ctx = irgl.Context(logical_partitions=P) if P > 1 else irgl.Context()
 while time.time() < t_end:
     kind = rng.integers(0, 3)
     if kind == 0:
-        og = O.rmat(int(rng.integers(8, 17)), seed=int(rng.integers(1, 1000)), wseed=int(rng.integers(1, 1000)))
+        og = O.rmat(int(rng.integers(6, 19)), seed=int(rng.integers(1, 1000)), wseed=int(rng.integers(1, 1000)))
     elif kind == 1:
         W, H = int(rng.integers(2, 200)), int(rng.integers(2, 200))
         og = O.grid(W, H, perc_keep=float(rng.uniform(0.3, 1.0)), perc_seed=int(rng.integers(1, 1000)))
@@ -67,7 +67,11 @@ while time.time() < t_end:
         ref_r, _ = O.pagerank(og, max_iter=pst.rounds)
         err = np.abs(r - ref_r).sum() / max(np.abs(ref_r).sum(), 1e-300)
     assert err <= 1e-6, ("pr", kind, og.n, err, pst.rounds, it)
-    n_checks += 4
+    tc, _ = irgl.triangle_count(ctx, g)
+    assert int(tc) == O.tc(og), ("tc", kind, og.n)
+    (mw, me), _ = irgl.mst(ctx, g)
+    assert (int(mw), int(me)) == O.mst(og), ("mst", kind, og.n)
+    n_checks += 6
     p.close()
     g.close()
 print(f"stress ok: {n_checks} checks in {secs:.0f} s", flush=True)
