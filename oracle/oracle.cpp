@@ -800,3 +800,54 @@ extern "C" int64_t orc_sssp_bsp_omp(const orc_graph* g, int64_t src, int32_t* di
   if (edges_out) *edges_out = edges;
   return rounds;
 }
+
+// ------------------------------------------------------------------------------------------
+// Size-independent certificates for results too large for an oracle run (RMAT-27: 4.2G directed
+// edges).  They take a borrowed CSR (e.g. downloaded from the device) and the result array and
+// check the property that characterises the answer exactly on a symmetric graph with symmetric
+// weights; return 0 when it holds, else a nonzero code naming the first violated clause.
+//   BFS : level[src] = 0; every edge inside the reached set joins levels that differ by <= 1 and
+//         no edge leaves it; every reached v != src has a neighbour at level[v] - 1  => hop
+//         distance (Listing 2).
+//   SSSP: dist[src] = 0; dist[v] <= dist[u] + w(u,v) on every edge of the reached set, none
+//         leaves it; every reached v != src has a neighbour u with dist[u] + w(u,v) = dist[v]
+//         => shortest-path distances.
+extern "C" int orc_cert_bfs(int64_t n, const int64_t* rp, const int32_t* col, int64_t src,
+                            const int32_t* level) {
+  if (src < 0 || src >= n || level[src] != 0) return 1;
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : bad)
+  for (int64_t u = 0; u < n; ++u) {
+    const int32_t lu = level[u];
+    bool parent = (u == src);
+    for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+      const int32_t lv = level[col[k]];
+      if ((lu == ORC_INF) != (lv == ORC_INF)) { bad |= 2; break; }
+      if (lu == ORC_INF) continue;
+      if (lv < lu - 1 || lv > lu + 1) bad |= 4;
+      if (lv == lu - 1) parent = true;
+    }
+    if (lu != ORC_INF && !parent) bad |= 8;
+  }
+  return bad;
+}
+
+extern "C" int orc_cert_sssp(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* w,
+                             int64_t src, const int32_t* dist) {
+  if (src < 0 || src >= n || dist[src] != 0) return 1;
+  int bad = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : bad)
+  for (int64_t u = 0; u < n; ++u) {
+    const int64_t du = dist[u];
+    bool parent = (u == src);
+    for (int64_t k = rp[u]; k < rp[u + 1]; ++k) {
+      const int64_t dv = dist[col[k]];
+      if ((du == ORC_INF) != (dv == ORC_INF)) { bad |= 2; break; }
+      if (du == ORC_INF) continue;
+      if (dv > du + w[k]) bad |= 4;          // violated edge u -> v
+      if (dv + w[k] == du) parent = true;    // tight edge into u (w symmetric)
+    }
+    if (du != ORC_INF && !parent) bad |= 8;
+  }
+  return bad;
+}

@@ -145,6 +145,14 @@ int64_t orc_sssp_bsp_omp(const orc_graph* g, int64_t src, int32_t* dist, int thr
                          int64_t* edges_out);
 int orc_max_threads(void);
 
+/* Certificates over a borrowed CSR (symmetric graph, symmetric weights); 0 = holds, else a bit
+ * mask of the violated clauses (1 source, 2 edge leaves the reached set, 4 edge inequality,
+ * 8 reached vertex without a tight parent).  For sizes no oracle run finishes (RMAT-27). */
+int orc_cert_bfs(int64_t n, const int64_t* rp, const int32_t* col, int64_t src,
+                 const int32_t* level);
+int orc_cert_sssp(int64_t n, const int64_t* rp, const int32_t* col, const int32_t* w, int64_t src,
+                  const int32_t* dist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,10 @@ def lib():
         L.orc_sssp_bsp_omp.restype = C.c_int64
         L.orc_sssp_bsp_omp.argtypes = [P, C.c_int64, i32p, C.c_int, i64p]
         L.orc_max_threads.restype = C.c_int
+        L.orc_cert_bfs.restype = C.c_int
+        L.orc_cert_bfs.argtypes = [C.c_int64, i64p, i32p, C.c_int64, i32p]
+        L.orc_cert_sssp.restype = C.c_int
+        L.orc_cert_sssp.argtypes = [C.c_int64, i64p, i32p, i32p, C.c_int64, i32p]
         _lib = L
     return _lib
 
@@ -283,3 +287,22 @@ def sssp_bsp_omp(g: Graph, src: int, threads=0):
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+def cert_bfs(row_ptr, col, src: int, level) -> int:
+    """0 when `level` is the hop distance from src on the symmetric CSR (see oracle.h)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(col, dtype=np.int32)
+    lv = np.ascontiguousarray(level, dtype=np.int32)
+    return int(lib().orc_cert_bfs(len(rp) - 1, _p(rp, C.c_int64), _p(cl, C.c_int32), src,
+                                  _p(lv, C.c_int32)))
+
+
+def cert_sssp(row_ptr, col, w, src: int, dist) -> int:
+    """0 when `dist` is the shortest-path distance from src (symmetric weights; see oracle.h)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(col, dtype=np.int32)
+    ww = np.ascontiguousarray(w, dtype=np.int32)
+    d = np.ascontiguousarray(dist, dtype=np.int32)
+    return int(lib().orc_cert_sssp(len(rp) - 1, _p(rp, C.c_int64), _p(cl, C.c_int32),
+                                   _p(ww, C.c_int32), src, _p(d, C.c_int32)))

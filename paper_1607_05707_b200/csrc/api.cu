@@ -359,7 +359,7 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
     CK(cudaSetDevice(pr.dev));
     for (int k = 0; k < 4; ++k)
       if (!gp.pr[k]) CK(cudaMalloc(&gp.pr[k], std::max<int64_t>(g->n, 1) * sizeof(double)));
-    CK(launch_pr_init(gp.pr[0], reinterpret_cast<float*>(gp.pr[2]), gp.row_ptr, g->n, pr.st));
+    CK(launch_pr_init(gp.pr[0], gp.pr[2], gp.row_ptr, g->n, pr.st));
     CK(cudaStreamSynchronize(pr.st));
     gp.pr_cur = 0;
     g->lab_op = op;
@@ -413,10 +413,18 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
     CK(cudaSetDevice(pr.dev));
     CK(cudaStreamSynchronize(pr.st));
     std::memcpy(&cnt[(size_t)ctx->gpart(l) * P], pr.h_pin, P * 4);
-    for (int q = 0; q < P; ++q)  // a bucket holds part_size ids: more means dropped pushes
-      if (cnt[(size_t)ctx->gpart(l) * P + q] > (uint64_t)ps)
-        return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
   }
+  // A bucket holds part_size ids: more means dropped pushes.  The test runs on the full P x P
+  // matrix, which every rank holds only after the counts AllGather in NCCL mode — a rank that
+  // failed alone would leave its peers blocked in the collective — so with a communicator it
+  // runs after (i) below, on every rank alike; the packs clamp to the bucket meanwhile.
+  auto bucket_overflow = [&]() {
+    for (uint32_t c : cnt)
+      if (c > (uint64_t)ps) return true;
+    return false;
+  };
+  if (!ctx->comm && bucket_overflow())
+    return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
   // 2. pack values (SSSP / CC_LP): current ghost label of each bucket entry
   if (vals)
     for (int l = 0; l < L; ++l) {
@@ -424,7 +432,7 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       GraphPart& gp = g->parts[l];
       CK(cudaSetDevice(pr.dev));
       for (int q = 0; q < P; ++q) {
-        const uint32_t c = cnt[(size_t)ctx->gpart(l) * P + q];
+        const uint32_t c = std::min<uint32_t>(cnt[(size_t)ctx->gpart(l) * P + q], (uint32_t)ps);
         if (c) CK(launch_pack_values(gp.lab, gp.send + (int64_t)q * ps, gp.send_val + (int64_t)q * ps, c, pr.st));
       }
     }
@@ -443,6 +451,8 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
     CK(cudaMemcpyAsync(cnt.data(), ctx->cnt_dev + (size_t)L * P, (size_t)P * P * 4,
                        cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
+    if (bucket_overflow())  // the same matrix on every rank: all ranks fail here together
+      return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
     // (ii) payloads: grouped send/recv (all-to-all-v).  Every rank walks the (src, dst) partition
     // pairs in the same global order, so the per-peer order of sends matches the receiver's
     // order of recvs (NCCL matches point-to-point calls per peer in issue order).
@@ -1338,8 +1348,8 @@ static irgl_status_t topo_invoke(irgl_ctx* ctx, irgl_graph* g, int op, const irg
     PrHubs hubs;
     irgl_status_t hs = ensure_pr_hubs(ctx, gp, g->relabeled, &hubs);
     if (hs != IRGL_OK) return hs;
-    CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
-                       reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, 0, gm, hubs, pr.st));
+    CK(launch_pr_sweep(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c],
+                       gp.pr[3 - c], d, tol, g->n, gp.ctl, 0, gm, hubs, pr.st));
     stt->launches += 1;
     CK(cudaMemcpyAsync(&cell, &gp.ctl->red[0], 4, cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
@@ -1400,8 +1410,8 @@ static irgl_status_t pr_outlined(irgl_ctx* ctx, irgl_graph* g, const irgl_op_arg
   CK(cudaMemsetAsync(gp.ctl->red, 0, sizeof(gp.ctl->red), pr.st));
   CK(cudaMemsetAsync(gp.ctl->tile_ctr, 0, sizeof(gp.ctl->tile_ctr), pr.st));
   CK(cudaEventRecord(ctx->kev0, pr.st));
-  CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], reinterpret_cast<float*>(gp.pr[2 + c]),
-                          reinterpret_cast<float*>(gp.pr[3 - c]), d, tol, g->n, gp.ctl, o.max_rounds,
+  CK(launch_pr_persistent(gp.csr(), gp.pr[c], gp.pr[1 - c], gp.pr[2 + c],
+                          gp.pr[3 - c], d, tol, g->n, gp.ctl, o.max_rounds,
                           o.cond_mode, bps * pr.sms, hubs, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   Ctl h;
@@ -1917,6 +1927,9 @@ irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end) {
     uint32_t zeros[4] = {0, 0, 0, 0};
     zeros[pp.c_in] = (uint32_t)(e - b);
     CK(cudaMemcpyAsync(pp.ctl->cnt, zeros, sizeof(zeros), cudaMemcpyHostToDevice, pr.st));
+    // a fresh WorklistInit: clear the sticky overflow flag and chunk counters as pipe_set_in does
+    CK(cudaMemsetAsync(pp.ctl->chunk_cnt, 0, sizeof(pp.ctl->chunk_cnt), pr.st));
+    CK(cudaMemsetAsync(&pp.ctl->overflow, 0, sizeof(uint32_t), pr.st));
     CK(cudaStreamSynchronize(pr.st));
     pp.n_in = (uint32_t)(e - b);
   }
@@ -1931,6 +1944,8 @@ irgl_status_t irgl_pipe_size(const irgl_pipe* p, irgl_wl which, int64_t* out) {
     CK(cudaSetDevice(ctx->parts[l].dev));
     const int slot = which == IRGL_WL_IN ? pp.c_in : which == IRGL_WL_OUT ? pp.c_out : pp.c_retry;
     uint32_t c = 0;
+    // the pipe's writes are queued on the (non-blocking) partition stream: read after them
+    CK(cudaStreamSynchronize(ctx->parts[l].st));
     CK(cudaMemcpy(&c, &pp.ctl->cnt[slot], 4, cudaMemcpyDeviceToHost));
     tot += c;
   }
@@ -1947,6 +1962,7 @@ irgl_status_t irgl_pipe_read(irgl_pipe* p, irgl_wl which, int64_t* items, int64_
     const int slot = which == IRGL_WL_IN ? pp.c_in : which == IRGL_WL_OUT ? pp.c_out : pp.c_retry;
     const int buf = which == IRGL_WL_IN ? pp.b_in : which == IRGL_WL_OUT ? pp.b_out : pp.b_retry;
     uint32_t c = 0;
+    CK(cudaStreamSynchronize(ctx->parts[l].st));  // after the pipe's queued writes
     CK(cudaMemcpy(&c, &pp.ctl->cnt[slot], 4, cudaMemcpyDeviceToHost));
     c = (uint32_t)std::min<int64_t>(c, p->cap);
     std::vector<uint32_t> h(c);
@@ -2239,6 +2255,7 @@ irgl_status_t irgl_graph_perm(irgl_graph* g, int32_t* new_of_old) {
     return IRGL_OK;
   }
   CK(cudaSetDevice(ctx->parts[0].dev));
+  CK(cudaStreamSynchronize(ctx->parts[0].st));  // the relabel kernels run on the stream
   CK(cudaMemcpy(new_of_old, g->perm, g->n * 4, cudaMemcpyDeviceToHost));
   return IRGL_OK;
 }
@@ -2249,6 +2266,7 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
     if (!ctx->test_log) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "no test operator has run");
     const size_t nb = std::min(bytes, (size_t)ctx->test_log_cap * 4);
     CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaStreamSynchronize(ctx->parts[0].st));  // after the operator's queued work
     CK(cudaMemcpy(host_out, ctx->test_log, nb, cudaMemcpyDeviceToHost));
     return IRGL_OK;
   }
@@ -2262,6 +2280,7 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
     if (bytes < 16) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "MST result is uint64[2]");
     if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "MST has not run on this graph");
     CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaStreamSynchronize(ctx->parts[0].st));
     CK(cudaMemcpy(host_out, &g->parts[0].ctl->mst_w, 16, cudaMemcpyDeviceToHost));
     return IRGL_OK;
   }

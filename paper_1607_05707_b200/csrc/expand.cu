@@ -55,6 +55,18 @@ constexpr bool is_bfs(int op) { return op == IRGL_OP_BFS || op == kOpBfsDO; }
 constexpr bool is_sssp(int op) { return op == IRGL_OP_SSSP || op == kOpSsspNF || op == kOpSssp8; }
 constexpr bool w8_op(int op) { return op == kOpSssp8; }
 constexpr bool has_far(int op) { return op == kOpSsspNF; }
+
+// Push dedupe by stamp.  Stamp ids only grow (one per round / split, monotonic across
+// traversals; the array is cleared when the id space wraps), so a push claims its vertex with
+// atomicMax and pushes iff the previous code was smaller.  Near-far ops code a near push as
+// (sid << 1) | 1 and a far push (and a send to a remote owner) as sid << 1: within a round the
+// near claim dominates, so a late far claim working from a stale label can never undo it and let
+// a later near candidate push the vertex twice.  Other ops use sid << 1 (the dense-round mark).
+template <int OP>
+__device__ __forceinline__ int32_t stamp_code(int32_t sid, int kind) {
+  return has_far(OP) ? ((sid << 1) | (kind == 1 ? 1 : 0)) : (sid << 1);
+}
+__device__ __forceinline__ bool stamp_claim(int32_t* s, int32_t code) { return atomicMax(s, code) < code; }
 constexpr bool has_mf(int op) { return op == kOpBfsDO; }
 constexpr int minb_for(int op) { return is_sssp(op) ? IRGL_MINB_SSSP : IRGL_MINB; }
 
@@ -156,15 +168,13 @@ __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb,
     if (nd >= cur) return 0;
     const int32_t old = atomicMin(p.lab + dst, nd);
     if (nd >= old) return 0;
-    // push dedupe per round and per pile: stamp code = 2*round_id + (far ? 1 : 0).  A vertex
-    // first pushed far and then improved below the threshold in the same round is pushed near
-    // too; its stale far entry is dropped by the split (dist < old threshold).
+    // push dedupe per round and per pile (stamp_code).  A vertex first pushed far and then
+    // improved below the threshold in the same round is pushed near too; its stale far entry is
+    // dropped by the split (dist < old threshold).
     const int kind = (has_far(OP) && nd >= rb.threshold) ? 2 : 1;
     // dst now holds <= nd and sits in the near out worklist (pushed here or earlier this round)
     if (is_sssp(OP) && kind == 1) q.dmin = min(q.dmin, nd);
-    const int32_t code = (rb.stamp_id << 1) | (kind - 1);
-    if (atomicExch(p.stamp + dst, code) == code) return 0;
-    return kind;
+    return stamp_claim(p.stamp + dst, stamp_code<OP>(rb.stamp_id, kind)) ? kind : 0;
   }
 }
 
@@ -241,24 +251,24 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
       // a vertex another partition owns is sent once per round whatever its pile (the owner
       // decides near / far): one code for both kinds
       const bool remote = has_far(OP) && p.dr.nparts > 1 && (int64_t)dst[j] / p.dr.part_size != p.dr.me;
-      code[j] = (rb.stamp_id << 1) | (remote ? 0 : kind[j] - 1);
+      code[j] = stamp_code<OP>(rb.stamp_id, remote ? 2 : kind[j]);
       if (has_far(OP)) old[j] = cand[j] ? atomicMin(p.lab + dst[j], nd[j]) : 0;
       else if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
     }
-    // Near-far: only a candidate that lowered the distance may claim the stamp.  A far candidate
-    // working from a stale label that arrives after the vertex was pushed near would otherwise
-    // flip the stamp to the far code, and the next near candidate would push the vertex near a
-    // second time (more than n pushes in a round: worklist overflow, found by tools/stress.py).
+    // Near-far: only a candidate that lowered the distance claims the stamp (a far candidate
+    // from a stale label needs no push: the vertex is already queued near or lower), and the
+    // near code dominates the far one (stamp_code), so no interleaving pushes a vertex near twice
+    // in a round (more than n pushes: worklist overflow, found by tools/stress.py).
     if (has_far(OP)) {
 #pragma unroll
       for (int j = 0; j < K; ++j) cand[j] = cand[j] && nd[j] < old[j];
     }
 #pragma unroll
-    for (int j = 0; j < K; ++j) prev[j] = cand[j] ? atomicExch(p.stamp + dst[j], code[j]) : code[j];
+    for (int j = 0; j < K; ++j) prev[j] = cand[j] ? atomicMax(p.stamp + dst[j], code[j]) : code[j];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       if (is_sssp(OP) && cand[j] && kind[j] == 1) q.dmin = min(q.dmin, nd[j]);
-      kind[j] = (cand[j] && prev[j] != code[j]) ? kind[j] : 0;
+      kind[j] = (cand[j] && prev[j] < code[j]) ? kind[j] : 0;
     }
   }
 }
@@ -516,9 +526,9 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
     if (__any_sync(FULL, defer)) {
       int kind = 0;
       if (defer) {
-        const int32_t code = rb.stamp_id << 1;
+        const int32_t code = stamp_code<OP>(rb.stamp_id, 1);
         if (!has_far(OP) && rb.dense) atomicMax(p.stamp + v, code);  // mark (compaction pushes)
-        else kind = atomicExch(p.stamp + v, code) != code ? 1 : 0;
+        else kind = stamp_claim(p.stamp + v, code) ? 1 : 0;
         q.dmin = min(q.dmin, sv);
         deg = 0;
       }
@@ -865,8 +875,7 @@ __device__ void far_split(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs&
       const int32_t dv = ld_label_cg(p.lab + v);
       if (dv >= t_old) {
         const int k = dv < rb.threshold ? 1 : 2;
-        const int32_t code = (rb.stamp_id << 1) | (k - 1);
-        if (atomicExch(p.stamp + v, code) != code) {
+        if (stamp_claim(p.stamp + v, stamp_code<kOpSsspNF>(rb.stamp_id, k))) {
           kind = k;
           if (kind == 2) mymin = min(mymin, (uint32_t)dv);
         }

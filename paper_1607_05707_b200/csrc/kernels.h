@@ -134,7 +134,7 @@ int expand_blocks_per_sm(int op);
 cudaError_t launch_cc_hook(const DevCSR& g, int32_t* parent, Ctl* ctl, int red_slot, int grid,
                            cudaStream_t st);
 cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st);
-cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr, int64_t n,
+cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
                            cudaStream_t st);
 // PageRank hub split (built once per graph): hub_of[v] = hub index of vertex v (valid when
 // deg(v) >= hub_t), hub k's chunks are [hfirst[k], hfirst[k+1]), chunk c = edges
@@ -150,10 +150,10 @@ struct PrHubs {
   int32_t cta_tiles;  // sweep layout: 1 CTA tiles (degree-ordered ids), 0 warp tiles
 };
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
-                            const float* contrib, float* contrib_next, double d, double tol,
+                            const double* contrib, double* contrib_next, double d, double tol,
                             int64_t n_global, Ctl* ctl, int red_slot, int grid, const PrHubs& h,
                             cudaStream_t st);
-cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float* ca, float* cb,
+cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double* ca, double* cb,
                                  double d, double tol, int64_t n_global, Ctl* ctl,
                                  int64_t max_rounds, int cond_mode, int grid, const PrHubs& h,
                                  cudaStream_t st);

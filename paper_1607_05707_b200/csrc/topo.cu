@@ -140,30 +140,30 @@ __device__ __forceinline__ float ld_cg_f32(const float* p) {
   asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(r) : "l"(p));
   return r;
 }
-__device__ __forceinline__ float ld_ca_f32(const float* p) {
-  float r;
-  asm volatile("ld.global.ca.f32 %0, [%1];" : "=f"(r) : "l"(p));
+__device__ __forceinline__ double ld_ca_f64(const double* p) {
+  double r;
+  asm volatile("ld.global.ca.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
 
 // Sum of contrib[col[k]] for k = k0, k0+S, k0+2S, ... < e, U gathers in flight per step; the
 // summation order is fixed (deterministic per vertex for a given launch shape).
 template <int S, int U = 8>
-__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ col, const float* contrib,
+__device__ __forceinline__ double gather_sum(const int32_t* __restrict__ col, const double* contrib,
                                              int64_t k0, int64_t e) {
   double s = 0.0;
   int64_t k = k0;
   for (; k + (U - 1) * S < e; k += U * S) {
     int32_t c[U];
-    float v[U];
+    double v[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) c[j] = ld_stream(col + k + j * S);
 #pragma unroll
-    for (int j = 0; j < U; ++j) v[j] = ld_ca_f32(contrib + c[j]);
+    for (int j = 0; j < U; ++j) v[j] = ld_ca_f64(contrib + c[j]);
 #pragma unroll
-    for (int j = 0; j < U; ++j) s += (double)v[j];
+    for (int j = 0; j < U; ++j) s += v[j];
   }
-  for (; k < e; k += S) s += (double)ld_ca_f32(contrib + ld_stream(col + k));
+  for (; k < e; k += S) s += ld_ca_f64(contrib + ld_stream(col + k));
   return s;
 }
 
@@ -178,7 +178,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 // (phase A), and the vertex's sweep adds its partials in chunk order (phase B) — deterministic,
 // and no CTA walks a run of hubs alone: with degree-ordered ids every hub sits in the first
 // vertex tiles (without the split PR on relabelled RMAT-24 took 18.5 ms per sweep instead of 2.8).
-__device__ void pr_hub_chunks(const DevCSR& g, const float* contrib, const PrHubs& h) {
+__device__ void pr_hub_chunks(const DevCSR& g, const double* contrib, const PrHubs& h) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < h.nchunks; c += nw) {
@@ -200,8 +200,8 @@ __shared__ int32_t s_pr_slot;
 // s = slot (host-loop kernel, a constant-bank parameter).
 template <bool kSmemSlot>
 __device__ void pr_sweep_cta(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
-                               double* __restrict__ rank_new, const float* __restrict__ contrib,
-                               float* __restrict__ contrib_next, double d, double tol,
+                               double* __restrict__ rank_new, const double* __restrict__ contrib,
+                               double* __restrict__ contrib_next, double d, double tol,
                                double base, int red, Ctl* ctl, int slot, const PrHubs& h) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t nloc = g.hi - g.lo;
@@ -267,7 +267,7 @@ __device__ void pr_sweep_cta(PrSmem& sm, const DevCSR& g, const double* __restri
       const int64_t v = g.lo + i;
       const double r = base + d * mysum;
       rank_new[v] = r;
-      contrib_next[v] = deg0 > 0 ? (float)(r / (double)deg0) : 0.0f;
+      contrib_next[v] = deg0 > 0 ? r / (double)deg0 : 0.0;
       changed = fabs(r - ld_cg_f64(rank_old + v)) > tol;
     }
     const int sl = kSmemSlot ? *(volatile int32_t*)&s_pr_slot : slot;
@@ -287,8 +287,8 @@ __device__ void pr_sweep_cta(PrSmem& sm, const DevCSR& g, const double* __restri
 constexpr int kPrWarpTile = 32;
 template <bool kSmemSlot>
 __device__ void pr_sweep_warp(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
-                               double* __restrict__ rank_new, const float* __restrict__ contrib,
-                               float* __restrict__ contrib_next, double d, double tol,
+                               double* __restrict__ rank_new, const double* __restrict__ contrib,
+                               double* __restrict__ contrib_next, double d, double tol,
                                double base, int red, Ctl* ctl, int slot, const PrHubs& h) {
   (void)sm;
   const int lane = threadIdx.x & 31;
@@ -333,7 +333,7 @@ __device__ void pr_sweep_warp(PrSmem& sm, const DevCSR& g, const double* __restr
         const int64_t v = g.lo + i;
         const double r = base + d * mysum;
         rank_new[v] = r;
-        contrib_next[v] = deg0 > 0 ? (float)(r / (double)deg0) : 0.0f;
+        contrib_next[v] = deg0 > 0 ? r / (double)deg0 : 0.0;
         changed = fabs(r - ld_cg_f64(rank_old + v)) > tol;
       }
       const int sl = kSmemSlot ? *(volatile int32_t*)&s_pr_slot : slot;
@@ -347,8 +347,8 @@ __device__ void pr_sweep_warp(PrSmem& sm, const DevCSR& g, const double* __restr
 // RMAT-22), warp tiles otherwise (2.30 vs 2.53 on RMAT-24).
 template <bool kSmemSlot>
 __device__ __forceinline__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, const double* __restrict__ rank_old,
-                                               double* __restrict__ rank_new, const float* __restrict__ contrib,
-                                               float* __restrict__ contrib_next, double d, double tol,
+                                               double* __restrict__ rank_new, const double* __restrict__ contrib,
+                                               double* __restrict__ contrib_next, double d, double tol,
                                                double base, int red, Ctl* ctl, int slot, const PrHubs& h) {
   if (h.cta_tiles)
     pr_sweep_cta<kSmemSlot>(sm, g, rank_old, rank_new, contrib, contrib_next, d, tol, base, red, ctl, slot, h);
@@ -357,8 +357,8 @@ __device__ __forceinline__ void pr_sweep_tiles(PrSmem& sm, const DevCSR& g, cons
 }
 
 __global__ void __launch_bounds__(kBlock) pr_sweep_kernel(DevCSR g, const double* rank_old,
-                                                          double* rank_new, const float* contrib,
-                                                          float* contrib_next, double d,
+                                                          double* rank_new, const double* contrib,
+                                                          double* contrib_next, double d,
                                                           double tol, double base, PrHubs h, Ctl* ctl,
                                                           int slot) {
   __shared__ PrSmem sm;
@@ -366,17 +366,17 @@ __global__ void __launch_bounds__(kBlock) pr_sweep_kernel(DevCSR g, const double
                         ctl, slot, h);
 }
 
-__global__ void __launch_bounds__(kBlock) pr_hub_kernel(DevCSR g, const float* contrib, PrHubs h) {
+__global__ void __launch_bounds__(kBlock) pr_hub_kernel(DevCSR g, const double* contrib, PrHubs h) {
   pr_hub_chunks(g, contrib, h);
 }
 
-__global__ void pr_init_kernel(double* rank, float* contrib, const int64_t* row_ptr, int64_t n) {
+__global__ void pr_init_kernel(double* rank, double* contrib, const int64_t* row_ptr, int64_t n) {
   const double r0 = 1.0 / (double)n;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     rank[v] = r0;
     const int64_t deg = row_ptr[v + 1] - row_ptr[v];
-    contrib[v] = deg > 0 ? (float)(r0 / (double)deg) : 0.0f;
+    contrib[v] = deg > 0 ? r0 / (double)deg : 0.0;
   }
 }
 
@@ -384,7 +384,7 @@ __global__ void pr_init_kernel(double* rank, float* contrib, const int64_t* row_
 // Cells rotate over 3 slots: cell (r+1)%3 is reset during round r (last read at the start of r-1).
 // Returns true when the Iterate stops after round r.
 __device__ __forceinline__ bool pr_round(PrSmem& sm, cg::grid_group& grid, const DevCSR& g,
-                                         const double* ro, double* rn, const float* co, float* cn,
+                                         const double* ro, double* rn, const double* co, double* cn,
                                          double d, double tol, double base, Ctl* ctl,
                                          int64_t max_rounds, int cond_mode, const PrHubs& h,
                                          int64_t r) {
@@ -423,7 +423,7 @@ __device__ __forceinline__ bool pr_round(PrSmem& sm, cg::grid_group& grid, const
 // (r & 1) cost 40 B of spills at the 40-register budget and made the sweep 25% slower than the
 // host-loop kernel on RMAT-24.
 __global__ void __launch_bounds__(kBlock, 6) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
-                                                               float* ca, float* cb, double d,
+                                                               double* ca, double* cb, double d,
                                                                double tol, double base, Ctl* ctl,
                                                                int64_t max_rounds, int cond_mode,
                                                                PrHubs h) {
@@ -624,7 +624,7 @@ cudaError_t launch_cc_compress(int32_t* parent, int64_t n, cudaStream_t st) {
   cc_compress_kernel<<<grid, 256, 0, st>>>(parent, n);
   return cudaGetLastError();
 }
-cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr, int64_t n,
+cudaError_t launch_pr_init(double* rank, double* contrib, const int64_t* row_ptr, int64_t n,
                            cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   note_launch();
@@ -632,7 +632,7 @@ cudaError_t launch_pr_init(double* rank, float* contrib, const int64_t* row_ptr,
   return cudaGetLastError();
 }
 cudaError_t launch_pr_sweep(const DevCSR& g, const double* rank_old, double* rank_new,
-                            const float* contrib, float* contrib_next, double d, double tol,
+                            const double* contrib, double* contrib_next, double d, double tol,
                             int64_t n_global, Ctl* ctl, int red_slot, int grid, const PrHubs& h,
                             cudaStream_t st) {
   const double base = (1.0 - d) / (double)n_global;
@@ -651,7 +651,7 @@ int pr_persistent_blocks_per_sm() {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pr_persistent_kernel, kBlock, 0);
   return nb;
 }
-cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, float* ca, float* cb,
+cudaError_t launch_pr_persistent(const DevCSR& g, double* ra, double* rb, double* ca, double* cb,
                                  double d, double tol, int64_t n_global, Ctl* ctl,
                                  int64_t max_rounds, int cond_mode, int grid, const PrHubs& hubs,
                                  cudaStream_t st) {
