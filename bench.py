@@ -67,11 +67,17 @@ class ClockSampler:
     a thread (nvidia-smi's 100 ms loop misses a region of a few tens of ms); nvidia-smi fallback."""
     NAMES = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, start=True):
         self.rows = []  # (sm_mhz, max_mhz, reasons bitmask-decoded tuple)
         self.stop_ev = threading.Event()
         self.proc = None
         self.t = None
+        self.gpu_index = gpu_index
+        if start:
+            self.start()
+
+    def start(self):
+        gpu_index = self.gpu_index
         try:
             import pynvml as N
             N.nvmlInit()
@@ -137,9 +143,9 @@ class ClockSampler:
 
 # ---- distributed plumbing (gloo for host-side barrier / reductions / NCCL id broadcast) ---------
 class Dist:
-    def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
+    def __init__(self, single=False):
+        self.world = 1 if single else int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = 0 if single else int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         if self.world > 1:
@@ -191,14 +197,36 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(op, scale):
+def kernel_source_hash():
+    """sha256 (16 hex) over the library's kernel sources and build flags: the stamp a committed
+    ncu capture carries, so a capture of an older kernel is never reported as this one's traffic."""
+    import glob
+    import hashlib
+    h = hashlib.sha256()
+    pkg = os.path.join(ROOT, "paper_1607_05707_b200")
+    files = sorted(glob.glob(os.path.join(pkg, "csrc", "*.cu")) + glob.glob(os.path.join(pkg, "csrc", "*.cuh"))
+                   + glob.glob(os.path.join(pkg, "csrc", "kernels.h")) + [os.path.join(pkg, "Makefile")])
+    for f in files:
+        with open(f, "rb") as fh:
+            h.update(os.path.basename(f).encode() + b"\0" + fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(op, scale, world=1, relabel=1):
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture of
+    this workload (profiles/ncu_<op>_rmat<scale>.json, written by tools/ncu_json.py); null when
+    the capture's kernel-source stamp differs from the current sources (stale) or is absent."""
+    if world > 1 or not relabel:
+        return None, "no capture for this configuration"
     p = os.path.join(ROOT, "profiles", f"ncu_{op}_rmat{scale}.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch"), d
     except Exception:
-        return None, None
+        return None, "no capture"
+    if d.get("source_hash") != kernel_source_hash():
+        return None, f"stale capture ({os.path.basename(p)}: source_hash {d.get('source_hash')} != {kernel_source_hash()})"
+    return d.get("dram_bytes_per_launch"), f"profiles/{os.path.basename(p)} (source_hash {d['source_hash']})"
 
 
 # ---- CPU arms --------------------------------------------------------------------------------------
@@ -206,6 +234,8 @@ def cpu_run(op, scale, steps, warmup, budget_s=None):
     """Oracle OpenMP BSP executor on host cores; returns (GTEPS, cores, sample, host graph)."""
     from oracle import oracle as O  # checker / CPU baseline only
     O.build()
+    # every host core: torchrun exports OMP_NUM_THREADS=1 per rank (only rank 0 runs this arm)
+    O.set_threads(len(os.sched_getaffinity(0)))
     og = O.rmat(scale)
     srcs = [int(s) for s in og.sources(16)]
     fn = O.sssp_bsp_omp if op == "sssp" else O.bfs_bsp_omp
@@ -226,21 +256,55 @@ def cpu_run(op, scale, steps, warmup, budget_s=None):
     return gteps, O.max_threads(), done, tot_t, og, srcs
 
 
+CPU_ALGO = {"sssp": "data-driven Bellman-Ford: every round relaxes all edges of the frontier, "
+                    "the IrGL SSSP program's semantics; no priority ordering",
+            "bfs": "Listing-2 top-down BFS, one level per round"}
+
+
+def cpu_serial(op, og, srcs, budget_s=10.0):
+    """CPU(i) of SURVEY §8d: the serial textbook algorithm on one core (queue BFS / binary-heap
+    Dijkstra), a bounded sample of the same sources."""
+    from oracle import oracle as O
+    deg = og.degrees()
+    tot_e, tot_t, done = 0, 0.0, 0
+    for s in srcs:
+        t0 = time.perf_counter()
+        res = O.sssp(og, s) if op == "sssp" else O.bfs(og, s)[0]
+        tot_t += time.perf_counter() - t0
+        tot_e += int(deg[res < INF].sum())
+        done += 1
+        if tot_t > budget_s:
+            break
+    return {"value": round(tot_e / 2 / tot_t / 1e9, 4), "unit": "GTEPS", "cores": 1,
+            "algorithm": "binary-heap Dijkstra" if op == "sssp" else "queue BFS",
+            "sample": f"{done} single-source traversals, {tot_t:.1f} s"}
+
+
+def scaling_of(args):
+    # N=1: configs[1] on one GPU; N>1: configs[4], one RMAT-27 graph split over the N GPUs
+    return "strong" if args.gpus > 1 else "weak"
+
+
 def run_reference(args, d):
     if d.rank != 0:
         return 0
     scale = args.scale
-    gteps, cores, done, tt, _, _ = cpu_run(args.op, scale, args.steps, args.warmup)
+    gteps, cores, done, tt, og, srcs = cpu_run(args.op, scale, args.steps, args.warmup,
+                                               budget_s=60.0 if scale > 24 else None)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS",
         "n_gpus": args.gpus, "steps": done, "warmup": args.warmup,
         "ms_per_step": round(tt / max(done, 1) * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "vs_baseline": None, "dtype": "int32",
         "data": "synthetic Philox RMAT (host-generated, identical to the device graph)",
-        "config": workload_config(args, None),
+        "scaling": scaling_of(args),
+        "config": workload_config(args, None, layout="generator (Philox-scrambled) ids, one host "
+                                                     "CSR (the CPU arm does not relabel)"),
         "cpu_baseline": {"value": round(gteps, 4), "unit": "GTEPS", "cores": cores, "kind": "port",
                          "sample": f"{done} single-source {args.op.upper()} traversals of "
-                                   f"RMAT-{scale} on the OpenMP bulk-synchronous IrGL executor"},
+                                   f"RMAT-{scale} on the OpenMP bulk-synchronous IrGL executor "
+                                   f"({CPU_ALGO[args.op]})",
+                         "serial": cpu_serial(args.op, og, srcs)},
         "e2e": {"value": round(gteps, 4), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -248,15 +312,19 @@ def run_reference(args, d):
     return 0
 
 
-def workload_config(args, g):
+def workload_config(args, g, layout=None):
     cfg = {"workload": f"{args.op.upper()}{'-DO' if args.direction and args.op == 'bfs' else ''} "
                        f"on RMAT-{args.scale} (edge factor 16, weights [1,255]), "
                        f"one traversal per step over 16 sources",
            "op": args.op, "graph": "rmat", "scale": args.scale, "edge_factor": 16,
            "sources": 16, "partitions": args.gpus, "outline": args.outline,
            "l2": "inputs larger than L2 (CSR col+weight >> 126 MB); no flush",
-           "layout": ("degree-ordered vertex relabelling (untimed preprocessing; API ids unchanged)"
-                      if args.relabel and args.gpus == 1 else "generator ids")}
+           "layout": layout or ("degree-ordered vertex relabelling (untimed preprocessing; API ids "
+                                "unchanged)" if args.relabel and args.gpus == 1 else
+                                "generator (Philox-scrambled) ids, 1D vertex partition"
+                                if args.gpus > 1 else "generator (Philox-scrambled) ids")}
+    if args.gpus > 1:
+        cfg["partition"] = "1D vertex ranges of ceil(N/P), one per GPU, NCCL exchange per round"
     if g is not None:
         cfg["n"] = int(g.n)
         cfg["m_directed"] = int(g.m)
@@ -264,10 +332,104 @@ def workload_config(args, g):
 
 
 # ---- GPU arm -----------------------------------------------------------------------------------------
+def _sources_and_work(ctx, g, p, d, relabelled):
+    """16 sources (the oracle's Philox stream over degrees in the caller's ids) and E_r / V_r per
+    source from one BFS each (BFS expands every reached vertex exactly once)."""
+    import paper_1607_05707_b200 as irgl
+    info = g.info
+    rp = _local_row_ptr(ctx, g)
+    lo, hi = info.lo, info.hi
+    if relabelled:  # degrees in the caller's ids for the source pick
+        dg = np.diff(rp)[g.perm()]
+        rp = np.zeros(g.n + 1, dtype=np.int64)
+        rp[1:] = np.cumsum(dg)
+
+    def local_deg(x):
+        return int(rp[x - lo + 1] - rp[x - lo]) if lo <= x < hi else 0
+
+    cand = pick_sources(g.n, lambda x: d.reduce(local_deg(x), "sum"))
+    er, vr = [], []
+    for s in cand:
+        p.init_scalars([s])
+        st = ctx.iterate(irgl.BFS, g, p)
+        er.append(d.reduce(st.edges, "sum"))
+        vr.append(d.reduce(st.popped, "sum"))
+    return cand, er, vr
+
+
+def _timed_traversals(args, d, ctx, g, p, op_id, cand, er, vr, kw, sampler=None):
+    """W untimed traversals, then K timed ones issued as one irgl_traverse_batch (or per-step
+    calls), CUDA events on the runtime's stream; returns the device numbers, max over ranks."""
+    import paper_1607_05707_b200 as irgl
+
+    def step(i):
+        p.init_scalars([cand[i % 16]])
+        return ctx.iterate(op_id, g, p, **kw)
+
+    for i in range(args.warmup):
+        step(i)
+    d.barrier()
+    ctx.sync()
+    if sampler is not None:
+        sampler.start()
+    l0 = irgl.launch_count()
+    ctx.event_record(0)
+    if args.batch:  # the K steps as one irgl_traverse_batch call (no per-step Python overhead)
+        stats = ctx.traverse_batch(op_id, g, p, [cand[(args.warmup + i) % 16] for i in range(args.steps)],
+                                   **kw)
+    else:
+        stats = [step(args.warmup + i) for i in range(args.steps)]
+    ctx.event_record(1)
+    ctx.sync()
+    launches = irgl.launch_count() - l0
+    dev_ms = ctx.event_elapsed(0, 1)
+    d.barrier()
+    clocks = sampler.stop() if sampler is not None else None
+    kms, tot_e, tot_b = 0.0, 0.0, 0.0
+    for i, st in enumerate(stats):
+        k = (args.warmup + i) % 16
+        kms += st.kernel_ms
+        tot_e += er[k]
+        # direction-optimising BFS examines fewer edges than E_r: bytes from the actual counter
+        # (SURVEY §8f F1); otherwise the fixed work-efficient formula of §8d
+        e_bytes = d.reduce(st.edges, "sum") if kw else er[k]
+        tot_b += algorithmic_bytes(args.op, vr[k], e_bytes)
+    return dict(dev_ms=d.reduce(dev_ms, "max"), kms=d.reduce(kms, "max"), tot_e=tot_e, tot_b=tot_b,
+                stats=stats, launches=int(d.reduce(launches, "sum")), clocks=clocks, step=step)
+
+
+def one_gpu_reference_point(args, op_id, kw, relabel):
+    """configs[4]'s one-GPU reference point (run by rank 0 before the partitioned run, on its own
+    GPU alone): the same RMAT-27 graph, sources and K steps in one partition."""
+    import paper_1607_05707_b200 as irgl
+    solo = Dist(single=True)
+    with irgl.Context(devices=[int(os.environ.get("LOCAL_RANK", "0"))], outline=args.outline) as c1:
+        g1 = c1.generate_rmat(args.scale)
+        if relabel:
+            g1.relabel()
+        p1 = c1.pipe(g1.n)
+        cand, er, vr = _sources_and_work(c1, g1, p1, solo, relabel)
+        r = _timed_traversals(args, solo, c1, g1, p1, op_id, cand, er, vr, kw)
+        gteps = r["tot_e"] / 2 / (r["dev_ms"] * 1e-3) / 1e9
+        out = {"value": round(gteps, 4), "unit": "GTEPS", "ms_per_step": round(r["dev_ms"] / args.steps, 4),
+               "layout": "degree-ordered ids" if relabel else "generator ids (the partitioned layout)"}
+        g1.close()
+        p1.close()
+    return out
+
+
 def run_irgl(args, d):
     import paper_1607_05707_b200 as irgl
     op_id = irgl.SSSP if args.op == "sssp" else irgl.BFS
+    kw = {"direction": 1} if (args.op == "bfs" and args.direction) else {}
+    one_gpu = None
     if d.world > 1:
+        # the scaling denominator of configs[4]: rank 0 alone on its GPU first (others wait)
+        if d.rank == 0 and not args.no_one_gpu_point:
+            one_gpu = {"generator_ids": one_gpu_reference_point(args, op_id, kw, relabel=False)}
+            if args.relabel:
+                one_gpu["degree_ordered"] = one_gpu_reference_point(args, op_id, kw, relabel=True)
+        d.barrier()
         uid = d.bcast_bytes(irgl.nccl_unique_id() if d.rank == 0 else None)
         ctx = irgl.Context(nccl=(d.local_rank, d.rank, d.world, uid), outline=args.outline)
     else:
@@ -283,71 +445,22 @@ def run_irgl(args, d):
         g.relabel()
         relabel_s = time.time() - t0
     info = g.info
-    # local degrees -> sources (Philox stream of the oracle), agreed across ranks
-    rp = _local_row_ptr(ctx, g)
-    lo, hi = info.lo, info.hi
-    if relabel_s is not None:  # degrees in the caller's ids for the source pick
-        dg = np.diff(rp)[g.perm()]
-        rp = np.zeros(g.n + 1, dtype=np.int64)
-        rp[1:] = np.cumsum(dg)
-
-    def local_deg(x):
-        return int(rp[x - lo + 1] - rp[x - lo]) if lo <= x < hi else 0
-
-    cand = pick_sources(g.n, lambda x: d.reduce(local_deg(x), "sum"))
     p = ctx.pipe(max(info.local_n, 1) if d.world > 1 else g.n)
+    cand, er, vr = _sources_and_work(ctx, g, p, d, relabel_s is not None)
 
-    # E_r / V_r per source from one BFS each (BFS expands every reached vertex exactly once)
-    er, vr = [], []
-    for s in cand:
-        p.init_scalars([s])
-        st = ctx.iterate(irgl.BFS, g, p)
-        er.append(d.reduce(st.edges, "sum"))
-        vr.append(d.reduce(st.popped, "sum"))
-
-    kw = {"direction": 1} if (args.op == "bfs" and args.direction) else {}
-
-    def step(i):
-        s = cand[i % 16]
-        p.init_scalars([s])
-        return ctx.iterate(op_id, g, p, **kw)
-
-    for i in range(args.warmup):
-        step(i)
     # ---- device-timed region: inputs resident in HBM
-    d.barrier()
-    ctx.sync()
-    sampler = ClockSampler(d.local_rank) if d.rank == 0 else None
-    l0 = irgl.launch_count()
-    ctx.event_record(0)
-    kms, tot_e, tot_b = 0.0, 0.0, 0.0
-    if args.batch:  # the K steps as one irgl_traverse_batch call (no per-step Python overhead)
-        stats = ctx.traverse_batch(op_id, g, p, [cand[(args.warmup + i) % 16] for i in range(args.steps)],
-                                   **kw)
-    else:
-        stats = [step(args.warmup + i) for i in range(args.steps)]
-    ctx.event_record(1)
-    ctx.sync()
-    for i, st in enumerate(stats):
-        k = (args.warmup + i) % 16
-        kms += st.kernel_ms
-        tot_e += er[k]
-        # direction-optimising BFS examines fewer edges than E_r: bytes from the actual counter
-        # (SURVEY §8f F1); otherwise the fixed work-efficient formula of §8d
-        e_bytes = d.reduce(st.edges, "sum") if kw else er[k]
-        tot_b += algorithmic_bytes(args.op, vr[k], e_bytes)
-    dev_ms = ctx.event_elapsed(0, 1)
-    launches = irgl.launch_count() - l0
-    d.barrier()
-    clocks = sampler.stop() if sampler else None
-    dev_ms = d.reduce(dev_ms, "max")
-    kms = d.reduce(kms, "max")
+    sampler = ClockSampler(d.local_rank, start=False) if d.rank == 0 else None
+    r = _timed_traversals(args, d, ctx, g, p, op_id, cand, er, vr, kw, sampler)
+    dev_ms, kms, tot_e, tot_b, stats = r["dev_ms"], r["kms"], r["tot_e"], r["tot_b"], r["stats"]
+    step = r["step"]
     gteps = tot_e / 2 / (dev_ms * 1e-3) / 1e9
 
     # ---- end to end through the public API: host source in, host distances out (pinned).  Queries
     # are pipelined the way a serving loop would issue them: each step's result copy is queued
     # (irgl_read_result_async) and overlaps the next traversal, which writes the graph's second
     # label buffer; every copy has landed before the timed region closes (irgl_results_wait).
+    # At N>1 each rank copies its own vertex range (the result is distributed like the graph).
+    nres = int(info.local_n) if d.world > 1 else int(g.n)
     try:
         import torch
         host_out = [torch.empty(g.n, dtype=torch.int32, pin_memory=True).numpy() for _ in range(2)]
@@ -378,38 +491,43 @@ def run_irgl(args, d):
     for _ in range(4):
         ctx.read_result_async(op_id, g, host_out[0])
         ctx.results_wait()
-    d2h_gbps = 4 * 4 * int(g.n) / (time.perf_counter() - t1) / 1e9
+    d2h_gbps = 4 * 4 * nres / (time.perf_counter() - t1) / 1e9
 
     peak, peak_kind = load_peaks()
     achieved = tot_b / (kms * 1e-3) / 1e9 if kms > 0 else None
-    traffic, ncu = ncu_traffic(args.op, args.scale)
+    traffic, traffic_note = ncu_traffic(args.op, args.scale, d.world, args.relabel)
+    assert d.world == args.gpus, (d.world, args.gpus)
     line = {
         "metric": METRIC, "value": round(gteps, 4), "unit": "GTEPS", "n_gpus": d.world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dev_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "scaling": scaling_of(args), "vs_baseline": None, "dtype": "int32",
         "data": "synthetic: device Philox RMAT (Graph500 .57/.19/.19/.05, ef 16, scrambled ids, "
                 "seed 1), int32 weights in [1,255] (seed 11)",
         "config": workload_config(args, g),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                      "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4) if achieved else None,
-                     "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic": traffic, "traffic_source": traffic_note, "peak_kind": peak_kind,
                      "kernel": (f"persistent_kernel<{args.op.upper()}> (outlined Iterate)"
                                 if not kw else "persistent_bfs_do_kernel (outlined, direction-optimising)")
-                     if args.outline != 0 else "expand_kernel + chunk_kernel",
+                     if args.outline != 0 and d.world == 1 else "expand_kernel + chunk_kernel",
                      "algorithmic_bytes_per_step": round(tot_b / args.steps),
                      "kernel_ms_per_step": round(kms / args.steps, 4)},
-        "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": 8,
+        "e2e": {"value": round(e2e, 4), "unit": "GTEPS", "h2d_bytes_per_step": 8 * d.world,
                 "d2h_bytes_per_step": 4 * int(g.n), "d2h_GBps_alone": round(d2h_gbps, 1)},
-        "gpu_launches": int(launches),
-        "clocks": clocks,
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
         "detail": {"gen_s": round(gen_s, 3), "relabel_s": round(relabel_s, 3) if relabel_s else None, "rounds_per_step": float(np.mean([s.rounds for s in stats])),
                    "edges_scanned_per_step": float(np.mean([s.edges for s in stats])),
                    "E_r_mean": float(np.mean(er)), "V_r_mean": float(np.mean(vr)),
                    "outlined": int(stats[-1].outlined) if stats else None,
                    "directed_edges_per_s": round(tot_e / (dev_ms * 1e-3), 1)},
     }
+    if d.world > 1:
+        line["detail"]["exchange_bytes_per_step"] = float(np.mean([s.exchange_bytes for s in stats]))
+        if one_gpu:
+            line["detail"]["one_gpu"] = one_gpu  # scaling denominator: same graph on one GPU
     # ---- CPU baseline (rank 0, N=1 only): oracle OpenMP executor on the host cores
     if d.world == 1 and not args.no_cpu_baseline:
         cg, cores, done, tt, og, osrc = cpu_run(args.op, args.scale, 16, 1, budget_s=12.0)
@@ -417,7 +535,8 @@ def run_irgl(args, d):
                                 "kind": "port",
                                 "sample": f"{done} single-source {args.op.upper()} traversals of "
                                           f"RMAT-{args.scale} (OpenMP bulk-synchronous IrGL "
-                                          f"executor, {tt:.1f} s)"}
+                                          f"executor, {CPU_ALGO[args.op]}; {tt:.1f} s)",
+                                "serial": cpu_serial(args.op, og, osrc[:4], budget_s=8.0)}
         # parity of the measured workload: GPU result == oracle for source 0
         from oracle import oracle as O
         assert osrc == cand, "source selection differs from the oracle"
@@ -441,6 +560,23 @@ def _local_row_ptr(ctx, g):
     return rp
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(n):
+    """`python bench.py --gpus N` without a launcher: start the N ranks ourselves (one process per
+    GPU, the same torchrun command the driver uses) and pass rank 0's JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, IRGL_BENCH_SELF_LAUNCHED="1")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -451,6 +587,8 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-one-gpu-point", action="store_true",
+                    help="N>1: skip the one-GPU RMAT-27 reference point in detail.one_gpu")
     ap.add_argument("--batch", type=int, default=1,
                     help="1: the K steps as one irgl_traverse_batch call; 0: one Python-level "
                          "init/iterate/read per step")
@@ -459,11 +597,16 @@ def main():
     ap.add_argument("--direction", type=int, default=0,
                     help="BFS: 1 = direction-optimising (SURVEY §8f F1), 0 = Listing-2 top-down")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
     d = Dist()
-    if d.world > 1:
-        args.gpus = d.world
+    if d.world > 1 and args.gpus != d.world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={d.world}")
+    args.gpus = d.world
     if args.scale <= 0:
-        args.scale = 22 + int(round(math.log2(max(args.gpus, 1))))
+        # N=1: configs[1] (SSSP RMAT-22); N>1: configs[4] (RMAT-27 vertex-partitioned over the N
+        # GPUs, total work fixed -> strong scaling)
+        args.scale = 22 if args.gpus == 1 else 27
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args, d)

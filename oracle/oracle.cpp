@@ -712,6 +712,7 @@ extern "C" int orc_iterate(const orc_graph* g, const orc_iter_cfg* cfg, const in
 // ------------------------------------------------------------------------------------------
 // OpenMP bulk-synchronous BFS / SSSP — the timed CPU baseline.
 extern "C" int orc_max_threads(void) { return omp_get_max_threads(); }
+extern "C" void orc_set_threads(int t) { if (t > 0) omp_set_num_threads(t); }
 
 extern "C" int64_t orc_bfs_bsp_omp(const orc_graph* g, int64_t src, int32_t* level, int threads,
                                    int64_t* edges_out) {

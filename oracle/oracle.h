@@ -144,6 +144,7 @@ int64_t orc_bfs_bsp_omp(const orc_graph* g, int64_t src, int32_t* level, int thr
 int64_t orc_sssp_bsp_omp(const orc_graph* g, int64_t src, int32_t* dist, int threads,
                          int64_t* edges_out);
 int orc_max_threads(void);
+void orc_set_threads(int t); /* omp_set_num_threads (torchrun exports OMP_NUM_THREADS=1) */
 
 /* Certificates over a borrowed CSR (symmetric graph, symmetric weights); 0 = holds, else a bit
  * mask of the violated clauses (1 source, 2 edge leaves the reached set, 4 edge inequality,

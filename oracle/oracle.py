@@ -102,6 +102,7 @@ def lib():
         L.orc_sssp_bsp_omp.restype = C.c_int64
         L.orc_sssp_bsp_omp.argtypes = [P, C.c_int64, i32p, C.c_int, i64p]
         L.orc_max_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
         L.orc_cert_bfs.restype = C.c_int
         L.orc_cert_bfs.argtypes = [C.c_int64, i64p, i32p, C.c_int64, i32p]
         L.orc_cert_sssp.restype = C.c_int
@@ -283,6 +284,10 @@ def sssp_bsp_omp(g: Graph, src: int, threads=0):
     e = C.c_int64(0)
     r = lib().orc_sssp_bsp_omp(g.handle, src, _p(dist, C.c_int32), threads, C.byref(e))
     return dist, int(r), int(e.value)
+
+
+def set_threads(t: int):
+    lib().orc_set_threads(int(t))
 
 
 def max_threads() -> int:
