@@ -99,7 +99,9 @@ typedef struct irgl_config {
   int32_t cta_threshold;         /* rounds with at most one tile per warp: degrees below this are
                                     expanded by the popping warp (no chunk phase); 0 -> 256      */
   int32_t chunk_edges;           /* edges per chunk descriptor (<= 65535); 0 -> 512            */
-  int32_t l2_persist;            /* 1: L2 persisting access-policy window on label arrays      */
+  int32_t l2_persist;            /* 1: L2 persisting access-policy window on the array the outlined
+                                    kernels gather per edge (labels / distances, BFS visited
+                                    bitmap), sized to the device set-aside                      */
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
   int32_t dense_div;             /* outlined rounds whose frontier has >= n/dense_div vertices run
                                     dense: relaxations mark (fire-and-forget stores / REDs) and a

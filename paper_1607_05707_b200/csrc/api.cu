@@ -30,6 +30,9 @@ struct PartRT {  // one vertex partition hosted by this process
   // traversal i's results are read on the host
   Ctl* h_snap[2] = {nullptr, nullptr};
   cudaEvent_t bev[2][4] = {};
+  // L2 persisting window currently set on `st` (l2_window)
+  const void* l2_base = nullptr;
+  size_t l2_bytes = 0;
 };
 }  // namespace irgl
 
@@ -1023,6 +1026,51 @@ static void fill_persist_args(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int
   }
 }
 
+// ---- L2 persisting window (irgl_config.l2_persist) ----------------------
+// The outlined kernels gather one label (or visited-bitmap word) per edge while the CSR streams
+// through L2 once; marking the gathered array "persisting" keeps it from being evicted by the
+// stream.  One window per stream: it covers the array the hot loop gathers (SSSP / CC_LP: the
+// distance / label array; BFS with the visited bitmap: the bitmap, else the level array), at
+// most the device's set-aside.  IRGL_L2_PERSIST=0/1 overrides the config flag (A/B tuning).
+static bool l2_persist_on(irgl_ctx* ctx) {
+  const char* e = getenv("IRGL_L2_PERSIST");
+  return e ? atoi(e) != 0 : ctx->cfg.l2_persist != 0;
+}
+static irgl_status_t l2_window(irgl_ctx* ctx, PartRT& pr, const void* base, size_t bytes) {
+  if (!l2_persist_on(ctx)) base = nullptr, bytes = 0;
+  if (base == pr.l2_base && bytes == pr.l2_bytes) return IRGL_OK;  // the stream's window already
+  pr.l2_base = base;
+  pr.l2_bytes = bytes;
+  cudaStreamAttrValue v{};
+  if (base && bytes) {
+    int maxwin = 0, maxset = 0;
+    CK(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, pr.dev));
+    CK(cudaDeviceGetAttribute(&maxset, cudaDevAttrMaxPersistingL2CacheSize, pr.dev));
+    size_t setaside = 0;
+    CK(cudaDeviceGetLimit(&setaside, cudaLimitPersistingL2CacheSize));
+    const size_t want = std::min<size_t>(bytes, (size_t)maxset);
+    if (setaside < want) {
+      CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+      CK(cudaDeviceGetLimit(&setaside, cudaLimitPersistingL2CacheSize));
+    }
+    const size_t win = std::min<size_t>(bytes, (size_t)maxwin);
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = setaside >= win ? 1.0f : (float)setaside / (float)win;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    v.accessPolicyWindow.num_bytes = 0;  // no window (also clears an earlier one)
+  }
+  CK(cudaStreamSetAttribute(pr.st, cudaStreamAttributeAccessPolicyWindow, &v));
+  return IRGL_OK;
+}
+static irgl_status_t l2_window_for(irgl_ctx* ctx, PartRT& pr, irgl_graph* g, GraphPart& gp, int op,
+                                   const uint32_t* visk) {
+  if (op == IRGL_OP_BFS && visk) return l2_window(ctx, pr, visk, ((size_t)g->n + 31) / 32 * 4);
+  return l2_window(ctx, pr, gp.lab, (size_t)g->n * 4);
+}
+
 // ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
 static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                        int64_t level0, const irgl_iterate_opts& o,
@@ -1063,6 +1111,10 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   // reads levels anyway: RMAT-22 0.193 vs 0.204 ms with the bitmap)
   uint32_t* visk = gp.vis_k();
   if (pa.dir_opt && ctx->cfg.bfs_bitmap_min_n == 0 && g->n < (12ll << 20)) visk = nullptr;
+  {
+    irgl_status_t ls = l2_window_for(ctx, pr, g, gp, op, visk);
+    if (ls != IRGL_OK) return ls;
+  }
   CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, visk, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
   CK(cudaEventRecord(ctx->kev1, pr.st));
   // (a kernel writing host-mapped memory instead was slower with an async readback in flight:
@@ -2488,6 +2540,7 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
     uint32_t* visk = gp.vis_k();
     if (pa.dir_opt && ctx->cfg.bfs_bitmap_min_n == 0 && g->n < (12ll << 20)) visk = nullptr;
     CK(launch_ctl_prepare(pp.ctl, pr.st));
+    if ((s = l2_window_for(ctx, pr, g, gp, op, visk)) != IRGL_OK) return s;
     CK(cudaEventRecord(pr.bev[b][1], pr.st));
     CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, visk, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));
     CK(cudaEventRecord(pr.bev[b][2], pr.st));

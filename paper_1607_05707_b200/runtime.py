@@ -283,7 +283,7 @@ class Context:
 
     def __init__(self, devices=(0,), *, outline=-1, blocks_per_sm=0, retry_serialize_after=0,
                  warp_threshold=0, cta_threshold=0, chunk_edges=0, logical_partitions=0,
-                 dense_div=0, bfs_bitmap_min_n=0, nccl=None):
+                 dense_div=0, bfs_bitmap_min_n=0, l2_persist=0, nccl=None):
         L = load_library()
         cfg = Config()
         cfg.outline = outline
@@ -295,6 +295,7 @@ class Context:
         cfg.logical_partitions = logical_partitions
         cfg.dense_div = dense_div
         cfg.bfs_bitmap_min_n = bfs_bitmap_min_n
+        cfg.l2_persist = l2_persist
         h = C.c_void_p()
         if nccl is not None:  # (device, rank, nranks, uid)
             dev, rank, nranks, uid = nccl

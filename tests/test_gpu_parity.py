@@ -590,3 +590,19 @@ def test_pagerank_parity_rmat18(ctx, irgl, oracle):
         err = np.abs(r - ref).sum() / np.abs(ref).sum()
         assert err <= 1e-6, err
         assert st.rounds == it, (st.rounds, it)
+
+
+def test_l2_persist_window_same_results(irgl, oracle):
+    """irgl_config.l2_persist = 1 (L2 persisting window over the gathered array):
+    same levels and distances as without; measured slower or neutral (profiles/r2_rejected.txt)."""
+    og = oracle.rmat(14)
+    with irgl.Context(l2_persist=1) as c:
+        g = c.graph_from_csr(og.row_ptr, og.col, og.weight)
+        for relabel in (False, True):
+            if relabel:
+                g.relabel()
+            for s in og.sources(2):
+                lv, _ = irgl.bfs(c, g, int(s), outline=1)
+                np.testing.assert_array_equal(lv, oracle.bfs(og, int(s))[0])
+                d, _ = irgl.sssp(c, g, int(s), outline=1)
+                np.testing.assert_array_equal(d, oracle.sssp(og, int(s)))
