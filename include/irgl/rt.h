@@ -299,6 +299,48 @@ irgl_status_t irgl_t_control(const irgl_block_constraint* cs, int n, int32_t* ou
 irgl_status_t irgl_op_plan(irgl_ctx* ctx, irgl_op op, irgl_block_constraint* block,
                            int32_t* grid_outlined, int32_t* grid_fixed);
 
+/* ---- multi-member Pipe (ast.hpp:206-210) -------- */
+/* A Pipe body as a list of member statements over the pipe's shared {in, out, retry}: each stage
+ * is an Invoke or an Iterate of one operator; a stage may be guarded by the previous stage's
+ * reduced return value (dynamic piping, Listing 4).  Looping Pipe: the body repeats
+ * while `in` is non-empty at the start of a pass; Pipe Once: one pass. */
+typedef enum { IRGL_STAGE_INVOKE = 0, IRGL_STAGE_ITERATE = 1 } irgl_stage_kind;
+typedef enum { IRGL_WHEN_ALWAYS = 0, IRGL_WHEN_PREV_TRUE = 1, IRGL_WHEN_PREV_FALSE = 2 } irgl_stage_when;
+typedef struct irgl_pipe_stage {
+  int32_t op;         /* member kernel (irgl_op)                                                 */
+  int32_t kind;       /* irgl_stage_kind                                                         */
+  int32_t reduction;  /* Any|All return cell of each invocation                                  */
+  int32_t when;       /* irgl_stage_when                                                         */
+  int32_t cond_mode;  /* Iterate stage: While|Until on the reduced value                         */
+  int32_t reserved0;
+  int64_t max_rounds; /* Iterate stage: ExtraCond rounds >= max_rounds (Or)                     */
+  irgl_block_constraint block; /* the member kernel's block-size domain      */
+  irgl_op_args args;
+} irgl_pipe_stage;
+typedef struct irgl_pipe_opts {
+  int32_t once;       /* 1: Pipe Once                                                            */
+  int32_t outline;    /* 1: one cooperative control kernel launched at T_control (error
+                         IRGL_E_OUTLINE_EMPTY when the members' domains do not intersect, or
+                         IRGL_E_UNSUPPORTED for members without a device body on that path);
+                         0: host-orchestrated; -1: outlined when possible, else host (the SPEC's
+                         fallback "with a warning")                                */
+  int64_t max_rounds; /* looping Pipe: at most this many passes (0 = until empty)               */
+  int32_t reserved[4];
+} irgl_pipe_opts;
+typedef struct irgl_pipe_result {
+  int32_t outlined;       /* 1 if the Pipe ran as one control kernel                            */
+  int32_t block;          /* control kernel block size (T_control), 0 when host-orchestrated    */
+  int32_t last_reduced;   /* the last executed invocation's return value, -1 if none            */
+  int32_t reserved0;
+  int32_t stage_reduced[8]; /* per stage: its last invocation's return value, -1 if none          */
+} irgl_pipe_result;
+/* Members on the outlined path: the test operators COUNTDOWN, RETRY_ODD, RESPAWN_ODD, REDUCE,
+ * NOPUSH, PUSHPOP (at most 8 stages); the host path takes any worklist operator. */
+irgl_status_t irgl_pipe_run(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g /*nullable*/,
+                            const irgl_pipe_stage* stages, int32_t nstages,
+                            const irgl_pipe_opts* opts, irgl_iter_stats* stats /*nullable*/,
+                            irgl_pipe_result* result /*nullable*/);
+
 #ifdef __cplusplus
 }
 #endif

@@ -490,6 +490,7 @@ static int launch_wl(OpState& st, PipeCtx& p, int reduction, bool serial) {
           if (n + 1 < st.cfg->guard) push.push_back(n + 1);
           break;
         case ORC_OP_TEST_RETRY_ODD:
+        case ORC_OP_TEST_RESPAWN_ODD:
           if ((n & 1) && st.rcount[n] < (st.cfg->guard > 0 ? st.cfg->guard : 1)) {
             st.rcount[n]++;
             retry.push_back(n);  // Retry n
@@ -702,6 +703,104 @@ extern "C" int orc_iterate(const orc_graph* g, const orc_iter_cfg* cfg, const in
   if (final_in && final_in_len) {
     int64_t cap = *final_in_len;
     int64_t k = std::min<int64_t>(cap, (int64_t)p.in.items.size());
+    for (int64_t i = 0; i < k; ++i) final_in[i] = p.in.items[i];
+    *final_in_len = (int64_t)p.in.items.size();
+  }
+  if (stats) *stats = s;
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// Multi-member Pipe: member statements over one pipe context (see oracle.h).  Each Invoke is the
+// run_pipe swap protocol of orc_iterate: launch; while retry != {}: swap
+// in<->retry, relaunch with out kept (serialised after retry_serialize_after rounds unless the
+// operator uses Respawn); then swap in<->out.
+extern "C" int orc_pipe_run(const orc_pipe_stage* stages, int n, int once, int64_t max_rounds,
+                            int64_t cap, const int64_t* init, int64_t ninit, const int32_t* values,
+                            int retry_serialize_after, int32_t* rcount, int32_t* log,
+                            int32_t* stage_reduced, orc_stats* stats, int64_t* final_in,
+                            int64_t* final_in_len) {
+  if (!stages || n < 1 || cap < 1 || ninit > cap) return -1;
+  orc_stats s;
+  std::memset(&s, 0, sizeof(s));
+  s.last_reduced = -1;
+  PipeCtx p;
+  p.cap = cap;
+  for (int64_t i = 0; i < ninit; ++i) p.in.items.push_back(init[i]);
+  OpState st;
+  st.g = nullptr;
+  st.values = values;
+  st.round = 1;
+  st.rcount.assign(cap, 0);
+  st.popped_at.assign(cap, -1);
+  const int rsa = retry_serialize_after > 0 ? retry_serialize_after : 4;
+  std::vector<orc_iter_cfg> cfgs(n);
+  for (int k = 0; k < n; ++k) {
+    if (stages[k].op < ORC_OP_TEST_COUNTDOWN || stages[k].op > ORC_OP_TEST_RESPAWN_ODD ||
+        stages[k].op == 105)
+      return -1;
+    std::memset(&cfgs[k], 0, sizeof(orc_iter_cfg));
+    cfgs[k].op = stages[k].op;
+    cfgs[k].reduction = stages[k].reduction;
+    cfgs[k].guard = stages[k].guard;
+    cfgs[k].threads = 1;  // one ordered thread: item order inside a worklist is immaterial
+    if (stage_reduced) stage_reduced[k] = -1;
+  }
+  auto invoke = [&](int k) {
+    const orc_iter_cfg& cfg = cfgs[k];
+    st.cfg = &cfg;
+    int red = launch_wl(st, p, cfg.reduction, false);
+    s.launches++;
+    s.popped += (int64_t)p.in.items.size();
+    int retry_rounds = 0;
+    while (!p.retry.items.empty()) {
+      std::swap(p.in, p.retry);
+      p.retry.items.clear();
+      p.in.epoch++;
+      s.retries += (int64_t)p.in.items.size();
+      ++retry_rounds;
+      const bool serial = cfg.op != ORC_OP_TEST_RESPAWN_ODD && retry_rounds > rsa;
+      if (serial) s.serial_launches++;
+      const int r2 = launch_wl(st, p, cfg.reduction, serial);
+      if (cfg.reduction == ORC_RED_ANY) red = red | r2;
+      if (cfg.reduction == ORC_RED_ALL) red = red & r2;
+      s.launches++;
+      s.popped += (int64_t)p.in.items.size();
+    }
+    s.pushes += (int64_t)p.out.items.size();
+    std::swap(p.in, p.out);
+    p.out.items.clear();
+    p.in.epoch++;
+    p.out.epoch = p.in.epoch;
+    return cfg.reduction == ORC_RED_NONE ? -1 : red;
+  };
+  int prev = -1;
+  int64_t passes = 0;
+  for (;;) {
+    if (!once && p.in.items.empty()) break;
+    for (int k = 0; k < n; ++k) {
+      const orc_pipe_stage& S = stages[k];
+      if (S.when == 1 && prev != 1) continue;
+      if (S.when == 2 && prev != 0) continue;
+      for (int64_t it = 0;; ++it) {
+        if (S.kind == 1 && (p.in.items.empty() || (S.max_rounds > 0 && it >= S.max_rounds))) break;
+        prev = invoke(k);
+        if (p.overflow) return -2;
+        if (stage_reduced) stage_reduced[k] = prev;
+        if (S.kind == 0) break;
+        if (S.cond_mode == ORC_COND_WHILE && prev == 0) break;
+        if (S.cond_mode == ORC_COND_UNTIL && prev == 1) break;
+      }
+    }
+    ++passes;
+    if (once || (max_rounds > 0 && passes >= max_rounds)) break;
+  }
+  s.rounds = passes;
+  s.last_reduced = prev;
+  if (rcount) std::memcpy(rcount, st.rcount.data(), cap * sizeof(int32_t));
+  if (log) std::memcpy(log, st.popped_at.data(), cap * sizeof(int32_t));
+  if (final_in && final_in_len) {
+    const int64_t k = std::min<int64_t>(*final_in_len, (int64_t)p.in.items.size());
     for (int64_t i = 0; i < k; ++i) final_in[i] = p.in.items[i];
     *final_in_len = (int64_t)p.in.items.size();
   }

@@ -88,7 +88,8 @@ enum { ORC_OP_BFS = 0, ORC_OP_SSSP = 1, ORC_OP_CC = 2, ORC_OP_PR = 3, ORC_OP_TC 
        ORC_OP_TEST_RETRY_ODD = 101,   /* odd items retried once, then pushed */
        ORC_OP_TEST_REDUCE = 102,      /* ReduceAndReturn(values[x]) per item */
        ORC_OP_TEST_NOPUSH = 103,      /* pops, never pushes */
-       ORC_OP_TEST_PUSHPOP = 104      /* pushes x+guard, records what it popped */
+       ORC_OP_TEST_PUSHPOP = 104,     /* pushes x+guard, records what it popped */
+       ORC_OP_TEST_RESPAWN_ODD = 106  /* RETRY_ODD through Respawn: never serialised */
 };
 enum { ORC_RED_NONE = 0, ORC_RED_ANY = 1, ORC_RED_ALL = 2 };
 enum { ORC_COND_NONE = 0, ORC_COND_WHILE = 1, ORC_COND_UNTIL = 2 };
@@ -129,6 +130,24 @@ typedef struct {
 int orc_iterate(const orc_graph* g, const orc_iter_cfg* cfg, const int64_t* init, int64_t ninit,
                 int from_array, const int32_t* values, void* node_out, orc_stats* stats,
                 int64_t* trace, int64_t trace_cap, int64_t* final_in, int64_t* final_in_len);
+
+/* Multi-member Pipe (ast.hpp:206-210): one pipe
+ * context {in, out, retry} shared by the member statements, each an Invoke (kind 0) or an
+ * Iterate (kind 1: until in is empty [Or rounds >= max_rounds], While|Until on the reduced value)
+ * of a test operator; `when` guards a stage on the previous invocation's reduced value (0
+ * always, 1 previous true, 2 previous false: dynamic piping, Listing 4).  Looping Pipe
+ * (once = 0): repeat the body while `in` is non-empty at the start of a pass [at most max_rounds
+ * passes]; Pipe Once: one pass.  rcount/log (cap entries, log initialised to -1 by the caller)
+ * are the test operators' per-item state; stage_reduced[k] = last return value of stage k.
+ * stats->rounds = passes.  Returns 0, -2 on worklist overflow, -1 on invalid input. */
+typedef struct {
+  int op, kind, reduction, when, cond_mode;
+  int64_t max_rounds, guard;
+} orc_pipe_stage;
+int orc_pipe_run(const orc_pipe_stage* stages, int n, int once, int64_t max_rounds, int64_t cap,
+                 const int64_t* init, int64_t ninit, const int32_t* values,
+                 int retry_serialize_after, int32_t* rcount, int32_t* log, int32_t* stage_reduced,
+                 orc_stats* stats, int64_t* final_in, int64_t* final_in_len);
 
 /* Invoke once (no loop) of a non-worklist reduce kernel over `n` items: the ReduceAndReturn
  * fold with identities Any->0, All->1. */

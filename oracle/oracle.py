@@ -20,6 +20,9 @@ INF = 2147483647
 OP_BFS, OP_SSSP, OP_CC, OP_PR, OP_TC, OP_CC_LP = 0, 1, 2, 3, 4, 5
 OP_TEST_COUNTDOWN, OP_TEST_RETRY_ODD, OP_TEST_REDUCE, OP_TEST_NOPUSH, OP_TEST_PUSHPOP = (
     100, 101, 102, 103, 104)
+OP_TEST_RESPAWN_ODD = 106
+STAGE_INVOKE, STAGE_ITERATE = 0, 1
+WHEN_ALWAYS, WHEN_PREV_TRUE, WHEN_PREV_FALSE = 0, 1, 2
 RED_NONE, RED_ANY, RED_ALL = 0, 1, 2
 COND_NONE, COND_WHILE, COND_UNTIL = 0, 1, 2
 COMB_OR, COMB_AND = 0, 1
@@ -37,6 +40,11 @@ class IterCfg(C.Structure):
                 ("extra_comb", C.c_int), ("max_rounds", C.c_int64), ("round_start", C.c_int64),
                 ("guard", C.c_int64), ("retry_serialize_after", C.c_int), ("threads", C.c_int),
                 ("pr_d", C.c_double), ("pr_tol", C.c_double), ("capacity", C.c_int64)]
+
+
+class PipeStage(C.Structure):
+    _fields_ = [("op", C.c_int), ("kind", C.c_int), ("reduction", C.c_int), ("when", C.c_int),
+                ("cond_mode", C.c_int), ("max_rounds", C.c_int64), ("guard", C.c_int64)]
 
 
 def build(force: bool = False) -> str:
@@ -102,6 +110,10 @@ def lib():
         L.orc_sssp_bsp_omp.restype = C.c_int64
         L.orc_sssp_bsp_omp.argtypes = [P, C.c_int64, i32p, C.c_int, i64p]
         L.orc_max_threads.restype = C.c_int
+        L.orc_pipe_run.restype = C.c_int
+        L.orc_pipe_run.argtypes = [C.POINTER(PipeStage), C.c_int, C.c_int, C.c_int64, C.c_int64,
+                                   i64p, C.c_int64, i32p, C.c_int, i32p, i32p, i32p,
+                                   C.POINTER(Stats), i64p, i64p]
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_cert_bfs.restype = C.c_int
         L.orc_cert_bfs.argtypes = [C.c_int64, i64p, i32p, C.c_int64, i32p]
@@ -311,3 +323,29 @@ def cert_sssp(row_ptr, col, w, src: int, dist) -> int:
     d = np.ascontiguousarray(dist, dtype=np.int32)
     return int(lib().orc_cert_sssp(len(rp) - 1, _p(rp, C.c_int64), _p(cl, C.c_int32),
                                    _p(ww, C.c_int32), src, _p(d, C.c_int32)))
+
+
+def pipe_run(stages, init, cap, *, once=False, max_rounds=0, values=None, retry_serialize_after=4):
+    """Multi-member Pipe of test operators (see oracle.h).  stages: dicts with op, kind,
+    reduction, when, cond_mode, max_rounds, guard.  Returns (stats, final_in, rcount, log,
+    stage_reduced)."""
+    n = len(stages)
+    arr = (PipeStage * n)(*[PipeStage(d.get("op"), d.get("kind", STAGE_INVOKE),
+                                      d.get("reduction", RED_NONE), d.get("when", WHEN_ALWAYS),
+                                      d.get("cond_mode", COND_NONE), d.get("max_rounds", 0),
+                                      d.get("guard", 0)) for d in stages])
+    init = np.ascontiguousarray(np.asarray(init, dtype=np.int64))
+    vals = np.ascontiguousarray(values, dtype=np.int32) if values is not None else None
+    rc = np.zeros(cap, dtype=np.int32)
+    log = np.zeros(cap, dtype=np.int32)
+    red = np.zeros(n, dtype=np.int32)
+    fin = np.zeros(cap, dtype=np.int64)
+    fl = C.c_int64(cap)
+    st = Stats()
+    r = lib().orc_pipe_run(arr, n, int(once), max_rounds, cap, _p(init, C.c_int64), len(init),
+                           _p(vals, C.c_int32) if vals is not None else None, retry_serialize_after,
+                           _p(rc, C.c_int32), _p(log, C.c_int32), _p(red, C.c_int32), C.byref(st),
+                           _p(fin, C.c_int64), C.byref(fl))
+    if r != 0:
+        raise RuntimeError(f"orc_pipe_run failed rc={r}")
+    return st, fin[: min(fl.value, cap)].copy(), rc, log, red

@@ -10,7 +10,7 @@ from .runtime import (  # noqa: F401
     TEST_NOPUSH, TEST_PUSHPOP, TEST_REDUCE, TEST_RESPAWN_ODD, TEST_RETRY_ODD, WL_IN, WL_OUT, WL_RETRY,
     BLOCK_ELASTIC, BLOCK_FIXED, BLOCK_SHRINKABLE, EXPORTS, LIB_PATH, Context, Graph, IrglError,
     Module, Pipe, Stats, bfs, cc, cc_lp, launch_count, load_library, mst, nccl_unique_id, pagerank, sssp, t_control,
-    triangle_count,
+    triangle_count, STAGE_INVOKE, STAGE_ITERATE, WHEN_ALWAYS, WHEN_PREV_TRUE, WHEN_PREV_FALSE,
 )
 
 load_library()

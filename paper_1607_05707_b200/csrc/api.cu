@@ -2678,3 +2678,201 @@ irgl_status_t irgl_op_plan(irgl_ctx* ctx, irgl_op op, irgl_block_constraint* blo
 }
 
 }  // extern "C"
+
+// ---- multi-member Pipe (A11: SPEC.md:363-381) -----------------------
+static bool pipe_device_op(int op) {
+  return op == IRGL_OP_TEST_COUNTDOWN || op == IRGL_OP_TEST_RETRY_ODD || op == IRGL_OP_TEST_RESPAWN_ODD ||
+         op == IRGL_OP_TEST_REDUCE || op == IRGL_OP_TEST_NOPUSH || op == IRGL_OP_TEST_PUSHPOP;
+}
+
+// Host orchestration of the Pipe body: every member statement through irgl_invoke, in the same
+// order and with the same guards as the control kernel.
+static irgl_status_t pipe_run_host(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g,
+                                   const irgl_pipe_stage* stages, int32_t n, const irgl_pipe_opts& o,
+                                   irgl_iter_stats* st, irgl_pipe_result* res) {
+  int32_t prev = -1;
+  int64_t rounds = 0;
+  for (;;) {
+    int64_t nin = 0;
+    irgl_status_t s = irgl_pipe_size(pipe, IRGL_WL_IN, &nin);
+    if (s != IRGL_OK) return s;
+    if (!o.once && nin == 0) break;  // looping Pipe: until in is empty at the start of a pass
+    for (int k = 0; k < n; ++k) {
+      const irgl_pipe_stage& S = stages[k];
+      if (S.when == IRGL_WHEN_PREV_TRUE && prev != 1) continue;
+      if (S.when == IRGL_WHEN_PREV_FALSE && prev != 0) continue;
+      for (int64_t it = 0;; ++it) {
+        if (S.kind == IRGL_STAGE_ITERATE) {
+          if ((s = irgl_pipe_size(pipe, IRGL_WL_IN, &nin)) != IRGL_OK) return s;
+          if (nin == 0 || (S.max_rounds > 0 && it >= S.max_rounds)) break;
+        }
+        irgl_iter_stats one{};
+        int32_t r = -1;
+        s = irgl_invoke(ctx, pipe, g, (irgl_op)S.op, &S.args, (irgl_reduction)S.reduction, &r, &one);
+        if (s != IRGL_OK) return s;
+        prev = S.reduction == IRGL_RED_NONE ? -1 : r;
+        res->stage_reduced[k] = prev;
+        st->launches += one.launches;
+        st->popped += one.popped;
+        st->pushes += one.pushes;
+        st->retries += one.retries;
+        st->serial_launches += one.serial_launches;
+        st->edges += one.edges;
+        if (S.kind == IRGL_STAGE_INVOKE) break;
+        if (S.cond_mode == IRGL_COND_WHILE && prev == 0) break;
+        if (S.cond_mode == IRGL_COND_UNTIL && prev == 1) break;
+      }
+    }
+    ++rounds;
+    if (o.once || (o.max_rounds > 0 && rounds >= o.max_rounds)) break;
+  }
+  st->rounds = rounds;
+  st->last_reduced = prev;
+  res->last_reduced = prev;
+  return IRGL_OK;
+}
+
+static irgl_status_t pipe_run_outlined(irgl_ctx* ctx, irgl_pipe* pipe, const irgl_pipe_stage* stages,
+                                       int32_t n, const irgl_pipe_opts& o, int32_t block,
+                                       irgl_iter_stats* st, irgl_pipe_result* res) {
+  PartRT& pr = ctx->parts[0];
+  PipePart& pp = pipe->parts[0];
+  CK(cudaSetDevice(pr.dev));
+  irgl_status_t s = test_ensure(ctx, pipe->cap);
+  if (s != IRGL_OK) return s;
+  const int bps = pipe_control_blocks_per_sm(block);
+  if (bps <= 0)
+    return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "Pipe control kernel cannot be co-resident at T_control");
+  PipeProgDev P{};
+  std::vector<int32_t*> vals;
+  for (int k = 0; k < n; ++k) {
+    const irgl_pipe_stage& S = stages[k];
+    int32_t* dv = nullptr;
+    if ((s = upload_values(ctx, &S.args, &dv)) != IRGL_OK) break;
+    vals.push_back(dv);
+    P.st[k] = PipeStageDev{S.op, S.kind, S.reduction, S.when, S.cond_mode, S.args.mapping,
+                           S.args.guard, S.max_rounds, dv};
+  }
+  // device scratch: per-buffer counts [3] + state [4] + per-stage reduced [8] (int32), stats [8]
+  int32_t* scratch = nullptr;
+  int64_t* dstats = nullptr;
+  if (s == IRGL_OK && cudaMalloc(&scratch, 16 * sizeof(int32_t)) != cudaSuccess) s = fail(ctx, IRGL_E_OOM, "E_OOM", "pipe scratch");
+  if (s == IRGL_OK && cudaMalloc(&dstats, 8 * sizeof(int64_t)) != cudaSuccess) s = fail(ctx, IRGL_E_OOM, "E_OOM", "pipe stats");
+  if (s == IRGL_OK) {
+    int32_t h[16] = {0};
+    h[pp.b_in] = (int32_t)pp.n_in;  // counts by buffer: only `in` holds items between statements
+    h[3] = pp.b_in, h[4] = pp.b_out, h[5] = pp.b_retry, h[6] = (int32_t)ctx->test_launch_no;
+    for (int k = 0; k < 8; ++k) h[7 + k] = -1;
+    CK(cudaMemcpy(scratch, h, sizeof(h), cudaMemcpyHostToDevice));
+    CK(cudaMemset(dstats, 0, 8 * sizeof(int64_t)));
+    CK(cudaMemset(&ctx->test_ctl->overflow, 0, 4));
+    P.n = n;
+    P.once = o.once;
+    P.rsa = ctx->cfg.retry_serialize_after > 0 ? ctx->cfg.retry_serialize_after : 4;
+    P.max_rounds = o.max_rounds;
+    for (int b = 0; b < 3; ++b) P.buf[b] = pp.buf[b];
+    P.cnt = reinterpret_cast<uint32_t*>(scratch);
+    P.cap = (uint32_t)pipe->cap;
+    P.rcount = ctx->test_rcount;
+    P.log = ctx->test_log;
+    P.red = &ctx->test_ctl->red[0];
+    P.overflow = &ctx->test_ctl->overflow;
+    P.state = scratch + 3;
+    P.stats = dstats;
+    P.reds = scratch + 7;
+    P.trace = nullptr;
+    P.trace_cap = 0;
+    CK(launch_pipe_control(P, bps * pr.sms, block, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    int64_t hs[8];
+    uint32_t ovf = 0;
+    CK(cudaMemcpy(h, scratch, sizeof(h), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&ovf, &ctx->test_ctl->overflow, 4, cudaMemcpyDeviceToHost));
+    // the pipe adopts the kernel's buffer roles; its counter slots get the final counts
+    pp.b_in = h[3], pp.b_out = h[4], pp.b_retry = h[5];
+    pp.n_in = (uint32_t)h[pp.b_in];
+    const uint32_t zc[4] = {0, 0, 0, 0};
+    CK(cudaMemcpy(pp.ctl->cnt, zc, sizeof(zc), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(&pp.ctl->cnt[pp.c_in], &pp.n_in, 4, cudaMemcpyHostToDevice));
+    ctx->test_launch_no = h[6];
+    st->launches = hs[0];
+    st->popped = hs[1];
+    st->pushes = hs[2];
+    st->retries = hs[3];
+    st->serial_launches = hs[4];
+    st->rounds = hs[5];
+    st->last_reduced = (int32_t)hs[7];
+    st->outlined = 1;
+    res->last_reduced = (int32_t)hs[7];
+    for (int k = 0; k < n; ++k) res->stage_reduced[k] = h[7 + k];
+    res->outlined = 1;
+    res->block = block;
+    if (ovf) s = fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+  }
+  for (int32_t* dv : vals)
+    if (dv) cudaFree(dv);
+  if (scratch) cudaFree(scratch);
+  if (dstats) cudaFree(dstats);
+  return s;
+}
+
+irgl_status_t irgl_pipe_run(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, const irgl_pipe_stage* stages,
+                            int32_t nstages, const irgl_pipe_opts* opts, irgl_iter_stats* stats,
+                            irgl_pipe_result* result) {
+  if (!ctx) return IRGL_E_INVALID;
+  if (!pipe || !stages || nstages < 1 || nstages > kPipeMaxStages)
+    return fail(ctx, IRGL_E_INVALID, "E_INVALID", "Pipe needs a pipe context and 1..8 member statements");
+  irgl_pipe_opts o{};
+  o.outline = -1;
+  if (opts) o = *opts;
+  bool device_ok = ctx->ptotal() == 1;
+  std::vector<irgl_block_constraint> cs;
+  for (int k = 0; k < nstages; ++k) {
+    const irgl_pipe_stage& S = stages[k];
+    irgl_status_t s = check_call(ctx, pipe, g, S.op);
+    if (s != IRGL_OK) return s;
+    if (S.kind != IRGL_STAGE_INVOKE && S.kind != IRGL_STAGE_ITERATE)
+      return fail(ctx, IRGL_E_INVALID, "E_INVALID", "stage kind must be Invoke or Iterate");
+    if (S.when < IRGL_WHEN_ALWAYS || S.when > IRGL_WHEN_PREV_FALSE)
+      return fail(ctx, IRGL_E_INVALID, "E_INVALID", "stage guard must be always / prev true / prev false");
+    device_ok = device_ok && pipe_device_op(S.op);
+    cs.push_back(S.block);
+  }
+  // T_control = max of the members' intersected block-size domains
+  int32_t tc = 0;
+  const irgl_status_t ts = irgl_t_control(cs.data(), nstages, &tc);
+  if (ts != IRGL_OK && ts != IRGL_E_OUTLINE_EMPTY) return fail(ctx, ts, "E_INVALID", "invalid block constraint");
+  bool outlined = false;
+  if (o.outline == 1) {
+    if (ts == IRGL_E_OUTLINE_EMPTY)
+      return fail(ctx, IRGL_E_OUTLINE_EMPTY, "E_OUTLINE_EMPTY",
+                  "iteration outlining cannot be performed on this Pipe: the members' block sizes do not intersect (PAPER.md:438)");
+    if (!device_ok)
+      return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
+                  "outlined Pipe members must be test operators on one partition (graph operators outline per Iterate)");
+    outlined = true;
+  } else if (o.outline < 0) {
+    outlined = ts == IRGL_OK && device_ok;  // else the host fallback
+  }
+  irgl_iter_stats st{};
+  st.last_reduced = -1;
+  irgl_pipe_result res{};
+  res.last_reduced = -1;
+  for (int k = 0; k < 8; ++k) res.stage_reduced[k] = -1;
+  const PartRT& pr0 = ctx->parts[0];
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaEventRecord(ctx->ev0, pr0.st));
+  irgl_status_t s = outlined ? pipe_run_outlined(ctx, pipe, stages, nstages, o, tc, &st, &res)
+                             : pipe_run_host(ctx, pipe, g, stages, nstages, o, &st, &res);
+  if (s != IRGL_OK) return s;
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaEventRecord(ctx->ev1, pr0.st));
+  CK(cudaEventSynchronize(ctx->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  st.device_ms = ms;
+  if (stats) *stats = st;
+  if (result) *result = res;
+  return IRGL_OK;
+}

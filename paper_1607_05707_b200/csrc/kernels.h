@@ -222,6 +222,36 @@ struct TestArgs {
 };
 cudaError_t launch_test_op(const TestArgs& a, int threads, cudaStream_t st);
 
+// Outlined multi-member Pipe of test operators: the program the control kernel
+// runs.  Buffer roles are indices into buf[3] / cnt[3] (count of each buffer); state[] carries
+// {in, out, retry, launch_no} in and out; stats[] = {launches, popped, pushes, retries,
+// serial_launches, rounds, trace_len, last_reduced}.
+constexpr int kPipeMaxStages = 8;
+struct PipeStageDev {
+  int32_t op, kind, reduction, when, cond_mode, mapping;
+  int64_t guard, max_rounds;
+  const int32_t* values;
+};
+struct PipeProgDev {
+  PipeStageDev st[kPipeMaxStages];
+  int32_t n, once, rsa;
+  int64_t max_rounds;
+  uint32_t* buf[3];
+  uint32_t* cnt;
+  uint32_t cap;
+  int32_t* rcount;
+  int32_t* log;
+  uint32_t* red;
+  uint32_t* overflow;
+  int32_t* state;
+  int64_t* stats;
+  int32_t* reds;      // per stage: last reduced value
+  int64_t* trace;     // [trace_cap][4]
+  int64_t trace_cap;
+};
+cudaError_t launch_pipe_control(const PipeProgDev& prog, int grid, int block, cudaStream_t st);
+int pipe_control_blocks_per_sm(int block);
+
 // ---- graph generation (gen.cu) ------------------------------------------------------------------
 // Builds the CSR rows [lo, hi) of the generated graph on the device.
 cudaError_t gen_partition(const irgl_gen_spec& s, int64_t n, int64_t lo, int64_t hi,

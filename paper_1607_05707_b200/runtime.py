@@ -105,6 +105,27 @@ class BlockConstraint(C.Structure):
     _fields_ = [("kind", C.c_int32), ("value", C.c_int32)]
 
 
+class PipeStage(C.Structure):
+    """irgl_pipe_stage: one member statement of a Pipe body (rt.h)."""
+    _fields_ = [("op", C.c_int32), ("kind", C.c_int32), ("reduction", C.c_int32),
+                ("when", C.c_int32), ("cond_mode", C.c_int32), ("reserved0", C.c_int32),
+                ("max_rounds", C.c_int64), ("block", BlockConstraint), ("args", OpArgs)]
+
+
+class PipeOpts(C.Structure):
+    _fields_ = [("once", C.c_int32), ("outline", C.c_int32), ("max_rounds", C.c_int64),
+                ("reserved", C.c_int32 * 4)]
+
+
+class PipeResult(C.Structure):
+    _fields_ = [("outlined", C.c_int32), ("block", C.c_int32), ("last_reduced", C.c_int32),
+                ("reserved0", C.c_int32), ("stage_reduced", C.c_int32 * 8)]
+
+
+STAGE_INVOKE, STAGE_ITERATE = 0, 1
+WHEN_ALWAYS, WHEN_PREV_TRUE, WHEN_PREV_FALSE = 0, 1, 2
+BLOCK_ELASTIC, BLOCK_SHRINKABLE, BLOCK_FIXED = 0, 1, 2
+
 # every symbol include/irgl/rt.h declares (tests check the .so exports all of them)
 EXPORTS = [
     "irgl_ctx_create", "irgl_nccl_unique_id", "irgl_ctx_create_nccl", "irgl_ctx_destroy",
@@ -115,7 +136,7 @@ EXPORTS = [
     "irgl_op_reset", "irgl_invoke", "irgl_iterate", "irgl_read_result", "irgl_t_control",
     "irgl_op_plan", "irgl_event_record", "irgl_event_elapsed", "irgl_launch_count",
     "irgl_read_result_async", "irgl_results_wait", "irgl_graph_relabel", "irgl_graph_perm",
-    "irgl_traverse_batch",
+    "irgl_traverse_batch", "irgl_pipe_run",
 ]
 
 # every symbol include/irgl/frontend.h declares
@@ -185,6 +206,8 @@ def load_library(path: str | None = None):
         "irgl_event_record": ([P, C.c_int], i32),
         "irgl_event_elapsed": ([P, C.c_int, C.c_int, C.POINTER(C.c_double)], i32),
         "irgl_launch_count": ([], i64),
+        "irgl_pipe_run": ([P, P, P, C.POINTER(PipeStage), C.c_int32, C.POINTER(PipeOpts),
+                           C.POINTER(IterStats), C.POINTER(PipeResult)], i32),
         # IrGL source front end (include/irgl/frontend.h)
         "irgl_module_parse": ([C.c_char_p, C.c_char_p, pp, C.c_char_p, C.c_size_t], i32),
         "irgl_module_destroy": ([P], i32),
@@ -424,6 +447,36 @@ class Context:
             if once or (max_rounds is not None and n >= max_rounds):
                 break
         return n
+
+    def pipe_run(self, pipe, stages, *, graph=None, once=False, outline=-1, max_rounds=0):
+        """Pipe [Once] { member statements } as one call (irgl_pipe_run): `stages` are dicts
+        {op, kind=STAGE_INVOKE|STAGE_ITERATE, reduction, when=WHEN_*, cond, max_rounds,
+        block=(BLOCK_*, value), **op args}.  outline=1 runs the whole Pipe as one cooperative
+        control kernel at T_control (IRGL_E_OUTLINE_EMPTY when the members' block domains do
+        not intersect), 0 host-orchestrated, -1 outlined when possible.
+        Returns (Stats, PipeResult)."""
+        arr = (PipeStage * len(stages))()
+        keep = []
+        for k, d in enumerate(stages):
+            d = dict(d)
+            st = arr[k]
+            st.op = d.pop("op")
+            st.kind = d.pop("kind", STAGE_INVOKE)
+            st.reduction = d.pop("reduction", RED_NONE)
+            st.when = d.pop("when", WHEN_ALWAYS)
+            st.cond_mode = d.pop("cond", COND_NONE)
+            st.max_rounds = d.pop("max_rounds", 0)
+            bk, bv = d.pop("block", (BLOCK_ELASTIC, 0))
+            st.block.kind, st.block.value = bk, bv
+            a, kp = _op_args(**d)
+            st.args = a
+            keep.append(kp)
+        o = PipeOpts()
+        o.once, o.outline, o.max_rounds = int(bool(once)), int(outline), int(max_rounds)
+        stt, res = IterStats(), PipeResult()
+        self._chk(self._lib.irgl_pipe_run(self._h, pipe.handle, graph.handle if graph else None,
+                                          arr, len(stages), C.byref(o), C.byref(stt), C.byref(res)))
+        return Stats(**stt.as_dict()), res
 
     def read_result(self, op, graph=None, size=None):
         if op == TC:
