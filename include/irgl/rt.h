@@ -44,7 +44,9 @@ enum {
   IRGL_E_OUTLINE_EMPTY = 6,  /* T_control = empty set                     */
   IRGL_E_CUDA = 7,           /* CUDA runtime error (message in irgl_last_error)                */
   IRGL_E_NCCL = 8,           /* NCCL error / async error                                       */
-  IRGL_E_UNSUPPORTED = 9     /* combination not supported by this build                        */
+  IRGL_E_UNSUPPORTED = 9,    /* combination not supported by this build                        */
+  IRGL_E_RANGE = 10          /* an SSSP path weight sum reaches INF = INT32_MAX: distances are
+                                int32 (SPEC.md:421's Int narrowed); the traversal is not valid  */
 };
 
 /* ast.hpp:90 Reduction {Any, All}; NONE = invocation without a return cell. */
@@ -201,8 +203,11 @@ const char* irgl_last_error(const irgl_ctx* ctx); /* ctx may be NULL: last globa
 int irgl_abi_version(void);
 
 /* ---- graph (reference Value::Graph; builtins edges/dst/weight) ----- */
-/* Column ids must be in [0, n) and weights >= 0 (IRGL_E_INVALID otherwise); distances are int32,
- * so a path's weight sum must stay below INT32_MAX (= INF). */
+/* Column ids must be in [0, n) and weights >= 0 (IRGL_E_INVALID otherwise); distances are int32:
+ * an SSSP in which a vertex's shortest-path weight reaches INT32_MAX (= INF) returns IRGL_E_RANGE
+ * (every relaxation sum is range-checked; a sum beyond the range into an unreached vertex triggers
+ * an exact check of the finished distances on one partition — conservatively reported on several
+ * partitions and inside irgl_traverse_batch).  Never a wrapped distance. */
 irgl_status_t irgl_graph_create_csr(irgl_ctx* ctx, int64_t n, int64_t m, const int64_t* row_ptr,
                                     const int32_t* col, const int32_t* weight /*nullable*/,
                                     irgl_graph** out);

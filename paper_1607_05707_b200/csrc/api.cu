@@ -177,6 +177,15 @@ static irgl_status_t fail(irgl_ctx* ctx, irgl_status_t st, const char* rule, con
   set_error(ctx, st, rule, m);
   return st;
 }
+// The pipe's overflow word: bit 4 = an SSSP path sum beyond the int32 distance range, else a push
+// (bit 1) or edge-chunk descriptor (bit 2) beyond capacity.
+static irgl_status_t overflow_fail(irgl_ctx* ctx, uint32_t flags) {
+  if ((flags & 3u) == 0u && (flags & 4u))
+    return fail(ctx, IRGL_E_RANGE, "E_RANGE",
+                "a path weight sum reaches INF = INT32_MAX (distances are int32; SPEC.md:421)");
+  return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
+              flags & 2u ? "edge-chunk descriptors beyond capacity" : "push beyond worklist capacity");
+}
 
 static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   ExpandCfg ec;
@@ -769,7 +778,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
       PipePart& pp = pipe->parts[l];
       CK(cudaSetDevice(pr.dev));
       CK(cudaStreamSynchronize(pr.st));
-      if (pr.h_pin[1]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+      if (pr.h_pin[1] & 3u) return overflow_fail(ctx, pr.h_pin[1]);
       if (l == 0) {
         float kms = 0.f;
         CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
@@ -895,7 +904,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     uint64_t total_in = 0, local_in = 0;
     for (int p = 0; p < P; ++p) {
       total_in += hdr[(size_t)p * H + P];
-      if (hdr[(size_t)p * H + P + 1]) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+      if (hdr[(size_t)p * H + P + 1] & 3u) return overflow_fail(ctx, hdr[(size_t)p * H + P + 1]);
     }
     for (int l = 0; l < L; ++l) local_in += hdr[(size_t)ctx->gpart(l) * H + P];
     if (stt->rounds > 0) stt->pushes += (int64_t)local_in;  // last round's out = this round's in
@@ -1071,6 +1080,41 @@ static irgl_status_t l2_window_for(irgl_ctx* ctx, PartRT& pr, irgl_graph* g, Gra
   return l2_window(ctx, pr, gp.lab, (size_t)g->n * 4);
 }
 
+// Bit 4 of a pipe's overflow word (path_sum): some relaxation's sum reached INF while its target was
+// unreached.  One partition: check the finished distances exactly (range_check_kernel) and fail
+// only if a reached vertex has an unreached neighbour; several partitions: report it as is.
+static irgl_status_t range_verify(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g) {
+  uint32_t any = 0;
+  for (size_t l = 0; l < pipe->parts.size(); ++l) {
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    uint32_t f = 0;
+    CK(cudaMemcpyAsync(pr.h_pin, &pipe->parts[l].ctl->overflow, 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    f = pr.h_pin[0];
+    if (f & 4u) {
+      any = 1;
+      const uint32_t keep = f & ~4u;
+      CK(cudaMemcpy(&pipe->parts[l].ctl->overflow, &keep, 4, cudaMemcpyHostToDevice));
+    }
+  }
+  if (!any) return IRGL_OK;
+  if (g->parts.size() == 1 && ctx->ptotal() == 1) {
+    GraphPart& gp = g->parts[0];
+    PartRT& pr = ctx->parts[0];
+    CK(cudaSetDevice(pr.dev));
+    uint32_t* bad = nullptr;
+    CK(cudaMallocAsync(&bad, 4, pr.st));
+    CK(cudaMemsetAsync(bad, 0, 4, pr.st));
+    CK(launch_range_check(gp.csr(), gp.lab, bad, pr.st));
+    CK(cudaMemcpyAsync(pr.h_pin, bad, 4, cudaMemcpyDeviceToHost, pr.st));
+    CK(cudaFreeAsync(bad, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    if (pr.h_pin[0] == 0) return IRGL_OK;  // every sum that overflowed was a useless one
+  }
+  return overflow_fail(ctx, 4u);
+}
+
 // ---- E3: outlined Iterate (P == 1) -------------------------------------------------------------
 static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                        int64_t level0, const irgl_iterate_opts& o,
@@ -1144,7 +1188,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     }
   }
   g->stamp_epoch += h.stamp_used;  // also on failure: the ids are in the stamp array
-  if (h.overflow)
+  if (h.overflow & 3u)
     return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
                 std::string(h.overflow & 2 ? "edge-chunk descriptors beyond capacity" : "push beyond worklist capacity") +
                     " (rounds " + std::to_string(h.rounds) + ", far piles " + std::to_string(h.far_cnt[0]) + "/" +
@@ -2111,6 +2155,7 @@ irgl_status_t irgl_invoke(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_op
     NearFar nf;  // a single Invoke is one plain round
     s = pipe_counters(ctx, pipe, nullptr);
     if (s == IRGL_OK) s = wl_graph_rounds(ctx, pipe, g, op, level, o, true, nf, &st);
+    if (s == IRGL_OK && op == IRGL_OP_SSSP) s = range_verify(ctx, pipe, g);
     if (s == IRGL_OK) s = pipe_counters(ctx, pipe, &st);
     if (reduced) *reduced = red == IRGL_RED_ALL ? 1 : red == IRGL_RED_ANY ? 0 : -1;  // identity
   } else {
@@ -2189,6 +2234,7 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
     else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
+    if (s == IRGL_OK && op == IRGL_OP_SSSP) s = range_verify(ctx, pipe, g);
     if (s != IRGL_OK) return s;
     // edges scanned / remote updates (the outlined path read them with its control block)
     s = pipe_counters(ctx, pipe, outlined ? nullptr : &st);
@@ -2482,7 +2528,7 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
     CK(cudaEventSynchronize(pr.bev[b][3]));
     const Ctl& h = *pr.h_snap[b];
     g->stamp_epoch += h.stamp_used;  // also on failure: the ids are in the stamp array
-    if (h.overflow) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "push beyond worklist capacity");
+    if (h.overflow) return overflow_fail(ctx, h.overflow);
     last_rounds = h.rounds;
     if (stats) {
       irgl_iter_stats& st = stats[j];

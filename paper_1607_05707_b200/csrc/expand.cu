@@ -146,6 +146,21 @@ __device__ __forceinline__ int32_t gather_cur(const KParams& p, uint32_t dst) {
   return ld_label(p.lab + dst);
 }
 
+// SSSP path sum nd = dist[n] + weight(e) in int32 storage (INF = INT32_MAX, SPEC.md:421 maps the
+// 64-bit Int onto it).  A sum that reaches INF is not representable: it is never a candidate, and
+// when its target is still unreached (cur == INF) the pipe's overflow word gets bit 4 — the
+// target may have a true distance >= INF.  The host then checks the finished traversal exactly
+// (an edge from a reached to an unreached vertex exists only through such a sum) and reports
+// IRGL_E_RANGE instead of an unreachable label.  Weights are >= 0 (validated) and dist[n] < INF.
+__device__ __forceinline__ int32_t path_sum(const KParams& p, int32_t sv, int32_t wt, int32_t cur) {
+  const uint32_t s = (uint32_t)sv + (uint32_t)wt;
+  if (s >= (uint32_t)kInf) {
+    if (cur == kInf) atomicOr(&p.ctl->overflow, 4u);
+    return kInf;
+  }
+  return (int32_t)s;
+}
+
 // ---- relax: the operator body for one edge (n -> dst) ----------------------------------------
 // BFS   : if level[dst]==INF { level[dst]=LEVEL; push(dst) }   CAS dedupes the push.
 // SSSP  : nd = dist[n]+w;  if atomicMin(dist[dst],nd) > nd and stamp[dst] != round: push(dst)
@@ -164,7 +179,7 @@ __device__ __forceinline__ int relax_with(const KParams& p, const RoundBufs& rb,
     }
     return atomicCAS(p.lab + dst, kInf, rb.level) == kInf ? 1 : 0;
   } else {
-    const int32_t nd = (is_sssp(OP)) ? sv + wt : sv;
+    const int32_t nd = (is_sssp(OP)) ? path_sum(p, sv, wt, cur) : sv;
     if (nd >= cur) return 0;
     const int32_t old = atomicMin(p.lab + dst, nd);
     if (nd >= old) return 0;
@@ -208,7 +223,7 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
       const int32_t code = rb.stamp_id << 1;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const int32_t nd = is_sssp(OP) ? sv[j] + wt[j] : sv[j];
+        const int32_t nd = is_sssp(OP) && act[j] ? path_sum(p, sv[j], wt[j], cur[j]) : sv[j];
         if (act[j] && nd < cur[j]) {
           atomicMin(p.lab + dst[j], nd);    // RED.MIN
           atomicMax(p.stamp + dst[j], code);  // RED.MAX: stamp ids only grow
@@ -245,7 +260,7 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
     int32_t old[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      nd[j] = (is_sssp(OP)) ? sv[j] + wt[j] : sv[j];
+      nd[j] = is_sssp(OP) && act[j] ? path_sum(p, sv[j], wt[j], cur[j]) : sv[j];
       cand[j] = act[j] && nd[j] < cur[j];
       kind[j] = (has_far(OP) && nd[j] >= rb.threshold) ? 2 : 1;
       // a vertex another partition owns is sent once per round whatever its pile (the owner
@@ -1499,6 +1514,20 @@ cudaError_t launch_pack_values(const int32_t* lab, const uint32_t* items, int32_
   return cudaGetLastError();
 }
 
+// IRGL_E_RANGE check of a finished one-partition SSSP (path_sum): an edge u -> v with u reached
+// and v unreached can only come from a path sum beyond the int32 range.
+__global__ void range_check_kernel(DevCSR g, const int32_t* dist, uint32_t* bad) {
+  const int64_t n = g.hi - g.lo;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    if (dist[g.lo + u] == kInf) continue;
+    for (int64_t e = g.row_ptr[u]; e < g.row_ptr[u + 1]; ++e)
+      if (dist[g.col[e]] == kInf) {
+        atomicOr(bad, 1u);
+        break;
+      }
+  }
+}
+
 __global__ void ctl_prepare_kernel(Ctl* c) {
   const int t = threadIdx.x;
   if (t < 3) {
@@ -1516,6 +1545,12 @@ __global__ void ctl_prepare_kernel(Ctl* c) {
     c->rounds = 0;
     c->bu_scanned = 0;
   }
+}
+
+cudaError_t launch_range_check(const DevCSR& g, const int32_t* dist, uint32_t* bad, cudaStream_t st) {
+  note_launch();
+  range_check_kernel<<<148 * 8, 256, 0, st>>>(g, dist, bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ctl_prepare(Ctl* ctl, cudaStream_t st) {

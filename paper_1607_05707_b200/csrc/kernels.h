@@ -126,6 +126,8 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
 // variant: 0 the operator's base kernel, 1 its direction-optimising (BFS) / near-far (SSSP)
 // kernel, -1 the minimum over both (a grid valid for either)
 int persistent_blocks_per_sm(int op, int variant = -1);
+// *bad |= 1 if an edge leads from a reached to an unreached vertex (the IRGL_E_RANGE check)
+cudaError_t launch_range_check(const DevCSR& g, const int32_t* dist, uint32_t* bad, cudaStream_t st);
 // w8[k] = w[k] for k < m; *bad = 1 if some weight is outside [0, 255]
 cudaError_t launch_weights_u8(const int32_t* w, int64_t m, uint8_t* w8, uint32_t* bad, cudaStream_t st);
 int expand_blocks_per_sm(int op);

@@ -33,7 +33,7 @@ OK, E_INVALID, E_USAGE, E_OOM, E_WL_OVERFLOW, E_OCCUPANCY, E_OUTLINE_EMPTY, E_CU
     E_UNSUPPORTED = range(10)
 STATUS_NAMES = {0: "OK", 1: "E_INVALID", 2: "E_USAGE", 3: "E_OOM", 4: "E_WL_OVERFLOW",
                 5: "E_OCCUPANCY", 6: "E_OUTLINE_EMPTY", 7: "E_CUDA", 8: "E_NCCL",
-                9: "E_UNSUPPORTED"}
+                9: "E_UNSUPPORTED", 10: "E_RANGE"}
 # enums
 RED_NONE, RED_ANY, RED_ALL = 0, 1, 2
 WL_IN, WL_OUT, WL_RETRY = 0, 1, 2

@@ -606,3 +606,22 @@ def test_l2_persist_window_same_results(irgl, oracle):
                 np.testing.assert_array_equal(lv, oracle.bfs(og, int(s))[0])
                 d, _ = irgl.sssp(c, g, int(s), outline=1)
                 np.testing.assert_array_equal(d, oracle.sssp(og, int(s)))
+
+
+@pytest.mark.parametrize("outline", [0, 1])
+def test_sssp_path_sum_beyond_int32_is_an_error(ctx, irgl, outline):
+    """A path whose weight sum reaches INF = INT32_MAX cannot be stored in the int32 distances:
+    the runtime reports IRGL_E_RANGE instead of a wrapped distance (rt.h)."""
+    big = 2**30
+    # path 0 - 1 - 2 - 3 with weights 2^30: dist(2) = 2^31 overflows
+    rp = np.array([0, 1, 3, 5, 6], dtype=np.int64)
+    col = np.array([1, 0, 2, 1, 3, 2], dtype=np.int32)
+    w = np.full(6, big, dtype=np.int32)
+    g = ctx.graph_from_csr(rp, col, w)
+    with pytest.raises(irgl.IrglError) as e:
+        irgl.sssp(ctx, g, 0, outline=outline)
+    assert e.value.status == 10
+    # just below the range: fine
+    w2 = np.full(6, (2**31 - 2) // 3, dtype=np.int32)
+    d, _ = irgl.sssp(ctx, ctx.graph_from_csr(rp, col, w2), 0, outline=outline)
+    assert d.tolist() == [0, int(w2[0]), 2 * int(w2[0]), 3 * int(w2[0])]

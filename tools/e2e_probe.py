@@ -1,5 +1,5 @@
 import os, sys, time, ctypes as C
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1607_05707_b200 as irgl, bench
 ctx = irgl.Context()
