@@ -197,6 +197,21 @@ irgl_status_t irgl_ctx_create(const int* devices, int ndev, const irgl_config* c
 irgl_status_t irgl_nccl_unique_id(void* id128);
 irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void* id128,
                                    const irgl_config* cfg, irgl_ctx** out);
+/* One process per GPU without NCCL: the round headers and payloads of a vertex-partitioned
+ * graph go through the caller's collectives (e.g. an MPI communicator or a torch.distributed
+ * gloo group), staged in pinned host memory.  Every rank calls the same runtime functions in the
+ * same order, so the callbacks are invoked collectively.  Return 0 on success. */
+typedef struct irgl_transport {
+  void* user;
+  /* every rank contributes `bytes` bytes at send; recv receives nranks * bytes in rank order */
+  int32_t (*allgather)(void* user, const void* send, void* recv, size_t bytes);
+  /* all-to-all-v of byte blocks: send holds send_bytes[r] bytes for each rank r back to back in
+   * rank order, recv receives recv_bytes[r] bytes from each rank r likewise */
+  int32_t (*alltoallv)(void* user, const void* send, const int64_t* send_bytes, void* recv,
+                       const int64_t* recv_bytes);
+} irgl_transport;
+irgl_status_t irgl_ctx_create_transport(int device, int rank, int nranks, const irgl_transport* t,
+                                        const irgl_config* cfg, irgl_ctx** out);
 irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx);
 irgl_status_t irgl_ctx_sync(irgl_ctx* ctx);
 const char* irgl_last_error(const irgl_ctx* ctx); /* ctx may be NULL: last global error */

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <atomic>
+#include <cstdint>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -43,8 +44,11 @@ struct irgl_ctx {
   ncclComm_t comm = nullptr;
   const irgl::NcclApi* nccl = nullptr;
   int64_t route_size = INT64_MAX;   // partition size of the last graph (pipe routing)
-  uint32_t* cnt_dev = nullptr;      // NCCL count exchange scratch [L*P + P*P]
-  uint32_t* hdr_all = nullptr;      // NCCL round-header gather [(L + P) * (P + 2)]
+  irgl_transport xport{};          // host transport plugin (irgl_ctx_create_transport)
+  void* xbuf = nullptr;             // its pinned staging (send | recv halves)
+  size_t xbuf_bytes = 0;
+  uint32_t* cnt_dev = nullptr;      // multi-rank count exchange scratch [L*P + P*P]
+  uint32_t* hdr_all = nullptr;      // multi-rank round-header gather [(L + P) * (P + 2)]
   std::string err;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t kev0 = nullptr, kev1 = nullptr;  // hot-kernel timing (iter_stats.kernel_ms)
@@ -405,6 +409,91 @@ static irgl_status_t op_reset(irgl_ctx* ctx, irgl_graph* g, int op, irgl_pipe* p
   return fail(ctx, IRGL_E_INVALID, "E_INVALID", "unknown operator");
 }
 
+// ---- rank transport ----------------------------------------------------------------------------
+// A multi-rank ctx (one process per GPU) moves the round headers and the payloads either with NCCL
+// (device buffers, stream-ordered: irgl_ctx_create_nccl) or through a host transport plugin (the
+// caller's collectives over pinned staging, e.g. an MPI or torch.distributed group:
+// irgl_ctx_create_transport).  The round protocol above the primitives is the same.
+static bool multi_rank(const irgl_ctx* ctx) { return ctx->comm != nullptr || ctx->xport.allgather != nullptr; }
+
+static irgl_status_t x_staging(irgl_ctx* ctx, size_t bytes) {
+  if (ctx->xbuf_bytes >= bytes) return IRGL_OK;
+  if (ctx->xbuf) cudaFreeHost(ctx->xbuf);
+  ctx->xbuf = nullptr;
+  ctx->xbuf_bytes = 0;
+  const size_t b = std::max<size_t>(bytes, (size_t)1 << 20);
+  CK(cudaHostAlloc(&ctx->xbuf, b, cudaHostAllocDefault));
+  ctx->xbuf_bytes = b;
+  return IRGL_OK;
+}
+
+// AllGather: `bytes` from device dsend on every rank -> device drecv (nranks * bytes, rank order).
+static irgl_status_t x_allgather(irgl_ctx* ctx, PartRT& pr, const void* dsend, void* drecv, size_t bytes) {
+  if (ctx->comm) {
+    NCK(ctx->nccl->AllGather(dsend, drecv, bytes, ncclUint8, ctx->comm, pr.st));
+    return IRGL_OK;
+  }
+  irgl_status_t s = x_staging(ctx, bytes * (1 + (size_t)ctx->nranks));
+  if (s != IRGL_OK) return s;
+  char* h = static_cast<char*>(ctx->xbuf);
+  CK(cudaMemcpyAsync(h, dsend, bytes, cudaMemcpyDeviceToHost, pr.st));
+  CK(cudaStreamSynchronize(pr.st));
+  if (ctx->xport.allgather(ctx->xport.user, h, h + bytes, bytes) != 0)
+    return fail(ctx, IRGL_E_NCCL, "E_TRANSPORT", "transport allgather failed");
+  CK(cudaMemcpyAsync(drecv, h + bytes, bytes * ctx->nranks, cudaMemcpyHostToDevice, pr.st));
+  return IRGL_OK;
+}
+
+// Grouped point-to-point exchange: sends[i] goes to rank sends[i].peer, recvs[i] arrives from
+// rank recvs[i].peer; blocks between one pair of ranks are matched in list order (both sides
+// build their lists in the same global order).
+struct XBlock {
+  int peer;
+  void* dptr;
+  size_t bytes;
+};
+static irgl_status_t x_exchange(irgl_ctx* ctx, PartRT& pr, const std::vector<XBlock>& sends,
+                                const std::vector<XBlock>& recvs) {
+  if (sends.empty() && recvs.empty() && ctx->comm) return IRGL_OK;
+  if (ctx->comm) {
+    NCK(ctx->nccl->GroupStart());
+    for (const XBlock& b : sends)
+      if (b.bytes) NCK(ctx->nccl->Send(b.dptr, b.bytes, ncclUint8, b.peer, ctx->comm, pr.st));
+    for (const XBlock& b : recvs)
+      if (b.bytes) NCK(ctx->nccl->Recv(b.dptr, b.bytes, ncclUint8, b.peer, ctx->comm, pr.st));
+    NCK(ctx->nccl->GroupEnd());
+    return IRGL_OK;
+  }
+  // host plugin: one alltoallv of byte blocks, per destination rank in list order
+  const int R = ctx->nranks;
+  std::vector<int64_t> sb(R, 0), rb(R, 0), so(R + 1, 0), ro(R + 1, 0);
+  for (const XBlock& b : sends) sb[b.peer] += (int64_t)b.bytes;
+  for (const XBlock& b : recvs) rb[b.peer] += (int64_t)b.bytes;
+  for (int r = 0; r < R; ++r) {
+    so[r + 1] = so[r] + sb[r];
+    ro[r + 1] = ro[r] + rb[r];
+  }
+  irgl_status_t s = x_staging(ctx, (size_t)(so[R] + ro[R]) + 16);
+  if (s != IRGL_OK) return s;
+  char* hs = static_cast<char*>(ctx->xbuf);
+  char* hr = hs + so[R];
+  std::vector<int64_t> at(so.begin(), so.end() - 1);
+  for (const XBlock& b : sends) {
+    if (b.bytes) CK(cudaMemcpyAsync(hs + at[b.peer], b.dptr, b.bytes, cudaMemcpyDeviceToHost, pr.st));
+    at[b.peer] += (int64_t)b.bytes;
+  }
+  CK(cudaStreamSynchronize(pr.st));
+  if (ctx->xport.alltoallv(ctx->xport.user, hs, sb.data(), hr, rb.data()) != 0)
+    return fail(ctx, IRGL_E_NCCL, "E_TRANSPORT", "transport alltoallv failed");
+  std::vector<int64_t> rat(ro.begin(), ro.end() - 1);
+  for (const XBlock& b : recvs) {
+    if (b.bytes) CK(cudaMemcpyAsync(b.dptr, hr + rat[b.peer], b.bytes, cudaMemcpyHostToDevice, pr.st));
+    rat[b.peer] += (int64_t)b.bytes;
+  }
+  CK(cudaStreamSynchronize(pr.st));  // the staging is reused by the next exchange
+  return IRGL_OK;
+}
+
 // ---- multi-partition exchange (E5) -------------------------------------------------------------
 // After every local expansion: bucket counts -> (pack values) -> transport -> owner-side apply.
 static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe* pipe, int op,
@@ -435,7 +524,7 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       if (c > (uint64_t)ps) return true;
     return false;
   };
-  if (!ctx->comm && bucket_overflow())
+  if (!multi_rank(ctx) && bucket_overflow())
     return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
   // 2. pack values (SSSP / CC_LP): current ghost label of each bucket entry
   if (vals)
@@ -449,27 +538,28 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
       }
     }
   // 3. transport
-  if (ctx->comm) {
-    // NCCL transport (R ranks x L partitions; all partitions of a rank share its device).
+  if (multi_rank(ctx)) {
+    // rank transport (R ranks x L partitions; all partitions of a rank share its device).
     for (int l = 0; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // packs done
     PartRT& pr = ctx->parts[0];
     CK(cudaSetDevice(pr.dev));
-    // (i) counts: every rank contributes its L rows of the P x P matrix (ncclAllGather)
+    // (i) counts: every rank contributes its L rows of the P x P matrix
     for (int l = 0; l < L; ++l)
       CK(cudaMemcpyAsync(ctx->cnt_dev + (size_t)l * P, g->parts[l].send_cnt, P * 4,
                          cudaMemcpyDeviceToDevice, pr.st));
-    NCK(ctx->nccl->AllGather(ctx->cnt_dev, ctx->cnt_dev + (size_t)L * P, (size_t)L * P, ncclUint32,
-                             ctx->comm, pr.st));
+    {
+      irgl_status_t xs = x_allgather(ctx, pr, ctx->cnt_dev, ctx->cnt_dev + (size_t)L * P, (size_t)L * P * 4);
+      if (xs != IRGL_OK) return xs;
+    }
     CK(cudaMemcpyAsync(cnt.data(), ctx->cnt_dev + (size_t)L * P, (size_t)P * P * 4,
                        cudaMemcpyDeviceToHost, pr.st));
     CK(cudaStreamSynchronize(pr.st));
     if (bucket_overflow())  // the same matrix on every rank: all ranks fail here together
       return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the exchange bucket");
-    // (ii) payloads: grouped send/recv (all-to-all-v).  Every rank walks the (src, dst) partition
-    // pairs in the same global order, so the per-peer order of sends matches the receiver's
-    // order of recvs (NCCL matches point-to-point calls per peer in issue order).
+    // (ii) payloads: grouped point-to-point (all-to-all-v).  Every rank walks the (src, dst)
+    // partition pairs in the same global order, so per pair of ranks the blocks match in order.
     const int lo_part = ctx->gpart(0);
-    NCK(ctx->nccl->GroupStart());
+    std::vector<XBlock> sends, recvs;
     for (int p = 0; p < P; ++p)
       for (int q = 0; q < P; ++q) {
         if (p == q) continue;
@@ -479,17 +569,20 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
         const bool dst_local = q >= lo_part && q < lo_part + L;
         if (src_local) {
           GraphPart& sp = g->parts[p - lo_part];
-          NCK(ctx->nccl->Send(sp.send + (int64_t)q * ps, c, ncclUint32, q / L, ctx->comm, pr.st));
-          if (vals) NCK(ctx->nccl->Send(sp.send_val + (int64_t)q * ps, c, ncclInt32, q / L, ctx->comm, pr.st));
+          sends.push_back({q / L, sp.send + (int64_t)q * ps, (size_t)c * 4});
+          if (vals) sends.push_back({q / L, sp.send_val + (int64_t)q * ps, (size_t)c * 4});
           stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
         }
         if (dst_local) {
           GraphPart& dp = g->parts[q - lo_part];
-          NCK(ctx->nccl->Recv(dp.recv + (int64_t)p * ps, c, ncclUint32, p / L, ctx->comm, pr.st));
-          if (vals) NCK(ctx->nccl->Recv(dp.recv_val + (int64_t)p * ps, c, ncclInt32, p / L, ctx->comm, pr.st));
+          recvs.push_back({p / L, dp.recv + (int64_t)p * ps, (size_t)c * 4});
+          if (vals) recvs.push_back({p / L, dp.recv_val + (int64_t)p * ps, (size_t)c * 4});
         }
       }
-    NCK(ctx->nccl->GroupEnd());
+    {
+      irgl_status_t xs = x_exchange(ctx, pr, sends, recvs);
+      if (xs != IRGL_OK) return xs;
+    }
     CK(cudaStreamSynchronize(pr.st));  // payloads landed before the per-partition applies
   } else {
     for (int l = 0; l < L; ++l) {
@@ -533,30 +626,42 @@ static irgl_status_t exchange_and_apply(irgl_ctx* ctx, irgl_graph* g, irgl_pipe*
 }
 
 static irgl_status_t allreduce_sum_u64(irgl_ctx* ctx, uint64_t* v) {
-  if (!ctx->comm) return IRGL_OK;
+  if (!multi_rank(ctx)) return IRGL_OK;
   PartRT& pr = ctx->parts[0];
   CK(cudaSetDevice(pr.dev));
   unsigned long long* d = nullptr;
-  CK(cudaMallocAsync(&d, 8, pr.st));
+  const int R = ctx->nranks;
+  CK(cudaMallocAsync(&d, 8 * (1 + (size_t)R), pr.st));
   CK(cudaMemcpyAsync(d, v, 8, cudaMemcpyHostToDevice, pr.st));
-  NCK(ctx->nccl->AllReduce(d, d, 1, ncclUint64, ncclSum, ctx->comm, pr.st));
-  CK(cudaMemcpyAsync(v, d, 8, cudaMemcpyDeviceToHost, pr.st));
+  irgl_status_t s = x_allgather(ctx, pr, d, d + 1, 8);  // tiny: gather, fold on the host
+  if (s != IRGL_OK) return s;
+  std::vector<uint64_t> all(R);
+  CK(cudaMemcpyAsync(all.data(), d + 1, 8 * (size_t)R, cudaMemcpyDeviceToHost, pr.st));
   CK(cudaFreeAsync(d, pr.st));
   CK(cudaStreamSynchronize(pr.st));
+  uint64_t acc = 0;
+  for (uint64_t x : all) acc += x;
+  *v = acc;
   return IRGL_OK;
 }
 
 static irgl_status_t allreduce_min_u64(irgl_ctx* ctx, uint64_t* v) {
-  if (!ctx->comm) return IRGL_OK;
+  if (!multi_rank(ctx)) return IRGL_OK;
   PartRT& pr = ctx->parts[0];
   CK(cudaSetDevice(pr.dev));
   unsigned long long* d = nullptr;
-  CK(cudaMallocAsync(&d, 8, pr.st));
+  const int R = ctx->nranks;
+  CK(cudaMallocAsync(&d, 8 * (1 + (size_t)R), pr.st));
   CK(cudaMemcpyAsync(d, v, 8, cudaMemcpyHostToDevice, pr.st));
-  NCK(ctx->nccl->AllReduce(d, d, 1, ncclUint64, ncclMin, ctx->comm, pr.st));
-  CK(cudaMemcpyAsync(v, d, 8, cudaMemcpyDeviceToHost, pr.st));
+  irgl_status_t s = x_allgather(ctx, pr, d, d + 1, 8);  // tiny: gather, fold on the host
+  if (s != IRGL_OK) return s;
+  std::vector<uint64_t> all(R);
+  CK(cudaMemcpyAsync(all.data(), d + 1, 8 * (size_t)R, cudaMemcpyDeviceToHost, pr.st));
   CK(cudaFreeAsync(d, pr.st));
   CK(cudaStreamSynchronize(pr.st));
+  uint64_t acc = UINT64_MAX;
+  for (uint64_t x : all) acc = std::min(acc, x);
+  *v = acc;
   return IRGL_OK;
 }
 
@@ -830,7 +935,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     CK(cudaSetDevice(pr.dev));
     if (!pr.hdr) CK(cudaMalloc(&pr.hdr, (size_t)H * 4));
   }
-  if (ctx->comm && !ctx->hdr_all) {
+  if (multi_rank(ctx) && !ctx->hdr_all) {
     CK(cudaSetDevice(ctx->parts[0].dev));
     CK(cudaMalloc(&ctx->hdr_all, (size_t)(L + P) * H * 4));
   }
@@ -868,15 +973,17 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     }
     if (dtrace) t_a = now_us();
     // 2. gather the headers: the round's one host synchronisation
-    if (ctx->comm) {
+    if (multi_rank(ctx)) {
       PartRT& pr = ctx->parts[0];
       CK(cudaSetDevice(pr.dev));
       for (int l = 1; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // same device
       for (int l = 0; l < L; ++l)
         CK(cudaMemcpyAsync(ctx->hdr_all + (size_t)l * H, ctx->parts[l].hdr, (size_t)H * 4,
                            cudaMemcpyDeviceToDevice, pr.st));
-      NCK(ctx->nccl->AllGather(ctx->hdr_all, ctx->hdr_all + (size_t)L * H, (size_t)L * H, ncclUint32,
-                               ctx->comm, pr.st));
+      {
+        irgl_status_t xs = x_allgather(ctx, pr, ctx->hdr_all, ctx->hdr_all + (size_t)L * H, (size_t)L * H * 4);
+        if (xs != IRGL_OK) return xs;
+      }
       CK(cudaMemcpyAsync(pr.h_pin, ctx->hdr_all + (size_t)L * H, (size_t)P * H * 4,
                          cudaMemcpyDeviceToHost, pr.st));
       CK(cudaStreamSynchronize(pr.st));
@@ -913,12 +1020,12 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     if (dtrace) t_c = now_us();
     // 3. payloads: grouped send/recv (NCCL) or peer copies (one process), then owner-side applies
     auto count = [&](int p, int q) { return hdr[(size_t)p * H + q]; };
-    if (ctx->comm) {
+    if (multi_rank(ctx)) {
       PartRT& pr = ctx->parts[0];
       CK(cudaSetDevice(pr.dev));
       for (int l = 1; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // packs done
       const int lo_part = ctx->gpart(0);
-      NCK(ctx->nccl->GroupStart());
+      std::vector<XBlock> sends, recvs;
       for (int p = 0; p < P; ++p)
         for (int q = 0; q < P; ++q) {
           if (p == q) continue;
@@ -928,17 +1035,20 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
           const bool dst_local = q >= lo_part && q < lo_part + L;
           if (src_local) {
             GraphPart& sp = g->parts[p - lo_part];
-            NCK(ctx->nccl->Send(sp.send + (int64_t)q * ps, c, ncclUint32, q / L, ctx->comm, pr.st));
-            if (vals) NCK(ctx->nccl->Send(sp.send_val + (int64_t)q * ps, c, ncclInt32, q / L, ctx->comm, pr.st));
+            sends.push_back({q / L, sp.send + (int64_t)q * ps, (size_t)c * 4});
+            if (vals) sends.push_back({q / L, sp.send_val + (int64_t)q * ps, (size_t)c * 4});
             stt->exchange_bytes += (int64_t)c * (vals ? 8 : 4);
           }
           if (dst_local) {
             GraphPart& dp = g->parts[q - lo_part];
-            NCK(ctx->nccl->Recv(dp.recv + (int64_t)p * ps, c, ncclUint32, p / L, ctx->comm, pr.st));
-            if (vals) NCK(ctx->nccl->Recv(dp.recv_val + (int64_t)p * ps, c, ncclInt32, p / L, ctx->comm, pr.st));
+            recvs.push_back({p / L, dp.recv + (int64_t)p * ps, (size_t)c * 4});
+            if (vals) recvs.push_back({p / L, dp.recv_val + (int64_t)p * ps, (size_t)c * 4});
           }
         }
-      NCK(ctx->nccl->GroupEnd());
+      {
+        irgl_status_t xs = x_exchange(ctx, pr, sends, recvs);
+        if (xs != IRGL_OK) return xs;
+      }
       if (L > 1) CK(cudaStreamSynchronize(pr.st));  // other local partitions apply on their streams
     } else {
       for (int q = 0; q < L; ++q) {
@@ -1692,6 +1802,29 @@ irgl_status_t irgl_ctx_create_nccl(int device, int rank, int nranks, const void*
   return IRGL_OK;
 }
 
+irgl_status_t irgl_ctx_create_transport(int device, int rank, int nranks, const irgl_transport* t,
+                                        const irgl_config* cfg, irgl_ctx** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || !t || !t->allgather || !t->alltoallv) {
+    set_error(nullptr, IRGL_E_INVALID, "E_INVALID", "irgl_ctx_create_transport: bad arguments");
+    return IRGL_E_INVALID;
+  }
+  auto c = std::make_unique<irgl_ctx>();
+  if (cfg) c->cfg = *cfg;
+  const int L = c->cfg.logical_partitions > 1 ? c->cfg.logical_partitions : 1;
+  irgl_status_t s = ctx_init_parts(c.get(), &device, 1, L);
+  if (s != IRGL_OK) return s;
+  c->xport = *t;
+  c->rank = rank;
+  c->nranks = nranks;
+  const int P = nranks * L;
+  if (cudaMalloc(&c->cnt_dev, ((size_t)L * P + (size_t)P * P) * 4) != cudaSuccess) {
+    set_error(nullptr, IRGL_E_OOM, "E_OOM", "count exchange scratch");
+    return IRGL_E_OOM;
+  }
+  *out = c.release();
+  return IRGL_OK;
+}
+
 irgl_status_t irgl_ctx_sync(irgl_ctx* ctx) {
   if (!ctx) return IRGL_E_INVALID;
   for (auto& p : ctx->parts) {
@@ -1713,6 +1846,7 @@ irgl_status_t irgl_ctx_destroy(irgl_ctx* ctx) {
     cudaStreamSynchronize(p.st);
   }
   if (ctx->comm) ctx->nccl->CommDestroy(ctx->comm);
+  if (ctx->xbuf) cudaFreeHost(ctx->xbuf);
   cudaSetDevice(ctx->parts[0].dev);
   if (ctx->test_log) cudaFree(ctx->test_log);
   if (ctx->test_rcount) cudaFree(ctx->test_rcount);

@@ -128,7 +128,8 @@ BLOCK_ELASTIC, BLOCK_SHRINKABLE, BLOCK_FIXED = 0, 1, 2
 
 # every symbol include/irgl/rt.h declares (tests check the .so exports all of them)
 EXPORTS = [
-    "irgl_ctx_create", "irgl_nccl_unique_id", "irgl_ctx_create_nccl", "irgl_ctx_destroy",
+    "irgl_ctx_create", "irgl_nccl_unique_id", "irgl_ctx_create_nccl", "irgl_ctx_create_transport",
+    "irgl_ctx_destroy",
     "irgl_ctx_sync", "irgl_last_error", "irgl_abi_version", "irgl_graph_create_csr",
     "irgl_graph_generate", "irgl_graph_read_edgelist", "irgl_graph_info_get", "irgl_graph_download", "irgl_graph_destroy",
     "irgl_pipe_create", "irgl_pipe_init_scalars", "irgl_pipe_init_from_array",
@@ -171,6 +172,7 @@ def load_library(path: str | None = None):
         "irgl_ctx_create": ([C.POINTER(C.c_int), C.c_int, C.POINTER(Config), pp], i32),
         "irgl_nccl_unique_id": ([P], i32),
         "irgl_ctx_create_nccl": ([C.c_int, C.c_int, C.c_int, P, C.POINTER(Config), pp], i32),
+        "irgl_ctx_create_transport": ([C.c_int, C.c_int, C.c_int, P, C.POINTER(Config), pp], i32),
         "irgl_ctx_destroy": ([P], i32),
         "irgl_ctx_sync": ([P], i32),
         "irgl_last_error": ([P], C.c_char_p),
@@ -306,7 +308,7 @@ class Context:
 
     def __init__(self, devices=(0,), *, outline=-1, blocks_per_sm=0, retry_serialize_after=0,
                  warp_threshold=0, cta_threshold=0, chunk_edges=0, logical_partitions=0,
-                 dense_div=0, bfs_bitmap_min_n=0, l2_persist=0, nccl=None):
+                 dense_div=0, bfs_bitmap_min_n=0, l2_persist=0, nccl=None, transport=None):
         L = load_library()
         cfg = Config()
         cfg.outline = outline
@@ -320,7 +322,11 @@ class Context:
         cfg.bfs_bitmap_min_n = bfs_bitmap_min_n
         cfg.l2_persist = l2_persist
         h = C.c_void_p()
-        if nccl is not None:  # (device, rank, nranks, uid)
+        self._transport = transport
+        if transport is not None:  # dist.TorchTransport (or any object with .struct/.rank/...)
+            _check(L.irgl_ctx_create_transport(transport.device, transport.rank, transport.nranks,
+                                               C.byref(transport.struct), C.byref(cfg), C.byref(h)))
+        elif nccl is not None:  # (device, rank, nranks, uid)
             dev, rank, nranks, uid = nccl
             _check(L.irgl_ctx_create_nccl(dev, rank, nranks, uid, C.byref(cfg), C.byref(h)))
         else:
