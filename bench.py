@@ -418,6 +418,56 @@ def one_gpu_reference_point(args, op_id, kw, relabel):
     return out
 
 
+def secondary_entries(args, scales_ops):
+    """Secondary driver-timed workloads of the same metric (BASELINE configs: BFS on RMAT-22, the
+    north-star RMAT-24 BFS / SSSP), each on its own context in the bench's layout (degree-ordered
+    ids), K traversals over the 16 sources through irgl_traverse_batch, with the roofline of
+    SURVEY §8d and bit-exact parity of source 0 against the oracle."""
+    import argparse as _ap
+    import paper_1607_05707_b200 as irgl
+    from oracle import oracle as O  # checker only
+    solo = Dist(single=True)
+    peak, _ = load_peaks()
+    out = []
+    og_cache = {}
+    for scale, op in scales_ops:
+        a = _ap.Namespace(**vars(args))
+        a.scale, a.op = scale, op
+        op_id = irgl.SSSP if op == "sssp" else irgl.BFS
+        with irgl.Context(devices=[int(os.environ.get("LOCAL_RANK", "0"))], outline=args.outline) as c:
+            g = c.generate_rmat(scale)
+            g.relabel()
+            p = c.pipe(g.n)
+            cand, er, vr = _sources_and_work(c, g, p, solo, True)
+            r = _timed_traversals(a, solo, c, g, p, op_id, cand, er, vr, {})
+            gteps = r["tot_e"] / 2 / (r["dev_ms"] * 1e-3) / 1e9
+            ach = r["tot_b"] / (r["kms"] * 1e-3) / 1e9 if r["kms"] > 0 else None
+            p.init_scalars([cand[0]])
+            c.iterate(op_id, g, p)
+            gpu = c.read_result(op_id, g)
+            p.close()
+            g.close()
+        if scale not in og_cache:
+            og_cache.clear()
+            og_cache[scale] = O.rmat(scale)
+        og = og_cache[scale]
+        ref = O.sssp(og, cand[0]) if op == "sssp" else O.bfs(og, cand[0])[0]
+        traffic, note = ncu_traffic(op, scale, 1, 1)
+        out.append({"workload": f"{op.upper()} on RMAT-{scale} (degree-ordered ids), {args.steps} "
+                                f"traversals over 16 sources", "value": round(gteps, 3),
+                    "unit": "GTEPS", "ms_per_step": round(r["dev_ms"] / args.steps, 4),
+                    "roofline": {"achieved": round(ach, 1) if ach else None, "peak": peak,
+                                 "frac": round(ach / peak, 4) if ach else None,
+                                 "kernel_ms_per_step": round(r["kms"] / args.steps, 4),
+                                 "algorithmic_bytes_per_step": round(r["tot_b"] / args.steps),
+                                 "traffic": traffic, "traffic_source": note},
+                    "gpu_launches": r["launches"],
+                    "parity": "bit-exact" if np.array_equal(gpu, ref) else "MISMATCH",
+                    "parity_check": f"source {cand[0]} against the serial oracle "
+                                    f"({'Dijkstra' if op == 'sssp' else 'queue BFS'})"})
+    return out
+
+
 def run_irgl(args, d):
     import paper_1607_05707_b200 as irgl
     op_id = irgl.SSSP if args.op == "sssp" else irgl.BFS
@@ -545,9 +595,12 @@ def run_irgl(args, d):
         gpu = ctx.read_result(op_id, g)
         ref = O.sssp(og, cand[0]) if args.op == "sssp" else O.bfs(og, cand[0])[0]
         line["parity"] = "bit-exact" if np.array_equal(gpu, ref) else "MISMATCH"
+    ctx.close()
+    # ---- secondary entries (N=1): BFS at the headline scale, the north-star RMAT-24 BFS / SSSP
+    if d.world == 1 and args.secondary and args.scale == 22 and args.op == "sssp" and not args.direction:
+        line["detail"]["secondary"] = secondary_entries(args, [(22, "bfs"), (24, "bfs"), (24, "sssp")])
     if d.rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
     return 0
 
 
@@ -587,6 +640,9 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", type=int, default=1,
+                    help="N=1 default workload: also time BFS RMAT-22 and BFS / SSSP RMAT-24 "
+                         "(detail.secondary, with parity)")
     ap.add_argument("--no-one-gpu-point", action="store_true",
                     help="N>1: skip the one-GPU RMAT-27 reference point in detail.one_gpu")
     ap.add_argument("--batch", type=int, default=1,
