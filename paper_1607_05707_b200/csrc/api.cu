@@ -1251,10 +1251,14 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   pa.trace = nullptr;
   pa.trace_cap = 0;
   const char* tr = getenv("IRGL_ROUND_TRACE");
-  if (tr && *tr == '1') {
+  // IRGL_ROUND_TRACE=2 also records every CTA's item-phase end (first 64 rounds): the spread of
+  // those times is the item phase's tail
+  const size_t cta_words = (tr && *tr == '2') ? 64 * (size_t)grid : 0;
+  if (tr && (*tr == '1' || *tr == '2')) {
     pa.trace_cap = 4096;
-    CK(cudaMallocAsync(&pa.trace, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
-    CK(cudaMemsetAsync(pa.trace, 0, (8 * (size_t)pa.trace_cap + 1) * 8, pr.st));
+    pa.trace_cta = cta_words ? 64 : 0;
+    CK(cudaMallocAsync(&pa.trace, (8 * (size_t)pa.trace_cap + 1 + cta_words) * 8, pr.st));
+    CK(cudaMemsetAsync(pa.trace, 0, (8 * (size_t)pa.trace_cap + 1 + cta_words) * 8, pr.st));
   }
   if (o.max_rounds > 0 && pa.max_rounds == 0) return IRGL_OK;
   // one launch resets the control block for the outlined loop (chunk / tile / far counters, deferral
@@ -1282,7 +1286,7 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
     stt->kernel_ms += kms;
   }
   if (pa.trace) {
-    std::vector<unsigned long long> t(8 * (size_t)pa.trace_cap + 1);
+    std::vector<unsigned long long> t(8 * (size_t)pa.trace_cap + 1 + cta_words);
     CK(cudaMemcpy(t.data(), pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
     CK(cudaFree(pa.trace));
     unsigned long long prev = t[8 * (size_t)pa.trace_cap], e0 = 0;
@@ -1293,6 +1297,18 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
       fprintf(stderr, "irgl-trace op=%d round=%llu us=%.2f in=%llu out=%llu edges=%llu item=%.2f flush=%.2f sync1=%.2f chunk=%.2f nch=%llu\n",
               op, (unsigned long long)r, us(q[0]), q[1] & 0xffffffffull, q[2], q[3] - e0, us(q[4]), us(q[5]), us(q[6]),
               us(q[7]), q[1] >> 32);
+      if (cta_words && r < 64) {  // item-phase end per CTA, relative to the round start
+        std::vector<double> ct;
+        for (int b = 0; b < grid; ++b) {
+          const unsigned long long x = t[8 * (size_t)pa.trace_cap + 1 + r * (size_t)grid + b];
+          if (x) ct.push_back((x - prev) * 1e-3);
+        }
+        std::sort(ct.begin(), ct.end());
+        if (!ct.empty())
+          fprintf(stderr, "irgl-trace-cta round=%llu ctas=%zu item_end_us min=%.2f p50=%.2f p90=%.2f p99=%.2f max=%.2f\n",
+                  (unsigned long long)r, ct.size(), ct.front(), ct[ct.size() / 2], ct[ct.size() * 9 / 10],
+                  ct[ct.size() * 99 / 100], ct.back());
+      }
       prev = q[0];
       e0 = q[3];
     }

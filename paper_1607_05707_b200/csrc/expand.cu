@@ -1080,6 +1080,8 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 4]));
     wflush_all<OP>(sm, q, p, rr);
     if (leader && a.trace && r < a.trace_cap) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * r + 5]));
+    if (a.trace && r < a.trace_cta && threadIdx.x == 0)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(a.trace[8 * (size_t)a.trace_cap + 1 + (size_t)r * gridDim.x + blockIdx.x]));
     // the deferral minimum of round r+1 is final at the round's last barrier: thread 0 of each CTA
     // fetches it into shared memory there (no per-warp reads of one hot cell)
     auto fetch_dmin = [&]() {

@@ -113,6 +113,7 @@ struct PersistArgs {
   int64_t dense_min;   // rounds with |in| >= dense_min run dense (0 = never)
   unsigned long long* trace;  // optional per-round trace [4 * trace_cap + 1] (IRGL_ROUND_TRACE)
   uint32_t trace_cap;
+  uint32_t trace_cta = 0;     // rounds with per-CTA item-phase end times after the round trace
   // device-resident stamp epoch (pipelined batches): when set, the kernel takes its first stamp
   // id from *stamp_base + 1 instead of stamp0 and leaves its last used id there, so a traversal
   // can be launched before the previous one's stamp count reached the host

@@ -1,7 +1,7 @@
 """Per-round trace of one outlined traversal: IRGL_ROUND_TRACE=1 python tools/round_trace.py
 [scale] [op] [defer]   (op: bfs|bfs-do|sssp; RELABEL=1: degree-ordered ids).  The runtime prints one line per round to stderr."""
 import ctypes as C, os, sys
-os.environ["IRGL_ROUND_TRACE"] = "1"
+os.environ.setdefault("IRGL_ROUND_TRACE", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
