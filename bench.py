@@ -321,6 +321,9 @@ def workload_config(args, g, layout=None):
            "l2": "inputs larger than L2 (CSR col+weight >> 126 MB); no flush",
            "layout": layout or ("degree-ordered vertex relabelling (untimed preprocessing; API ids "
                                 "unchanged)" if args.relabel and args.gpus == 1 else
+                                "1D vertex partition, block-diagonal degree order (each rank "
+                                "renumbers its own range; untimed; API ids unchanged)"
+                                if args.relabel else
                                 "generator (Philox-scrambled) ids, 1D vertex partition"
                                 if args.gpus > 1 else "generator (Philox-scrambled) ids")}
     if args.gpus > 1:
@@ -339,13 +342,13 @@ def _sources_and_work(ctx, g, p, d, relabelled):
     info = g.info
     rp = _local_row_ptr(ctx, g)
     lo, hi = info.lo, info.hi
-    if relabelled:  # degrees in the caller's ids for the source pick
-        dg = np.diff(rp)[g.perm()]
-        rp = np.zeros(g.n + 1, dtype=np.int64)
-        rp[1:] = np.cumsum(dg)
+    perm = g.perm() if relabelled else None  # caller id -> new id (same owner range)
 
-    def local_deg(x):
-        return int(rp[x - lo + 1] - rp[x - lo]) if lo <= x < hi else 0
+    def local_deg(x):  # degree of caller id x if this rank owns it
+        if not (lo <= x < hi):
+            return 0
+        y = int(perm[x]) if perm is not None else x
+        return int(rp[y - lo + 1] - rp[y - lo])
 
     cand = pick_sources(g.n, lambda x: d.reduce(local_deg(x), "sum"))
     er, vr = [], []
@@ -488,9 +491,10 @@ def run_irgl(args, d):
     g = ctx.generate_rmat(args.scale)
     gen_s = time.time() - t0
     relabel_s = None
-    if args.relabel and d.world == 1:
-        # data layout: degree-ordered vertex ids (preprocessing, like the CSR build: untimed);
-        # every id crossing the API stays the generator's
+    if args.relabel:
+        # data layout: degree-ordered vertex ids (preprocessing, like the CSR build: untimed); at
+        # N > 1 block-diagonal (each rank orders its own range); every id crossing the API stays
+        # the generator's
         t0 = time.time()
         g.relabel()
         relabel_s = time.time() - t0

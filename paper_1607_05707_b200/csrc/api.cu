@@ -68,6 +68,11 @@ struct irgl_ctx {
 namespace irgl {
 struct GraphPart {
   int64_t lo = 0, hi = 0, m = 0, maxdeg = 0;
+  // block-diagonal degree order of a P > 1 graph (irgl_graph_relabel): every partition's new ids
+  // (n entries, on this partition's device) and this partition's inverse (new local -> old)
+  int32_t* perm_g = nullptr;
+  int32_t* inv_l = nullptr;
+  int32_t* res_part = nullptr;  // staging of this partition's results in the caller's ids
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
   int32_t* w = nullptr;
@@ -2108,7 +2113,8 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
                   gp.tc_rp, gp.tc_cl, gp.tc_src, gp.vis, gp.lab_buf[1], gp.pr_hub_of, gp.pr_hfirst, gp.pr_cbeg,
                   gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
-                  gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8};
+                  gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8, gp.perm_g, gp.inv_l,
+                  gp.res_part};
     for (void* p : ps)
       if (p) cudaFree(p);
   }
@@ -2271,10 +2277,13 @@ static irgl_status_t map_pipe(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g) {
   if (!pipe || !g || !g->relabeled || pipe->mapped_for == g) return IRGL_OK;
   if (pipe->mapped_for)
     return fail(ctx, IRGL_E_USAGE, "E_USAGE", "pipe items carry another relabelled graph's ids; re-initialise it");
-  PipePart& pp = pipe->parts[0];
-  PartRT& pr = ctx->parts[0];
-  CK(cudaSetDevice(pr.dev));
-  CK(launch_map_items(pp.buf[pp.b_in], pp.n_in, g->perm, pr.st));
+  for (size_t l = 0; l < pipe->parts.size(); ++l) {  // each partition's items are its own ids
+    PipePart& pp = pipe->parts[l];
+    PartRT& pr = ctx->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    const int32_t* table = g->parts.size() > 1 || ctx->ptotal() > 1 ? g->parts[l].perm_g : g->perm;
+    CK(launch_map_items(pp.buf[pp.b_in], pp.n_in, table, pr.st));
+  }
   pipe->mapped_for = g;
   return IRGL_OK;
 }
@@ -2461,12 +2470,89 @@ static irgl_status_t stage_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, int 
   return IRGL_OK;
 }
 
+// P > 1: block-diagonal degree order.  Every partition renumbers its own vertices inside its own
+// id range (degree descending), so owners, routing, buckets and pipe contents keep their meaning;
+// the partitions' new ids are then gathered (peer copies in one process, the rank transport across
+// processes) so each partition can map its column ids, and each CSR is rewritten and re-sorted.
+static irgl_status_t relabel_partitioned(irgl_ctx* ctx, irgl_graph* g) {
+  const int L = (int)g->parts.size();
+  const int64_t ps = g->part_size;
+  for (int l = 0; l < L; ++l) {  // phase 1: each partition's own order
+    PartRT& pr = ctx->parts[l];
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    CK(cudaStreamSynchronize(pr.st));
+    int32_t* perm_local = nullptr;
+    CK(relabel_order(gp.hi - gp.lo, gp.lo, gp.maxdeg, gp.row_ptr, &perm_local, &gp.inv_l, pr.st));
+    CK(cudaMalloc(&gp.perm_g, std::max<int64_t>(g->n, 1) * 4));
+    if (gp.hi > gp.lo)
+      CK(cudaMemcpy(gp.perm_g + gp.lo, perm_local, (gp.hi - gp.lo) * 4, cudaMemcpyDeviceToDevice));
+    cudaFree(perm_local);
+  }
+  // phase 1b: every partition's new ids everywhere
+  if (multi_rank(ctx)) {
+    // this rank's L partitions are contiguous: ranks exchange blocks of L * part_size ids
+    PartRT& pr = ctx->parts[0];
+    CK(cudaSetDevice(pr.dev));
+    const int64_t blk = (int64_t)L * ps;
+    int32_t* all = nullptr;
+    CK(cudaMalloc(&all, (size_t)blk * (ctx->nranks + 1) * 4));
+    const int64_t lo0 = g->parts[0].lo;
+    for (int l = 0; l < L; ++l) {
+      GraphPart& gp = g->parts[l];
+      if (gp.hi > gp.lo)
+        CK(cudaMemcpyAsync(all + (gp.lo - lo0), gp.perm_g + gp.lo, (gp.hi - gp.lo) * 4,
+                           cudaMemcpyDeviceToDevice, pr.st));
+    }
+    irgl_status_t xs = x_allgather(ctx, pr, all, all + blk, (size_t)blk * 4);
+    if (xs != IRGL_OK) return xs;
+    CK(cudaStreamSynchronize(pr.st));
+    for (int l = 0; l < L; ++l)
+      CK(cudaMemcpyAsync(g->parts[l].perm_g, all + blk, g->n * 4, cudaMemcpyDeviceToDevice, pr.st));
+    CK(cudaStreamSynchronize(pr.st));
+    cudaFree(all);
+  } else {
+    for (int l = 0; l < L; ++l)
+      for (int k = 0; k < L; ++k) {
+        if (k == l) continue;
+        GraphPart& src = g->parts[k];
+        if (src.hi > src.lo)
+          CK(cudaMemcpyPeer(g->parts[l].perm_g + src.lo, ctx->parts[l].dev, src.perm_g + src.lo,
+                            ctx->parts[k].dev, (src.hi - src.lo) * 4));
+      }
+  }
+  for (int l = 0; l < L; ++l) {  // phase 2: CSR rewrite
+    PartRT& pr = ctx->parts[l];
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    int64_t* rp_new = nullptr;
+    CK(relabel_rewrite(gp.hi - gp.lo, gp.lo, g->n, gp.m, gp.row_ptr, gp.perm_g + gp.lo, gp.inv_l,
+                       gp.perm_g, &gp.col, &gp.w, &rp_new, pr.st));
+    CK(cudaFree(gp.row_ptr));
+    gp.row_ptr = rp_new;
+    if (gp.w8) cudaFree(gp.w8);  // the weights were permuted
+    gp.w8 = nullptr;
+    gp.w8_state = 0;
+  }
+  // host inverse for worklist reads (pipe items of the local partitions)
+  g->inv_host.resize(g->n);
+  for (int64_t v = 0; v < g->n; ++v) g->inv_host[v] = (int32_t)v;
+  for (int l = 0; l < L; ++l) {
+    GraphPart& gp = g->parts[l];
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    if (gp.hi > gp.lo)
+      CK(cudaMemcpy(g->inv_host.data() + gp.lo, gp.inv_l, (gp.hi - gp.lo) * 4, cudaMemcpyDeviceToHost));
+  }
+  g->lab_op = -1;
+  g->relabeled = true;
+  return IRGL_OK;
+}
+
 irgl_status_t irgl_graph_relabel(irgl_ctx* ctx, irgl_graph* g) {
   if (!ctx || !g || g->ctx != ctx) return IRGL_E_INVALID;
-  if (g->parts.size() != 1 || ctx->ptotal() != 1)
-    return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED", "relabelling needs a one-partition graph");
   if (g->relabeled) return IRGL_OK;
   if (g->n >= (1ll << 31)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "relabelling needs n < 2^31");
+  if (g->parts.size() != 1 || ctx->ptotal() != 1) return relabel_partitioned(ctx, g);
   PartRT& pr = ctx->parts[0];
   GraphPart& gp = g->parts[0];
   CK(cudaSetDevice(pr.dev));
@@ -2504,7 +2590,8 @@ irgl_status_t irgl_graph_perm(irgl_graph* g, int32_t* new_of_old) {
   }
   CK(cudaSetDevice(ctx->parts[0].dev));
   CK(cudaStreamSynchronize(ctx->parts[0].st));  // the relabel kernels run on the stream
-  CK(cudaMemcpy(new_of_old, g->perm, g->n * 4, cudaMemcpyDeviceToHost));
+  const int32_t* perm = g->parts[0].perm_g ? g->parts[0].perm_g : g->perm;
+  CK(cudaMemcpy(new_of_old, perm, g->n * 4, cudaMemcpyDeviceToHost));
   return IRGL_OK;
 }
 
@@ -2535,6 +2622,24 @@ irgl_status_t irgl_read_result(irgl_ctx* ctx, irgl_graph* g, irgl_op op, void* h
   if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
   const size_t esz = op == IRGL_OP_PR ? 8 : 4;
   if (bytes < (size_t)g->n * esz) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  if (g->relabeled && (g->parts.size() > 1 || ctx->ptotal() > 1)) {
+    // block-diagonal order: each partition gathers its own range back through perm
+    if (op != IRGL_OP_BFS && op != IRGL_OP_SSSP)
+      return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
+                  "results of a relabelled vertex-partitioned graph: BFS and SSSP");
+    for (size_t l = 0; l < g->parts.size(); ++l) {
+      GraphPart& gp = g->parts[l];
+      PartRT& pr = ctx->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      const int64_t nloc = gp.hi - gp.lo;
+      if (nloc <= 0) continue;
+      if (!gp.res_part) CK(cudaMalloc(&gp.res_part, nloc * 4));
+      CK(launch_gather_range_i32(gp.res_part, gp.lab, gp.perm_g, gp.lo, nloc, pr.st));
+      CK(cudaMemcpyAsync((int32_t*)host_out + gp.lo, gp.res_part, nloc * 4, cudaMemcpyDeviceToHost, pr.st));
+      CK(cudaStreamSynchronize(pr.st));
+    }
+    return IRGL_OK;
+  }
   if (g->relabeled) {  // back to the caller's vertex ids on the device, then one copy
     const int k = g->res_sel;
     if (g->res_pending[k]) {
@@ -2569,6 +2674,8 @@ irgl_status_t irgl_read_result_async(irgl_ctx* ctx, irgl_graph* g, irgl_op op, v
     return irgl_read_result(ctx, g, op, host_out, bytes);  // small or host-side results: synchronous
   if (g->lab_op != op) return fail(ctx, IRGL_E_USAGE, "E_USAGE", "operator has not run on this graph");
   if (bytes < (size_t)g->n * 4) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "result buffer too small");
+  if (g->relabeled && (g->parts.size() > 1 || ctx->ptotal() > 1))
+    return irgl_read_result(ctx, g, op, host_out, bytes);  // partition-wise gather (synchronous)
   if (g->relabeled) {  // stage into one of two result buffers, copy from it in pieces
     PartRT& pr = ctx->parts[0];
     const int k = g->res_sel;

@@ -192,6 +192,16 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
                            cudaStream_t st);
 cudaError_t launch_map_items(uint32_t* items, uint32_t n, const int32_t* table, cudaStream_t st);
 cudaError_t launch_gather_i32(int32_t* out, const int32_t* src, const int32_t* perm, int64_t n, cudaStream_t st);
+cudaError_t launch_gather_range_i32(int32_t* out, const int32_t* src, const int32_t* perm, int64_t lo,
+                                   int64_t nloc, cudaStream_t st);
+// Block-diagonal degree order of a vertex partition (relabel.cu): phase 1 orders the partition's
+// own rows, phase 2 rewrites its CSR once every partition's new ids are known (perm_global).
+cudaError_t relabel_order(int64_t nloc, int64_t lo, int64_t maxdeg, const int64_t* rp_old,
+                          int32_t** perm_local, int32_t** inv_local, cudaStream_t st);
+cudaError_t relabel_rewrite(int64_t nloc, int64_t lo, int64_t n, int64_t m, const int64_t* rp_old,
+                            const int32_t* perm_local, const int32_t* inv_local,
+                            const int32_t* perm_global, int32_t** col_io, int32_t** w_io,
+                            int64_t** rp_new, cudaStream_t st);
 cudaError_t launch_gather_f64(double* out, const double* src, const int32_t* perm, int64_t n, cudaStream_t st);
 cudaError_t launch_cc_labels_original(int32_t* out, const int32_t* lab, const int32_t* perm, const int32_t* inv,
                                       int32_t* cmin, int64_t n, cudaStream_t st);

@@ -24,24 +24,40 @@ __global__ void deg_key_kernel(const int64_t* rp, int64_t n, int64_t maxdeg, uin
   }
 }
 
-__global__ void perm_kernel(const int32_t* inv, int64_t n, int32_t* perm, const int64_t* rp_old,
-                            int64_t* deg_new) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t old = inv[i];
-    perm[old] = (int32_t)i;
+// inv_rel[i] = old local index of new local index i -> perm[old local] = lo + i, inv[i] = lo + old
+__global__ void perm_range_kernel(const int32_t* inv_rel, int64_t nloc, int64_t lo, int32_t* perm,
+                                  int32_t* inv) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t old = inv_rel[i];
+    perm[old] = (int32_t)(lo + i);
+    inv[i] = (int32_t)(lo + old);
+  }
+}
+
+__global__ void deg_new_kernel(const int32_t* inv, int64_t nloc, int64_t lo, const int64_t* rp_old,
+                               int64_t* deg_new) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t old = inv[i] - lo;
     deg_new[i] = rp_old[old + 1] - rp_old[old];
   }
 }
 
-// warp per old vertex: key = perm[u] << 32 | perm[v]
-__global__ void edge_key_kernel(const int64_t* rp, const int32_t* col, const int32_t* perm, int64_t n,
-                                uint64_t* key) {
+// warp per old local row u: key = (perm_local[u] - lo) << 32 | perm_global[v]
+__global__ void edge_key_kernel(const int64_t* rp, const int32_t* col, const int32_t* perm_local, int64_t lo,
+                                const int32_t* perm_global, int64_t nloc, uint64_t* key) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
-    const uint64_t hi = (uint64_t)(uint32_t)perm[u] << 32;
-    for (int64_t k = rp[u] + lane; k < rp[u + 1]; k += 32) key[k] = hi | (uint32_t)perm[col[k]];
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nloc; u += nw) {
+    const uint64_t hi = (uint64_t)(uint32_t)(perm_local[u] - lo) << 32;
+    for (int64_t k = rp[u] + lane; k < rp[u + 1]; k += 32) key[k] = hi | (uint32_t)perm_global[col[k]];
   }
+}
+
+// out[i] = src[perm[lo + i]] for i < nloc (a partition's results in the caller's ids)
+__global__ void gather_range_kernel(int32_t* out, const int32_t* src, const int32_t* perm, int64_t lo,
+                                    int64_t nloc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloc; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = src[perm[lo + i]];
 }
 
 __global__ void low_word_kernel(const uint64_t* key, int64_t m, int32_t* col) {
@@ -89,10 +105,12 @@ inline int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64
     if (_e != cudaSuccess) return _e;    \
   } while (0)
 
-cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* rp_old, int32_t** col_io,
-                           int32_t** w_io, int64_t** rp_new, int32_t** perm_out, int32_t** inv_out,
-                           cudaStream_t st) {
-  // 1. vertex order: stable sort of (maxdeg - degree) keys carrying the old ids
+// Phase 1 for the partition of rows [lo, lo + nloc): its vertices ordered by (degree descending,
+// old id ascending) inside their own id range — perm_local[v - lo] = new id (global, in the same
+// range), inv_local[i] = old id of new id lo + i.  One partition: lo = 0, nloc = n.
+cudaError_t relabel_order(int64_t nloc, int64_t lo, int64_t maxdeg, const int64_t* rp_old,
+                          int32_t** perm_local, int32_t** inv_local, cudaStream_t st) {
+  const int64_t n = std::max<int64_t>(nloc, 1);
   uint32_t *ka = nullptr, *kb = nullptr;
   int32_t *ia = nullptr, *ib = nullptr;
   RL_CK(cudaMallocAsync(&ka, n * 4, st));
@@ -100,48 +118,65 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
   RL_CK(cudaMallocAsync(&ia, n * 4, st));
   RL_CK(cudaMallocAsync(&ib, n * 4, st));
   note_launch();
-  deg_key_kernel<<<grid_for(n), 256, 0, st>>>(rp_old, n, maxdeg, ka, ia);
+  deg_key_kernel<<<grid_for(nloc), 256, 0, st>>>(rp_old, nloc, maxdeg, ka, ia);
   int bits = 1;
   while (bits < 32 && (1ull << bits) <= (uint64_t)maxdeg) ++bits;
   cub::DoubleBuffer<uint32_t> dk(ka, kb);
   cub::DoubleBuffer<int32_t> dv(ia, ib);
   size_t tmp = 0;
-  RL_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, n, 0, bits, st));
+  RL_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, nloc, 0, bits, st));
   void* t = nullptr;
   RL_CK(cudaMallocAsync(&t, tmp, st));
-  RL_CK(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, n, 0, bits, st));
+  RL_CK(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, nloc, 0, bits, st));
   cudaFreeAsync(t, st);
-  int32_t* inv = dv.Current();
-  cudaFreeAsync(dv.Alternate(), st);
   cudaFreeAsync(ka, st);
   cudaFreeAsync(kb, st);
-  // 2. perm = inv^-1, new degrees, new row offsets
-  int32_t* perm = nullptr;
+  int32_t* inv_rel = dv.Current();  // local old index of new local index i
+  int32_t *perm = nullptr, *inv = nullptr;
+  RL_CK(cudaMalloc(&perm, n * 4));
+  RL_CK(cudaMalloc(&inv, n * 4));
+  note_launch();
+  perm_range_kernel<<<grid_for(nloc), 256, 0, st>>>(inv_rel, nloc, lo, perm, inv);
+  cudaFreeAsync(dv.Current(), st);
+  cudaFreeAsync(dv.Alternate(), st);
+  *perm_local = perm;
+  *inv_local = inv;
+  return cudaStreamSynchronize(st);
+}
+
+// Phase 2: the partition's CSR in the new numbering — row i (new local index) is old row
+// inv_local[i] - lo, columns mapped through perm_global[n] (every partition's new ids), each row
+// sorted by new neighbour id; weights ride along.  The old col / w are released.
+cudaError_t relabel_rewrite(int64_t nloc, int64_t lo, int64_t n, int64_t m, const int64_t* rp_old,
+                            const int32_t* perm_local, const int32_t* inv_local,
+                            const int32_t* perm_global, int32_t** col_io, int32_t** w_io,
+                            int64_t** rp_new, cudaStream_t st) {
   int64_t* deg_new = nullptr;
   int64_t* rp = nullptr;
-  RL_CK(cudaMallocAsync(&perm, n * 4, st));
-  RL_CK(cudaMallocAsync(&deg_new, (n + 1) * 8, st));
-  RL_CK(cudaMalloc(&rp, (n + 1) * 8));
+  void* t = nullptr;
+  size_t tmp = 0;
+  RL_CK(cudaMallocAsync(&deg_new, (nloc + 1) * 8, st));
+  RL_CK(cudaMalloc(&rp, (nloc + 1) * 8));
   note_launch();
-  perm_kernel<<<grid_for(n), 256, 0, st>>>(inv, n, perm, rp_old, deg_new);
-  RL_CK(cudaMemsetAsync(deg_new + n, 0, 8, st));
-  tmp = 0;
-  RL_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg_new, rp, n + 1, st));
+  deg_new_kernel<<<grid_for(nloc), 256, 0, st>>>(inv_local, nloc, lo, rp_old, deg_new);
+  RL_CK(cudaMemsetAsync(deg_new + nloc, 0, 8, st));
+  RL_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg_new, rp, nloc + 1, st));
   RL_CK(cudaMallocAsync(&t, tmp, st));
-  RL_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg_new, rp, n + 1, st));
+  RL_CK(cub::DeviceScan::ExclusiveSum(t, tmp, deg_new, rp, nloc + 1, st));
   cudaFreeAsync(t, st);
   cudaFreeAsync(deg_new, st);
-  // 3. edges (perm[u], perm[v]) sorted; weights ride along; the old col/w are released first
   uint64_t *ea = nullptr, *eb = nullptr;
   RL_CK(cudaMallocAsync(&ea, std::max<int64_t>(m, 1) * 8, st));
   note_launch();
-  edge_key_kernel<<<148 * 16, 256, 0, st>>>(rp_old, *col_io, perm, n, ea);
+  edge_key_kernel<<<148 * 16, 256, 0, st>>>(rp_old, *col_io, perm_local, lo, perm_global, nloc, ea);
   RL_CK(cudaStreamSynchronize(st));
   cudaFree(*col_io);  // allocated with cudaMalloc or cudaMallocAsync: cudaFree handles both
   *col_io = nullptr;
   RL_CK(cudaMallocAsync(&eb, std::max<int64_t>(m, 1) * 8, st));
   int ebits = 1;
   while (ebits < 32 && (1ull << ebits) < (uint64_t)n) ++ebits;
+  int hbits = 1;
+  while (hbits < 31 && (1ull << hbits) < (uint64_t)nloc) ++hbits;
   cub::DoubleBuffer<uint64_t> de(ea, eb);
   int32_t* wa = *w_io;
   int32_t* wb = nullptr;
@@ -149,9 +184,9 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
   if (wa) {
     RL_CK(cudaMallocAsync(&wb, std::max<int64_t>(m, 1) * 4 + 16, st));
     cub::DoubleBuffer<int32_t> dw(wa, wb);
-    RL_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, de, dw, m, 0, 32 + ebits, st));
+    RL_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, de, dw, m, 0, 32 + hbits, st));
     RL_CK(cudaMallocAsync(&t, tmp, st));
-    RL_CK(cub::DeviceRadixSort::SortPairs(t, tmp, de, dw, m, 0, 32 + ebits, st));
+    RL_CK(cub::DeviceRadixSort::SortPairs(t, tmp, de, dw, m, 0, 32 + hbits, st));
     cudaFreeAsync(t, st);
     // keep the sorted weights in a cudaMalloc'd (+4 padded) array like every CSR array
     int32_t* w = nullptr;
@@ -162,11 +197,12 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
     cudaFree(wb);
     *w_io = w;
   } else {
-    RL_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, de, m, 0, 32 + ebits, st));
+    RL_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, de, m, 0, 32 + hbits, st));
     RL_CK(cudaMallocAsync(&t, tmp, st));
-    RL_CK(cub::DeviceRadixSort::SortKeys(t, tmp, de, m, 0, 32 + ebits, st));
+    RL_CK(cub::DeviceRadixSort::SortKeys(t, tmp, de, m, 0, 32 + hbits, st));
     cudaFreeAsync(t, st);
   }
+  (void)ebits;
   int32_t* col = nullptr;
   RL_CK(cudaMalloc(&col, (m + 4) * 4));
   note_launch();
@@ -175,9 +211,14 @@ cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* 
   cudaFreeAsync(eb, st);
   *col_io = col;
   *rp_new = rp;
-  *perm_out = perm;
-  *inv_out = inv;
   return cudaStreamSynchronize(st);
+}
+
+cudaError_t relabel_degree(int64_t n, int64_t m, int64_t maxdeg, const int64_t* rp_old, int32_t** col_io,
+                           int32_t** w_io, int64_t** rp_new, int32_t** perm_out, int32_t** inv_out,
+                           cudaStream_t st) {
+  RL_CK(relabel_order(n, 0, maxdeg, rp_old, perm_out, inv_out, st));
+  return relabel_rewrite(n, 0, n, m, rp_old, *perm_out, *inv_out, *perm_out, col_io, w_io, rp_new, st);
 }
 
 cudaError_t launch_weights_u8(const int32_t* w, int64_t m, uint8_t* w8, uint32_t* bad, cudaStream_t st) {
@@ -197,6 +238,14 @@ cudaError_t launch_map_items(uint32_t* items, uint32_t n, const int32_t* table, 
 cudaError_t launch_gather_i32(int32_t* out, const int32_t* src, const int32_t* perm, int64_t n, cudaStream_t st) {
   note_launch();
   gather_kernel<int32_t><<<grid_for(n), 256, 0, st>>>(out, src, perm, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_range_i32(int32_t* out, const int32_t* src, const int32_t* perm, int64_t lo,
+                                   int64_t nloc, cudaStream_t st) {
+  if (nloc <= 0) return cudaSuccess;
+  note_launch();
+  gather_range_kernel<<<grid_for(nloc), 256, 0, st>>>(out, src, perm, lo, nloc);
   return cudaGetLastError();
 }
 

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, spec, logical, q):
+def _rank_main(rank, world, port, spec, logical, q, relabel=False):
     try:
         import torch.distributed as dist
         sys.path.insert(0, ROOT)
@@ -38,6 +38,8 @@ def _rank_main(rank, world, port, spec, logical, q):
         ctx = irgl.Context(transport=TorchTransport(device=0), logical_partitions=logical)
         g = ctx.generate_rmat(spec["scale"]) if spec["kind"] == "rmat" else \
             ctx.generate_grid(spec["w"], spec["h"], perc_keep=spec.get("keep", 1.0))
+        if relabel:  # block-diagonal degree order (perm blocks exchanged through the transport)
+            g.relabel()
         info = g.info
         out = {"n": g.n, "m": g.m, "parts": info.partitions, "lo": info.lo, "local_n": info.local_n}
         res = {}
@@ -47,8 +49,9 @@ def _rank_main(rank, world, port, spec, logical, q):
             for delta, defer in ((0, 0), (0, -1), (8, 0)):
                 d, st = irgl.sssp(ctx, g, s, delta=delta, defer=defer)
                 res[("sssp", s, delta, defer)] = (d, st.rounds, st.exchange_bytes)
-        lab, _ = irgl.cc_lp(ctx, g, outline=0)
-        res[("cc_lp",)] = (lab, 0, 0)
+        if not relabel:
+            lab, _ = irgl.cc_lp(ctx, g, outline=0)
+            res[("cc_lp",)] = (lab, 0, 0)
         # each rank owns [lo, lo + local_n): keep that slice, gather on rank 0
         lo, hi = info.lo, info.lo + info.local_n
         mine = {k: (v[0][lo:hi].copy(), v[1], v[2]) for k, v in res.items()}
@@ -70,12 +73,13 @@ def _rank_main(rank, world, port, spec, logical, q):
         raise
 
 
-def _run(spec, world=2, logical=0):
+def _run(spec, world=2, logical=0, relabel=False):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_rank_main, args=(r, world, port, spec, logical, q)) for r in range(world)]
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, spec, logical, q, relabel))
+          for r in range(world)]
     for p in ps:
         p.start()
     msg = q.get(timeout=600)
@@ -110,3 +114,18 @@ def test_two_process_percolated_grid(oracle):
         np.testing.assert_array_equal(res[("bfs", s)][0], oracle.bfs(og, s)[0])
         np.testing.assert_array_equal(res[("sssp", s, 0, 0)][0], oracle.sssp(og, s))
     np.testing.assert_array_equal(res[("cc_lp",)][0], oracle.cc(og))
+
+
+def test_two_process_relabelled(oracle):
+    """Block-diagonal degree order across two processes: each rank orders its own range, the
+    ranks exchange their new ids through the transport, results come back in the caller's ids."""
+    og = oracle.rmat(12)
+    srcs = [int(s) for s in og.sources(2)]
+    info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs}, 2, 0, relabel=True)
+    for s in srcs:
+        ref, ecc = oracle.bfs(og, s)
+        lv, rounds, _ = res[("bfs", s)]
+        np.testing.assert_array_equal(lv, ref)
+        assert set(rounds) == {ecc + 1}
+        for delta, defer in ((0, 0), (0, -1), (8, 0)):
+            np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], oracle.sssp(og, s))

@@ -71,9 +71,45 @@ def test_relabelled_pipe_read_and_async(irgl, oracle):
             np.testing.assert_array_equal(out, oracle.sssp(og, x))
 
 
-def test_relabel_partitioned_unsupported(irgl, oracle):
+def test_relabel_partitioned_cc_results_unsupported(irgl, oracle):
+    """Relabelled vertex-partitioned graphs return BFS / SSSP results; CC labels (the smallest
+    original id per component needs a global reduction) are refused, not wrong."""
     og = oracle.rmat(10)
     with irgl.Context(logical_partitions=2) as c:
         g = _upload(c, og)
+        g.relabel()
         with pytest.raises(irgl.IrglError):
-            g.relabel()
+            irgl.cc_lp(c, g, outline=0)
+
+
+@pytest.mark.parametrize("P,nccl", [(2, False), (3, False), (4, True)])
+def test_block_diagonal_relabel_partitioned(irgl, oracle, P, nccl):
+    """P > 1: every partition renumbers its own vertices by degree inside its own id range
+    (block-diagonal order; owners and routing unchanged).  BFS levels, invocation counts and SSSP
+    distances stay bit-exact in the caller's ids through the partitioned (exchange) path."""
+    og = oracle.rmat(12)
+    kw = dict(logical_partitions=P)
+    if nccl:
+        kw["nccl"] = (0, 0, 1, irgl.nccl_unique_id())
+    with irgl.Context(**kw) as c:
+        g = c.generate_rmat(12)
+        g.relabel()
+        perm = g.perm()
+        ps = -(-g.n // P)
+        assert np.array_equal(np.sort(perm), np.arange(g.n))
+        assert np.array_equal(perm // ps, np.arange(g.n) // ps)       # block-diagonal
+        rp, col, w = g.download()
+        deg_new = np.diff(rp)
+        np.testing.assert_array_equal(deg_new[perm], og.degrees())
+        for p0 in range(P):                                             # degree-ordered per block
+            d = deg_new[p0 * ps:(p0 + 1) * ps]
+            assert np.all(d[:-1] >= d[1:])
+        for s in og.sources(2):
+            s = int(s)
+            ref, ecc = oracle.bfs(og, s)
+            lv, st = irgl.bfs(c, g, s)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1
+            for delta, defer in ((0, 0), (0, -1), (8, 0)):
+                d, _ = irgl.sssp(c, g, s, delta=delta, defer=defer)
+                np.testing.assert_array_equal(d, oracle.sssp(og, s))
