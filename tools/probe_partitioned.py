@@ -1,6 +1,6 @@
 """Host-orchestrated multi-partition path on one GPU (P logical partitions, NCCL 1-rank transport
 or loopback): per-traversal time and rounds, to size the per-round exchange overhead.
-python tools/probe_partitioned.py [scale] [P] [nccl 0|1] [relabel 0|1]"""
+python tools/probe_partitioned.py [scale] [P] [nccl 0|1] [relabel 0|1] [outline -1|0|1]"""
 import ctypes as C, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -11,7 +11,8 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 use_nccl = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 relabel = int(sys.argv[4]) if len(sys.argv) > 4 else 0
-kw = dict(logical_partitions=P)
+outline = int(sys.argv[5]) if len(sys.argv) > 5 else -1
+kw = dict(logical_partitions=P, outline=outline)
 if use_nccl:
     kw["nccl"] = (0, 0, 1, irgl.nccl_unique_id())
 ctx = irgl.Context(**kw)
@@ -29,6 +30,6 @@ for op, name in ((irgl.BFS, "bfs"), (irgl.SSSP, "sssp")):
         p.init_scalars([s])
         t0 = time.perf_counter(); st = ctx.iterate(op, g, p); t.append(time.perf_counter() - t0)
         r.append(st.rounds); e.append(st.edges)
-    print(f"RMAT-{scale} P={P} nccl={use_nccl} relabel={relabel} {name}: {1e3*np.mean(t):.2f} ms/traversal, rounds {np.mean(r):.1f}, "
+    print(f"RMAT-{scale} P={P} nccl={use_nccl} relabel={relabel} outline={outline} {name}: {1e3*np.mean(t):.2f} ms/traversal, rounds {np.mean(r):.1f}, "
           f"{1e6*np.mean(t)/np.mean(r):.0f} us/round, kernel {st.kernel_ms:.2f} ms", flush=True)
 ctx.close()
