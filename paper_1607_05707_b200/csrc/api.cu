@@ -161,6 +161,13 @@ struct irgl_pipe {
   std::vector<irgl::PipePart> parts;
   const irgl_graph* mapped_for = nullptr;  // relabelled graph whose ids the items now carry
   int64_t id_bound = 0;  // every item id is < id_bound (host inits: max + 1; after a graph op: n)
+  // P > 1: a WorklistInit is routed to owner partitions by the partition size of the ctx's most
+  // recent graph; until the first operator runs the initialiser is kept, so a pipe initialised
+  // while several graphs exist is re-routed for the graph it is first used with
+  int64_t route_size = INT64_MAX;
+  bool pristine = false;
+  std::vector<int64_t> init_items;
+  int64_t init_range[2] = {-1, -1};
 };
 
 // ----------------------------------------------------------------------------------------------
@@ -273,6 +280,12 @@ static irgl_status_t pipe_init_items(irgl_pipe* p, const int64_t* items, int64_t
   irgl_ctx* ctx = p->ctx;
   p->mapped_for = nullptr;  // caller ids; mapped at the first Iterate / Invoke on a relabelled graph
   if (count < 0 || (count > 0 && !items)) return fail(ctx, IRGL_E_INVALID, "E_INVALID", "bad init array");
+  if (ctx->ptotal() > 1) {
+    if (items != p->init_items.data()) p->init_items.assign(items, items + count);
+    p->init_range[0] = p->init_range[1] = -1;
+    p->route_size = ctx->route_size;
+    p->pristine = true;
+  }
   const int L = (int)ctx->parts.size();
   std::vector<std::vector<uint32_t>> per(L);
   p->id_bound = 0;
@@ -922,7 +935,7 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
 // Owner-side applies are stream-ordered after the receives; the in/out swap needs no counts.
 static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                           int64_t level0, const irgl_iterate_opts& o, NearFar& nf,
-                                          irgl_iter_stats* stt) {
+                                          irgl_iter_stats* stt, int dir_opt = 0) {
   const int L = (int)ctx->parts.size();
   const int P = ctx->ptotal();
   const int H = P + 2;  // header words per partition
@@ -952,8 +965,140 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
   };
   double t_a = 0, t_b = 0, t_c = 0, t_d = 0;
+  // F1 on a partitioned graph (BFS, direction-optimising; Beamer's alpha / beta switch on the
+  // global frontier size and edge count): bottom-up rounds need no remote updates — every
+  // partition tests its own unvisited vertices against the global frontier, an n-bit bitmap of
+  // which each partition fills its own part_size / 32 words and the partitions exchange them
+  // (peer copies, or the rank transport's allgather) instead of id lists.
+  const bool do_bfs = op == IRGL_OP_BFS && dir_opt;
+  const int64_t wpp = (ps + 31) / 32;
+  bool bottom_up = false;
+  uint64_t explored = 0;
+  unsigned long long* fstats = nullptr;  // [L * 2] local stats, then [nranks * L * 2] gathered
+  std::vector<uint32_t*> fbits(L, nullptr);
+  struct DoFree {
+    std::vector<uint32_t*>* b;
+    unsigned long long** f;
+    irgl_ctx* c;
+    ~DoFree() {
+      for (size_t l = 0; l < b->size(); ++l)
+        if ((*b)[l]) { cudaSetDevice(c->parts[l].dev); cudaFree((*b)[l]); }
+      if (*f) { cudaSetDevice(c->parts[0].dev); cudaFree(*f); }
+    }
+  } do_free{&fbits, &fstats, ctx};
+  if (do_bfs) {
+    CK(cudaSetDevice(ctx->parts[0].dev));
+    CK(cudaMalloc(&fstats, (size_t)2 * L * (1 + ctx->nranks) * 8));
+    for (int l = 0; l < L; ++l) {
+      CK(cudaSetDevice(ctx->parts[l].dev));
+      CK(cudaMalloc(&fbits[l], (size_t)P * wpp * 4));
+    }
+  }
   for (;;) {
     if (o.max_rounds > 0 && stt->rounds >= o.max_rounds) break;  // ExtraCond (Or)
+    if (do_bfs) {
+      // frontier size / edges of every partition's in-worklist
+      std::vector<unsigned long long> fs((size_t)2 * P, 0);
+      for (int l = 0; l < L; ++l) {
+        PartRT& pr = ctx->parts[l];
+        PipePart& pp = pipe->parts[l];
+        GraphPart& gp = g->parts[l];
+        CK(cudaSetDevice(pr.dev));
+        unsigned long long* dst = fstats + 2 * l;
+        if (pr.dev != ctx->parts[0].dev) {  // stats of a partition on another device: own slot
+          unsigned long long* tmp = nullptr;
+          CK(cudaMalloc(&tmp, 16));
+          CK(launch_frontier_stats(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], gp.row_ptr, gp.lo, tmp, pr.st));
+          CK(cudaMemcpyAsync(&fs[2 * ctx->gpart(l)], tmp, 16, cudaMemcpyDeviceToHost, pr.st));
+          CK(cudaStreamSynchronize(pr.st));
+          cudaFree(tmp);
+          continue;
+        }
+        CK(launch_frontier_stats(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], gp.row_ptr, gp.lo, dst, pr.st));
+        CK(cudaStreamSynchronize(pr.st));
+      }
+      {
+        PartRT& pr = ctx->parts[0];
+        CK(cudaSetDevice(pr.dev));
+        if (multi_rank(ctx)) {
+          irgl_status_t xs = x_allgather(ctx, pr, fstats, fstats + 2 * L, (size_t)2 * L * 8);
+          if (xs != IRGL_OK) return xs;
+          CK(cudaMemcpyAsync(fs.data(), fstats + 2 * L, (size_t)2 * P * 8, cudaMemcpyDeviceToHost, pr.st));
+        } else {
+          for (int l = 0; l < L; ++l)
+            if (ctx->parts[l].dev == pr.dev)
+              CK(cudaMemcpyAsync(&fs[2 * ctx->gpart(l)], fstats + 2 * l, 16, cudaMemcpyDeviceToHost, pr.st));
+        }
+        CK(cudaStreamSynchronize(pr.st));
+      }
+      uint64_t fn = 0, fm = 0;
+      for (int p = 0; p < P; ++p) {
+        fn += fs[2 * p];
+        fm += fs[2 * p + 1];
+      }
+      if (fn == 0) break;  // every in worklist is empty: the Iterate ends
+      constexpr double kAlpha = 14.0, kBeta = 24.0;
+      const double mu = (double)g->m - (double)explored;
+      if (!bottom_up && stt->rounds > 0 && (double)fm > mu / kAlpha) bottom_up = true;
+      else if (bottom_up && (double)fn < (double)g->n / kBeta) bottom_up = false;
+      explored += fm;
+      if (bottom_up) {
+        for (int l = 0; l < L; ++l) {  // this partition's block of the frontier bitmap
+          PartRT& pr = ctx->parts[l];
+          PipePart& pp = pipe->parts[l];
+          CK(cudaSetDevice(pr.dev));
+          CK(cudaMemsetAsync(fbits[l], 0, (size_t)P * wpp * 4, pr.st));
+          CK(launch_frontier_bits(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], fbits[l], pr.st));
+          CK(cudaStreamSynchronize(pr.st));
+        }
+        if (multi_rank(ctx)) {  // the rank's L blocks are contiguous: one allgather of L * wpp words
+          PartRT& pr = ctx->parts[0];
+          CK(cudaSetDevice(pr.dev));
+          uint32_t* all = nullptr;
+          const size_t blk = (size_t)L * wpp;
+          CK(cudaMalloc(&all, blk * 4 * (1 + (size_t)ctx->nranks)));
+          for (int l = 0; l < L; ++l)
+            CK(cudaMemcpyAsync(all + (size_t)l * wpp, fbits[l] + (size_t)ctx->gpart(l) * wpp, wpp * 4,
+                               cudaMemcpyDeviceToDevice, pr.st));
+          irgl_status_t xs = x_allgather(ctx, pr, all, all + blk, blk * 4);
+          if (xs != IRGL_OK) { cudaFree(all); return xs; }
+          for (int l = 0; l < L; ++l)
+            CK(cudaMemcpyAsync(fbits[l], all + blk, (size_t)P * wpp * 4, cudaMemcpyDeviceToDevice, pr.st));
+          CK(cudaStreamSynchronize(pr.st));
+          cudaFree(all);
+        } else {
+          for (int l = 0; l < L; ++l)
+            for (int k = 0; k < L; ++k)
+              if (k != l)
+                CK(cudaMemcpyPeer(fbits[l] + (size_t)ctx->gpart(k) * wpp, ctx->parts[l].dev,
+                                  fbits[k] + (size_t)ctx->gpart(k) * wpp, ctx->parts[k].dev, wpp * 4));
+        }
+        uint64_t local_in = 0;
+        for (int l = 0; l < L; ++l) local_in += fs[2 * ctx->gpart(l)];
+        for (int l = 0; l < L; ++l) {  // bottom-up over each partition's own vertices
+          PartRT& pr = ctx->parts[l];
+          GraphPart& gp = g->parts[l];
+          PipePart& pp = pipe->parts[l];
+          CK(cudaSetDevice(pr.dev));
+          RoundBufs rb = round_bufs(pipe, gp, pp, (int32_t)level, (int32_t)(++g->stamp_epoch), nf);
+          CK(launch_bu_part(gp.csr(), gp.lab, gp.vis_k(), pp.ctl, rb, fbits[l], pr.st));
+          // in <- the finds; the consumed in-count becomes the (empty) out counter
+          CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_in], 0, 4, pr.st));
+          std::swap(pp.b_in, pp.b_out);
+          std::swap(pp.c_in, pp.c_out);
+          stt->launches += 1;
+        }
+        for (int l = 0; l < L; ++l) {
+          CK(cudaSetDevice(ctx->parts[l].dev));
+          CK(cudaStreamSynchronize(ctx->parts[l].st));
+        }
+        if (stt->rounds > 0) stt->pushes += (int64_t)local_in;
+        stt->popped += (int64_t)local_in;
+        stt->rounds++;
+        ++level;
+        continue;
+      }
+    }
     const int32_t stamp_id = (int32_t)(++g->stamp_epoch);
     std::vector<RoundBufs> rbs(L);
     // 1. local expansion + remote-update pack + round header (all stream-ordered)
@@ -1700,7 +1845,14 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
   return IRGL_OK;
 }
 
-static void partition_ranges(int64_t n, int P, int64_t* ps) { *ps = std::max<int64_t>((n + P - 1) / P, 1); }
+// Partition p owns [p * ps, (p + 1) * ps): ps = ceil(n / P) rounded up to a multiple of 32 when
+// P > 1, so the partitions' ranges never share a word of a vertex bitmap (the direction-optimising
+// BFS exchanges frontier bitmaps partition by partition).
+static void partition_ranges(int64_t n, int P, int64_t* ps) {
+  int64_t x = std::max<int64_t>((n + P - 1) / P, 1);
+  if (P > 1) x = (x + 31) & ~int64_t(31);
+  *ps = x;
+}
 
 }  // namespace irgl
 
@@ -2159,6 +2311,13 @@ irgl_status_t irgl_pipe_init_range(irgl_pipe* p, int64_t begin, int64_t end) {
   if (!p || begin < 0 || end < begin || end > 0xffffffffll) return IRGL_E_INVALID;
   irgl_ctx* ctx = p->ctx;
   const int L = (int)ctx->parts.size();
+  if (ctx->ptotal() > 1) {
+    p->init_items.clear();
+    p->init_range[0] = begin;
+    p->init_range[1] = end;
+    p->route_size = ctx->route_size;
+    p->pristine = true;
+  }
   for (int l = 0; l < L; ++l) {
     int64_t b = begin, e = end;
     if (ctx->ptotal() > 1 && ctx->route_size != INT64_MAX) {
@@ -2274,6 +2433,17 @@ static irgl_status_t check_call(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, i
 // A pipe initialised with caller ids meets a relabelled graph: map its items once (in, out and
 // retry; only `in` can be non-empty after an init).
 static irgl_status_t map_pipe(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g) {
+  if (pipe && g && ctx->ptotal() > 1 && pipe->pristine && pipe->route_size != g->part_size) {
+    // initialised for another graph's partition size: route the kept initialiser for this one
+    const int64_t keep = ctx->route_size;
+    ctx->route_size = g->part_size;
+    irgl_status_t s = pipe->init_range[0] >= 0
+                          ? irgl_pipe_init_range(pipe, pipe->init_range[0], pipe->init_range[1])
+                          : pipe_init_items(pipe, pipe->init_items.data(), (int64_t)pipe->init_items.size());
+    ctx->route_size = keep;
+    if (s != IRGL_OK) return s;
+  }
+  if (pipe) pipe->pristine = false;
   if (!pipe || !g || !g->relabeled || pipe->mapped_for == g) return IRGL_OK;
   if (pipe->mapped_for)
     return fail(ctx, IRGL_E_USAGE, "E_USAGE", "pipe items carry another relabelled graph's ids; re-initialise it");
@@ -2383,15 +2553,16 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
       }
     }
     const int dir_opt = args ? args->direction : 0;
-    if (dir_opt && !(outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30)))
+    const bool dist_capable = ctx->ptotal() > 1 && !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
+    if (dir_opt && !(outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30)) && !dist_capable)
       return fail(ctx, IRGL_E_UNSUPPORTED, "E_UNSUPPORTED",
-                  "direction-optimising BFS runs outlined on one partition");
+                  "direction-optimising BFS runs outlined on one partition or on a partitioned graph");
     // the outlined kernel's barrier word carries the out count in 30 bits
     const bool outlined = outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30);
     const bool dist_loop = !outlined && ctx->ptotal() > 1 && nf.delta <= 0 &&
                            !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
-    else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st);
+    else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st, dir_opt);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s == IRGL_OK && op == IRGL_OP_SSSP) s = range_verify(ctx, pipe, g);
     if (s != IRGL_OK) return s;

@@ -1349,6 +1349,72 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
   }
 }
 
+// ---- F1 on a vertex-partitioned graph: direction-optimising BFS rounds ---------------------------
+// The frontier's size and edge count per partition (Beamer's switch needs both, summed over the
+// partitions): out2 = {|in|, sum of the in-items' degrees}.
+__global__ void frontier_stats_kernel(const uint32_t* items, const uint32_t* cnt, const int64_t* rp,
+                                      int64_t lo, unsigned long long* out2) {
+  const uint32_t n = *(volatile const uint32_t*)cnt;
+  unsigned long long d = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)items[i] - lo;
+    d += (unsigned long long)(rp[v + 1] - rp[v]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(FULL, d, o);
+  if (lane_id() == 0 && d) atomicAdd(out2 + 1, d);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(out2, (unsigned long long)n);
+}
+
+// The global frontier as an n-bit bitmap: partition ranges are multiples of 32 vertices
+// (partition_ranges), so each partition fills its own words and the words are exchanged as they are.
+__global__ void frontier_bits_kernel(const uint32_t* items, const uint32_t* cnt, uint32_t* bits) {
+  const uint32_t n = *(volatile const uint32_t*)cnt;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = items[i];
+    atomicOr(bits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Bottom-up round of one partition: every owned unvisited vertex scans its (global-id) neighbours
+// for one in the level-(L-1) frontier (the blocked bitmap) and stops at the first; only the owner
+// writes its level, so no remote update is needed.  Finds are pushed (the next frontier).
+__global__ void __launch_bounds__(kBlock) bu_part_kernel(KParams p, RoundBufs rb, const uint32_t* fbits,
+                                                         unsigned long long* scanned) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  WarpQ q;
+  const int64_t n = p.g.hi - p.g.lo;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long sc = 0;
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); v0 < n; v0 += T) {
+    const int64_t lv = v0 + lane_id();
+    bool hit = false;
+    bool open = lv < n && ld_label(p.lab + p.g.lo + lv) == kInf;
+    if (open) {
+      const int64_t b = __ldg(p.g.row_ptr + lv), e = __ldg(p.g.row_ptr + lv + 1);
+      for (int64_t k = b; k < e && !hit; k += 4) {
+        int32_t u[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) u[j] = k + j < e ? ld_stream(p.g.col + k + j) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (u[j] >= 0) hit |= (ld_label(reinterpret_cast<const int32_t*>(fbits) + (u[j] >> 5)) >> (u[j] & 31)) & 1;
+        sc += (unsigned long long)(e - k < 4 ? e - k : 4);
+      }
+      if (hit) {
+        p.lab[p.g.lo + lv] = rb.level;
+        if (p.vis) atomicOr(p.vis + ((p.g.lo + lv) >> 5), 1u << ((p.g.lo + lv) & 31));
+      }
+    }
+    wpush<IRGL_OP_BFS, false>(sm, q, p, rb, hit ? 1 : 0, (uint32_t)(p.g.lo + lv));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(FULL, sc, o);
+  if (lane_id() == 0 && sc) atomicAdd(scanned, sc);
+  wflush_all<IRGL_OP_BFS>(sm, q, p, rb);
+}
+
 // ---- owner-side application of remote updates (E5 min-reduce) ---------------------------------
 // Owner-side apply of every peer's segment in one launch (ApplySegs): global index i belongs to
 // segment p with off[p] <= i < off[p+1].
@@ -1552,6 +1618,28 @@ __global__ void ctl_prepare_kernel(Ctl* c) {
 cudaError_t launch_range_check(const DevCSR& g, const int32_t* dist, uint32_t* bad, cudaStream_t st) {
   note_launch();
   range_check_kernel<<<148 * 8, 256, 0, st>>>(g, dist, bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frontier_stats(const uint32_t* items, const uint32_t* cnt, const int64_t* rp, int64_t lo,
+                                  unsigned long long* out2, cudaStream_t st) {
+  note_launch();
+  cudaMemsetAsync(out2, 0, 16, st);
+  frontier_stats_kernel<<<148 * 4, 256, 0, st>>>(items, cnt, rp, lo, out2);
+  return cudaGetLastError();
+}
+cudaError_t launch_frontier_bits(const uint32_t* items, const uint32_t* cnt, uint32_t* bits, cudaStream_t st) {
+  note_launch();
+  frontier_bits_kernel<<<148 * 4, 256, 0, st>>>(items, cnt, bits);
+  return cudaGetLastError();
+}
+cudaError_t launch_bu_part(const DevCSR& g, int32_t* lab, uint32_t* vis, Ctl* ctl, const RoundBufs& rb,
+                           const uint32_t* fbits, cudaStream_t st) {
+  KParams kp{g, lab, nullptr, vis, ctl, DistRoute{1, 0, 1, nullptr, nullptr}, ExpandCfg{128, 256, 512}};
+  const int64_t n = g.hi - g.lo;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 8));
+  note_launch();
+  bu_part_kernel<<<grid, kBlock, 0, st>>>(kp, rb, fbits, &ctl->edges);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,14 @@ cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* st
 // variant: 0 the operator's base kernel, 1 its direction-optimising (BFS) / near-far (SSSP)
 // kernel, -1 the minimum over both (a grid valid for either)
 int persistent_blocks_per_sm(int op, int variant = -1);
+// Direction-optimising BFS on a vertex-partitioned graph (host-orchestrated rounds): frontier
+// size / edge count of a partition's in-worklist, the partition-blocked frontier bitmap, and one
+// bottom-up round over the partition's own vertices.
+cudaError_t launch_frontier_stats(const uint32_t* items, const uint32_t* cnt, const int64_t* rp, int64_t lo,
+                                  unsigned long long* out2, cudaStream_t st);
+cudaError_t launch_frontier_bits(const uint32_t* items, const uint32_t* cnt, uint32_t* bits, cudaStream_t st);
+cudaError_t launch_bu_part(const DevCSR& g, int32_t* lab, uint32_t* vis, Ctl* ctl, const RoundBufs& rb,
+                           const uint32_t* fbits, cudaStream_t st);
 // *bad |= 1 if an edge leads from a reached to an unreached vertex (the IRGL_E_RANGE check)
 cudaError_t launch_range_check(const DevCSR& g, const int32_t* dist, uint32_t* bad, cudaStream_t st);
 // w8[k] = w[k] for k < m; *bad = 1 if some weight is outside [0, 255]

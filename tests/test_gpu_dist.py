@@ -46,6 +46,8 @@ def _rank_main(rank, world, port, spec, logical, q, relabel=False):
         for s in spec["sources"]:
             lv, st = irgl.bfs(ctx, g, s)
             res[("bfs", s)] = (lv, st.rounds, st.exchange_bytes)
+            lv, st = irgl.bfs(ctx, g, s, direction=1)  # direction-optimising (bitmap exchange)
+            res[("bfs-do", s)] = (lv, st.rounds, 0)
             for delta, defer in ((0, 0), (0, -1), (8, 0)):
                 d, st = irgl.sssp(ctx, g, s, delta=delta, defer=defer)
                 res[("sssp", s, delta, defer)] = (d, st.rounds, st.exchange_bytes)
@@ -100,6 +102,9 @@ def test_two_process_bfs_sssp_cc_rmat(oracle, world, logical):
         lv, rounds, xb = res[("bfs", s)]
         np.testing.assert_array_equal(lv, ref)
         assert set(rounds) == {ecc + 1} and xb > 0       # every rank ran ecc+1 rounds; data moved
+        lv, rounds, _ = res[("bfs-do", s)]
+        np.testing.assert_array_equal(lv, ref)
+        assert set(rounds) == {ecc + 1}
         dref = oracle.sssp(og, s)
         for delta, defer in ((0, 0), (0, -1), (8, 0)):
             d, _, xb = res[("sssp", s, delta, defer)]

@@ -572,11 +572,13 @@ def test_bfs_direction_optimising_parity(ctx, irgl, oracle):
 
 
 def test_bfs_direction_optimising_needs_outlined(irgl, oracle):
+    """One partition: direction-optimising BFS runs as the outlined kernel only (a host loop is
+    refused); partitioned graphs run it host-orchestrated (test_gpu_relabel.py)."""
     og = oracle.rmat(10)
-    with irgl.Context(logical_partitions=2) as c:
+    with irgl.Context() as c:
         g = c.graph_from_csr(og.row_ptr, og.col, og.weight)
         with pytest.raises(irgl.IrglError) as e:
-            irgl.bfs(c, g, 0, direction=1)
+            irgl.bfs(c, g, int(og.sources(1)[0]), direction=1, outline=0)
         assert e.value.status == 9
 
 

@@ -22,13 +22,13 @@ srcs = bench.pick_sources(g.n, lambda x: int(rp[x + 1] - rp[x]), count=4)
 if relabel:
     g.relabel()
 p = ctx.pipe(max(g.info.local_n, 1))
-for op, name in ((irgl.BFS, "bfs"), (irgl.SSSP, "sssp")):
+for op, name, kw2 in ((irgl.BFS, "bfs", {}), (irgl.BFS, "bfs-do", {"direction": 1}), (irgl.SSSP, "sssp", {})):
     for s in srcs[:1]:
-        p.init_scalars([s]); ctx.iterate(op, g, p)
+        p.init_scalars([s]); ctx.iterate(op, g, p, **kw2)
     t = []; r = []; e = []
     for s in srcs:
         p.init_scalars([s])
-        t0 = time.perf_counter(); st = ctx.iterate(op, g, p); t.append(time.perf_counter() - t0)
+        t0 = time.perf_counter(); st = ctx.iterate(op, g, p, **kw2); t.append(time.perf_counter() - t0)
         r.append(st.rounds); e.append(st.edges)
     print(f"RMAT-{scale} P={P} nccl={use_nccl} relabel={relabel} outline={outline} {name}: {1e3*np.mean(t):.2f} ms/traversal, rounds {np.mean(r):.1f}, "
           f"{1e6*np.mean(t)/np.mean(r):.0f} us/round, kernel {st.kernel_ms:.2f} ms", flush=True)
