@@ -314,7 +314,7 @@ typedef enum { IRGL_BLOCK_ELASTIC = 0, IRGL_BLOCK_SHRINKABLE = 1, IRGL_BLOCK_FIX
 typedef struct irgl_block_constraint { int32_t kind; int32_t value; } irgl_block_constraint;
 /* T_control = max(intersection of domains).  IRGL_E_OUTLINE_EMPTY if empty. */
 irgl_status_t irgl_t_control(const irgl_block_constraint* cs, int n, int32_t* out);
-/* The block constraint of this build's kernel for `op` (Fixed(256) for the nested-parallelism
+/* The block constraint of this build's kernel for `op` (Fixed(512) for the nested-parallelism
  * kernels) and the co-resident grid of its outlined variant. */
 irgl_status_t irgl_op_plan(irgl_ctx* ctx, irgl_op op, irgl_block_constraint* block,
                            int32_t* grid_outlined, int32_t* grid_fixed);

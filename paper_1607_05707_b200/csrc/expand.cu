@@ -39,12 +39,15 @@ namespace irgl {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int kWBuf = 256;  // per-warp push staging entries
+#ifndef IRGL_WBUF
+#define IRGL_WBUF 96  // a flush every >= 64 staged pushes; 256 cost L1 capacity (see kBlock)
+#endif
+constexpr int kWBuf = IRGL_WBUF;  // per-warp push staging entries
 #ifndef IRGL_MINB
-#define IRGL_MINB 6  // min co-resident CTAs per SM requested from ptxas: 40 registers, 48 warps/SM (tools/sweep.py)
+#define IRGL_MINB minb_for_threads(1536)  // 40 registers, 48 warps/SM (tools/sweep.py)
 #endif
 #ifndef IRGL_MINB_SSSP
-#define IRGL_MINB_SSSP 4  // SSSP (weights + batched relax): 64 registers, 32 warps/SM, no spills in the hot loop
+#define IRGL_MINB_SSSP minb_for_threads(1024)  // SSSP (weights + batched relax): 64 registers, 32 warps/SM
 #endif
 // Internal operator variants (template-level, so the common path carries no state of the others):
 // SSSP with near-far piles, and BFS accumulating the next frontier's degrees (direction-optimising).

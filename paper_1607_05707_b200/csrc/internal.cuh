@@ -13,7 +13,18 @@ namespace irgl {
 
 // Fixed(256): the nested-parallelism / cooperative-conversion kernels use shared memory sized by
 // the block, so their block constraint is Fixed.
-constexpr int kBlock = 256;
+// 512 threads: 2 (SSSP, 64 registers) or 3 (BFS / CC, 40 registers) CTAs per SM; against 256 it
+// halves the CTAs that arrive at every grid barrier and, with the smaller per-warp push staging
+// (expand.cu kWBuf), leaves more of the SM's 256 KB to L1 for the label gathers: SSSP RMAT-22
+// 1.227 -> 1.134 ms, RMAT-24 3.69 -> 3.64, BFS within 1% (profiles/r2_ab_blocks.txt).
+#ifndef IRGL_BLOCK
+#define IRGL_BLOCK 512
+#endif
+constexpr int kBlock = IRGL_BLOCK;  // threads per CTA of the hot kernels (tuning: IRGL_BLOCK)
+// minimum co-resident CTAs for __launch_bounds__, from a thread budget per SM
+constexpr int minb_for_threads(int threads_per_sm) {
+  return threads_per_sm / kBlock > 0 ? threads_per_sm / kBlock : 1;
+}
 constexpr int kWarps = kBlock / 32;
 constexpr int32_t kInf = 0x7fffffff;
 constexpr int kPushBuf = 2048;  // per-CTA shared-memory push staging (cooperative conversion)

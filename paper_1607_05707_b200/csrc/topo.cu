@@ -422,7 +422,7 @@ __device__ __forceinline__ bool pr_round(PrSmem& sm, cg::grid_group& grid, const
 // pointers stay kernel parameters (constant bank) instead of live registers: selecting them with
 // (r & 1) cost 40 B of spills at the 40-register budget and made the sweep 25% slower than the
 // host-loop kernel on RMAT-24.
-__global__ void __launch_bounds__(kBlock, 6) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
+__global__ void __launch_bounds__(kBlock, minb_for_threads(1536)) pr_persistent_kernel(DevCSR g, double* ra, double* rb,
                                                                double* ca, double* cb, double d,
                                                                double tol, double base, Ctl* ctl,
                                                                int64_t max_rounds, int cond_mode,
