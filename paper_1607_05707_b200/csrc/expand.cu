@@ -75,7 +75,6 @@ constexpr int minb_for(int op) { return is_sssp(op) ? IRGL_MINB_SSSP : IRGL_MINB
 
 struct Smem {
   uint32_t wbuf[kWarps][kWBuf];   // near pushes (E2)
-  uint32_t fbuf[kWarps][kWBuf];   // far pushes (SSSP near-far)
   uint32_t fl_cnt[2][kWarps];     // CTA flush: per-warp staged counts (near, far)
   uint32_t fl_off[2][kWarps];     // CTA flush: per-warp global offsets
   unsigned long long fl_edges[kWarps];
@@ -95,6 +94,10 @@ struct KParams {
 // Multi-partition kernels also stage remote pushes per warp: entries (owner << 28 | v), flushed
 // to the per-owner send buckets with one reservation per owner per flush (the owner counters are
 // a handful of addresses every warp of the grid would otherwise hit once per push).
+// Far-pile staging of the near-far SSSP kernels: only kernels instantiated for a near-far operator
+// reference it, so the others keep that shared memory for L1 (the label gathers' cache).
+__shared__ uint32_t s_fbuf[kWarps][kWBuf];
+
 struct SmemDist : Smem {
   uint32_t rbuf[kWarps][kWBuf];
 };
@@ -389,10 +392,12 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
     q.n += __popc(mn);
     if (q.n > kWBuf - 32) wflush(sm.wbuf[warp], q.n, rb.out, rb.out_cnt, rb.cap, &p.ctl->overflow);
   }
-  if (has_far(OP) && mf) {
-    if (kind == 2) sm.fbuf[warp][q.nf + __popc(mf & lt)] = v;
-    q.nf += __popc(mf);
-    if (q.nf > kWBuf - 32) wflush(sm.fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
+  if constexpr (has_far(OP)) {
+    if (mf) {
+      if (kind == 2) s_fbuf[warp][q.nf + __popc(mf & lt)] = v;
+      q.nf += __popc(mf);
+      if (q.nf > kWBuf - 32) wflush(s_fbuf[warp], q.nf, rb.far, rb.far_cnt, rb.far_cap, &p.ctl->overflow);
+    }
   }
 }
 
@@ -442,11 +447,12 @@ __device__ __forceinline__ void wflush_all(Smem& sm, WarpQ& q, const KParams& p,
     if (qq < rb.cap) rb.out[qq] = sm.wbuf[warp][i];
     else atomicOr(&p.ctl->overflow, 1u);
   }
-  if (has_far(OP))
-  for (uint32_t i = lane; i < q.nf; i += 32) {
-    const uint32_t qq = o1 + i;
-    if (qq < rb.far_cap) rb.far[qq] = sm.fbuf[warp][i];
-    else atomicOr(&p.ctl->overflow, 1u);
+  if constexpr (has_far(OP)) {
+    for (uint32_t i = lane; i < q.nf; i += 32) {
+      const uint32_t qq = o1 + i;
+      if (qq < rb.far_cap) rb.far[qq] = s_fbuf[warp][i];
+      else atomicOr(&p.ctl->overflow, 1u);
+    }
   }
   if (lane == 0) sm.fl_edges[warp] = 0;  // read by thread 0 before the second barrier
   __syncwarp();
