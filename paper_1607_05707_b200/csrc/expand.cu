@@ -128,6 +128,21 @@ __device__ __forceinline__ int32_t ld_stream_u8(const uint8_t* p) {
 }
 __device__ __forceinline__ int32_t w8_at(uint32_t x, int t) { return (int32_t)((x >> (8 * t)) & 255u); }
 
+// Row offsets of popped vertices: read-only, touched once per expansion, so kept out of L1
+// (IRGL_ROWPTR_NA=0: the cached __ldg path) — L1 is for the label gathers
+#ifndef IRGL_ROWPTR_NA
+#define IRGL_ROWPTR_NA 1
+#endif
+__device__ __forceinline__ int64_t ld_rowptr(const int64_t* p) {
+#if IRGL_ROWPTR_NA
+  int64_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(r) : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ uint32_t ld_item(const uint32_t* p) {
   uint32_t r;
   asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
@@ -536,8 +551,8 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   if (valid) {
     v = ld_item(rb.in + i);  // n = wl.pop(i)
     const int64_t lv = (int64_t)v - p.g.lo;
-    beg = __ldg(p.g.row_ptr + lv);
-    end = __ldg(p.g.row_ptr + lv + 1);
+    beg = ld_rowptr(p.g.row_ptr + lv);
+    end = ld_rowptr(p.g.row_ptr + lv + 1);
     if (!is_bfs(OP)) sv = ld_label_cg(p.lab + v);
   }
   int64_t deg = end - beg;
