@@ -2653,9 +2653,10 @@ static irgl_status_t relabel_partitioned(irgl_ctx* ctx, irgl_graph* g) {
     GraphPart& gp = g->parts[l];
     CK(cudaSetDevice(pr.dev));
     CK(cudaStreamSynchronize(pr.st));
+    CK(cudaMalloc(&gp.perm_g, std::max<int64_t>(g->n, 1) * 4));
+    if (gp.hi <= gp.lo) continue;  // an empty partition (ranges are multiples of 32 vertices)
     int32_t* perm_local = nullptr;
     CK(relabel_order(gp.hi - gp.lo, gp.lo, gp.maxdeg, gp.row_ptr, &perm_local, &gp.inv_l, pr.st));
-    CK(cudaMalloc(&gp.perm_g, std::max<int64_t>(g->n, 1) * 4));
     if (gp.hi > gp.lo)
       CK(cudaMemcpy(gp.perm_g + gp.lo, perm_local, (gp.hi - gp.lo) * 4, cudaMemcpyDeviceToDevice));
     cudaFree(perm_local);
@@ -2696,6 +2697,7 @@ static irgl_status_t relabel_partitioned(irgl_ctx* ctx, irgl_graph* g) {
     PartRT& pr = ctx->parts[l];
     GraphPart& gp = g->parts[l];
     CK(cudaSetDevice(pr.dev));
+    if (gp.hi <= gp.lo) continue;
     int64_t* rp_new = nullptr;
     CK(relabel_rewrite(gp.hi - gp.lo, gp.lo, g->n, gp.m, gp.row_ptr, gp.perm_g + gp.lo, gp.inv_l,
                        gp.perm_g, &gp.col, &gp.w, &rp_new, pr.st));

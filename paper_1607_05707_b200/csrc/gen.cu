@@ -304,9 +304,10 @@ cudaError_t max_degree(const int64_t* row_ptr, int64_t nrows, int64_t* out, cuda
   cudaError_t e = cudaMallocAsync(&d, 8, st);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(d, 0, 8, st);
-  if (nrows > 0)
+  if (nrows > 0) {  // an empty partition launches nothing (a zero grid is a launch error)
     note_launch();
     max_deg_kernel<<<(int)std::min<int64_t>((nrows + 255) / 256, 148 * 8), 256, 0, st>>>(row_ptr, nrows, d);
+  }
   unsigned long long h = 0;
   cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d, st);

@@ -136,3 +136,24 @@ def test_direction_optimising_bfs_partitioned(irgl, oracle, P, nccl, relabel):
                 lv, st = irgl.bfs(c, g, s, direction=1)
                 np.testing.assert_array_equal(lv, ref, err_msg=f"n={og.n} src={s}")
                 assert st.rounds == ecc + 1
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_tiny_partitioned_graphs_with_empty_partitions(irgl, oracle, P):
+    """Partition ranges are multiples of 32 vertices, so graphs below 32 (P - 1) vertices have
+    empty partitions: upload, relabelling, BFS and SSSP stay correct (an empty partition once
+    launched a zero-size grid whose sticky error surfaced in the next library call)."""
+    rng = np.random.default_rng(5)
+    with irgl.Context(logical_partitions=P) as c:
+        for n in list(range(2, 70, 3)) + [200]:
+            m = int(rng.integers(1, 4 * n))
+            og = oracle.from_edges(n, rng.integers(0, n, m).tolist(), rng.integers(0, n, m).tolist())
+            g = c.graph_from_csr(og.row_ptr, og.col, og.weight)
+            if n % 2:
+                g.relabel()
+            s = int(og.sources(1)[0]) if og.m else 0
+            lv, _ = irgl.bfs(c, g, s)
+            np.testing.assert_array_equal(lv, oracle.bfs(og, s)[0])
+            d, _ = irgl.sssp(c, g, s)
+            np.testing.assert_array_equal(d, oracle.sssp(og, s))
+            g.close()
