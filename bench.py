@@ -147,6 +147,14 @@ class Dist:
         self.world = 1 if single else int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = 0 if single else int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        # the rank's GPU: LOCAL_RANK, wrapped when ranks outnumber the box's GPUs (--transport gloo)
+        self.device = self.local_rank
+        if os.environ.get("IRGL_BENCH_WRAP_DEVICES") == "1":
+            try:
+                import torch
+                self.device = self.local_rank % max(torch.cuda.device_count(), 1)
+            except Exception:
+                pass
         self.pg = None
         if self.world > 1:
             import torch.distributed as dist
@@ -327,7 +335,9 @@ def workload_config(args, g, layout=None):
                                 "generator (Philox-scrambled) ids, 1D vertex partition"
                                 if args.gpus > 1 else "generator (Philox-scrambled) ids")}
     if args.gpus > 1:
-        cfg["partition"] = "1D vertex ranges of ceil(N/P), one per GPU, NCCL exchange per round"
+        cfg["partition"] = ("1D vertex ranges of ceil(N/P) (multiples of 32), one per GPU, exchange per "
+                            "round over " + ("NCCL" if getattr(args, "transport", "nccl") == "nccl" else
+                                             "the host transport plugin (gloo; ranks may share a GPU)"))
     if g is not None:
         cfg["n"] = int(g.n)
         cfg["m_directed"] = int(g.m)
@@ -483,10 +493,17 @@ def run_irgl(args, d):
             if args.relabel:
                 one_gpu["degree_ordered"] = one_gpu_reference_point(args, op_id, kw, relabel=True)
         d.barrier()
-        uid = d.bcast_bytes(irgl.nccl_unique_id() if d.rank == 0 else None)
-        ctx = irgl.Context(nccl=(d.local_rank, d.rank, d.world, uid), outline=args.outline)
+        if args.transport == "gloo":
+            # the rank transport over the bench's own gloo group (irgl_ctx_create_transport):
+            # the multi-process path on a box with fewer GPUs than ranks (ranks share devices;
+            # NCCL refuses two ranks on one device) — a plumbing check, not a scaling number
+            from paper_1607_05707_b200.dist import TorchTransport
+            ctx = irgl.Context(transport=TorchTransport(device=d.device), outline=args.outline)
+        else:
+            uid = d.bcast_bytes(irgl.nccl_unique_id() if d.rank == 0 else None)
+            ctx = irgl.Context(nccl=(d.device, d.rank, d.world, uid), outline=args.outline)
     else:
-        ctx = irgl.Context(devices=[d.local_rank], outline=args.outline)
+        ctx = irgl.Context(devices=[d.device], outline=args.outline)
     t0 = time.time()
     g = ctx.generate_rmat(args.scale)
     gen_s = time.time() - t0
@@ -503,7 +520,7 @@ def run_irgl(args, d):
     cand, er, vr = _sources_and_work(ctx, g, p, d, relabel_s is not None)
 
     # ---- device-timed region: inputs resident in HBM
-    sampler = ClockSampler(d.local_rank, start=False) if d.rank == 0 else None
+    sampler = ClockSampler(d.device, start=False) if d.rank == 0 else None
     r = _timed_traversals(args, d, ctx, g, p, op_id, cand, er, vr, kw, sampler)
     dev_ms, kms, tot_e, tot_b, stats = r["dev_ms"], r["kms"], r["tot_e"], r["tot_b"], r["stats"]
     step = r["step"]
@@ -644,6 +661,9 @@ def main():
     ap.add_argument("--scale", type=int, default=0)
     ap.add_argument("--outline", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 rank transport: NCCL (default) or the host plugin over gloo (ranks may "
+                         "share a GPU: a plumbing check on boxes with fewer GPUs than ranks)")
     ap.add_argument("--secondary", type=int, default=1,
                     help="N=1 default workload: also time BFS RMAT-22 and BFS / SSSP RMAT-24 "
                          "(detail.secondary, with parity)")
@@ -657,6 +677,8 @@ def main():
     ap.add_argument("--direction", type=int, default=0,
                     help="BFS: 1 = direction-optimising (SURVEY §8f F1), 0 = Listing-2 top-down")
     args = ap.parse_args()
+    if args.transport == "gloo":
+        os.environ["IRGL_BENCH_WRAP_DEVICES"] = "1"
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return self_launch(args.gpus)
     d = Dist()
