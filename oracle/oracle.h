@@ -163,6 +163,10 @@ int64_t orc_bfs_bsp_omp(const orc_graph* g, int64_t src, int32_t* level, int thr
 int64_t orc_sssp_bsp_omp(const orc_graph* g, int64_t src, int32_t* dist, int threads,
                          int64_t* edges_out);
 int orc_max_threads(void);
+/* Work-efficient variant of the OpenMP executor (the GPU's degree-scaled deferral, budget
+ * defer_k): the bench's cpu_baseline.work_efficient figure.  Same distances. */
+int64_t orc_sssp_defer_omp(const orc_graph* g, int64_t src, int32_t* dist, int threads,
+                           int64_t defer_k, int64_t* edges_out);
 void orc_set_threads(int t); /* omp_set_num_threads (torchrun exports OMP_NUM_THREADS=1) */
 
 /* Certificates over a borrowed CSR (symmetric graph, symmetric weights); 0 = holds, else a bit

@@ -110,6 +110,8 @@ def lib():
         L.orc_sssp_bsp_omp.restype = C.c_int64
         L.orc_sssp_bsp_omp.argtypes = [P, C.c_int64, i32p, C.c_int, i64p]
         L.orc_max_threads.restype = C.c_int
+        L.orc_sssp_defer_omp.restype = C.c_int64
+        L.orc_sssp_defer_omp.argtypes = [P, C.c_int64, i32p, C.c_int, C.c_int64, i64p]
         L.orc_pipe_run.restype = C.c_int
         L.orc_pipe_run.argtypes = [C.POINTER(PipeStage), C.c_int, C.c_int, C.c_int64, C.c_int64,
                                    i64p, C.c_int64, i32p, C.c_int, i32p, i32p, i32p,
@@ -295,6 +297,13 @@ def sssp_bsp_omp(g: Graph, src: int, threads=0):
     dist = np.empty(g.n, dtype=np.int32)
     e = C.c_int64(0)
     r = lib().orc_sssp_bsp_omp(g.handle, src, _p(dist, C.c_int32), threads, C.byref(e))
+    return dist, int(r), int(e.value)
+
+
+def sssp_defer_omp(g: Graph, src: int, threads=0, defer_k=1024):
+    dist = np.empty(g.n, dtype=np.int32)
+    e = C.c_int64(0)
+    r = lib().orc_sssp_defer_omp(g.handle, src, _p(dist, C.c_int32), threads, defer_k, C.byref(e))
     return dist, int(r), int(e.value)
 
 
