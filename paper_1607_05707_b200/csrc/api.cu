@@ -73,6 +73,7 @@ struct GraphPart {
   int32_t* perm_g = nullptr;
   int32_t* inv_l = nullptr;
   int32_t* res_part = nullptr;  // staging of this partition's results in the caller's ids
+  uint32_t* recv_cnt = nullptr;  // peer inbox exchange: updates received from each partition [P]
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
   int32_t* w = nullptr;
@@ -958,6 +959,40 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     CK(cudaMalloc(&ctx->hdr_all, (size_t)(L + P) * H * 4));
   }
   std::vector<uint32_t> hdr((size_t)P * H, 0);
+  // Peer inbox exchange (one process; every partition reachable by loads / stores from every
+  // other: the same device or peer access): the expansion stores remote updates straight into
+  // the owner's inbox segment, the owner's apply reads each update's value from the sender's
+  // label array — no pack launch, no copies.  Cross-stream events order the rounds: an owner's
+  // header / apply run after every sender's expansion, a sender's next expansion after every
+  // owner's apply (which consumed and cleared its inbox).  IRGL_PEER_INBOX=0 keeps the buckets.
+  bool peer = !multi_rank(ctx) && L > 1 && P <= kMaxParts;
+  {
+    const char* e = getenv("IRGL_PEER_INBOX");
+    if (e && atoi(e) == 0) peer = false;
+  }
+  for (int a = 0; peer && a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      const int da = ctx->parts[a].dev, db = ctx->parts[b].dev;
+      int can = 1;
+      if (da != db) cudaDeviceCanAccessPeer(&can, da, db);
+      if (!can) peer = false;
+    }
+  std::vector<cudaEvent_t> ev_exp(peer ? L : 0), ev_app(peer ? L : 0);
+  struct EvFree {
+    std::vector<cudaEvent_t>* a;
+    std::vector<cudaEvent_t>* b;
+    ~EvFree() {
+      for (auto* v : {a, b})
+        for (cudaEvent_t e : *v)
+          if (e) cudaEventDestroy(e);
+    }
+  } ev_free{&ev_exp, &ev_app};
+  for (int l = 0; peer && l < L; ++l) {
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    CK(cudaEventCreateWithFlags(&ev_exp[l], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_app[l], cudaEventDisableTiming));
+  }
+  bool applied_once = false;
   // IRGL_DIST_TRACE=1: host-side phase times per round (us) to stderr
   const char* dtr = getenv("IRGL_DIST_TRACE");
   const bool dtrace = dtr && *dtr == '1';
@@ -1110,14 +1145,39 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       rbs[l].nin_dev = &pp.ctl->cnt[pp.c_in];
       DistRoute dr{P, ctx->gpart(l), ps, gp.send, gp.send_cnt};
+      if (peer) {
+        for (int o = 0; o < L; ++o) {  // owner o's inbox segment for this partition, and counter
+          if (o == l) continue;
+          dr.inbox[o] = g->parts[o].recv + (int64_t)l * ps;
+          dr.inbox_cnt[o] = g->parts[o].recv_cnt + l;
+        }
+        if (applied_once)  // every owner has consumed the previous round's inbox
+          for (int o = 0; o < L; ++o)
+            if (o != l) CK(cudaStreamWaitEvent(pr.st, ev_app[o], 0));
+      }
       if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
       CK(launch_expand_round(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, rbs[l], dr, ec, grid_max(ctx, pr, op), pr.st));
       if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
       stt->launches += 2;
+      if (peer) {
+        CK(cudaEventRecord(ev_exp[l], pr.st));
+        continue;  // the header follows every sender's expansion (below)
+      }
       if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
       // the header launch also resets the counters this round used (chunk / tile) and its
       // deferral minimum, which accumulates the next round's (irgl_iterate reset both cells)
       CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow,
+                             pp.ctl->chunk_cnt, pp.ctl->tile_ctr,
+                             nf.defer_k > 0 ? &pp.ctl->dmin[nf.dsel] : nullptr, pr.st));
+    }
+    for (int l = 0; peer && l < L; ++l) {  // owner headers: the counts RECEIVED from each sender
+      PartRT& pr = ctx->parts[l];
+      GraphPart& gp = g->parts[l];
+      PipePart& pp = pipe->parts[l];
+      CK(cudaSetDevice(pr.dev));
+      for (int o = 0; o < L; ++o)
+        if (o != l) CK(cudaStreamWaitEvent(pr.st, ev_exp[o], 0));
+      CK(launch_round_header(pr.hdr, gp.recv_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow,
                              pp.ctl->chunk_cnt, pp.ctl->tile_ctr,
                              nf.defer_k > 0 ? &pp.ctl->dmin[nf.dsel] : nullptr, pr.st));
     }
@@ -1169,7 +1229,13 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     stt->popped += (int64_t)local_in;
     if (dtrace) t_c = now_us();
     // 3. payloads: grouped send/recv (NCCL) or peer copies (one process), then owner-side applies
-    auto count = [&](int p, int q) { return hdr[(size_t)p * H + q]; };
+    // count(p, q): updates partition p sent to q (peer inbox: q's header holds what it received)
+    auto count = [&](int p, int q) { return peer ? hdr[(size_t)q * H + p] : hdr[(size_t)p * H + q]; };
+    if (peer)  // an inbox segment holds part_size ids: more means dropped updates
+      for (int p = 0; p < P; ++p)
+        for (int q = 0; q < P; ++q)
+          if (p != q && count(p, q) > (uint64_t)ps)
+            return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the inbox segment");
     if (multi_rank(ctx)) {
       PartRT& pr = ctx->parts[0];
       CK(cudaSetDevice(pr.dev));
@@ -1200,7 +1266,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         if (xs != IRGL_OK) return xs;
       }
       if (L > 1) CK(cudaStreamSynchronize(pr.st));  // other local partitions apply on their streams
-    } else {
+    } else if (!peer) {
       for (int q = 0; q < L; ++q) {
         PartRT& dst = ctx->parts[q];
         CK(cudaSetDevice(dst.dev));
@@ -1230,13 +1296,22 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       for (int p = 0; p < P; ++p) sg.off[p + 1] = sg.off[p] + (p == q ? 0u : count(p, q));
       // 4. swap in/out: the launch also clears the send counts and the consumed in-count (the new
       // out counter) in stream order
-      sg.zero_send = gp.send_cnt;
+      sg.zero_send = peer ? gp.recv_cnt : gp.send_cnt;
       sg.zero_cnt = &pp.ctl->cnt[pp.c_in];
+      if (peer) {
+        for (int p = 0; p < L; ++p)
+          if (p != l) {
+            sg.peer_lab[p] = g->parts[p].lab;  // values: the senders' ghost labels
+            stt->exchange_bytes += (int64_t)count(p, q) * (vals ? 8 : 4);
+          }
+      }
       CK(launch_apply_remote_segs(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv,
                                   vals ? gp.recv_val : nullptr, sg, rbs[l], pr.st));
+      if (peer) CK(cudaEventRecord(ev_app[l], pr.st));
       std::swap(pp.b_in, pp.b_out);
       std::swap(pp.c_in, pp.c_out);
     }
+    applied_once = peer;
     if (dtrace) {
       t_d = now_us();
       static double t_prev = 0;
@@ -1838,6 +1913,8 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
       CK(cudaMalloc(&gp.recv, tot * 4));
       CK(cudaMalloc(&gp.recv_val, tot * 4));
       CK(cudaMalloc(&gp.send_cnt, P * 4));
+      CK(cudaMalloc(&gp.recv_cnt, P * 4));
+      CK(cudaMemset(gp.recv_cnt, 0, P * 4));
       CK(cudaMemset(gp.send_cnt, 0, P * 4));
     }
   }
@@ -2266,7 +2343,7 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
                   gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8, gp.perm_g, gp.inv_l,
-                  gp.res_part};
+                  gp.res_part, gp.recv_cnt};
     for (void* p : ps)
       if (p) cudaFree(p);
   }

@@ -345,10 +345,12 @@ __device__ __noinline__ void wflush_remote(SmemDist& sd, WarpQ& q, const KParams
     const uint32_t tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0) continue;
     uint32_t base = 0;
-    if (lane == 31) base = atomicAdd(p.dr.send_cnt + o, tot);
+    // peer inbox: reserve in the owner's counter and store into the owner's segment directly
+    uint32_t* const ocnt = p.dr.inbox[o] ? p.dr.inbox_cnt[o] : p.dr.send_cnt + o;
+    if (lane == 31) base = atomicAdd(ocnt, tot);
     base = __shfl_sync(FULL, base, 31);
     uint32_t pos = base + incl - c;
-    uint32_t* bucket = p.dr.send + (int64_t)o * p.dr.part_size;
+    uint32_t* bucket = p.dr.inbox[o] ? p.dr.inbox[o] : p.dr.send + (int64_t)o * p.dr.part_size;
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t e = sd.rbuf[warp][i];
       if ((e >> 28) == (uint32_t)o) {
@@ -1463,7 +1465,9 @@ __global__ void __launch_bounds__(kBlock) apply_segs_kernel(KParams p, RoundBufs
       const int64_t at = (int64_t)s * sg.stride + (i - sg.off[s]);
       v = items[at];
       const int32_t cur = gather_cur<OP>(p, v);
-      kind = relax_with<OP>(p, rb, q, cur, is_bfs(OP) ? 0 : values[at], 0, v);
+      int32_t val = 0;  // the sender's ghost label: packed, or read from the sender (peer inbox)
+      if (!is_bfs(OP)) val = sg.peer_lab[s] ? ld_label_cg(sg.peer_lab[s] + v) : values[at];
+      kind = relax_with<OP>(p, rb, q, cur, val, 0, v);
     }
     wpush<OP, false>(sm, q, p, rb, kind, v);
   }

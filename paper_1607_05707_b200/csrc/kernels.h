@@ -16,12 +16,19 @@ struct DevCSR {
 };
 
 // Routing of pushes whose destination is owned by another partition (1D vertex partition).
+constexpr int kMaxParts = 16;
 struct DistRoute {
   int nparts;          // 1 => no routing
   int me;
-  int64_t part_size;   // ceil(N / nparts); owner(v) = v / part_size
+  int64_t part_size;   // owner(v) = v / part_size
   uint32_t* send;      // [N]: bucket of peer q is send[q*part_size ...]
   uint32_t* send_cnt;  // [nparts]
+  // peer inbox exchange (one process, partitions on devices with peer access): remote updates are
+  // stored straight into owner o's inbox segment for this partition, inbox[o], reserving with
+  // atomics on inbox_cnt[o] (owner-side counters; P2P atomics when o is another device); null:
+  // the local buckets above, packed and moved after the expansion
+  uint32_t* inbox[kMaxParts] = {};
+  uint32_t* inbox_cnt[kMaxParts] = {};
 };
 
 struct ExpandCfg {
@@ -73,6 +80,9 @@ struct ApplySegs {
   // [P] and the consumed in-count — the next round's out counter after the swap
   uint32_t* zero_send = nullptr;
   uint32_t* zero_cnt = nullptr;
+  // peer inbox exchange: the value of an update from sender p is read from p's label array at
+  // apply time (the sender's ghost label is final once its expansion is done); null: values[]
+  const int32_t* peer_lab[kMaxParts] = {};
 };
 cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                      const uint32_t* items, const int32_t* values,
