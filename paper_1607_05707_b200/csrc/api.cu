@@ -74,6 +74,13 @@ struct GraphPart {
   int32_t* inv_l = nullptr;
   int32_t* res_part = nullptr;  // staging of this partition's results in the caller's ids
   uint32_t* recv_cnt = nullptr;  // peer inbox exchange: updates received from each partition [P]
+  // IPC pull exchange: second-parity buckets (a round writes parity r % 2 while owners may still
+  // be reading the other), and every partition's buckets mapped into this process [P][parity]
+  uint32_t* send_b = nullptr;
+  int32_t* send_val_b = nullptr;
+  std::vector<const uint32_t*> ipc_send[2];
+  std::vector<const int32_t*> ipc_val[2];
+  std::vector<void*> ipc_opened;  // handles this process opened (closed with the graph)
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
   int32_t* w = nullptr;
@@ -140,6 +147,7 @@ struct irgl_graph {
   // degree-ordered relabelling (irgl_graph_relabel; one partition): device perm[old] = new,
   // inv[new] = old, host inv for worklist reads, result staging (two buffers for async reads)
   bool relabeled = false;
+  int ipc_state = 0;  // IPC pull exchange: 0 undecided, 1 mapped, -1 not used
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   std::vector<int32_t> inv_host;
@@ -927,6 +935,114 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
   return IRGL_OK;
 }
 
+// IPC pull exchange (one process per GPU on one node): every rank maps every other rank's send
+// buckets (both parities) once per graph — the handles travel over the rank transport — and each
+// owner's apply kernel then reads its updates straight out of the senders' buckets over NVLink:
+// no send / recv.  The per-round header allgather is the barrier that makes a round's buckets
+// complete before they are read; buckets alternate by round parity, so a bucket is rewritten only
+// after every rank passed the next round's allgather, i.e. finished reading it.  IRGL_IPC=0 keeps
+// the NCCL / transport point-to-point exchange; so does any failure to map a peer's memory.
+static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
+  const char* e = getenv("IRGL_IPC");
+  if ((e && atoi(e) == 0) || !multi_rank(ctx)) return false;  // the same on every rank
+  const int L = (int)g->parts.size(), P = ctx->ptotal();
+  if (P > kMaxParts) return false;
+  if (g->ipc_state != 0) return g->ipc_state > 0;  // decided once per graph, collectively
+  g->ipc_state = -1;
+  const bool dbg = getenv("IRGL_IPC_DEBUG") != nullptr;
+  constexpr int kH = (int)sizeof(cudaIpcMemHandle_t);
+  PartRT& pr = ctx->parts[0];
+  cudaSetDevice(pr.dev);
+  // every rank contributes {ok flag, L partitions x {send, send_b, send_val, send_val_b} handles}
+  // to one allgather whatever happens locally, then a second one agrees on the mapping: a rank
+  // never leaves its peers alone in a collective
+  const size_t blk = 16 + (size_t)L * 4 * kH;
+  std::vector<char> mine(blk, 0);
+  int32_t ok1 = 1;
+  for (int l = 0; l < L && ok1; ++l) {
+    GraphPart& gp = g->parts[l];
+    void* bufs[4] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b};
+    for (int k = 0; k < 4 && ok1; ++k)
+      if (!bufs[k] || cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(&mine[16 + ((size_t)l * 4 + k) * kH]),
+                                          bufs[k]) != cudaSuccess) {
+        cudaGetLastError();
+        ok1 = 0;
+      }
+  }
+  std::memcpy(mine.data(), &ok1, 4);
+  auto gather = [&](const void* src, size_t bytes, std::vector<char>& out) {
+    char* d = nullptr;
+    if (cudaMalloc(&d, bytes * (1 + (size_t)ctx->nranks)) != cudaSuccess) return false;
+    // every copy on the partition stream (a legacy-stream copy is not ordered with it)
+    bool ok = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, pr.st) == cudaSuccess &&
+              cudaStreamSynchronize(pr.st) == cudaSuccess &&
+              x_allgather(ctx, pr, d, d + bytes, bytes) == IRGL_OK;
+    out.resize(bytes * ctx->nranks);
+    ok = ok && cudaMemcpyAsync(out.data(), d + bytes, out.size(), cudaMemcpyDeviceToHost, pr.st) == cudaSuccess &&
+         cudaStreamSynchronize(pr.st) == cudaSuccess;
+    cudaFree(d);
+    return ok;
+  };
+  std::vector<char> all;
+  if (!gather(mine.data(), blk, all)) return false;
+  for (int r = 0; r < ctx->nranks; ++r) {
+    int32_t f = 0;
+    std::memcpy(&f, &all[(size_t)r * blk], 4);
+    if (!f) return false;  // some rank cannot export: every rank decides the same
+  }
+  if (dbg) fprintf(stderr, "irgl-ipc rank %d: handles gathered\n", ctx->rank);
+  std::vector<void*> opened;
+  std::vector<void*> ptr((size_t)P * 4, nullptr);
+  int32_t ok2 = 1;
+  for (int p = 0; p < P && ok2; ++p) {
+    const int r = p / L;
+    for (int k = 0; k < 4 && ok2; ++k) {
+      if (r == ctx->rank) {  // this rank's own partitions: direct pointers
+        GraphPart& gp = g->parts[p % L];
+        void* bufs[4] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b};
+        ptr[(size_t)p * 4 + k] = bufs[k];
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, &all[(size_t)r * blk + 16 + ((size_t)(p % L) * 4 + k) * kH], kH);
+      void* q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok2 = 0;
+        break;
+      }
+      opened.push_back(q);
+      ptr[(size_t)p * 4 + k] = q;
+    }
+  }
+  if (dbg) fprintf(stderr, "irgl-ipc rank %d: opened %zu handles ok=%d\n", ctx->rank, opened.size(), ok2);
+  std::vector<char> oks;
+  bool agree = gather(&ok2, 4, oks);
+  for (int r = 0; agree && r < ctx->nranks; ++r) {
+    int32_t f = 0;
+    std::memcpy(&f, &oks[(size_t)r * 4], 4);
+    agree = f != 0;
+  }
+  if (!agree) {
+    for (void* q : opened) cudaIpcCloseMemHandle(q);
+    return false;
+  }
+  for (int l = 0; l < L; ++l) {  // the mapping (all partitions of this rank share one device)
+    GraphPart& gp = g->parts[l];
+    for (int par = 0; par < 2; ++par) {
+      gp.ipc_send[par].resize(P);
+      gp.ipc_val[par].resize(P);
+      for (int p = 0; p < P; ++p) {
+        gp.ipc_send[par][p] = static_cast<const uint32_t*>(ptr[(size_t)p * 4 + par]);
+        gp.ipc_val[par][p] = static_cast<const int32_t*>(ptr[(size_t)p * 4 + 2 + par]);
+      }
+    }
+  }
+  g->parts[0].ipc_opened = opened;
+  g->ipc_state = 1;
+  return true;
+}
+
 // ---- multi-partition rounds with one host synchronisation each -----------------------------------
 // Per round: expand every local partition (the in-count is read on the device), pack the remote
 // updates' ghost labels (counts read on the device), write a round header {send counts, in-count,
@@ -993,6 +1109,8 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
     CK(cudaEventCreateWithFlags(&ev_app[l], cudaEventDisableTiming));
   }
   bool applied_once = false;
+  const bool ipc = !peer && ipc_setup(ctx, g);
+  int64_t par_round = 0;  // IPC pull: bucket parity of the round
   // IRGL_DIST_TRACE=1: host-side phase times per round (us) to stderr
   const char* dtr = getenv("IRGL_DIST_TRACE");
   const bool dtrace = dtr && *dtr == '1';
@@ -1144,7 +1262,10 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       CK(cudaSetDevice(pr.dev));
       rbs[l] = round_bufs(pipe, gp, pp, (int32_t)level, stamp_id, nf);
       rbs[l].nin_dev = &pp.ctl->cnt[pp.c_in];
-      DistRoute dr{P, ctx->gpart(l), ps, gp.send, gp.send_cnt};
+      const bool odd = ipc && (par_round & 1);
+      uint32_t* sendb = odd ? gp.send_b : gp.send;  // this round's buckets (IPC pull: by parity)
+      int32_t* sendv = odd ? gp.send_val_b : gp.send_val;
+      DistRoute dr{P, ctx->gpart(l), ps, sendb, gp.send_cnt};
       if (peer) {
         for (int o = 0; o < L; ++o) {  // owner o's inbox segment for this partition, and counter
           if (o == l) continue;
@@ -1163,7 +1284,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         CK(cudaEventRecord(ev_exp[l], pr.st));
         continue;  // the header follows every sender's expansion (below)
       }
-      if (vals) CK(launch_pack_all(gp.lab, gp.send, gp.send_val, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
+      if (vals) CK(launch_pack_all(gp.lab, sendb, sendv, gp.send_cnt, P, ctx->gpart(l), ps, pr.st));
       // the header launch also resets the counters this round used (chunk / tile) and its
       // deferral minimum, which accumulates the next round's (irgl_iterate reset both cells)
       CK(launch_round_header(pr.hdr, gp.send_cnt, P, &pp.ctl->cnt[pp.c_in], &pp.ctl->overflow,
@@ -1236,7 +1357,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         for (int q = 0; q < P; ++q)
           if (p != q && count(p, q) > (uint64_t)ps)
             return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the inbox segment");
-    if (multi_rank(ctx)) {
+    if (multi_rank(ctx) && !ipc) {
       PartRT& pr = ctx->parts[0];
       CK(cudaSetDevice(pr.dev));
       for (int l = 1; l < L; ++l) CK(cudaStreamSynchronize(ctx->parts[l].st));  // packs done
@@ -1305,6 +1426,15 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
             stt->exchange_bytes += (int64_t)count(p, q) * (vals ? 8 : 4);
           }
       }
+      if (ipc) {
+        const int par = (int)(par_round & 1);
+        for (int p = 0; p < P; ++p)
+          if (p != q) {  // sender p's bucket for this owner, read in place
+            sg.seg_items[p] = gp.ipc_send[par][p] + (int64_t)q * ps;
+            if (vals) sg.seg_vals[p] = gp.ipc_val[par][p] + (int64_t)q * ps;
+            stt->exchange_bytes += (int64_t)count(p, q) * (vals ? 8 : 4);
+          }
+      }
       CK(launch_apply_remote_segs(op, gp.lab, gp.stamp, gp.vis_k(), pp.ctl, gp.recv,
                                   vals ? gp.recv_val : nullptr, sg, rbs[l], pr.st));
       if (peer) CK(cudaEventRecord(ev_app[l], pr.st));
@@ -1312,6 +1442,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       std::swap(pp.c_in, pp.c_out);
     }
     applied_once = peer;
+    ++par_round;
     if (dtrace) {
       t_d = now_us();
       static double t_prev = 0;
@@ -1915,6 +2046,10 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
       CK(cudaMalloc(&gp.send_cnt, P * 4));
       CK(cudaMalloc(&gp.recv_cnt, P * 4));
       CK(cudaMemset(gp.recv_cnt, 0, P * 4));
+      if (multi_rank(ctx)) {
+        CK(cudaMalloc(&gp.send_b, tot * 4));
+        CK(cudaMalloc(&gp.send_val_b, tot * 4));
+      }
       CK(cudaMemset(gp.send_cnt, 0, P * 4));
     }
   }
@@ -2343,9 +2478,10 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
                   gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8, gp.perm_g, gp.inv_l,
-                  gp.res_part, gp.recv_cnt};
+                  gp.res_part, gp.recv_cnt, gp.send_b, gp.send_val_b};
     for (void* p : ps)
       if (p) cudaFree(p);
+    for (void* p : gp.ipc_opened) cudaIpcCloseMemHandle(p);
   }
   if (g->relabeled) {
     cudaSetDevice(ctx->parts[0].dev);

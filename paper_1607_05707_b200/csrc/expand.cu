@@ -1463,10 +1463,14 @@ __global__ void __launch_bounds__(kBlock) apply_segs_kernel(KParams p, RoundBufs
       int s = 0;
       while (s + 1 < sg.P && sg.off[s + 1] <= i) ++s;
       const int64_t at = (int64_t)s * sg.stride + (i - sg.off[s]);
-      v = items[at];
+      const uint32_t k = i - sg.off[s];
+      // ids: received, or pulled from the sender's bucket (IPC pull) — an L2-coherent load either way
+      v = sg.seg_items[s] ? ld_item(sg.seg_items[s] + k) : items[at];
       const int32_t cur = gather_cur<OP>(p, v);
-      int32_t val = 0;  // the sender's ghost label: packed, or read from the sender (peer inbox)
-      if (!is_bfs(OP)) val = sg.peer_lab[s] ? ld_label_cg(sg.peer_lab[s] + v) : values[at];
+      int32_t val = 0;  // the sender's ghost label: packed, pulled, or read from the sender's labels
+      if (!is_bfs(OP))
+        val = sg.seg_vals[s] ? ld_label_cg(sg.seg_vals[s] + k)
+            : sg.peer_lab[s] ? ld_label_cg(sg.peer_lab[s] + v) : values[at];
       kind = relax_with<OP>(p, rb, q, cur, val, 0, v);
     }
     wpush<OP, false>(sm, q, p, rb, kind, v);

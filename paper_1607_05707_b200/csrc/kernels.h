@@ -83,6 +83,10 @@ struct ApplySegs {
   // peer inbox exchange: the value of an update from sender p is read from p's label array at
   // apply time (the sender's ghost label is final once its expansion is done); null: values[]
   const int32_t* peer_lab[kMaxParts] = {};
+  // IPC pull exchange (one process per GPU, same node): segment p is read from sender p's own
+  // bucket for this owner (ids / values), mapped into this process; null: items / values
+  const uint32_t* seg_items[kMaxParts] = {};
+  const int32_t* seg_vals[kMaxParts] = {};
 };
 cudaError_t launch_apply_remote_segs(int op, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                      const uint32_t* items, const int32_t* values,
