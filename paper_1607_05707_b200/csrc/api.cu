@@ -81,6 +81,11 @@ struct GraphPart {
   std::vector<const uint32_t*> ipc_send[2];
   std::vector<const int32_t*> ipc_val[2];
   std::vector<void*> ipc_opened;  // handles this process opened (closed with the graph)
+  // partitioned DO-BFS scratch, kept across Iterates: the n-bit frontier bitmap [P * words per
+  // partition]; on partition 0 also the frontier stats and the rank transport's bitmap staging
+  uint32_t* do_bits = nullptr;
+  unsigned long long* do_stats = nullptr;
+  uint32_t* do_all = nullptr;
   int64_t* row_ptr = nullptr;
   int32_t* col = nullptr;
   int32_t* w = nullptr;
@@ -148,6 +153,7 @@ struct irgl_graph {
   // inv[new] = old, host inv for worklist reads, result staging (two buffers for async reads)
   bool relabeled = false;
   int ipc_state = 0;  // IPC pull exchange: 0 undecided, 1 mapped, -1 not used
+  irgl::XRendezvous* xr = nullptr;  // distributed persistent kernel's rendezvous (partition 0's device)
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   std::vector<int32_t> inv_host;
@@ -1129,27 +1135,34 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
   uint64_t explored = 0;
   unsigned long long* fstats = nullptr;  // [L * 2] local stats, then [nranks * L * 2] gathered
   std::vector<uint32_t*> fbits(L, nullptr);
-  struct DoFree {
-    std::vector<uint32_t*>* b;
-    unsigned long long** f;
-    irgl_ctx* c;
-    ~DoFree() {
-      for (size_t l = 0; l < b->size(); ++l)
-        if ((*b)[l]) { cudaSetDevice(c->parts[l].dev); cudaFree((*b)[l]); }
-      if (*f) { cudaSetDevice(c->parts[0].dev); cudaFree(*f); }
-    }
-  } do_free{&fbits, &fstats, ctx};
+  uint32_t* xbits = nullptr;  // multi-rank: [L * wpp] this rank's blocks, then every rank's
   if (do_bfs) {
-    CK(cudaSetDevice(ctx->parts[0].dev));
-    CK(cudaMalloc(&fstats, (size_t)2 * L * (1 + ctx->nranks) * 8));
     for (int l = 0; l < L; ++l) {
+      GraphPart& gp = g->parts[l];
       CK(cudaSetDevice(ctx->parts[l].dev));
-      CK(cudaMalloc(&fbits[l], (size_t)P * wpp * 4));
+      if (!gp.do_bits) CK(cudaMalloc(&gp.do_bits, (size_t)P * wpp * 4));
+      if (l > 0 && !gp.do_stats) CK(cudaMalloc(&gp.do_stats, 16));  // a partition's own stats slot
+      fbits[l] = gp.do_bits;
     }
+    GraphPart& g0 = g->parts[0];
+    CK(cudaSetDevice(ctx->parts[0].dev));
+    if (!g0.do_stats) CK(cudaMalloc(&g0.do_stats, (size_t)2 * L * (1 + ctx->nranks) * 8));
+    if (multi_rank(ctx) && !g0.do_all) CK(cudaMalloc(&g0.do_all, (size_t)L * wpp * 4 * (1 + ctx->nranks)));
+    fstats = g0.do_stats;
+    xbits = g0.do_all;
   }
+  double t_m = dtrace ? now_us() : 0;
+  auto mark = [&](const char* what) {  // IRGL_DIST_TRACE: host time of the DO-BFS phases
+    if (!dtrace) return;
+    const double t = now_us();
+    fprintf(stderr, "irgl-dist   %s %.1f us\n", what, t - t_m);
+    t_m = t;
+  };
+  mark("entry");
   for (;;) {
     if (o.max_rounds > 0 && stt->rounds >= o.max_rounds) break;  // ExtraCond (Or)
     if (do_bfs) {
+      mark("round start");
       // frontier size / edges of every partition's in-worklist
       std::vector<unsigned long long> fs((size_t)2 * P, 0);
       for (int l = 0; l < L; ++l) {
@@ -1159,16 +1172,15 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         CK(cudaSetDevice(pr.dev));
         unsigned long long* dst = fstats + 2 * l;
         if (pr.dev != ctx->parts[0].dev) {  // stats of a partition on another device: own slot
-          unsigned long long* tmp = nullptr;
-          CK(cudaMalloc(&tmp, 16));
-          CK(launch_frontier_stats(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], gp.row_ptr, gp.lo, tmp, pr.st));
-          CK(cudaMemcpyAsync(&fs[2 * ctx->gpart(l)], tmp, 16, cudaMemcpyDeviceToHost, pr.st));
-          CK(cudaStreamSynchronize(pr.st));
-          cudaFree(tmp);
+          CK(launch_frontier_stats(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], gp.row_ptr, gp.lo, gp.do_stats, pr.st));
+          CK(cudaMemcpyAsync(&fs[2 * ctx->gpart(l)], gp.do_stats, 16, cudaMemcpyDeviceToHost, pr.st));
           continue;
         }
         CK(launch_frontier_stats(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], gp.row_ptr, gp.lo, dst, pr.st));
-        CK(cudaStreamSynchronize(pr.st));
+      }
+      for (int l = 0; l < L; ++l) {  // every partition's stats launched: one wait each
+        CK(cudaSetDevice(ctx->parts[l].dev));
+        CK(cudaStreamSynchronize(ctx->parts[l].st));
       }
       {
         PartRT& pr = ctx->parts[0];
@@ -1189,6 +1201,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
         fn += fs[2 * p];
         fm += fs[2 * p + 1];
       }
+      mark("frontier stats");
       if (fn == 0) break;  // every in worklist is empty: the Iterate ends
       constexpr double kAlpha = 14.0, kBeta = 24.0;
       const double mu = (double)g->m - (double)explored;
@@ -1196,29 +1209,38 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
       else if (bottom_up && (double)fn < (double)g->n / kBeta) bottom_up = false;
       explored += fm;
       if (bottom_up) {
+        // peer-reachable partitions share partition 0's bitmap: each fills its own block, every
+        // bottom-up launch waits for all blocks (events) and reads the shared words in place
+        uint32_t* shared = peer ? fbits[0] : nullptr;
         for (int l = 0; l < L; ++l) {  // this partition's block of the frontier bitmap
           PartRT& pr = ctx->parts[l];
           PipePart& pp = pipe->parts[l];
           CK(cudaSetDevice(pr.dev));
-          CK(cudaMemsetAsync(fbits[l], 0, (size_t)P * wpp * 4, pr.st));
-          CK(launch_frontier_bits(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], fbits[l], pr.st));
-          CK(cudaStreamSynchronize(pr.st));
+          uint32_t* bits = shared ? shared : fbits[l];
+          CK(cudaMemsetAsync(bits + (size_t)ctx->gpart(l) * wpp, 0, wpp * 4, pr.st));
+          CK(launch_frontier_bits(pp.buf[pp.b_in], &pp.ctl->cnt[pp.c_in], bits, pr.st));
+          if (shared) CK(cudaEventRecord(ev_exp[l], pr.st));
+          else CK(cudaStreamSynchronize(pr.st));
         }
-        if (multi_rank(ctx)) {  // the rank's L blocks are contiguous: one allgather of L * wpp words
+        if (shared) {
+          for (int l = 0; l < L; ++l) {
+            CK(cudaSetDevice(ctx->parts[l].dev));
+            for (int k = 0; k < L; ++k)
+              if (k != l) CK(cudaStreamWaitEvent(ctx->parts[l].st, ev_exp[k], 0));
+          }
+        } else if (multi_rank(ctx)) {  // the rank's L blocks are contiguous: one allgather of L * wpp words
           PartRT& pr = ctx->parts[0];
           CK(cudaSetDevice(pr.dev));
-          uint32_t* all = nullptr;
+          uint32_t* all = xbits;
           const size_t blk = (size_t)L * wpp;
-          CK(cudaMalloc(&all, blk * 4 * (1 + (size_t)ctx->nranks)));
           for (int l = 0; l < L; ++l)
             CK(cudaMemcpyAsync(all + (size_t)l * wpp, fbits[l] + (size_t)ctx->gpart(l) * wpp, wpp * 4,
                                cudaMemcpyDeviceToDevice, pr.st));
           irgl_status_t xs = x_allgather(ctx, pr, all, all + blk, blk * 4);
-          if (xs != IRGL_OK) { cudaFree(all); return xs; }
+          if (xs != IRGL_OK) return xs;
           for (int l = 0; l < L; ++l)
             CK(cudaMemcpyAsync(fbits[l], all + blk, (size_t)P * wpp * 4, cudaMemcpyDeviceToDevice, pr.st));
           CK(cudaStreamSynchronize(pr.st));
-          cudaFree(all);
         } else {
           for (int l = 0; l < L; ++l)
             for (int k = 0; k < L; ++k)
@@ -1226,6 +1248,7 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
                 CK(cudaMemcpyPeer(fbits[l] + (size_t)ctx->gpart(k) * wpp, ctx->parts[l].dev,
                                   fbits[k] + (size_t)ctx->gpart(k) * wpp, ctx->parts[k].dev, wpp * 4));
         }
+        mark("bitmap exchange");
         uint64_t local_in = 0;
         for (int l = 0; l < L; ++l) local_in += fs[2 * ctx->gpart(l)];
         for (int l = 0; l < L; ++l) {  // bottom-up over each partition's own vertices
@@ -1234,17 +1257,15 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
           PipePart& pp = pipe->parts[l];
           CK(cudaSetDevice(pr.dev));
           RoundBufs rb = round_bufs(pipe, gp, pp, (int32_t)level, (int32_t)(++g->stamp_epoch), nf);
-          CK(launch_bu_part(gp.csr(), gp.lab, gp.vis_k(), pp.ctl, rb, fbits[l], pr.st));
+          CK(launch_bu_part(gp.csr(), gp.lab, gp.vis_k(), pp.ctl, rb, shared ? shared : fbits[l], pr.st));
           // in <- the finds; the consumed in-count becomes the (empty) out counter
           CK(cudaMemsetAsync(&pp.ctl->cnt[pp.c_in], 0, 4, pr.st));
           std::swap(pp.b_in, pp.b_out);
           std::swap(pp.c_in, pp.c_out);
           stt->launches += 1;
         }
-        for (int l = 0; l < L; ++l) {
-          CK(cudaSetDevice(ctx->parts[l].dev));
-          CK(cudaStreamSynchronize(ctx->parts[l].st));
-        }
+        // (the next round's frontier stats wait for these launches on every stream)
+        mark("bottom-up kernels");
         if (stt->rounds > 0) stt->pushes += (int64_t)local_in;
         stt->popped += (int64_t)local_in;
         stt->rounds++;
@@ -1472,9 +1493,9 @@ static irgl_status_t wl_graph_rounds_dist(irgl_ctx* ctx, irgl_pipe* pipe, irgl_g
 // the pipelined batch of irgl_traverse_batch).
 static void fill_persist_args(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op, int64_t level0,
                               const irgl_iterate_opts& o, const NearFar& nf, int dir_opt,
-                              int64_t rounds_done, PersistArgs* pa) {
-  GraphPart& gp = g->parts[0];
-  PipePart& pp = pipe->parts[0];
+                              int64_t rounds_done, PersistArgs* pa, int l = 0) {
+  GraphPart& gp = g->parts[l];
+  PipePart& pp = pipe->parts[l];
   pa->buf_a = pp.buf[pp.b_in];
   pa->buf_b = pp.buf[pp.b_out];
   pa->slot[0] = pp.c_in;
@@ -1691,6 +1712,193 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   stt->launches += 1;
   stt->popped += (int64_t)h.popped;
   stt->pushes += (int64_t)h.pushes;
+  stt->outlined = 1;
+  return IRGL_OK;
+}
+
+// ---- E3 across partitions (one process): wl_graph_dist_outlined -------------------------------------
+// The Iterate of a partitioned graph as one cooperative persistent kernel per partition
+// (dist_persistent_kernel, expand.cu), the partitions meeting at a device-side rendezvous twice a
+// round instead of at a host synchronisation: remote updates go straight into the owners' inboxes
+// (the peer inbox layout of wl_graph_rounds_dist), owners read the values from the senders' labels.
+// Partitions sharing a device split its co-resident CTAs, so every partition's grid is resident
+// at once (a rendezvous never waits on a kernel that cannot start; a bounded wait reports
+// IRGL_E_OCCUPANCY if one ever does).  Requires every partition reachable from every other (one
+// device or peer access); direction-optimising BFS and near-far SSSP keep the host rounds.
+static bool dist_outlined_ok(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op, const NearFar& nf,
+                             int dir_opt) {
+  const int L = (int)ctx->parts.size();
+  if (multi_rank(ctx) || L < 2 || L > kMaxParts || (int)g->parts.size() != L) return false;
+  if (dir_opt || nf.delta > 0 || pipe->cap >= (1ll << 30)) return false;
+  if (op != IRGL_OP_BFS && op != IRGL_OP_SSSP && op != IRGL_OP_CC_LP) return false;
+  const char* e = getenv("IRGL_DIST_OUTLINE");
+  if (e && atoi(e) == 0) return false;
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      const int da = ctx->parts[a].dev, db = ctx->parts[b].dev;
+      int can = 1;
+      if (da != db) cudaDeviceCanAccessPeer(&can, da, db);
+      if (!can) return false;
+    }
+  return dist_persistent_blocks_per_sm(op) > 0;
+}
+
+static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
+                                            int64_t level0, const irgl_iterate_opts& o, const NearFar& nf,
+                                            irgl_iter_stats* stt) {
+  const int L = (int)ctx->parts.size();
+  const int64_t ps = g->part_size;
+  uint64_t nin = 0;
+  for (int l = 0; l < L; ++l) nin += pipe->parts[l].n_in;
+  if (nin == 0) return IRGL_OK;
+  if (o.max_rounds > 0 && o.max_rounds <= stt->rounds) return IRGL_OK;
+  if (op == IRGL_OP_SSSP)
+    for (int l = 0; l < L; ++l) {
+      irgl_status_t ws = ensure_w8(ctx, g, l);
+      if (ws != IRGL_OK) return ws;
+    }
+  const int bps = dist_persistent_blocks_per_sm(op);
+  const char* dtr = getenv("IRGL_DIST_TRACE");
+  const bool dtrace = dtr && *dtr == '1';
+  PartRT& pr0 = ctx->parts[0];
+  CK(cudaSetDevice(pr0.dev));
+  if (!g->xr) CK(cudaMalloc(&g->xr, sizeof(XRendezvous)));
+  CK(cudaMemsetAsync(g->xr, 0, sizeof(XRendezvous), pr0.st));
+  cudaEvent_t ready = nullptr;
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t e;
+    ~EvGuard() { if (e) cudaEventDestroy(e); }
+  } ev_guard{ready};
+  CK(cudaEventRecord(ready, pr0.st));
+  const ExpandCfg ec = expand_cfg(ctx);
+  std::vector<int> grids(L);
+  for (int l = 0; l < L; ++l) {  // partitions sharing a device split its resident CTAs
+    int share = 0;
+    for (int k = 0; k < L; ++k) share += ctx->parts[k].dev == ctx->parts[l].dev;
+    grids[l] = bps * ctx->parts[l].sms / share;
+    if (grids[l] < 1)
+      return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "too many partitions share a device for co-resident kernels");
+  }
+  // every partition's launch state first, then the launches back to back
+  std::vector<DistPersistArgs> das(L);
+  std::vector<DistRoute> drs(L);
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    GraphPart& gp = g->parts[l];
+    PipePart& pp = pipe->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    DistPersistArgs& da = das[l];
+    fill_persist_args(ctx, pipe, g, op, level0, o, nf, 0, stt->rounds, &da.pa, l);
+    da.pa.dense_min = 0;
+    da.pa.trace = nullptr;
+    da.pa.trace_cap = 0;
+    if (dtrace) {  // per-round phase timestamps (expand.cu, dist_persistent_kernel)
+      da.pa.trace_cap = 1024;
+      CK(cudaMalloc(&da.pa.trace, 4 * 1024 * 8 + 8));
+      CK(cudaMemsetAsync(da.pa.trace, 0, 4 * 1024 * 8 + 8, pr.st));
+    }
+    da.pa.stamp_base = nullptr;
+    da.xr = g->xr;
+    da.nparts = L;
+    da.recv = gp.recv;
+    da.recv_cnt = gp.recv_cnt;
+    for (int k = 0; k < L; ++k) da.peer_lab[k] = g->parts[k].lab;
+    da.spin_ns = 5000000000ull;  // 5 s: far beyond any round; only a non-resident peer waits this long
+    DistRoute dr{L, ctx->gpart(l), ps, gp.send, gp.send_cnt};
+    for (int k = 0; k < L; ++k)
+      if (k != l) {
+        dr.inbox[k] = g->parts[k].recv + (int64_t)l * ps;
+        dr.inbox_cnt[k] = g->parts[k].recv_cnt + l;
+      }
+    drs[l] = dr;
+    CK(cudaMemsetAsync(gp.recv_cnt, 0, (size_t)L * 4, pr.st));
+    CK(launch_ctl_prepare(pp.ctl, pr.st));
+    if (l != 0) CK(cudaStreamWaitEvent(pr.st, ready, 0));
+  }
+  // the inbox counters are zeroed on their own streams: every launch waits for all of them
+  std::vector<cudaEvent_t> zev(L, nullptr);
+  struct EvVec {
+    std::vector<cudaEvent_t>* v;
+    ~EvVec() { for (cudaEvent_t e : *v) if (e) cudaEventDestroy(e); }
+  } zguard{&zev};
+  for (int l = 0; l < L; ++l) {
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    CK(cudaEventCreateWithFlags(&zev[l], cudaEventDisableTiming));
+    CK(cudaEventRecord(zev[l], ctx->parts[l].st));
+  }
+  for (int l = 0; l < L; ++l) {
+    PartRT& pr = ctx->parts[l];
+    GraphPart& gp = g->parts[l];
+    PipePart& pp = pipe->parts[l];
+    CK(cudaSetDevice(pr.dev));
+    for (int k = 0; k < L; ++k)
+      if (k != l) CK(cudaStreamWaitEvent(pr.st, zev[k], 0));
+    if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
+    CK(launch_dist_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, drs[l], das[l], ec, grids[l], pr.st));
+    if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
+    CK(cudaMemcpyAsync(pr.h_ctl, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
+  }
+  XRendezvous hx{};
+  for (int l = 0; l < L; ++l) {
+    CK(cudaSetDevice(ctx->parts[l].dev));
+    CK(cudaStreamSynchronize(ctx->parts[l].st));
+  }
+  CK(cudaSetDevice(pr0.dev));
+  CK(cudaMemcpy(&hx, g->xr, sizeof(hx), cudaMemcpyDeviceToHost));
+  {
+    float kms = 0.f;
+    CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
+    stt->kernel_ms += kms;
+  }
+  const Ctl& h0 = *pr0.h_ctl;
+  g->stamp_epoch += h0.stamp_used;
+  if (hx.abort)
+    return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY",
+                "partition kernels were not co-resident (rendezvous wait bound reached)");
+  uint32_t flags = 0;
+  for (int l = 0; l < L; ++l) flags |= hx.flags[l] | (ctx->parts[l].h_ctl->overflow & 3u);
+  if (flags & 4u) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the inbox segment");
+  if (flags & 3u)
+    return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
+                flags & 2 ? "edge-chunk descriptors beyond capacity" : "push beyond worklist capacity");
+  const int64_t K = (int64_t)h0.rounds;
+  for (int l = 0; l < L; ++l) {
+    const Ctl& h = *ctx->parts[l].h_ctl;
+    if ((int64_t)h.rounds != K)
+      return fail(ctx, IRGL_E_CUDA, "E_CUDA", "partitions left the distributed loop at different rounds");
+    PipePart& pp = pipe->parts[l];
+    const int slots[3] = {pp.c_in, pp.c_out, pp.c_spare};
+    if (K & 1) std::swap(pp.b_in, pp.b_out);
+    pp.c_in = slots[K % 3];
+    pp.c_out = slots[(K + 1) % 3];
+    pp.c_spare = slots[(K + 2) % 3];
+    pp.n_in = h.cnt[pp.c_in];
+    stt->edges += (int64_t)h.edges;
+    stt->remote_updates += (int64_t)h.remote;
+    stt->popped += (int64_t)h.popped;
+    stt->pushes += (int64_t)h.pushes;
+    stt->exchange_bytes += (int64_t)h.remote * (op == IRGL_OP_BFS ? 4 : 8);
+    if (dtrace) {
+      fprintf(stderr, "irgl-dist-outlined part=%d grid=%d rounds=%lld edges=%llu remote=%llu popped=%llu pushes=%llu\n", l,
+              grids[l], (long long)K, h.edges, h.remote, h.popped, h.pushes);
+      std::vector<unsigned long long> t(4 * 1024);
+      CK(cudaSetDevice(ctx->parts[l].dev));
+      CK(cudaMemcpy(t.data(), das[l].pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+      cudaFree(das[l].pa.trace);
+      for (int64_t r = 0; r < std::min<int64_t>(K, 1024); ++r) {
+        const unsigned long long* q = &t[4 * r];
+        const unsigned long long prev = r ? t[4 * (r - 1) + 3] : q[0];
+        // expand: since the previous round's end; wait: until every inbox is complete; apply;
+        // publish: the round-end rendezvous
+        fprintf(stderr, "irgl-dist-outlined part=%d round=%lld expand=%.1f wait=%.1f apply=%.1f publish=%.1f us\n", l,
+                (long long)r, (q[0] - prev) * 1e-3, (q[1] - q[0]) * 1e-3, q[2] ? (q[2] - q[1]) * 1e-3 : -1.0,
+                q[3] ? (q[3] - q[2]) * 1e-3 : -1.0);
+      }
+    }
+  }
+  stt->rounds += K;
+  stt->launches += L;
   stt->outlined = 1;
   return IRGL_OK;
 }
@@ -2478,10 +2686,14 @@ irgl_status_t irgl_graph_destroy(irgl_graph* g) {
                   gp.pr_clen, gp.pr_partial, gp.chunks, gp.ctl, gp.send, gp.send_cnt, gp.send_val, gp.recv,
                   gp.recv_val, gp.far[0], gp.far[1], gp.mst[0], gp.mst[1], gp.mst[2], gp.mst[3],
                   gp.mst[4], gp.mst[5], gp.mst_wl[0], gp.mst_wl[1], gp.w8, gp.perm_g, gp.inv_l,
-                  gp.res_part, gp.recv_cnt, gp.send_b, gp.send_val_b};
+                  gp.res_part, gp.recv_cnt, gp.send_b, gp.send_val_b, gp.do_bits, gp.do_stats, gp.do_all};
     for (void* p : ps)
       if (p) cudaFree(p);
     for (void* p : gp.ipc_opened) cudaIpcCloseMemHandle(p);
+  }
+  if (g->xr) {
+    cudaSetDevice(ctx->parts[0].dev);
+    cudaFree(g->xr);
   }
   if (g->relabeled) {
     cudaSetDevice(ctx->parts[0].dev);
@@ -2774,13 +2986,15 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     const bool outlined = outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30);
     const bool dist_loop = !outlined && ctx->ptotal() > 1 && nf.delta <= 0 &&
                            !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
+    const bool dist_outlined = dist_loop && outline && dist_outlined_ok(ctx, pipe, g, op, nf, dir_opt);
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
+    else if (dist_outlined) s = wl_graph_dist_outlined(ctx, pipe, g, op, level, o, nf, &st);
     else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st, dir_opt);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s == IRGL_OK && op == IRGL_OP_SSSP) s = range_verify(ctx, pipe, g);
     if (s != IRGL_OK) return s;
     // edges scanned / remote updates (the outlined path read them with its control block)
-    s = pipe_counters(ctx, pipe, outlined ? nullptr : &st);
+    s = pipe_counters(ctx, pipe, outlined || dist_outlined ? nullptr : &st);
     if (s != IRGL_OK) return s;
   } else if (op == IRGL_OP_PR && outline && ctx->ptotal() == 1 &&
              (o.cond_mode != IRGL_COND_NONE || o.max_rounds > 0)) {

@@ -378,13 +378,17 @@ __device__ __forceinline__ void wpush(Smem& sm, WarpQ& q, const KParams& p, cons
   if (m == 0) return;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   if (DIST) {
-    const int owner = kind ? (int)((int64_t)v / p.dr.part_size) : -1;
-    const bool remote = kind && owner != p.dr.me;
+    // local = inside this partition's id range (no division on the common path); the owner of
+    // a remote id is computed by the remote lanes only (ids < 2^28, part sizes < 2^31)
+    const bool remote = kind && (uint64_t)((int64_t)v - p.g.lo) >= (uint64_t)(p.g.hi - p.g.lo);
     const uint32_t rm = __ballot_sync(FULL, remote);
     if (rm) {
       if constexpr (DIST) {
         SmemDist& sd = static_cast<SmemDist&>(sm);
-        if (remote) sd.rbuf[warp][q.nr + __popc(rm & lanemask_lt())] = ((uint32_t)owner << 28) | v;
+        if (remote) {
+          const uint32_t owner = v / (uint32_t)p.dr.part_size;
+          sd.rbuf[warp][q.nr + __popc(rm & lanemask_lt())] = (owner << 28) | v;
+        }
         q.nr += __popc(rm);
         q.remote += __popc(rm);
         if (q.nr > kWBuf - 32) wflush_remote(sd, q, p);
@@ -1202,6 +1206,212 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
   }
 }
 
+// ---- E3 across partitions: the distributed persistent kernel (DistPersistArgs, kernels.h) ----------
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
+  asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// The partition's leader arrives at rendezvous k (1-based, monotonic within the launch) and waits
+// for every partition.  False when some partition gave up: a peer that does not arrive within
+// spin_ns (kernels not co-resident) sets the sticky abort word, and every partition leaves its
+// loop at its next rendezvous — a bounded failure the host reports, never a hang.  The grid
+// barrier before the arrival orders this partition's inbox stores (other CTAs) before the
+// system-scope release; the acquire orders the peers' stores before this partition's reads.
+__device__ bool x_arrive_wait(const DistPersistArgs& da, uint32_t k) {
+  __threadfence_system();
+  red_release_sys(&da.xr->arrive, 1u);
+  const unsigned target = k * (unsigned)da.nparts;
+  const unsigned long long t0 = gtimer();
+  while ((int)(ld_acquire_sys(&da.xr->arrive) - target) < 0) {
+    if (ld_ctl(&da.xr->abort)) return false;
+    if (gtimer() - t0 > da.spin_ns) {
+      atomicExch_system(&da.xr->abort, 1u);
+      return false;
+    }
+    __nanosleep(32);
+  }
+  return ld_ctl(&da.xr->abort) == 0;
+}
+
+// Grid barrier + rendezvous + grid barrier; the leader's outcome reaches every CTA through
+// Ctl::x_word.  PUBLISH (the round's end): the leader first clears the consumed inbox counters
+// (senders write the next round's only after this rendezvous), posts the partition's out count and
+// overflow flags, and after the rendezvous sums everyone's.
+template <bool PUBLISH>
+__device__ __forceinline__ void x_meet(const KParams& p, const DistPersistArgs& da, uint32_t k,
+                                       const uint32_t* cout, uint32_t* s_x) {
+  cg::this_grid().sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int me = p.dr.me;
+    if (PUBLISH) {
+      uint32_t fl = ld_ctl(&p.ctl->overflow) & 7u;
+      for (int s = 0; s < da.nparts; ++s)
+        if (s != me) {
+          if (ld_ctl(da.recv_cnt + s) > (uint32_t)p.dr.part_size) fl |= 4u;
+          da.recv_cnt[s] = 0u;
+        }
+      *(volatile uint32_t*)&da.xr->outc[me] = ld_ctl(cout);
+      *(volatile uint32_t*)&da.xr->flags[me] = fl;
+    }
+    const bool ok = x_arrive_wait(da, k);
+    unsigned long long tot = 0;
+    uint32_t fl = 0;
+    if (PUBLISH && ok)
+      for (int s = 0; s < da.nparts; ++s) {
+        tot += ld_ctl(&da.xr->outc[s]);
+        fl |= ld_ctl(&da.xr->flags[s]);
+      }
+    p.ctl->x_word[0] = ok ? 1u : 0u;
+    p.ctl->x_word[1] = (uint32_t)min(tot, 0xffffffffull);
+    p.ctl->x_word[2] = fl;
+  }
+  cg::this_grid().sync();
+  if (threadIdx.x < 3) s_x[threadIdx.x] = ld_ctl(&p.ctl->x_word[threadIdx.x]);
+  __syncthreads();
+}
+
+// Owner side of the round's exchange: every sender's inbox segment, values from the sender's
+// label array (its ghost label of the vertex: a real path length, so any value read is a valid
+// candidate), relaxed and pushed into this partition's out worklist with this round's stamp.
+template <int OP>
+__device__ void apply_inbox(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
+                            const DistPersistArgs& da) {
+  const uint32_t T = gridDim.x * blockDim.x;
+  for (int s = 0; s < da.nparts; ++s) {
+    if (s == p.dr.me) continue;
+    const uint32_t n = min(ld_ctl(da.recv_cnt + s), (uint32_t)p.dr.part_size);
+    const uint32_t* seg = da.recv + (int64_t)s * p.dr.part_size;
+    const int32_t* plab = da.peer_lab[s];
+    for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += T) {
+      const uint32_t i = i0 + lane_id();
+      int kind = 0;
+      uint32_t v = 0;
+      if (i < n) {
+        v = ld_item(seg + i);
+        const int32_t cur = gather_cur<OP>(p, v);
+        const int32_t val = is_bfs(OP) ? 0 : ld_label_cg(plab + v);
+        kind = relax_with<OP>(p, rb, q, cur, val, 0, v);
+      }
+      wpush<OP, false>(sm, q, p, rb, kind, v);
+    }
+  }
+}
+
+template <int OP>
+// (the operators' own occupancy: BFS at 48 warps / SM beat 32 by 4%, SSSP at 32 beat 48 — spills —
+// by 17%, RMAT-24 P=2, profiles/r2_dist_outlined.txt)
+__global__ void __launch_bounds__(kBlock, minb_for(OP)) dist_persistent_kernel(KParams p, DistPersistArgs da) {
+  __shared__ SmemDist sm;
+  smem_init(sm);
+  WarpQ q;
+  const PersistArgs& a = da.pa;
+  uint32_t* cnt = p.ctl->cnt;
+  const int32_t s0 = a.stamp0;
+  int32_t sid = s0;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));
+  __shared__ unsigned long long bslot;
+  __shared__ RoundBufs srb;
+  __shared__ int32_t s_dmin;
+  __shared__ uint32_t s_x[3];
+  uint32_t bidx = 0, xk = 0;
+  const bool dfr = is_sssp(OP) && a.defer_k > 0;
+  if (threadIdx.x == 0) s_dmin = dfr ? (int32_t)min(ld_ctl(&p.ctl->dmin[0]), (uint32_t)kInf) : kInf;
+  __syncthreads();
+  for (uint32_t r = 0;; ++r) {
+    uint32_t* cout = cnt + slot3(a, r + 1);
+    if (leader) {
+      cnt[slot3(a, r + 2)] = 0;
+      p.ctl->chunk_cnt[(r + 1) % 3] = 0;
+      p.ctl->tile_ctr[(r + 1) % 3] = 0;
+      p.ctl->dmin[(r + 2) % 3] = 0xffffffffu;
+    }
+    RoundBufs rb{};
+    rb.in = (r & 1) ? a.buf_b : a.buf_a;
+    rb.nin = nin_next;
+    rb.out = (r & 1) ? a.buf_a : a.buf_b;
+    rb.out_cnt = cout;
+    rb.cap = a.cap;
+    rb.chunks = a.chunks;
+    rb.chunk_cnt = &p.ctl->chunk_cnt[r % 3];
+    rb.chunk_cap = a.chunk_cap;
+    rb.tile_ctr = &p.ctl->tile_ctr[r % 3];
+    rb.level = a.level0 + (int32_t)r;
+    rb.stamp_id = sid++;
+    rb.threshold = kInf;
+    rb.defer_k = is_sssp(OP) ? a.defer_k : 0;
+    rb.dmin_val = s_dmin;
+    rb.dmin_next = rb.defer_k > 0 ? &p.ctl->dmin[(r + 1) % 3] : nullptr;
+    __syncthreads();  // readers of the previous round's view are done
+    if (threadIdx.x == 0) srb = rb;
+    __syncthreads();
+    const RoundBufs& rr = srb;
+    // 1. expansion of this partition's in-worklist; remote updates into the owners' inboxes
+    item_phase<OP, true>(sm, q, p, rr);
+    wflush_remote_all(sm, q, p);
+    wflush_all<OP>(sm, q, p, rr);
+    const unsigned long long w = grid_sync_bcast(
+        p.ctl, bidx, &bslot, [&]() { return pack_counts(ld_ctl(rr.chunk_cnt), 0); },
+        [](unsigned long long) {});
+    const uint32_t nch = unpack_nch(w);
+    if (nch) {
+      chunk_phase<OP, true>(sm, q, p, rr, nch);
+      wflush_remote_all(sm, q, p);
+      wflush_all<OP>(sm, q, p, rr);
+    }
+    // IRGL_DIST_TRACE: the leader stamps %globaltimer at the phase boundaries of each round
+    // {expansion done, inboxes complete, apply done, sums known}
+    unsigned long long* tr = (a.trace && r < a.trace_cap) ? a.trace + 4 * (size_t)r : nullptr;
+    if (leader && tr) {
+      cg::this_grid().sync();
+      tr[0] = gtimer();
+    } else if (tr) {
+      cg::this_grid().sync();
+    }
+    // 2. every partition's expansion done: the inboxes are complete
+    x_meet<false>(p, da, ++xk, cout, s_x);
+    if (leader && tr) tr[1] = gtimer();
+    bool stop = !s_x[0];
+    if (!stop) {
+      // 3. owner-side apply, 4. publish and sum the out counts
+      apply_inbox<OP>(sm, q, p, rr, da);
+      wflush_all<OP>(sm, q, p, rr);
+      if (tr) cg::this_grid().sync();
+      if (leader && tr) tr[2] = gtimer();
+      x_meet<true>(p, da, ++xk, cout, s_x);
+      if (leader && tr) tr[3] = gtimer();
+      if (threadIdx.x == 0 && dfr) s_dmin = (int32_t)min(ld_ctl(&p.ctl->dmin[(r + 1) % 3]), (uint32_t)kInf);
+      __syncthreads();
+      stop = !s_x[0] || s_x[1] == 0 || s_x[2] != 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
+    }
+    const uint32_t nout = ld_ctl(cout);
+    if (leader) {
+      p.ctl->popped += rr.nin;
+      p.ctl->pushes += nout;
+    }
+    nin_next = nout;
+    if (stop) {
+      if (leader) {
+        p.ctl->rounds = r + 1;
+        p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+        p.ctl->stamp_used = (uint32_t)(sid - s0);
+        p.ctl->overflow |= s_x[2] & 3u;  // any partition's overflow fails the Iterate
+      }
+      break;
+    }
+  }
+}
+
 // ---- F1: direction-optimising BFS (outlined, one partition) -----------------------------------------
 // Bottom-up round at level L: every unvisited vertex scans its neighbours for a parent at level
 // L-1 and stops at the first one (Beamer et al.).  Only the owning thread writes level[v], so a
@@ -1719,6 +1929,44 @@ int expand_blocks_per_sm(int op) {
       break;
   }
   return nb;
+}
+
+int dist_persistent_blocks_per_sm(int op) {
+  int nb = 0, n8 = 0;
+  switch (op) {
+    case IRGL_OP_BFS:
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dist_persistent_kernel<IRGL_OP_BFS>, kBlock, 0);
+      break;
+    case IRGL_OP_SSSP:
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dist_persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n8, dist_persistent_kernel<kOpSssp8>, kBlock, 0);
+      nb = min(nb, n8);
+      break;
+    case IRGL_OP_CC_LP:
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dist_persistent_kernel<IRGL_OP_CC_LP>, kBlock, 0);
+      break;
+  }
+  return nb;
+}
+
+cudaError_t launch_dist_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
+                                   const DistRoute& dr, const DistPersistArgs& da, const ExpandCfg& ec, int grid,
+                                   cudaStream_t st) {
+  KParams kp{g, lab, stamp, vis, ctl, dr, ec};
+  DistPersistArgs a = da;
+  void* args[] = {&kp, &a};
+  note_launch();
+  switch (op) {
+    case IRGL_OP_BFS:
+      return cudaLaunchCooperativeKernel((void*)dist_persistent_kernel<IRGL_OP_BFS>, grid, kBlock, args, 0, st);
+    case IRGL_OP_SSSP:
+      if (g.w8)
+        return cudaLaunchCooperativeKernel((void*)dist_persistent_kernel<kOpSssp8>, grid, kBlock, args, 0, st);
+      return cudaLaunchCooperativeKernel((void*)dist_persistent_kernel<IRGL_OP_SSSP>, grid, kBlock, args, 0, st);
+    case IRGL_OP_CC_LP:
+      return cudaLaunchCooperativeKernel((void*)dist_persistent_kernel<IRGL_OP_CC_LP>, grid, kBlock, args, 0, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,

@@ -77,6 +77,9 @@ struct Ctl {
   // release word {barrier tag, payload}, on separate L2 lines; zeroed before every launch
   alignas(256) unsigned int gb_arrive;
   alignas(256) unsigned long long gb_release;
+  // distributed persistent kernel: the leader's rendezvous outcome, broadcast to the CTAs through
+  // a grid barrier {ok, every partition's out count summed, every partition's flags OR-ed}
+  alignas(256) uint32_t x_word[4];
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -133,6 +133,31 @@ struct PersistArgs {
   // can be launched before the previous one's stamp count reached the host
   int32_t* stamp_base = nullptr;
 };
+// E3 across partitions (one process; every partition reachable by loads / stores from every
+// other: one device, or peer access): one cooperative persistent kernel per partition, the
+// partitions meeting twice per round at a device-side rendezvous in partition 0's memory instead
+// of at a host synchronisation.  Round r: expand (remote updates stored into the owners' inboxes,
+// DistRoute::inbox) -> rendezvous (every inbox complete) -> apply the inbox (values read from the
+// senders' labels) -> publish {out count, flags} -> rendezvous (every sum) -> next round or exit.
+struct XRendezvous {
+  alignas(256) unsigned int arrive;  // monotonic arrivals: rendezvous k completes at k * nparts
+  unsigned int abort;                // a partition waited spin_ns without the others: all leave
+  alignas(256) uint32_t outc[kMaxParts];   // out count of each partition's last round
+  uint32_t flags[kMaxParts];               // overflow bits (1 worklist, 2 chunks, 4 inbox)
+};
+struct DistPersistArgs {
+  PersistArgs pa;              // buffers, counter slots, capacities, level0, stamp0, defer_k ...
+  XRendezvous* xr;
+  int nparts;                  // partitions at the rendezvous (== DistRoute::nparts)
+  uint32_t* recv;              // this partition's inbox: sender s's segment at recv + s * part_size
+  uint32_t* recv_cnt;          // [nparts] updates stored by each sender (its atomics)
+  const int32_t* peer_lab[kMaxParts];  // senders' label arrays (the values of their updates)
+  unsigned long long spin_ns;  // rendezvous wait bound (the kernels must be co-resident)
+};
+cudaError_t launch_dist_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
+                                   const DistRoute& dr, const DistPersistArgs& da, const ExpandCfg& ec, int grid,
+                                   cudaStream_t st);
+int dist_persistent_blocks_per_sm(int op);
 // Outlined Iterate: whole loop in one cooperative persistent kernel (E3).
 cudaError_t launch_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                               const PersistArgs& pa, const ExpandCfg& ec, int grid,

@@ -12,7 +12,8 @@ P = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 use_nccl = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 relabel = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 outline = int(sys.argv[5]) if len(sys.argv) > 5 else -1
-kw = dict(logical_partitions=P, outline=outline)
+kw = dict(logical_partitions=P, outline=outline,
+          dense_div=int(os.environ.get("PROBE_DENSE_DIV", "0")))  # -1: no dense rounds
 if use_nccl:
     kw["nccl"] = (0, 0, 1, irgl.nccl_unique_id())
 ctx = irgl.Context(**kw)
@@ -31,5 +32,6 @@ for op, name, kw2 in ((irgl.BFS, "bfs", {}), (irgl.BFS, "bfs-do", {"direction": 
         t0 = time.perf_counter(); st = ctx.iterate(op, g, p, **kw2); t.append(time.perf_counter() - t0)
         r.append(st.rounds); e.append(st.edges)
     print(f"RMAT-{scale} P={P} nccl={use_nccl} relabel={relabel} outline={outline} {name}: {1e3*np.mean(t):.2f} ms/traversal, rounds {np.mean(r):.1f}, "
-          f"{1e6*np.mean(t)/np.mean(r):.0f} us/round, kernel {st.kernel_ms:.2f} ms", flush=True)
+          f"{1e6*np.mean(t)/np.mean(r):.0f} us/round, kernel {st.kernel_ms:.2f} ms, edges {np.mean(e)/1e6:.1f} M "
+          f"({np.mean(e)/np.mean(t)/1e9:.1f} G edges/s)", flush=True)
 ctx.close()
