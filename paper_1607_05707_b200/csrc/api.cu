@@ -81,6 +81,11 @@ struct GraphPart {
   std::vector<const uint32_t*> ipc_send[2];
   std::vector<const int32_t*> ipc_val[2];
   std::vector<void*> ipc_opened;  // handles this process opened (closed with the graph)
+  // distributed persistent kernel across processes (partition 0 of the rank holds the mapping):
+  // every partition's inbox ids / values / counters, by global partition, and rank 0's rendezvous
+  std::vector<uint32_t*> ipc_recv, ipc_recv_cnt;
+  std::vector<int32_t*> ipc_recv_val;
+  irgl::XRendezvous* ipc_xr = nullptr;
   // partitioned DO-BFS scratch, kept across Iterates: the n-bit frontier bitmap [P * words per
   // partition]; on partition 0 also the frontier stats and the rank transport's bitmap staging
   uint32_t* do_bits = nullptr;
@@ -154,6 +159,9 @@ struct irgl_graph {
   bool relabeled = false;
   int ipc_state = 0;  // IPC pull exchange: 0 undecided, 1 mapped, -1 not used
   irgl::XRendezvous* xr = nullptr;  // distributed persistent kernel's rendezvous (partition 0's device)
+  uint32_t xr_arrivals = 0;         // its arrival counter before the next launch (never reset)
+  bool dist_off = false;            // a hello failed once: host rounds from then on
+  bool ipc_shared_dev = false;      // two ranks on one physical GPU (ipc_setup)
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   std::vector<int32_t> inv_host;
@@ -941,13 +949,42 @@ static irgl_status_t wl_graph_rounds(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph*
   return IRGL_OK;
 }
 
-// IPC pull exchange (one process per GPU on one node): every rank maps every other rank's send
-// buckets (both parities) once per graph — the handles travel over the rank transport — and each
-// owner's apply kernel then reads its updates straight out of the senders' buckets over NVLink:
-// no send / recv.  The per-round header allgather is the barrier that makes a round's buckets
-// complete before they are read; buckets alternate by round parity, so a bucket is rewritten only
-// after every rank passed the next round's allgather, i.e. finished reading it.  IRGL_IPC=0 keeps
-// the NCCL / transport point-to-point exchange; so does any failure to map a peer's memory.
+#define CK_B(expr)                          \
+  do {                                      \
+    if ((expr) != cudaSuccess) {            \
+      cudaGetLastError();                   \
+      return false;                         \
+    }                                       \
+  } while (0)
+
+// Allgather of `bytes` host bytes over the rank transport (every copy on partition 0's stream:
+// a legacy-stream copy is not ordered with it).  Collective: every rank calls it.
+static bool ipc_gather(irgl_ctx* ctx, const void* src, size_t bytes, std::vector<char>& out) {
+  PartRT& pr = ctx->parts[0];
+  cudaSetDevice(pr.dev);
+  char* d = nullptr;
+  if (cudaMalloc(&d, bytes * (1 + (size_t)ctx->nranks)) != cudaSuccess) return false;
+  bool ok = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, pr.st) == cudaSuccess &&
+            cudaStreamSynchronize(pr.st) == cudaSuccess &&
+            x_allgather(ctx, pr, d, d + bytes, bytes) == IRGL_OK;
+  out.resize(bytes * ctx->nranks);
+  ok = ok && cudaMemcpyAsync(out.data(), d + bytes, out.size(), cudaMemcpyDeviceToHost, pr.st) == cudaSuccess &&
+       cudaStreamSynchronize(pr.st) == cudaSuccess;
+  cudaFree(d);
+  return ok;
+}
+
+// CUDA IPC across the ranks of one node (one process per GPU), set up once per graph: every rank
+// maps every other rank's
+//  - send buckets (both parities) and their packed values: the IPC pull exchange of the host
+//    rounds — each owner's apply kernel reads its updates straight out of the senders' buckets
+//    over NVLink, no send / recv.  The per-round header allgather is the barrier that makes a
+//    round's buckets complete before they are read; buckets alternate by round parity, so a
+//    bucket is rewritten only after every rank passed the next round's allgather;
+//  - inboxes (ids, values, counters) and rank 0's rendezvous: the distributed persistent kernel
+//    (wl_graph_dist_outlined), whose senders store into the owners' inboxes.
+// The handles travel over the rank transport.  IRGL_IPC=0 keeps the NCCL / transport
+// point-to-point exchange and host rounds; so does any failure to map a peer's memory.
 static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
   const char* e = getenv("IRGL_IPC");
   if ((e && atoi(e) == 0) || !multi_rank(ctx)) return false;  // the same on every rank
@@ -957,73 +994,96 @@ static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
   g->ipc_state = -1;
   const bool dbg = getenv("IRGL_IPC_DEBUG") != nullptr;
   constexpr int kH = (int)sizeof(cudaIpcMemHandle_t);
+  constexpr int kB = 7;  // buffers per partition
   PartRT& pr = ctx->parts[0];
   cudaSetDevice(pr.dev);
-  // every rank contributes {ok flag, L partitions x {send, send_b, send_val, send_val_b} handles}
-  // to one allgather whatever happens locally, then a second one agrees on the mapping: a rank
-  // never leaves its peers alone in a collective
-  const size_t blk = 16 + (size_t)L * 4 * kH;
+  // every rank contributes {ok flag, its rendezvous, L partitions x kB buffers} to one allgather
+  // whatever happens locally, then a second one agrees on the mapping: a rank never leaves its
+  // peers alone in a collective
+  const size_t blk = 32 + kH + (size_t)L * kB * kH;  // {ok, pad}, device uuid, handles
   std::vector<char> mine(blk, 0);
   int32_t ok1 = 1;
+  {
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, pr.dev) == cudaSuccess) std::memcpy(&mine[16], &prop.uuid, 16);
+  }
+  if (!g->xr) {
+    if (cudaMalloc(&g->xr, sizeof(XRendezvous)) != cudaSuccess ||
+        cudaMemset(g->xr, 0, sizeof(XRendezvous)) != cudaSuccess) {
+      cudaGetLastError();
+      ok1 = 0;
+    }
+    g->xr_arrivals = 0;
+  }
+  auto bufs_of = [&](GraphPart& gp, void** b) {
+    void* v[kB] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b, gp.recv, gp.recv_val, gp.recv_cnt};
+    for (int k = 0; k < kB; ++k) b[k] = v[k];
+  };
+  if (ok1 && cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(&mine[32]), g->xr) != cudaSuccess) {
+    cudaGetLastError();
+    ok1 = 0;
+  }
   for (int l = 0; l < L && ok1; ++l) {
-    GraphPart& gp = g->parts[l];
-    void* bufs[4] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b};
-    for (int k = 0; k < 4 && ok1; ++k)
-      if (!bufs[k] || cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(&mine[16 + ((size_t)l * 4 + k) * kH]),
+    void* bufs[kB];
+    bufs_of(g->parts[l], bufs);
+    for (int k = 0; k < kB && ok1; ++k)
+      if (!bufs[k] || cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(&mine[32 + kH + ((size_t)l * kB + k) * kH]),
                                           bufs[k]) != cudaSuccess) {
         cudaGetLastError();
         ok1 = 0;
       }
   }
   std::memcpy(mine.data(), &ok1, 4);
-  auto gather = [&](const void* src, size_t bytes, std::vector<char>& out) {
-    char* d = nullptr;
-    if (cudaMalloc(&d, bytes * (1 + (size_t)ctx->nranks)) != cudaSuccess) return false;
-    // every copy on the partition stream (a legacy-stream copy is not ordered with it)
-    bool ok = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, pr.st) == cudaSuccess &&
-              cudaStreamSynchronize(pr.st) == cudaSuccess &&
-              x_allgather(ctx, pr, d, d + bytes, bytes) == IRGL_OK;
-    out.resize(bytes * ctx->nranks);
-    ok = ok && cudaMemcpyAsync(out.data(), d + bytes, out.size(), cudaMemcpyDeviceToHost, pr.st) == cudaSuccess &&
-         cudaStreamSynchronize(pr.st) == cudaSuccess;
-    cudaFree(d);
-    return ok;
-  };
   std::vector<char> all;
-  if (!gather(mine.data(), blk, all)) return false;
+  if (!ipc_gather(ctx, mine.data(), blk, all)) return false;
   for (int r = 0; r < ctx->nranks; ++r) {
     int32_t f = 0;
     std::memcpy(&f, &all[(size_t)r * blk], 4);
     if (!f) return false;  // some rank cannot export: every rank decides the same
   }
-  if (dbg) fprintf(stderr, "irgl-ipc rank %d: handles gathered\n", ctx->rank);
+  // ranks time-sharing one GPU (no MPS) cannot run their persistent kernels at once: a
+  // rendezvous would cost a context switch (~2 ms, tools/two_proc_probe.py) — host rounds there
+  g->ipc_shared_dev = false;
+  for (int a = 0; a < ctx->nranks; ++a)
+    for (int b = a + 1; b < ctx->nranks; ++b)
+      if (std::memcmp(&all[(size_t)a * blk + 16], &all[(size_t)b * blk + 16], 16) == 0) g->ipc_shared_dev = true;
+  if (dbg) fprintf(stderr, "irgl-ipc rank %d: handles gathered (shared device %d)\n", ctx->rank, (int)g->ipc_shared_dev);
   std::vector<void*> opened;
-  std::vector<void*> ptr((size_t)P * 4, nullptr);
+  std::vector<void*> ptr((size_t)P * kB, nullptr);
+  void* xr0 = nullptr;
   int32_t ok2 = 1;
+  auto open = [&](const char* h_bytes, void** q) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, h_bytes, kH);
+    if (cudaIpcOpenMemHandle(q, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    opened.push_back(*q);
+    return true;
+  };
+  if (ctx->rank == 0) xr0 = g->xr;
+  else ok2 = open(&all[32], &xr0) ? 1 : 0;  // rank 0's rendezvous
   for (int p = 0; p < P && ok2; ++p) {
     const int r = p / L;
-    for (int k = 0; k < 4 && ok2; ++k) {
+    for (int k = 0; k < kB && ok2; ++k) {
       if (r == ctx->rank) {  // this rank's own partitions: direct pointers
-        GraphPart& gp = g->parts[p % L];
-        void* bufs[4] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b};
-        ptr[(size_t)p * 4 + k] = bufs[k];
+        void* bufs[kB];
+        bufs_of(g->parts[p % L], bufs);
+        ptr[(size_t)p * kB + k] = bufs[k];
         continue;
       }
-      cudaIpcMemHandle_t h;
-      std::memcpy(&h, &all[(size_t)r * blk + 16 + ((size_t)(p % L) * 4 + k) * kH], kH);
       void* q = nullptr;
-      if (cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        cudaGetLastError();
+      if (!open(&all[(size_t)r * blk + 32 + kH + ((size_t)(p % L) * kB + k) * kH], &q)) {
         ok2 = 0;
         break;
       }
-      opened.push_back(q);
-      ptr[(size_t)p * 4 + k] = q;
+      ptr[(size_t)p * kB + k] = q;
     }
   }
   if (dbg) fprintf(stderr, "irgl-ipc rank %d: opened %zu handles ok=%d\n", ctx->rank, opened.size(), ok2);
   std::vector<char> oks;
-  bool agree = gather(&ok2, 4, oks);
+  bool agree = ipc_gather(ctx, &ok2, 4, oks);
   for (int r = 0; agree && r < ctx->nranks; ++r) {
     int32_t f = 0;
     std::memcpy(&f, &oks[(size_t)r * 4], 4);
@@ -1039,12 +1099,22 @@ static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
       gp.ipc_send[par].resize(P);
       gp.ipc_val[par].resize(P);
       for (int p = 0; p < P; ++p) {
-        gp.ipc_send[par][p] = static_cast<const uint32_t*>(ptr[(size_t)p * 4 + par]);
-        gp.ipc_val[par][p] = static_cast<const int32_t*>(ptr[(size_t)p * 4 + 2 + par]);
+        gp.ipc_send[par][p] = static_cast<const uint32_t*>(ptr[(size_t)p * kB + par]);
+        gp.ipc_val[par][p] = static_cast<const int32_t*>(ptr[(size_t)p * kB + 2 + par]);
       }
     }
   }
-  g->parts[0].ipc_opened = opened;
+  GraphPart& g0 = g->parts[0];
+  g0.ipc_recv.resize(P);
+  g0.ipc_recv_val.resize(P);
+  g0.ipc_recv_cnt.resize(P);
+  for (int p = 0; p < P; ++p) {
+    g0.ipc_recv[p] = static_cast<uint32_t*>(ptr[(size_t)p * kB + 4]);
+    g0.ipc_recv_val[p] = static_cast<int32_t*>(ptr[(size_t)p * kB + 5]);
+    g0.ipc_recv_cnt[p] = static_cast<uint32_t*>(ptr[(size_t)p * kB + 6]);
+  }
+  g0.ipc_xr = static_cast<XRendezvous*>(xr0);
+  g0.ipc_opened = opened;
   g->ipc_state = 1;
   return true;
 }
@@ -1716,23 +1786,31 @@ static irgl_status_t wl_graph_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_grap
   return IRGL_OK;
 }
 
-// ---- E3 across partitions (one process): wl_graph_dist_outlined -------------------------------------
+// ---- E3 across partitions: wl_graph_dist_outlined ----------------------------------------------------
 // The Iterate of a partitioned graph as one cooperative persistent kernel per partition
 // (dist_persistent_kernel, expand.cu), the partitions meeting at a device-side rendezvous twice a
-// round instead of at a host synchronisation: remote updates go straight into the owners' inboxes
-// (the peer inbox layout of wl_graph_rounds_dist), owners read the values from the senders' labels.
-// Partitions sharing a device split its co-resident CTAs, so every partition's grid is resident
-// at once (a rendezvous never waits on a kernel that cannot start; a bounded wait reports
-// IRGL_E_OCCUPANCY if one ever does).  Requires every partition reachable from every other (one
-// device or peer access); direction-optimising BFS and near-far SSSP keep the host rounds.
+// round instead of at a host synchronisation (and NCCL / transport collectives): senders store
+// remote updates straight into the owners' inboxes and, after their expansion, the updates' values
+// beside them.  One process: the partitions' own buffers (one device or peer access).  Several
+// processes: the same buffers mapped with CUDA IPC (ipc_setup), the rendezvous in rank 0's memory.
+// Partitions sharing a device split its co-resident CTAs.  Every launch starts with a "hello"
+// rendezvous before anything is written: if a kernel never arrives (not co-resident: e.g. ranks
+// time-sharing one GPU without MPS), every partition leaves within spin_ns, all ranks agree that
+// nothing was touched, and the Iterate runs with host rounds (the graph then keeps them).
+// Direction-optimising BFS and near-far SSSP always use host rounds.
 static bool dist_outlined_ok(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op, const NearFar& nf,
                              int dir_opt) {
-  const int L = (int)ctx->parts.size();
-  if (multi_rank(ctx) || L < 2 || L > kMaxParts || (int)g->parts.size() != L) return false;
+  const int L = (int)ctx->parts.size(), P = ctx->ptotal();
+  if (P < 2 || P > kMaxParts || (int)g->parts.size() != L || g->dist_off) return false;
   if (dir_opt || nf.delta > 0 || pipe->cap >= (1ll << 30)) return false;
   if (op != IRGL_OP_BFS && op != IRGL_OP_SSSP && op != IRGL_OP_CC_LP) return false;
+  // IRGL_DIST_OUTLINE: 0 never, 2 also for ranks sharing a GPU (tests; time-sliced rendezvous);
+  // the same on every rank (launch environment)
   const char* e = getenv("IRGL_DIST_OUTLINE");
-  if (e && atoi(e) == 0) return false;
+  const int mode = e ? atoi(e) : 1;
+  if (mode == 0) return false;
+  if (dist_persistent_blocks_per_sm(op) <= 0) return false;
+  if (multi_rank(ctx)) return ipc_setup(ctx, g) && (!g->ipc_shared_dev || mode == 2);  // collective, once per graph
   for (int a = 0; a < L; ++a)
     for (int b = 0; b < L; ++b) {
       const int da = ctx->parts[a].dev, db = ctx->parts[b].dev;
@@ -1740,18 +1818,29 @@ static bool dist_outlined_ok(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int 
       if (da != db) cudaDeviceCanAccessPeer(&can, da, db);
       if (!can) return false;
     }
-  return dist_persistent_blocks_per_sm(op) > 0;
+  if (!g->xr) {
+    CK_B(cudaSetDevice(ctx->parts[0].dev));
+    CK_B(cudaMalloc(&g->xr, sizeof(XRendezvous)));
+    CK_B(cudaMemset(g->xr, 0, sizeof(XRendezvous)));
+    g->xr_arrivals = 0;
+  }
+  return true;
 }
 
+// 1: ran; 0: hello failed everywhere, nothing written (run host rounds); error status otherwise
 static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                             int64_t level0, const irgl_iterate_opts& o, const NearFar& nf,
-                                            irgl_iter_stats* stt) {
-  const int L = (int)ctx->parts.size();
+                                            irgl_iter_stats* stt, bool* ran) {
+  *ran = true;
+  const int L = (int)ctx->parts.size(), P = ctx->ptotal();
   const int64_t ps = g->part_size;
-  uint64_t nin = 0;
-  for (int l = 0; l < L; ++l) nin += pipe->parts[l].n_in;
-  if (nin == 0) return IRGL_OK;
+  const bool mr = multi_rank(ctx);
   if (o.max_rounds > 0 && o.max_rounds <= stt->rounds) return IRGL_OK;
+  if (!mr) {  // (across ranks every rank launches: the others may hold work)
+    uint64_t nin = 0;
+    for (int l = 0; l < L; ++l) nin += pipe->parts[l].n_in;
+    if (nin == 0) return IRGL_OK;
+  }
   if (op == IRGL_OP_SSSP)
     for (int l = 0; l < L; ++l) {
       irgl_status_t ws = ensure_w8(ctx, g, l);
@@ -1760,18 +1849,22 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
   const int bps = dist_persistent_blocks_per_sm(op);
   const char* dtr = getenv("IRGL_DIST_TRACE");
   const bool dtrace = dtr && *dtr == '1';
-  PartRT& pr0 = ctx->parts[0];
-  CK(cudaSetDevice(pr0.dev));
-  if (!g->xr) CK(cudaMalloc(&g->xr, sizeof(XRendezvous)));
-  CK(cudaMemsetAsync(g->xr, 0, sizeof(XRendezvous), pr0.st));
-  cudaEvent_t ready = nullptr;
-  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-  struct EvGuard {
-    cudaEvent_t e;
-    ~EvGuard() { if (e) cudaEventDestroy(e); }
-  } ev_guard{ready};
-  CK(cudaEventRecord(ready, pr0.st));
   const ExpandCfg ec = expand_cfg(ctx);
+  // every partition's inboxes (owner o's segment for sender q: recv + q * ps), by global index
+  std::vector<uint32_t*> recv(P), rcnt(P);
+  std::vector<int32_t*> rval(P);
+  XRendezvous* xr = mr ? g->parts[0].ipc_xr : g->xr;
+  for (int q = 0; q < P; ++q) {
+    if (mr) {
+      recv[q] = g->parts[0].ipc_recv[q];
+      rval[q] = g->parts[0].ipc_recv_val[q];
+      rcnt[q] = g->parts[0].ipc_recv_cnt[q];
+    } else {
+      recv[q] = g->parts[q].recv;
+      rval[q] = g->parts[q].recv_val;
+      rcnt[q] = g->parts[q].recv_cnt;
+    }
+  }
   std::vector<int> grids(L);
   for (int l = 0; l < L; ++l) {  // partitions sharing a device split its resident CTAs
     int share = 0;
@@ -1780,13 +1873,12 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     if (grids[l] < 1)
       return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "too many partitions share a device for co-resident kernels");
   }
-  // every partition's launch state first, then the launches back to back
   std::vector<DistPersistArgs> das(L);
-  std::vector<DistRoute> drs(L);
   for (int l = 0; l < L; ++l) {
     PartRT& pr = ctx->parts[l];
     GraphPart& gp = g->parts[l];
     PipePart& pp = pipe->parts[l];
+    const int me = ctx->gpart(l);
     CK(cudaSetDevice(pr.dev));
     DistPersistArgs& da = das[l];
     fill_persist_args(ctx, pipe, g, op, level0, o, nf, 0, stt->rounds, &da.pa, l);
@@ -1799,65 +1891,78 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
       CK(cudaMemsetAsync(da.pa.trace, 0, 4 * 1024 * 8 + 8, pr.st));
     }
     da.pa.stamp_base = nullptr;
-    da.xr = g->xr;
-    da.nparts = L;
+    da.xr = xr;
+    da.xbase = g->xr_arrivals;
+    da.nparts = P;
     da.recv = gp.recv;
+    da.recv_val = gp.recv_val;
     da.recv_cnt = gp.recv_cnt;
-    for (int k = 0; k < L; ++k) da.peer_lab[k] = g->parts[k].lab;
     da.spin_ns = 5000000000ull;  // 5 s: far beyond any round; only a non-resident peer waits this long
-    DistRoute dr{L, ctx->gpart(l), ps, gp.send, gp.send_cnt};
-    for (int k = 0; k < L; ++k)
-      if (k != l) {
-        dr.inbox[k] = g->parts[k].recv + (int64_t)l * ps;
-        dr.inbox_cnt[k] = g->parts[k].recv_cnt + l;
-      }
-    drs[l] = dr;
-    CK(cudaMemsetAsync(gp.recv_cnt, 0, (size_t)L * 4, pr.st));
+    // the inbox counters are zeroed on the owner's stream before its kernel arrives at the hello,
+    // and senders store only after the hello
+    CK(cudaMemsetAsync(gp.recv_cnt, 0, (size_t)P * 4, pr.st));
+    CK(cudaMemsetAsync(gp.send_cnt, 0, (size_t)P * 4, pr.st));
     CK(launch_ctl_prepare(pp.ctl, pr.st));
-    if (l != 0) CK(cudaStreamWaitEvent(pr.st, ready, 0));
-  }
-  // the inbox counters are zeroed on their own streams: every launch waits for all of them
-  std::vector<cudaEvent_t> zev(L, nullptr);
-  struct EvVec {
-    std::vector<cudaEvent_t>* v;
-    ~EvVec() { for (cudaEvent_t e : *v) if (e) cudaEventDestroy(e); }
-  } zguard{&zev};
-  for (int l = 0; l < L; ++l) {
-    CK(cudaSetDevice(ctx->parts[l].dev));
-    CK(cudaEventCreateWithFlags(&zev[l], cudaEventDisableTiming));
-    CK(cudaEventRecord(zev[l], ctx->parts[l].st));
+    (void)me;
   }
   for (int l = 0; l < L; ++l) {
     PartRT& pr = ctx->parts[l];
     GraphPart& gp = g->parts[l];
     PipePart& pp = pipe->parts[l];
+    const int me = ctx->gpart(l);
     CK(cudaSetDevice(pr.dev));
-    for (int k = 0; k < L; ++k)
-      if (k != l) CK(cudaStreamWaitEvent(pr.st, zev[k], 0));
+    DistRoute dr{P, me, ps, gp.send, gp.send_cnt};
+    for (int q = 0; q < P; ++q)
+      if (q != me) {
+        dr.inbox[q] = recv[q] + (int64_t)me * ps;
+        dr.inbox_cnt[q] = rcnt[q] + me;
+        if (op != IRGL_OP_BFS) dr.inbox_val[q] = rval[q] + (int64_t)me * ps;
+      }
     if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
-    CK(launch_dist_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, drs[l], das[l], ec, grids[l], pr.st));
+    CK(launch_dist_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, dr, das[l], ec, grids[l], pr.st));
     if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
     CK(cudaMemcpyAsync(pr.h_ctl, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
   }
-  XRendezvous hx{};
   for (int l = 0; l < L; ++l) {
     CK(cudaSetDevice(ctx->parts[l].dev));
     CK(cudaStreamSynchronize(ctx->parts[l].st));
   }
-  CK(cudaSetDevice(pr0.dev));
-  CK(cudaMemcpy(&hx, g->xr, sizeof(hx), cudaMemcpyDeviceToHost));
+  XRendezvous hx{};
+  CK(cudaSetDevice(ctx->parts[0].dev));
+  CK(cudaMemcpy(&hx, xr, sizeof(hx), cudaMemcpyDeviceToHost));
   {
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
     stt->kernel_ms += kms;
   }
-  const Ctl& h0 = *pr0.h_ctl;
-  g->stamp_epoch += h0.stamp_used;
-  if (hx.abort)
+  if (hx.abort) {
+    // some partition gave up waiting: fall back only if NO partition got past the hello (all
+    // ranks agree through one allgather; nothing was written anywhere), else fail everywhere
+    g->dist_off = true;
+    int32_t clean = 1;
+    for (int l = 0; l < L; ++l) clean &= ctx->parts[l].h_ctl->x_word[3] == 0 && ctx->parts[l].h_ctl->rounds == 0;
+    if (mr) {
+      std::vector<char> all;
+      if (!ipc_gather(ctx, &clean, 4, all)) return fail(ctx, IRGL_E_CUDA, "E_CUDA", "rendezvous agreement failed");
+      for (int r = 0; r < ctx->nranks; ++r) {
+        int32_t f = 0;
+        std::memcpy(&f, &all[(size_t)r * 4], 4);
+        clean &= f;
+      }
+    }
+    if (clean) {
+      *ran = false;
+      return IRGL_OK;
+    }
     return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY",
-                "partition kernels were not co-resident (rendezvous wait bound reached)");
+                "partition kernels were not co-resident (rendezvous wait bound reached mid-Iterate)");
+  }
+  const Ctl& h0 = *ctx->parts[0].h_ctl;
+  g->xr_arrivals += (uint32_t)P * h0.x_word[3];
+  g->stamp_epoch += h0.stamp_used;
   uint32_t flags = 0;
-  for (int l = 0; l < L; ++l) flags |= hx.flags[l] | (ctx->parts[l].h_ctl->overflow & 3u);
+  for (int q = 0; q < P; ++q) flags |= hx.flags[q];
+  for (int l = 0; l < L; ++l) flags |= ctx->parts[l].h_ctl->overflow & 3u;
   if (flags & 4u) return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW", "remote updates beyond the inbox segment");
   if (flags & 3u)
     return fail(ctx, IRGL_E_WL_OVERFLOW, "E_WL_OVERFLOW",
@@ -1865,7 +1970,7 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
   const int64_t K = (int64_t)h0.rounds;
   for (int l = 0; l < L; ++l) {
     const Ctl& h = *ctx->parts[l].h_ctl;
-    if ((int64_t)h.rounds != K)
+    if ((int64_t)h.rounds != K || h.x_word[3] != h0.x_word[3])
       return fail(ctx, IRGL_E_CUDA, "E_CUDA", "partitions left the distributed loop at different rounds");
     PipePart& pp = pipe->parts[l];
     const int slots[3] = {pp.c_in, pp.c_out, pp.c_spare};
@@ -1880,8 +1985,8 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     stt->pushes += (int64_t)h.pushes;
     stt->exchange_bytes += (int64_t)h.remote * (op == IRGL_OP_BFS ? 4 : 8);
     if (dtrace) {
-      fprintf(stderr, "irgl-dist-outlined part=%d grid=%d rounds=%lld edges=%llu remote=%llu popped=%llu pushes=%llu\n", l,
-              grids[l], (long long)K, h.edges, h.remote, h.popped, h.pushes);
+      fprintf(stderr, "irgl-dist-outlined part=%d grid=%d rounds=%lld edges=%llu remote=%llu popped=%llu pushes=%llu\n",
+              ctx->gpart(l), grids[l], (long long)K, h.edges, h.remote, h.popped, h.pushes);
       std::vector<unsigned long long> t(4 * 1024);
       CK(cudaSetDevice(ctx->parts[l].dev));
       CK(cudaMemcpy(t.data(), das[l].pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
@@ -1891,9 +1996,9 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
         const unsigned long long prev = r ? t[4 * (r - 1) + 3] : q[0];
         // expand: since the previous round's end; wait: until every inbox is complete; apply;
         // publish: the round-end rendezvous
-        fprintf(stderr, "irgl-dist-outlined part=%d round=%lld expand=%.1f wait=%.1f apply=%.1f publish=%.1f us\n", l,
-                (long long)r, (q[0] - prev) * 1e-3, (q[1] - q[0]) * 1e-3, q[2] ? (q[2] - q[1]) * 1e-3 : -1.0,
-                q[3] ? (q[3] - q[2]) * 1e-3 : -1.0);
+        fprintf(stderr, "irgl-dist-outlined part=%d round=%lld expand=%.1f wait=%.1f apply=%.1f publish=%.1f us\n",
+                ctx->gpart(l), (long long)r, (q[0] - prev) * 1e-3, (q[1] - q[0]) * 1e-3,
+                q[2] ? (q[2] - q[1]) * 1e-3 : -1.0, q[3] ? (q[3] - q[2]) * 1e-3 : -1.0);
       }
     }
   }
@@ -2986,10 +3091,14 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     const bool outlined = outline && ctx->ptotal() == 1 && pipe->cap < (1ll << 30);
     const bool dist_loop = !outlined && ctx->ptotal() > 1 && nf.delta <= 0 &&
                            !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
-    const bool dist_outlined = dist_loop && outline && dist_outlined_ok(ctx, pipe, g, op, nf, dir_opt);
+    bool dist_outlined = dist_loop && outline && dist_outlined_ok(ctx, pipe, g, op, nf, dir_opt);
+    if (dist_outlined) {
+      s = wl_graph_dist_outlined(ctx, pipe, g, op, level, o, nf, &st, &dist_outlined);
+      if (s != IRGL_OK) return s;
+    }
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);
-    else if (dist_outlined) s = wl_graph_dist_outlined(ctx, pipe, g, op, level, o, nf, &st);
-    else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st, dir_opt);
+    else if (dist_outlined) {
+    } else if (dist_loop) s = wl_graph_rounds_dist(ctx, pipe, g, op, level, o, nf, &st, dir_opt);
     else s = wl_graph_rounds(ctx, pipe, g, op, level, o, false, nf, &st);
     if (s == IRGL_OK && op == IRGL_OP_SSSP) s = range_verify(ctx, pipe, g);
     if (s != IRGL_OK) return s;

@@ -351,11 +351,20 @@ __device__ __noinline__ void wflush_remote(SmemDist& sd, WarpQ& q, const KParams
     base = __shfl_sync(FULL, base, 31);
     uint32_t pos = base + incl - c;
     uint32_t* bucket = p.dr.inbox[o] ? p.dr.inbox[o] : p.dr.send + (int64_t)o * p.dr.part_size;
+    // values sent later (dist_persistent_kernel's pack, after the whole expansion: a label can
+    // still drop after this flush): the ids also go to the local bucket at the same positions,
+    // and the local counter keeps the segment's length
+    uint32_t* lcopy = p.dr.inbox_val[o] ? p.dr.send + (int64_t)o * p.dr.part_size : nullptr;
+    if (lcopy && lane == 31) atomicAdd(p.dr.send_cnt + o, tot);
     for (uint32_t i = lane; i < n; i += 32) {
       const uint32_t e = sd.rbuf[warp][i];
       if ((e >> 28) == (uint32_t)o) {
-        if (pos < (uint32_t)p.dr.part_size) bucket[pos] = e & 0x0fffffffu;
-        else atomicOr(&p.ctl->overflow, 1u);
+        if (pos < (uint32_t)p.dr.part_size) {
+          bucket[pos] = e & 0x0fffffffu;
+          if (lcopy) lcopy[pos] = e & 0x0fffffffu;
+        } else {
+          atomicOr(&p.ctl->overflow, 1u);
+        }
         ++pos;
       }
     }
@@ -1230,7 +1239,7 @@ __device__ __forceinline__ void red_release_sys(unsigned* p, unsigned v) {
 __device__ bool x_arrive_wait(const DistPersistArgs& da, uint32_t k) {
   __threadfence_system();
   red_release_sys(&da.xr->arrive, 1u);
-  const unsigned target = k * (unsigned)da.nparts;
+  const unsigned target = da.xbase + k * (unsigned)da.nparts;
   const unsigned long long t0 = gtimer();
   while ((int)(ld_acquire_sys(&da.xr->arrive) - target) < 0) {
     if (ld_ctl(&da.xr->abort)) return false;
@@ -1249,10 +1258,12 @@ __device__ bool x_arrive_wait(const DistPersistArgs& da, uint32_t k) {
 // overflow flags, and after the rendezvous sums everyone's.
 template <bool PUBLISH>
 __device__ __forceinline__ void x_meet(const KParams& p, const DistPersistArgs& da, uint32_t k,
-                                       const uint32_t* cout, uint32_t* s_x) {
+                                       const uint32_t* cout, uint32_t* s_x, bool reset_sent = false) {
   cg::this_grid().sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int me = p.dr.me;
+    if (reset_sent)  // the pack has read them: the next round's flushes count from zero
+      for (int o = 0; o < da.nparts; ++o) p.dr.send_cnt[o] = 0u;
     if (PUBLISH) {
       uint32_t fl = ld_ctl(&p.ctl->overflow) & 7u;
       for (int s = 0; s < da.nparts; ++s)
@@ -1280,8 +1291,24 @@ __device__ __forceinline__ void x_meet(const KParams& p, const DistPersistArgs& 
   __syncthreads();
 }
 
-// Owner side of the round's exchange: every sender's inbox segment, values from the sender's
-// label array (its ghost label of the vertex: a real path length, so any value read is a valid
+// Sender side, after the whole expansion: the value of every update this partition stored in an
+// owner's inbox (its label of the vertex now — the lowest it reached this round), written beside
+// the id (a remote store when the owner is another GPU).
+template <int OP>
+__device__ void pack_sent(const KParams& p, const DistPersistArgs& da) {
+  const uint32_t T = gridDim.x * blockDim.x;
+  for (int o = 0; o < da.nparts; ++o) {
+    if (o == p.dr.me || !p.dr.inbox_val[o]) continue;
+    const uint32_t n = min(ld_ctl(p.dr.send_cnt + o), (uint32_t)p.dr.part_size);
+    const uint32_t* ids = p.dr.send + (int64_t)o * p.dr.part_size;
+    int32_t* vals = p.dr.inbox_val[o];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += T)
+      vals[i] = ld_label_cg(p.lab + ld_item(ids + i));
+  }
+}
+
+// Owner side of the round's exchange: every sender's inbox segment with the values the senders
+// stored (their ghost label of the vertex at the flush: a real path length, so a valid
 // candidate), relaxed and pushed into this partition's out worklist with this round's stamp.
 template <int OP>
 __device__ void apply_inbox(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb,
@@ -1291,7 +1318,7 @@ __device__ void apply_inbox(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
     if (s == p.dr.me) continue;
     const uint32_t n = min(ld_ctl(da.recv_cnt + s), (uint32_t)p.dr.part_size);
     const uint32_t* seg = da.recv + (int64_t)s * p.dr.part_size;
-    const int32_t* plab = da.peer_lab[s];
+    const int32_t* vseg = is_bfs(OP) ? nullptr : da.recv_val + (int64_t)s * p.dr.part_size;
     for (uint32_t i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += T) {
       const uint32_t i = i0 + lane_id();
       int kind = 0;
@@ -1299,7 +1326,7 @@ __device__ void apply_inbox(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
       if (i < n) {
         v = ld_item(seg + i);
         const int32_t cur = gather_cur<OP>(p, v);
-        const int32_t val = is_bfs(OP) ? 0 : ld_label_cg(plab + v);
+        const int32_t val = is_bfs(OP) ? 0 : ld_label_cg(vseg + i);
         kind = relax_with<OP>(p, rb, q, cur, val, 0, v);
       }
       wpush<OP, false>(sm, q, p, rb, kind, v);
@@ -1328,6 +1355,18 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) dist_persistent_kernel(K
   const bool dfr = is_sssp(OP) && a.defer_k > 0;
   if (threadIdx.x == 0) s_dmin = dfr ? (int32_t)min(ld_ctl(&p.ctl->dmin[0]), (uint32_t)kInf) : kInf;
   __syncthreads();
+  // hello: every partition's kernel is resident (and every inbox counter zeroed, on its own
+  // stream before its launch) before anything is written; a failed hello leaves all state as it
+  // was, so the host can run the Iterate with host rounds instead
+  x_meet<false>(p, da, ++xk, cnt, s_x);
+  if (!s_x[0]) {
+    if (leader) {
+      p.ctl->rounds = 0;
+      p.ctl->stamp_used = 0;
+      p.ctl->x_word[3] = 0;
+    }
+    return;
+  }
   for (uint32_t r = 0;; ++r) {
     uint32_t* cout = cnt + slot3(a, r + 1);
     if (leader) {
@@ -1378,8 +1417,12 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) dist_persistent_kernel(K
     } else if (tr) {
       cg::this_grid().sync();
     }
-    // 2. every partition's expansion done: the inboxes are complete
-    x_meet<false>(p, da, ++xk, cout, s_x);
+    // values of the remote updates (SSSP / CC_LP), then 2. every inbox is complete
+    if (!is_bfs(OP)) {
+      cg::this_grid().sync();
+      pack_sent<OP>(p, da);
+    }
+    x_meet<false>(p, da, ++xk, cout, s_x, !is_bfs(OP));
     if (leader && tr) tr[1] = gtimer();
     bool stop = !s_x[0];
     if (!stop) {
@@ -1406,6 +1449,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) dist_persistent_kernel(K
         p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
         p.ctl->stamp_used = (uint32_t)(sid - s0);
         p.ctl->overflow |= s_x[2] & 3u;  // any partition's overflow fails the Iterate
+        p.ctl->x_word[3] = s_x[0] ? xk : 0u;  // rendezvous completed (0: a partition gave up)
       }
       break;
     }

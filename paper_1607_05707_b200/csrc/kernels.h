@@ -29,6 +29,10 @@ struct DistRoute {
   // the local buckets above, packed and moved after the expansion
   uint32_t* inbox[kMaxParts] = {};
   uint32_t* inbox_cnt[kMaxParts] = {};
+  // with inbox: the value of each update (the sender's label at the flush) stored beside its id,
+  // inbox_val[o] parallel to inbox[o] (the distributed persistent kernel; null: the owner reads
+  // the sender's labels, or BFS — no values)
+  int32_t* inbox_val[kMaxParts] = {};
 };
 
 struct ExpandCfg {
@@ -133,12 +137,14 @@ struct PersistArgs {
   // can be launched before the previous one's stamp count reached the host
   int32_t* stamp_base = nullptr;
 };
-// E3 across partitions (one process; every partition reachable by loads / stores from every
-// other: one device, or peer access): one cooperative persistent kernel per partition, the
-// partitions meeting twice per round at a device-side rendezvous in partition 0's memory instead
-// of at a host synchronisation.  Round r: expand (remote updates stored into the owners' inboxes,
-// DistRoute::inbox) -> rendezvous (every inbox complete) -> apply the inbox (values read from the
-// senders' labels) -> publish {out count, flags} -> rendezvous (every sum) -> next round or exit.
+// E3 across partitions (every partition reachable by stores and atomics from every other: one
+// device, peer access, or — across processes — CUDA IPC mappings over NVLink): one cooperative
+// persistent kernel per partition, the partitions meeting at a device-side rendezvous in
+// partition 0's memory instead of at a host synchronisation.  Launch: rendezvous ("hello": every
+// kernel resident; nothing written before it).  Round r: expand (remote updates and their values
+// stored into the owners' inboxes, DistRoute::inbox / inbox_val) -> rendezvous (every inbox
+// complete) -> apply the own inbox -> publish {out count, flags} -> rendezvous (every sum) ->
+// next round or exit.
 struct XRendezvous {
   alignas(256) unsigned int arrive;  // monotonic arrivals: rendezvous k completes at k * nparts
   unsigned int abort;                // a partition waited spin_ns without the others: all leave
@@ -148,10 +154,11 @@ struct XRendezvous {
 struct DistPersistArgs {
   PersistArgs pa;              // buffers, counter slots, capacities, level0, stamp0, defer_k ...
   XRendezvous* xr;
+  unsigned int xbase;          // arrivals before this launch (the counter is never reset)
   int nparts;                  // partitions at the rendezvous (== DistRoute::nparts)
   uint32_t* recv;              // this partition's inbox: sender s's segment at recv + s * part_size
+  int32_t* recv_val;           // the updates' values, parallel to recv (null for BFS)
   uint32_t* recv_cnt;          // [nparts] updates stored by each sender (its atomics)
-  const int32_t* peer_lab[kMaxParts];  // senders' label arrays (the values of their updates)
   unsigned long long spin_ns;  // rendezvous wait bound (the kernels must be co-resident)
 };
 cudaError_t launch_dist_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,

@@ -26,10 +26,11 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, spec, logical, q, relabel=False):
+def _rank_main(rank, world, port, spec, logical, q, relabel=False, env=None):
     try:
         import torch.distributed as dist
         sys.path.insert(0, ROOT)
+        os.environ.update(env or {})
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,14 +44,19 @@ def _rank_main(rank, world, port, spec, logical, q, relabel=False):
         info = g.info
         out = {"n": g.n, "m": g.m, "parts": info.partitions, "lo": info.lo, "local_n": info.local_n}
         res = {}
+        outlined = []
         for s in spec["sources"]:
             lv, st = irgl.bfs(ctx, g, s)
             res[("bfs", s)] = (lv, st.rounds, st.exchange_bytes)
+            outlined.append(st.outlined)
             lv, st = irgl.bfs(ctx, g, s, direction=1)  # direction-optimising (bitmap exchange)
             res[("bfs-do", s)] = (lv, st.rounds, 0)
             for delta, defer in ((0, 0), (0, -1), (8, 0)):
                 d, st = irgl.sssp(ctx, g, s, delta=delta, defer=defer)
                 res[("sssp", s, delta, defer)] = (d, st.rounds, st.exchange_bytes)
+                if delta == 0:
+                    outlined.append(st.outlined)
+        out["outlined"] = outlined
         if not relabel:
             lab, _ = irgl.cc_lp(ctx, g, outline=0)
             res[("cc_lp",)] = (lab, 0, 0)
@@ -75,12 +81,12 @@ def _rank_main(rank, world, port, spec, logical, q, relabel=False):
         raise
 
 
-def _run(spec, world=2, logical=0, relabel=False):
+def _run(spec, world=2, logical=0, relabel=False, env=None):
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_rank_main, args=(r, world, port, spec, logical, q, relabel))
+    ps = [ctx.Process(target=_rank_main, args=(r, world, port, spec, logical, q, relabel, env))
           for r in range(world)]
     for p in ps:
         p.start()
@@ -134,3 +140,32 @@ def test_two_process_relabelled(oracle):
         assert set(rounds) == {ecc + 1}
         for delta, defer in ((0, 0), (0, -1), (8, 0)):
             np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], oracle.sssp(og, s))
+
+
+@pytest.mark.parametrize("logical", [0, 2])
+def test_two_process_distributed_persistent_kernel(oracle, logical):
+    # the distributed persistent kernel across processes: inboxes and rank 0's rendezvous mapped
+    # with CUDA IPC.  Two ranks on one GPU take turns (time-sliced contexts), so the runtime keeps
+    # host rounds for them unless forced (IRGL_DIST_OUTLINE=2); on separate GPUs it is the default.
+    og = oracle.rmat(12)
+    srcs = [int(s) for s in og.sources(2)]
+    info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs}, 2, logical,
+                     env={"IRGL_DIST_OUTLINE": "2"})
+    assert set(info["outlined"]) == {1}, info["outlined"]  # every BFS / delta=0 SSSP outlined
+    for s in srcs:
+        ref, ecc = oracle.bfs(og, s)
+        lv, rounds, _ = res[("bfs", s)]
+        np.testing.assert_array_equal(lv, ref)
+        assert set(rounds) == {ecc + 1}
+        dref = oracle.sssp(og, s)
+        for delta, defer in ((0, 0), (0, -1), (8, 0)):
+            np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], dref)
+    np.testing.assert_array_equal(res[("cc_lp",)][0], oracle.cc(og))
+
+
+def test_two_process_shared_gpu_keeps_host_rounds(oracle):
+    og = oracle.rmat(12)
+    srcs = [int(og.sources(1)[0])]
+    info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs})
+    assert set(info["outlined"]) == {0}  # ranks on one GPU: no time-sliced rendezvous
+    np.testing.assert_array_equal(res[("bfs", srcs[0])][0], oracle.bfs(og, srcs[0])[0])
