@@ -328,7 +328,7 @@ __device__ __forceinline__ void wflush(uint32_t* buf, uint32_t& n, uint32_t* out
 
 // Flush of the warp's staged remote pushes: per owner, count the warp's entries, reserve once,
 // write in staging order.  Warp-collective.
-__device__ __noinline__ void wflush_remote(SmemDist& sd, WarpQ& q, const KParams& p) {
+__device__ __forceinline__ void wflush_remote(SmemDist& sd, WarpQ& q, const KParams& p) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint32_t n = q.nr;
   __syncwarp();
