@@ -16,6 +16,8 @@ for W in "sssp 22" "bfs 22" "sssp 24" "bfs 24"; do
     "outlined persistent kernel, RMAT-$2 degree-ordered ids, one warm traversal (tools/one_traversal.py $1 $2 1)" \
     > $OUT/ncu_$1_rmat$2.json 2> $OUT/ncu_$1_rmat$2.err
   python tools/ncu_stalls.py $OUT/ncu_$1$2.ncu-rep 30 > $OUT/stalls_$1$2.txt 2>&1
+  # the report itself stays on the box unless asked for (gpurun copies back <= 64 MiB)
+  [ "${KEEP_NCU_REP:-0}" = 1 ] || rm -f $OUT/ncu_$1$2.ncu-rep
 done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file $OUT/launches_bench.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --secondary 0 > $OUT/bench_under_ncu.log 2>&1

@@ -31,8 +31,9 @@ while time.time() < t_end:
     srcs = [int(s) for s in og.sources(3, seed=int(rng.integers(1, 1000)))] or [0]
     for s in srcs:
         ref_l = O.bfs(og, s)[0]
-        for direction in ((0, 1) if P == 1 else (0,)):
-            lv, _ = irgl.bfs(ctx, g, s, direction=direction, outline=int(rng.integers(0, 2)) if not direction else 1)
+        for direction in (0, 1):  # P > 1: top-down distributed kernel or host rounds; DO host rounds
+            ol = int(rng.integers(0, 2)) if (not direction or P > 1) else 1
+            lv, _ = irgl.bfs(ctx, g, s, direction=direction, outline=ol)
             assert np.array_equal(lv, ref_l), ("bfs", kind, og.n, s, direction)
         ref_d = O.sssp(og, s)
         for delta, defer in ((0, -1), (0, 0), (int(rng.integers(1, 300)), 0), (0, int(rng.integers(1, 5000)))):
