@@ -83,7 +83,7 @@ struct GraphPart {
   std::vector<void*> ipc_opened;  // handles this process opened (closed with the graph)
   // distributed persistent kernel across processes (partition 0 of the rank holds the mapping):
   // every partition's inbox ids / values / counters, by global partition, and rank 0's rendezvous
-  std::vector<uint32_t*> ipc_recv, ipc_recv_cnt;
+  std::vector<uint32_t*> ipc_recv, ipc_recv_cnt, ipc_fbits;
   std::vector<int32_t*> ipc_recv_val;
   irgl::XRendezvous* ipc_xr = nullptr;
   // partitioned DO-BFS scratch, kept across Iterates: the n-bit frontier bitmap [P * words per
@@ -981,8 +981,8 @@ static bool ipc_gather(irgl_ctx* ctx, const void* src, size_t bytes, std::vector
 //    over NVLink, no send / recv.  The per-round header allgather is the barrier that makes a
 //    round's buckets complete before they are read; buckets alternate by round parity, so a
 //    bucket is rewritten only after every rank passed the next round's allgather;
-//  - inboxes (ids, values, counters) and rank 0's rendezvous: the distributed persistent kernel
-//    (wl_graph_dist_outlined), whose senders store into the owners' inboxes.
+//  - inboxes (ids, values, counters), frontier bitmaps and rank 0's rendezvous: the distributed
+//    persistent kernel (wl_graph_dist_outlined), whose senders store into the owners' inboxes.
 // The handles travel over the rank transport.  IRGL_IPC=0 keeps the NCCL / transport
 // point-to-point exchange and host rounds; so does any failure to map a peer's memory.
 static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
@@ -994,7 +994,7 @@ static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
   g->ipc_state = -1;
   const bool dbg = getenv("IRGL_IPC_DEBUG") != nullptr;
   constexpr int kH = (int)sizeof(cudaIpcMemHandle_t);
-  constexpr int kB = 7;  // buffers per partition
+  constexpr int kB = 8;  // buffers per partition
   PartRT& pr = ctx->parts[0];
   cudaSetDevice(pr.dev);
   // every rank contributes {ok flag, its rendezvous, L partitions x kB buffers} to one allgather
@@ -1016,7 +1016,7 @@ static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
     g->xr_arrivals = 0;
   }
   auto bufs_of = [&](GraphPart& gp, void** b) {
-    void* v[kB] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b, gp.recv, gp.recv_val, gp.recv_cnt};
+    void* v[kB] = {gp.send, gp.send_b, gp.send_val, gp.send_val_b, gp.recv, gp.recv_val, gp.recv_cnt, gp.do_bits};
     for (int k = 0; k < kB; ++k) b[k] = v[k];
   };
   if (ok1 && cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(&mine[32]), g->xr) != cudaSuccess) {
@@ -1108,10 +1108,12 @@ static bool ipc_setup(irgl_ctx* ctx, irgl_graph* g) {
   g0.ipc_recv.resize(P);
   g0.ipc_recv_val.resize(P);
   g0.ipc_recv_cnt.resize(P);
+  g0.ipc_fbits.resize(P);
   for (int p = 0; p < P; ++p) {
     g0.ipc_recv[p] = static_cast<uint32_t*>(ptr[(size_t)p * kB + 4]);
     g0.ipc_recv_val[p] = static_cast<int32_t*>(ptr[(size_t)p * kB + 5]);
     g0.ipc_recv_cnt[p] = static_cast<uint32_t*>(ptr[(size_t)p * kB + 6]);
+    g0.ipc_fbits[p] = static_cast<uint32_t*>(ptr[(size_t)p * kB + 7]);
   }
   g0.ipc_xr = static_cast<XRendezvous*>(xr0);
   g0.ipc_opened = opened;
@@ -1802,7 +1804,8 @@ static bool dist_outlined_ok(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int 
                              int dir_opt) {
   const int L = (int)ctx->parts.size(), P = ctx->ptotal();
   if (P < 2 || P > kMaxParts || (int)g->parts.size() != L || g->dist_off) return false;
-  if (dir_opt || nf.delta > 0 || pipe->cap >= (1ll << 30)) return false;
+  if (nf.delta > 0 || pipe->cap >= (1ll << 30)) return false;
+  if (dir_opt && op != IRGL_OP_BFS) return false;
   if (op != IRGL_OP_BFS && op != IRGL_OP_SSSP && op != IRGL_OP_CC_LP) return false;
   // IRGL_DIST_OUTLINE: 0 never, 2 also for ranks sharing a GPU (tests; time-sliced rendezvous);
   // the same on every rank (launch environment)
@@ -1830,7 +1833,7 @@ static bool dist_outlined_ok(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int 
 // 1: ran; 0: hello failed everywhere, nothing written (run host rounds); error status otherwise
 static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int op,
                                             int64_t level0, const irgl_iterate_opts& o, const NearFar& nf,
-                                            irgl_iter_stats* stt, bool* ran) {
+                                            int dir_opt, irgl_iter_stats* stt, bool* ran) {
   *ran = true;
   const int L = (int)ctx->parts.size(), P = ctx->ptotal();
   const int64_t ps = g->part_size;
@@ -1881,7 +1884,7 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     const int me = ctx->gpart(l);
     CK(cudaSetDevice(pr.dev));
     DistPersistArgs& da = das[l];
-    fill_persist_args(ctx, pipe, g, op, level0, o, nf, 0, stt->rounds, &da.pa, l);
+    fill_persist_args(ctx, pipe, g, op, level0, o, nf, dir_opt, stt->rounds, &da.pa, l);
     da.pa.dense_min = 0;
     da.pa.trace = nullptr;
     da.pa.trace_cap = 0;
@@ -1897,6 +1900,8 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     da.recv = gp.recv;
     da.recv_val = gp.recv_val;
     da.recv_cnt = gp.recv_cnt;
+    for (int q = 0; q < P; ++q) da.fbits[q] = mr ? g->parts[0].ipc_fbits[q] : g->parts[q].do_bits;
+    da.wpp = (ps + 31) / 32;
     da.spin_ns = 5000000000ull;  // 5 s: far beyond any round; only a non-resident peer waits this long
     // the inbox counters are zeroed on the owner's stream before its kernel arrives at the hello,
     // and senders store only after the hello
@@ -1958,6 +1963,7 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
                 "partition kernels were not co-resident (rendezvous wait bound reached mid-Iterate)");
   }
   const Ctl& h0 = *ctx->parts[0].h_ctl;
+  const int64_t da_wpp_bytes = (ps + 31) / 32 * 4;  // a bottom-up round's bitmap words, per copy
   g->xr_arrivals += (uint32_t)P * h0.x_word[3];
   g->stamp_epoch += h0.stamp_used;
   uint32_t flags = 0;
@@ -1979,11 +1985,11 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     pp.c_out = slots[(K + 1) % 3];
     pp.c_spare = slots[(K + 2) % 3];
     pp.n_in = h.cnt[pp.c_in];
-    stt->edges += (int64_t)h.edges;
+    stt->edges += (int64_t)(h.edges + h.bu_scanned);  // top-down + bottom-up scans
     stt->remote_updates += (int64_t)h.remote;
     stt->popped += (int64_t)h.popped;
     stt->pushes += (int64_t)h.pushes;
-    stt->exchange_bytes += (int64_t)h.remote * (op == IRGL_OP_BFS ? 4 : 8);
+    stt->exchange_bytes += (int64_t)h.remote * (op == IRGL_OP_BFS ? 4 : 8) + (int64_t)h.bu_rounds * (P - 1) * da_wpp_bytes;
     if (dtrace) {
       fprintf(stderr, "irgl-dist-outlined part=%d grid=%d rounds=%lld edges=%llu remote=%llu popped=%llu pushes=%llu\n",
               ctx->gpart(l), grids[l], (long long)K, h.edges, h.remote, h.popped, h.pushes);
@@ -2363,6 +2369,8 @@ static irgl_status_t graph_alloc_exchange(irgl_ctx* ctx, irgl_graph* g) {
         CK(cudaMalloc(&gp.send_b, tot * 4));
         CK(cudaMalloc(&gp.send_val_b, tot * 4));
       }
+      // the n-bit frontier bitmap of partitioned DO-BFS (allocated here: IPC maps it at setup)
+      CK(cudaMalloc(&gp.do_bits, (size_t)P * ((g->part_size + 31) / 32) * 4));
       CK(cudaMemset(gp.send_cnt, 0, P * 4));
     }
   }
@@ -3093,7 +3101,7 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
                            !(o.max_rounds > 0 && o.extra_comb == IRGL_COMB_AND);
     bool dist_outlined = dist_loop && outline && dist_outlined_ok(ctx, pipe, g, op, nf, dir_opt);
     if (dist_outlined) {
-      s = wl_graph_dist_outlined(ctx, pipe, g, op, level, o, nf, &st, &dist_outlined);
+      s = wl_graph_dist_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st, &dist_outlined);
       if (s != IRGL_OK) return s;
     }
     if (outlined) s = wl_graph_outlined(ctx, pipe, g, op, level, o, nf, dir_opt, &st);

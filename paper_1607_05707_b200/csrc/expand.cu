@@ -1258,7 +1258,8 @@ __device__ bool x_arrive_wait(const DistPersistArgs& da, uint32_t k) {
 // overflow flags, and after the rendezvous sums everyone's.
 template <bool PUBLISH>
 __device__ __forceinline__ void x_meet(const KParams& p, const DistPersistArgs& da, uint32_t k,
-                                       const uint32_t* cout, uint32_t* s_x, bool reset_sent = false) {
+                                       const uint32_t* cout, uint32_t* s_x, bool reset_sent = false,
+                                       const unsigned long long* mf = nullptr) {
   cg::this_grid().sync();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int me = p.dr.me;
@@ -1273,18 +1274,21 @@ __device__ __forceinline__ void x_meet(const KParams& p, const DistPersistArgs& 
         }
       *(volatile uint32_t*)&da.xr->outc[me] = ld_ctl(cout);
       *(volatile uint32_t*)&da.xr->flags[me] = fl;
+      if (mf) *(volatile unsigned long long*)&da.xr->mfc[me] = *(volatile const unsigned long long*)mf;
     }
     const bool ok = x_arrive_wait(da, k);
-    unsigned long long tot = 0;
+    unsigned long long tot = 0, mft = 0;
     uint32_t fl = 0;
     if (PUBLISH && ok)
       for (int s = 0; s < da.nparts; ++s) {
         tot += ld_ctl(&da.xr->outc[s]);
         fl |= ld_ctl(&da.xr->flags[s]);
+        if (mf) mft += *(volatile const unsigned long long*)&da.xr->mfc[s];
       }
     p.ctl->x_word[0] = ok ? 1u : 0u;
     p.ctl->x_word[1] = (uint32_t)min(tot, 0xffffffffull);
     p.ctl->x_word[2] = fl;
+    p.ctl->x_mf = mft;
   }
   cg::this_grid().sync();
   if (threadIdx.x < 3) s_x[threadIdx.x] = ld_ctl(&p.ctl->x_word[threadIdx.x]);
@@ -1659,11 +1663,9 @@ __global__ void frontier_bits_kernel(const uint32_t* items, const uint32_t* cnt,
 // Bottom-up round of one partition: every owned unvisited vertex scans its (global-id) neighbours
 // for one in the level-(L-1) frontier (the blocked bitmap) and stops at the first; only the owner
 // writes its level, so no remote update is needed.  Finds are pushed (the next frontier).
-__global__ void __launch_bounds__(kBlock) bu_part_kernel(KParams p, RoundBufs rb, const uint32_t* fbits,
-                                                         unsigned long long* scanned) {
-  __shared__ Smem sm;
-  smem_init(sm);
-  WarpQ q;
+template <int OP>
+__device__ void bu_part_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBufs& rb, const uint32_t* fbits,
+                              unsigned long long* scanned) {
   const int64_t n = p.g.hi - p.g.lo;
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
   unsigned long long sc = 0;
@@ -1687,12 +1689,153 @@ __global__ void __launch_bounds__(kBlock) bu_part_kernel(KParams p, RoundBufs rb
         if (p.vis) atomicOr(p.vis + ((p.g.lo + lv) >> 5), 1u << ((p.g.lo + lv) & 31));
       }
     }
-    wpush<IRGL_OP_BFS, false>(sm, q, p, rb, hit ? 1 : 0, (uint32_t)(p.g.lo + lv));
+    wpush<OP, false>(sm, q, p, rb, hit ? 1 : 0, (uint32_t)(p.g.lo + lv));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(FULL, sc, o);
   if (lane_id() == 0 && sc) atomicAdd(scanned, sc);
+}
+
+__global__ void __launch_bounds__(kBlock) bu_part_kernel(KParams p, RoundBufs rb, const uint32_t* fbits,
+                                                         unsigned long long* scanned) {
+  __shared__ Smem sm;
+  smem_init(sm);
+  WarpQ q;
+  bu_part_phase<IRGL_OP_BFS>(sm, q, p, rb, fbits, scanned);
   wflush_all<IRGL_OP_BFS>(sm, q, p, rb);
+}
+
+// F1 inside the distributed persistent kernel: top-down rounds as dist_persistent_kernel's (pushes
+// also sum the next frontier's degrees — the owner's for remote finds, in its apply), bottom-up
+// rounds over each partition's own unvisited vertices against the global frontier bitmap, which
+// every partition assembles by storing its own words into every partition's copy before the
+// rendezvous (posted stores over NVLink; no id lists).  Beamer's alpha / beta vote is taken by every
+// partition on the same sums, read at the round-end rendezvous, so the direction is uniform.
+__global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) dist_bfs_do_kernel(KParams p, DistPersistArgs da) {
+  __shared__ SmemDist sm;
+  smem_init(sm);
+  WarpQ q;
+  const PersistArgs& a = da.pa;
+  uint32_t* cnt = p.ctl->cnt;
+  const int32_t s0 = a.stamp0;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  const int me = p.dr.me;
+  uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));
+  __shared__ unsigned long long bslot;
+  __shared__ RoundBufs srb;
+  __shared__ uint32_t s_x[3];
+  __shared__ unsigned long long s_mf;
+  uint32_t bidx = 0, xk = 0, nbu = 0;
+  constexpr double kAlpha = 14.0, kBeta = 24.0;
+  bool bottom_up = false;
+  unsigned long long explored = 0;
+  x_meet<false>(p, da, ++xk, cnt, s_x);  // hello (see dist_persistent_kernel)
+  if (!s_x[0]) {
+    if (leader) {
+      p.ctl->rounds = 0;
+      p.ctl->stamp_used = 0;
+      p.ctl->x_word[3] = 0;
+    }
+    return;
+  }
+  const uint32_t T = gridDim.x * blockDim.x;
+  const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint32_t r = 0;; ++r) {
+    uint32_t* cout = cnt + slot3(a, r + 1);
+    if (leader) {
+      cnt[slot3(a, r + 2)] = 0;
+      p.ctl->chunk_cnt[(r + 1) % 3] = 0;
+      p.ctl->tile_ctr[(r + 1) % 3] = 0;
+      p.ctl->mf[(r + 1) % 3] = 0;
+    }
+    RoundBufs rb{};
+    rb.in = (r & 1) ? a.buf_b : a.buf_a;
+    rb.nin = nin_next;
+    rb.out = (r & 1) ? a.buf_a : a.buf_b;
+    rb.out_cnt = cout;
+    rb.cap = a.cap;
+    rb.chunks = a.chunks;
+    rb.chunk_cnt = &p.ctl->chunk_cnt[r % 3];
+    rb.chunk_cap = a.chunk_cap;
+    rb.tile_ctr = &p.ctl->tile_ctr[r % 3];
+    rb.level = a.level0 + (int32_t)r;
+    rb.stamp_id = s0 + (int32_t)r;
+    rb.threshold = kInf;
+    rb.mf_acc = &p.ctl->mf[r % 3];
+    __syncthreads();
+    if (threadIdx.x == 0) srb = rb;
+    __syncthreads();
+    const RoundBufs& rr = srb;
+    if (!bottom_up) {
+      item_phase<kOpBfsDO, true>(sm, q, p, rr);
+      wflush_remote_all(sm, q, p);
+      wflush_all<kOpBfsDO>(sm, q, p, rr);
+      const unsigned long long w = grid_sync_bcast(
+          p.ctl, bidx, &bslot, [&]() { return pack_counts(ld_ctl(rr.chunk_cnt), 0); }, [](unsigned long long) {});
+      const uint32_t nch = unpack_nch(w);
+      if (nch) {
+        chunk_phase<kOpBfsDO, true>(sm, q, p, rr, nch);
+        wflush_remote_all(sm, q, p);
+        wflush_all<kOpBfsDO>(sm, q, p, rr);
+      }
+      x_meet<false>(p, da, ++xk, cout, s_x);  // every inbox complete
+      if (s_x[0]) {
+        apply_inbox<kOpBfsDO>(sm, q, p, rr, da);
+        wflush_all<kOpBfsDO>(sm, q, p, rr);
+      }
+    } else {
+      // this partition's words of the frontier bitmap, then a copy into every partition's bitmap
+      uint32_t* own = da.fbits[me] + (int64_t)me * da.wpp;
+      for (int64_t i = gt; i < da.wpp; i += T) own[i] = 0u;
+      cg::this_grid().sync();
+      for (uint32_t i = gt; i < rr.nin; i += T) {
+        const uint32_t v = ld_item(rr.in + i);
+        atomicOr(da.fbits[me] + (v >> 5), 1u << (v & 31));
+      }
+      cg::this_grid().sync();
+      for (int qd = 0; qd < da.nparts; ++qd) {
+        if (qd == me) continue;
+        uint32_t* dst = da.fbits[qd] + (int64_t)me * da.wpp;
+        for (int64_t i = gt; i < da.wpp; i += T) dst[i] = own[i];
+      }
+      x_meet<false>(p, da, ++xk, cout, s_x);  // every bitmap complete
+      if (s_x[0]) {
+        bu_part_phase<kOpBfsDO>(sm, q, p, rr, da.fbits[me], &p.ctl->bu_scanned);
+        wflush_all<kOpBfsDO>(sm, q, p, rr);
+        ++nbu;
+      }
+    }
+    bool stop = !s_x[0];
+    if (!stop) {
+      x_meet<true>(p, da, ++xk, cout, s_x, false, &p.ctl->mf[r % 3]);
+      if (threadIdx.x == 0) s_mf = *(volatile unsigned long long*)&p.ctl->x_mf;
+      __syncthreads();
+      stop = !s_x[0] || s_x[1] == 0 || s_x[2] != 0 || (a.max_rounds > 0 && (int64_t)r + 1 >= a.max_rounds);
+    }
+    const uint32_t nout = ld_ctl(cout);
+    if (leader) {
+      p.ctl->popped += rr.nin;
+      p.ctl->pushes += nout;
+    }
+    nin_next = nout;
+    if (stop) {
+      if (leader) {
+        p.ctl->rounds = r + 1;
+        p.ctl->exit_in_slot = (int32_t)((r + 1) & 1);
+        p.ctl->stamp_used = r + 1;
+        p.ctl->bu_rounds = nbu;
+        p.ctl->overflow |= s_x[2] & 3u;
+        p.ctl->x_word[3] = s_x[0] ? xk : 0u;
+      }
+      break;
+    }
+    // direction of the next round: the same global sums in every partition
+    const unsigned long long nf = s_x[1], mf = s_mf;
+    explored += mf;
+    const double mu = (double)a.m - (double)explored;
+    if (!bottom_up && (double)mf > mu / kAlpha) bottom_up = true;
+    else if (bottom_up && (double)nf < (double)a.n / kBeta) bottom_up = false;
+  }
 }
 
 // ---- owner-side application of remote updates (E5 min-reduce) ---------------------------------
@@ -1980,6 +2123,8 @@ int dist_persistent_blocks_per_sm(int op) {
   switch (op) {
     case IRGL_OP_BFS:
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dist_persistent_kernel<IRGL_OP_BFS>, kBlock, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n8, dist_bfs_do_kernel, kBlock, 0);
+      nb = min(nb, n8);  // a grid valid for either direction mode
       break;
     case IRGL_OP_SSSP:
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dist_persistent_kernel<IRGL_OP_SSSP>, kBlock, 0);
@@ -2002,6 +2147,7 @@ cudaError_t launch_dist_persistent(int op, const DevCSR& g, int32_t* lab, int32_
   note_launch();
   switch (op) {
     case IRGL_OP_BFS:
+      if (a.pa.dir_opt) return cudaLaunchCooperativeKernel((void*)dist_bfs_do_kernel, grid, kBlock, args, 0, st);
       return cudaLaunchCooperativeKernel((void*)dist_persistent_kernel<IRGL_OP_BFS>, grid, kBlock, args, 0, st);
     case IRGL_OP_SSSP:
       if (g.w8)

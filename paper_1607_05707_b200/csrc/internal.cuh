@@ -80,6 +80,7 @@ struct Ctl {
   // distributed persistent kernel: the leader's rendezvous outcome, broadcast to the CTAs through
   // a grid barrier {ok, every partition's out count summed, every partition's flags OR-ed}
   alignas(256) uint32_t x_word[4];
+  unsigned long long x_mf;  // DO-BFS: every partition's next-frontier edge count summed
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -150,6 +150,7 @@ struct XRendezvous {
   unsigned int abort;                // a partition waited spin_ns without the others: all leave
   alignas(256) uint32_t outc[kMaxParts];   // out count of each partition's last round
   uint32_t flags[kMaxParts];               // overflow bits (1 worklist, 2 chunks, 4 inbox)
+  unsigned long long mfc[kMaxParts];       // DO-BFS: edges of each partition's next frontier
 };
 struct DistPersistArgs {
   PersistArgs pa;              // buffers, counter slots, capacities, level0, stamp0, defer_k ...
@@ -160,6 +161,10 @@ struct DistPersistArgs {
   int32_t* recv_val;           // the updates' values, parallel to recv (null for BFS)
   uint32_t* recv_cnt;          // [nparts] updates stored by each sender (its atomics)
   unsigned long long spin_ns;  // rendezvous wait bound (the kernels must be co-resident)
+  // direction-optimising BFS (pa.dir_opt): every partition's copy of the n-bit frontier bitmap
+  // (a partition stores its own words into each before a bottom-up round), words per partition
+  uint32_t* fbits[kMaxParts];
+  int64_t wpp;
 };
 cudaError_t launch_dist_persistent(int op, const DevCSR& g, int32_t* lab, int32_t* stamp, uint32_t* vis, Ctl* ctl,
                                    const DistRoute& dr, const DistPersistArgs& da, const ExpandCfg& ec, int grid,

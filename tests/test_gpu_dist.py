@@ -51,6 +51,7 @@ def _rank_main(rank, world, port, spec, logical, q, relabel=False, env=None):
             outlined.append(st.outlined)
             lv, st = irgl.bfs(ctx, g, s, direction=1)  # direction-optimising (bitmap exchange)
             res[("bfs-do", s)] = (lv, st.rounds, 0)
+            outlined.append(st.outlined)
             for delta, defer in ((0, 0), (0, -1), (8, 0)):
                 d, st = irgl.sssp(ctx, g, s, delta=delta, defer=defer)
                 res[("sssp", s, delta, defer)] = (d, st.rounds, st.exchange_bytes)
@@ -151,12 +152,13 @@ def test_two_process_distributed_persistent_kernel(oracle, logical):
     srcs = [int(s) for s in og.sources(2)]
     info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs}, 2, logical,
                      env={"IRGL_DIST_OUTLINE": "2"})
-    assert set(info["outlined"]) == {1}, info["outlined"]  # every BFS / delta=0 SSSP outlined
+    assert set(info["outlined"]) == {1}, info["outlined"]  # every BFS / DO-BFS / delta=0 SSSP outlined
     for s in srcs:
         ref, ecc = oracle.bfs(og, s)
-        lv, rounds, _ = res[("bfs", s)]
-        np.testing.assert_array_equal(lv, ref)
-        assert set(rounds) == {ecc + 1}
+        for key in ("bfs", "bfs-do"):
+            lv, rounds, _ = res[(key, s)]
+            np.testing.assert_array_equal(lv, ref)
+            assert set(rounds) == {ecc + 1}
         dref = oracle.sssp(og, s)
         for delta, defer in ((0, 0), (0, -1), (8, 0)):
             np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], dref)

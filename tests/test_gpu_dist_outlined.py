@@ -42,6 +42,35 @@ def test_outlined_partitioned_bfs_sssp_cc(irgl, oracle, P):
         assert st.outlined == 1
 
 
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_outlined_partitioned_direction_optimising_bfs(irgl, oracle, P):
+    # F1 inside the distributed kernel: bottom-up rounds against the frontier bitmap every
+    # partition stores into every partition's copy; Listing 2's levels and invocation count
+    for relabel in (False, True):
+        og = oracle.rmat(14)
+        with irgl.Context(logical_partitions=P) as c:
+            g = c.generate_rmat(14)
+            if relabel:
+                g.relabel()
+            for s in [int(x) for x in og.sources(3)]:
+                ref, ecc = oracle.bfs(og, s)
+                lv, st = irgl.bfs(c, g, s, direction=1)
+                np.testing.assert_array_equal(lv, ref, err_msg=f"P={P} relabel={relabel} src={s}")
+                assert st.rounds == ecc + 1 and st.outlined == 1 and st.launches == P
+                lv0, st0 = irgl.bfs(c, g, s, direction=1, outline=0)  # host rounds
+                np.testing.assert_array_equal(lv0, ref)
+                assert st0.outlined == 0 and st0.rounds == ecc + 1
+                assert st.edges < og.m  # bottom-up rounds stopped at the first parent
+    og = oracle.grid(64, 48, perc_keep=0.6)
+    with irgl.Context(logical_partitions=P) as c:
+        g = c.generate_grid(64, 48, perc_keep=0.6)
+        for s in (0, 1500):
+            ref, ecc = oracle.bfs(og, s)
+            lv, st = irgl.bfs(c, g, s, direction=1)
+            np.testing.assert_array_equal(lv, ref)
+            assert st.rounds == ecc + 1 and st.outlined == 1
+
+
 def test_outlined_partitioned_relabelled_and_grid(irgl, oracle):
     og = oracle.rmat(14)
     with irgl.Context(logical_partitions=2) as c:
