@@ -720,6 +720,8 @@ struct NearFar {
 // (dist - frontier min) * degree <= K.  From the RMAT-22/24 sweep (profiles/r1s2_defer_sweep.txt):
 // outlined rounds cost ~10 us, so the smaller budget (fewer re-scans, more rounds) wins; a
 // host-orchestrated round costs several times more, so it takes the larger one.
+// SSSP deferral budget: 1024 for the outlined kernels (one partition, and the distributed kernel:
+// RMAT-24 P=2 / P=4 within 1-2% of the best, profiles/r2_defer_partitioned.txt), 2048 for host rounds
 static int64_t default_defer(bool outlined) { return outlined ? 1024 : 2048; }
 
 static int32_t default_delta(const irgl_graph* g) {
@@ -3071,7 +3073,7 @@ irgl_status_t irgl_iterate(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, irgl_o
     if (op == IRGL_OP_SSSP) {
       nf.delta = !args ? 0 : (args->delta < 0 ? default_delta(g) : args->delta);
       nf.threshold = nf.delta;
-      nf.defer_k = !args ? 0 : (args->defer < 0 ? default_defer(outline && ctx->ptotal() == 1) : args->defer);
+      nf.defer_k = !args ? 0 : (args->defer < 0 ? default_defer(outline != 0) : args->defer);
       if (nf.defer_k > 0) {
         // the first round has no frontier minimum yet: no deferral
         for (size_t l = 0; l < pipe->parts.size(); ++l) {
