@@ -719,9 +719,8 @@ struct NearFar {
 // Deferral budget K (irgl_op_args.defer < 0): a popped vertex is expanded only when
 // (dist - frontier min) * degree <= K.  From the RMAT-22/24 sweep (profiles/r1s2_defer_sweep.txt):
 // outlined rounds cost ~10 us, so the smaller budget (fewer re-scans, more rounds) wins; a
-// host-orchestrated round costs several times more, so it takes the larger one.
-// SSSP deferral budget: 1024 for the outlined kernels (one partition, and the distributed kernel:
-// RMAT-24 P=2 / P=4 within 1-2% of the best, profiles/r2_defer_partitioned.txt), 2048 for host rounds
+// host-orchestrated round costs several times more, so it takes the larger one.  The distributed
+// kernel's rounds are outlined too (RMAT-24 P=2 / P=4: 1024 best, profiles/r2_defer_partitioned.txt).
 static int64_t default_defer(bool outlined) { return outlined ? 1024 : 2048; }
 
 static int32_t default_delta(const irgl_graph* g) {
