@@ -501,6 +501,53 @@ def secondary_entries(args, scales_ops):
     return out
 
 
+def partitioned_entry(args, scale=24, parts=(2, 4)):
+    """The multi-partition code path measured on the one GPU: RMAT-`scale` split into
+    P logical partitions (block-diagonal degree order), each Iterate the distributed persistent
+    kernel (one cooperative kernel per partition meeting at a device-side rendezvous); ms per
+    traversal from the runtime's CUDA events over 8 sources, parity of one source against the
+    oracle.  The partitions share this GPU's SMs and L2: a functional stand-in for P GPUs, not a
+    scaling number (the one-partition numbers are the secondary entries)."""
+    import paper_1607_05707_b200 as irgl
+    from oracle import oracle as O  # checker only
+    og = O.rmat(scale)
+    deg = np.diff(og.row_ptr)
+    srcs = pick_sources(og.n, lambda x: int(deg[x]), count=8)
+    refs = {"bfs": O.bfs(og, srcs[0])[0], "sssp": O.sssp(og, srcs[0])}
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    out = []
+    for P in parts:
+        ent = {"workload": f"RMAT-{scale} in {P} logical partitions on one GPU (distributed persistent "
+                           f"kernel, block-diagonal degree order), 8 sources", "P": P}
+        ok, outl = True, True
+        with irgl.Context(devices=[dev], logical_partitions=P, outline=args.outline) as c:
+            g = c.generate_rmat(scale)
+            g.relabel()
+            p = c.pipe(g.n)
+            for name, op_id, kw in (("bfs", irgl.BFS, {}), ("bfs_do", irgl.BFS, {"direction": 1}),
+                                    ("sssp", irgl.SSSP, {})):
+                ms, edges = [], []
+                for i, s in enumerate([srcs[0]] + list(srcs)):  # first: warm-up
+                    p.init_scalars([s])
+                    st = c.iterate(op_id, g, p, **kw)
+                    outl = outl and st.outlined == 1
+                    if i:
+                        ms.append(st.device_ms)
+                        edges.append(st.edges)
+                p.init_scalars([srcs[0]])
+                c.iterate(op_id, g, p, **kw)
+                ok = ok and np.array_equal(c.read_result(op_id, g), refs["sssp" if op_id == irgl.SSSP else "bfs"])
+                ent[f"{name}_ms_per_traversal"] = round(float(np.mean(ms)), 4)
+                ent[f"{name}_edges_scanned"] = int(np.mean(edges))
+            p.close()
+            g.close()
+        ent["outlined"] = outl
+        ent["parity"] = "bit-exact" if ok else "MISMATCH"
+        ent["parity_check"] = f"source {srcs[0]}: BFS, DO-BFS levels and SSSP distances against the serial oracle"
+        out.append(ent)
+    return out
+
+
 def run_irgl(args, d):
     import paper_1607_05707_b200 as irgl
     op_id = irgl.SSSP if args.op == "sssp" else irgl.BFS
@@ -642,6 +689,7 @@ def run_irgl(args, d):
     # ---- secondary entries (N=1): BFS at the headline scale, the north-star RMAT-24 BFS / SSSP
     if d.world == 1 and args.secondary and args.scale == 22 and args.op == "sssp" and not args.direction:
         line["detail"]["secondary"] = secondary_entries(args, [(22, "bfs"), (24, "bfs"), (24, "sssp")])
+        line["detail"]["partitioned_one_gpu"] = partitioned_entry(args)
     if d.rank == 0:
         print(json.dumps(line), flush=True)
     return 0
