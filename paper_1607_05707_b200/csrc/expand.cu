@@ -286,7 +286,8 @@ __device__ __forceinline__ void relax_batch(const KParams& p, const RoundBufs& r
       kind[j] = (has_far(OP) && nd[j] >= rb.threshold) ? 2 : 1;
       // a vertex another partition owns is sent once per round whatever its pile (the owner
       // decides near / far): one code for both kinds
-      const bool remote = has_far(OP) && p.dr.nparts > 1 && (int64_t)dst[j] / p.dr.part_size != p.dr.me;
+      const bool remote = has_far(OP) && p.dr.nparts > 1 &&
+                          (uint64_t)((int64_t)dst[j] - p.g.lo) >= (uint64_t)(p.g.hi - p.g.lo);
       code[j] = stamp_code<OP>(rb.stamp_id, remote ? 2 : kind[j]);
       if (has_far(OP)) old[j] = cand[j] ? atomicMin(p.lab + dst[j], nd[j]) : 0;
       else if (cand[j]) atomicMin(p.lab + dst[j], nd[j]);  // result unused -> RED.MIN
@@ -616,7 +617,9 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   {
     const bool big = deg >= p.ec.warp_t;
     const int64_t ce = p.ec.chunk_edges;
-    const uint32_t nchl = big ? (uint32_t)((deg + ce - 1) / ce) : 0u;
+    // 32-bit division (a 64-bit one is a ~70-instruction subroutine call per lane)
+    const uint32_t ce32 = (uint32_t)ce;
+    const uint32_t nchl = big ? ((uint32_t)(deg < 0xfffe0000ll ? deg : 0xfffe0000ll) + ce32 - 1u) / ce32 : 0u;
     uint32_t incl = nchl;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -771,7 +774,7 @@ __device__ void chunk_phase(Smem& sm, WarpQ& q, const KParams& p, const RoundBuf
     const ChunkDesc d = ld_desc(rb.chunks + gw / P);
     const uint32_t part = gw % P;
     const int64_t b = (int64_t)(d.beg_len >> 16), len = (int64_t)(d.beg_len & 0xffffu);
-    const int64_t per = (((len + P - 1) / P) + 3) & ~int64_t(3);
+    const int64_t per = (int64_t)(((((uint32_t)len + P - 1u) / P) + 3u) & ~3u);  // len < 2^16
     const int64_t b0 = b + part * per, e0 = min(b0 + per, b + len);
     if (b0 < e0) process_range<OP, DIST>(sm, q, p, rb, b0, e0, d.sv, gl);
     return;
