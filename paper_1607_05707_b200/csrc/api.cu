@@ -1993,7 +1993,7 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
     stt->exchange_bytes += (int64_t)h.remote * (op == IRGL_OP_BFS ? 4 : 8) + (int64_t)h.bu_rounds * (P - 1) * da_wpp_bytes;
     if (dtrace) {
       fprintf(stderr, "irgl-dist-outlined part=%d grid=%d rounds=%lld edges=%llu remote=%llu popped=%llu pushes=%llu\n",
-              ctx->gpart(l), grids[l], (long long)K, h.edges, h.remote, h.popped, h.pushes);
+              ctx->gpart(l), grids[l], (long long)K, h.edges + h.bu_scanned, h.remote, h.popped, h.pushes);
       std::vector<unsigned long long> t(4 * 1024);
       CK(cudaSetDevice(ctx->parts[l].dev));
       CK(cudaMemcpy(t.data(), das[l].pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
