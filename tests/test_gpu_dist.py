@@ -143,14 +143,14 @@ def test_two_process_relabelled(oracle):
             np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], oracle.sssp(og, s))
 
 
-@pytest.mark.parametrize("logical", [0, 2])
-def test_two_process_distributed_persistent_kernel(oracle, logical):
+@pytest.mark.parametrize("logical,relabel", [(0, False), (2, False), (0, True)])
+def test_two_process_distributed_persistent_kernel(oracle, logical, relabel):
     # the distributed persistent kernel across processes: inboxes and rank 0's rendezvous mapped
     # with CUDA IPC.  Two ranks on one GPU take turns (time-sliced contexts), so the runtime keeps
     # host rounds for them unless forced (IRGL_DIST_OUTLINE=2); on separate GPUs it is the default.
     og = oracle.rmat(12)
     srcs = [int(s) for s in og.sources(2)]
-    info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs}, 2, logical,
+    info, res = _run({"kind": "rmat", "scale": 12, "sources": srcs}, 2, logical, relabel=relabel,
                      env={"IRGL_DIST_OUTLINE": "2"})
     assert set(info["outlined"]) == {1}, info["outlined"]  # every BFS / DO-BFS / delta=0 SSSP outlined
     for s in srcs:
@@ -162,7 +162,8 @@ def test_two_process_distributed_persistent_kernel(oracle, logical):
         dref = oracle.sssp(og, s)
         for delta, defer in ((0, 0), (0, -1), (8, 0)):
             np.testing.assert_array_equal(res[("sssp", s, delta, defer)][0], dref)
-    np.testing.assert_array_equal(res[("cc_lp",)][0], oracle.cc(og))
+    if not relabel:
+        np.testing.assert_array_equal(res[("cc_lp",)][0], oracle.cc(og))
 
 
 def test_two_process_shared_gpu_keeps_host_rounds(oracle):
