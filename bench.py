@@ -526,7 +526,7 @@ def partitioned_entry(args, scale=24, parts=(2, 4)):
             p = c.pipe(g.n)
             for name, op_id, kw in (("bfs", irgl.BFS, {}), ("bfs_do", irgl.BFS, {"direction": 1}),
                                     ("sssp", irgl.SSSP, {})):
-                ms, edges = [], []
+                ms, edges, xb = [], [], []
                 for i, s in enumerate([srcs[0]] + list(srcs)):  # first: warm-up
                     p.init_scalars([s])
                     st = c.iterate(op_id, g, p, **kw)
@@ -534,11 +534,13 @@ def partitioned_entry(args, scale=24, parts=(2, 4)):
                     if i:
                         ms.append(st.device_ms)
                         edges.append(st.edges)
+                        xb.append(st.exchange_bytes)
                 p.init_scalars([srcs[0]])
                 c.iterate(op_id, g, p, **kw)
                 ok = ok and np.array_equal(c.read_result(op_id, g), refs["sssp" if op_id == irgl.SSSP else "bfs"])
                 ent[f"{name}_ms_per_traversal"] = round(float(np.mean(ms)), 4)
                 ent[f"{name}_edges_scanned"] = int(np.mean(edges))
+                ent[f"{name}_exchange_bytes"] = int(np.mean(xb))  # ids + values stored into peers' inboxes
             p.close()
             g.close()
         ent["outlined"] = outl
