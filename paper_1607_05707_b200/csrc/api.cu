@@ -1878,6 +1878,15 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
       return fail(ctx, IRGL_E_OCCUPANCY, "E_OCCUPANCY", "too many partitions share a device for co-resident kernels");
   }
   std::vector<DistPersistArgs> das(L);
+  struct TraceFree {  // IRGL_DIST_TRACE buffers, on every return path
+    std::vector<DistPersistArgs>* d;
+    irgl_ctx* c;
+    ~TraceFree() {
+      for (size_t l = 0; l < d->size(); ++l)
+        if ((*d)[l].pa.trace) { cudaSetDevice(c->parts[l].dev); cudaFree((*d)[l].pa.trace); }
+    }
+  } trace_free{&das, ctx};
+  cudaError_t launch_err = cudaSuccess;
   for (int l = 0; l < L; ++l) {
     PartRT& pr = ctx->parts[l];
     GraphPart& gp = g->parts[l];
@@ -1925,7 +1934,15 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
         if (op != IRGL_OP_BFS) dr.inbox_val[q] = rval[q] + (int64_t)me * ps;
       }
     if (l == 0) CK(cudaEventRecord(ctx->kev0, pr.st));
-    CK(launch_dist_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, dr, das[l], ec, grids[l], pr.st));
+    launch_err = launch_dist_persistent(op, gp.csr(), gp.lab, gp.stamp, gp.vis_k(), pp.ctl, dr, das[l], ec, grids[l], pr.st);
+    if (launch_err != cudaSuccess) {
+      // the partitions already launched (here and on other ranks) must not wait for this one:
+      // raise the shared abort word, then agree with the other ranks below like a failed hello
+      cudaGetLastError();
+      const unsigned int one = 1;
+      cudaMemcpy(&xr->abort, &one, sizeof(one), cudaMemcpyHostToDevice);
+      break;
+    }
     if (l == 0) CK(cudaEventRecord(ctx->kev1, pr.st));
     CK(cudaMemcpyAsync(pr.h_ctl, pp.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, pr.st));
   }
@@ -1936,6 +1953,15 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
   XRendezvous hx{};
   CK(cudaSetDevice(ctx->parts[0].dev));
   CK(cudaMemcpy(&hx, xr, sizeof(hx), cudaMemcpyDeviceToHost));
+  if (launch_err != cudaSuccess) {
+    g->dist_off = true;
+    if (mr) {  // every rank takes part in the agreement (the others saw the abort word)
+      int32_t clean = 0;
+      std::vector<char> all;
+      ipc_gather(ctx, &clean, 4, all);
+    }
+    return cuda_status(ctx, launch_err, "launch_dist_persistent");
+  }
   {
     float kms = 0.f;
     CK(cudaEventElapsedTime(&kms, ctx->kev0, ctx->kev1));
@@ -1997,7 +2023,6 @@ static irgl_status_t wl_graph_dist_outlined(irgl_ctx* ctx, irgl_pipe* pipe, irgl
       std::vector<unsigned long long> t(4 * 1024);
       CK(cudaSetDevice(ctx->parts[l].dev));
       CK(cudaMemcpy(t.data(), das[l].pa.trace, t.size() * 8, cudaMemcpyDeviceToHost));
-      cudaFree(das[l].pa.trace);
       for (int64_t r = 0; r < std::min<int64_t>(K, 1024); ++r) {
         const unsigned long long* q = &t[4 * r];
         const unsigned long long prev = r ? t[4 * (r - 1) + 3] : q[0];
