@@ -3522,6 +3522,10 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
     const int32_t e = (int32_t)g->stamp_epoch;
     CK(cudaMemcpy(&gp.ctl->stamp_base, &e, sizeof(e), cudaMemcpyHostToDevice));
   }
+  {  // node state for the traversals' prologues (allocated once; op_reset's first step)
+    irgl_status_t ls = ensure_lab(ctx, g, op != IRGL_OP_BFS);
+    if (ls != IRGL_OK) return ls;
+  }
   uint32_t last_rounds = 0;
   auto finish = [&](int32_t j) -> irgl_status_t {
     const int b = j & 1;
@@ -3567,17 +3571,25 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
       }
       return host_out ? irgl_results_wait(ctx) : IRGL_OK;
     }
-    // canonical slots, then Initial [source] (defines the whole worklist state)
+    // canonical slots; Initial [source], the node-state and control-block resets run in the
+    // kernel's own prologue (PersistArgs::src): one launch per traversal
     pp.b_in = 0, pp.b_out = 1, pp.b_retry = 2;
     pp.c_in = 0, pp.c_out = 1, pp.c_retry = 2, pp.c_spare = 3;
-    irgl_status_t s = irgl_pipe_init_scalars(pipe, sources + i, 1);
-    if (s != IRGL_OK) return s;
-    if ((s = map_pipe(ctx, pipe, g)) != IRGL_OK) return s;
+    irgl_status_t s = IRGL_OK;
     CK(cudaSetDevice(pr.dev));
+    if (gp.lab_buf[1]) {  // double-buffered labels (op_reset's rule): write the other buffer
+      gp.lab_sel ^= 1;
+      gp.lab = gp.lab_buf[gp.lab_sel];
+      if (gp.copy_pending[gp.lab_sel]) {
+        CK(cudaStreamWaitEvent(pr.st, gp.lab_copied[gp.lab_sel], 0));
+        gp.copy_pending[gp.lab_sel] = false;
+      }
+    }
+    g->lab_op = op;
+    pipe->pristine = false;
+    pipe->mapped_for = g->relabeled ? g : nullptr;
+    pp.n_in = 1;
     CK(cudaEventRecord(pr.bev[b][0], pr.st));
-    if ((s = op_reset(ctx, g, op, pipe)) != IRGL_OK) return s;
-    if ((s = pipe_counters(ctx, pipe, nullptr)) != IRGL_OK) return s;
-    if (nf.defer_k > 0) CK(cudaMemsetAsync(pp.ctl->dmin, 0xff, sizeof(pp.ctl->dmin), pr.st));
     PersistArgs pa;
     fill_persist_args(ctx, pipe, g, op, level, o, nf, dir_opt, 0, &pa);
     pa.trace = nullptr;
@@ -3585,7 +3597,9 @@ static irgl_status_t traverse_batch_pipelined(irgl_ctx* ctx, irgl_pipe* pipe, ir
     pa.stamp_base = &gp.ctl->stamp_base;
     uint32_t* visk = gp.vis_k();
     if (pa.dir_opt && ctx->cfg.bfs_bitmap_min_n == 0 && g->n < (12ll << 20)) visk = nullptr;
-    CK(launch_ctl_prepare(pp.ctl, pr.st));
+    pa.src = sources[i];
+    pa.src_map = g->relabeled ? g->perm : nullptr;
+    pa.reset_vis = op == IRGL_OP_BFS ? visk : nullptr;
     if ((s = l2_window_for(ctx, pr, g, gp, op, visk)) != IRGL_OK) return s;
     CK(cudaEventRecord(pr.bev[b][1], pr.st));
     CK(launch_persistent(op, gp.csr(), gp.lab, gp.stamp, visk, pp.ctl, pa, expand_cfg(ctx), grid, pr.st));

@@ -1049,6 +1049,48 @@ __device__ __forceinline__ int slot3(const PersistArgs& a, uint32_t i) {
   return m == 0 ? a.slot[0] : (m == 1 ? a.slot[1] : a.slot[2]);
 }
 
+// Fused traversal prologue (PersistArgs::src): labels = INF (16-byte stores), visited bitmap = 0,
+// control block reset (what ctl_prepare_kernel, pipe_counters and the pipe init do), then
+// Initial [src]: in = {src}, label[src] = 0 (and its visited bit) after a grid barrier, and a second
+// barrier before round 0 reads any of it.
+__device__ void traversal_prologue(const KParams& p, const PersistArgs& a) {
+  const int64_t n = a.n;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n4 = n >> 2;  // the label array is cudaMalloc'd: 16-byte aligned
+  const int4 inf4 = make_int4(kInf, kInf, kInf, kInf);
+  for (int64_t i = t; i < n4; i += T) reinterpret_cast<int4*>(p.lab)[i] = inf4;
+  for (int64_t i = (n4 << 2) + t; i < n; i += T) p.lab[i] = kInf;
+  if (a.reset_vis)
+    for (int64_t i = t; i < ((n + 31) >> 5); i += T) a.reset_vis[i] = 0u;
+  const uint32_t v = a.src_map ? (uint32_t)a.src_map[a.src] : (uint32_t)a.src;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    Ctl* c = p.ctl;
+    for (int k = 0; k < 4; ++k) c->cnt[k] = 0u;
+    c->cnt[a.slot[0]] = 1u;
+    for (int k = 0; k < 3; ++k) {
+      c->chunk_cnt[k] = 0u;
+      c->tile_ctr[k] = 0u;
+      c->dmin[k] = 0xffffffffu;  // round 0: no frontier minimum yet (no deferral)
+      c->mf[k] = 0ull;
+      c->bu_found[k] = 0ull;
+    }
+    c->far_cnt[0] = c->far_cnt[1] = 0u;
+    c->overflow = 0u;
+    c->popped = c->pushes = c->rounds = c->bu_scanned = 0ull;
+    c->edges = c->remote = 0ull;
+    c->gb_arrive = 0u;
+    c->gb_release = 0ull;
+    a.buf_a[0] = v;
+  }
+  cg::this_grid().sync();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    p.lab[v] = 0;
+    if (a.reset_vis) a.reset_vis[v >> 5] |= 1u << (v & 31);
+  }
+  cg::this_grid().sync();
+}
+
 template <int OP>
 __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParams p, PersistArgs a) {
   __shared__ Smem sm;
@@ -1063,6 +1105,7 @@ __global__ void __launch_bounds__(kBlock, minb_for(OP)) persistent_kernel(KParam
   uint32_t fsel = 0;            // which far buffer is current
   uint32_t nsplit = 0;          // splits so far (selects the minkeep slot)
   const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+  if (a.src >= 0) traversal_prologue(p, a);
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));  // round r's in-count = round r-1's out-count
   __shared__ unsigned long long bslot;  // barrier broadcast
   __shared__ RoundBufs srb;             // this round's view (no near-far)
@@ -1537,6 +1580,7 @@ __global__ void __launch_bounds__(kBlock, IRGL_DO_MINB) persistent_bfs_do_kernel
   uint32_t nbu = 0;
   unsigned long long explored = 0;               // edges of vertices already discovered
   const int32_t s0 = a.stamp_base ? *(volatile int32_t*)a.stamp_base + 1 : a.stamp0;
+  if (a.src >= 0) traversal_prologue(p, a);
   uint32_t nin_next = ld_ctl(cnt + slot3(a, 0));
   for (uint32_t r = 0;; ++r) {
     uint32_t* cout = cnt + slot3(a, r + 1);

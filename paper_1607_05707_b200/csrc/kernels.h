@@ -136,6 +136,12 @@ struct PersistArgs {
   // id from *stamp_base + 1 instead of stamp0 and leaves its last used id there, so a traversal
   // can be launched before the previous one's stamp count reached the host
   int32_t* stamp_base = nullptr;
+  // fused traversal prologue (irgl_traverse_batch): with src >= 0 the kernel itself resets the
+  // labels (and the BFS visited bitmap), the control block and the in-worklist to Initial [src]
+  // before round 0 — one launch per traversal instead of a dozen small copies, memsets and kernels
+  int64_t src = -1;                  // caller id
+  const int32_t* src_map = nullptr;  // relabelled graph: caller id -> vertex id
+  uint32_t* reset_vis = nullptr;     // BFS visited bitmap the kernel uses (n bits), or null
 };
 // E3 across partitions (every partition reachable by stores and atomics from every other: one
 // device, peer access, or — across processes — CUDA IPC mappings over NVLink): one cooperative
