@@ -670,12 +670,15 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
   }
   const uint32_t total = __shfl_sync(FULL, incl, 31);
   const int64_t off = beg - (int64_t)(incl - d);  // edge of slot k (owned here) = off + k
-  // 4 windows of 32 edge slots per iteration: each lane has 4 independent col/label chains in
+  // kWin windows of 32 edge slots per iteration: each lane has kWin independent col/label chains in
   // flight (memory-level parallelism); owner of slot k = #lanes with inclusive prefix <= k
 #ifndef IRGL_KWIN
 #define IRGL_KWIN 4
 #endif
-  constexpr int kWin = IRGL_KWIN;
+#ifndef IRGL_KWIN_SSSP
+#define IRGL_KWIN_SSSP 8  // SSSP-22 -2% at 8 windows, BFS flat (profiles/r2_kwin.txt)
+#endif
+  constexpr int kWin = is_sssp(OP) ? IRGL_KWIN_SSSP : IRGL_KWIN;
   for (uint32_t wb = 0; wb < total; wb += 32 * kWin) {
     uint32_t dst[kWin];
     int32_t wt[kWin], s[kWin], cur[kWin];
