@@ -230,9 +230,10 @@ static ExpandCfg expand_cfg(const irgl_ctx* ctx) {
   ExpandCfg ec;
   // degree < warp_t: the warp tile's fine-grained gather; >= warp_t: edge chunks of chunk_edges
   // drained by all warps (edge-balanced), except in small rounds (one tile per warp) where degrees
-  // below cta_t are expanded by the popping warp.  Defaults from the RMAT-22 sweep
-  // (profiles/r1s2_sched_sweep.txt).
-  ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 128;
+  // below cta_t are expanded by the popping warp.  Defaults from the RMAT-22 / 24 sweeps
+  // (profiles/r1s2_sched_sweep.txt; warp_t 128 -> 256 once SSSP's fine-grained gather kept 8
+  // windows in flight: profiles/r2_sched_sweep.txt).
+  ec.warp_t = ctx->cfg.warp_threshold > 0 ? ctx->cfg.warp_threshold : 256;
   ec.cta_t = ctx->cfg.cta_threshold > 0 ? ctx->cfg.cta_threshold : 256;
   ec.chunk_edges = ctx->cfg.chunk_edges > 0 ? ctx->cfg.chunk_edges : 512;
   ec.chunk_edges = std::max(4, std::min(ec.chunk_edges, 65535));  // 16-bit length in ChunkDesc

@@ -678,7 +678,9 @@ __device__ void expand_warp_tile(Smem& sm, WarpQ& q, const KParams& p, const Rou
 #ifndef IRGL_KWIN_SSSP
 #define IRGL_KWIN_SSSP 8  // SSSP-22 -2% at 8 windows, BFS flat (profiles/r2_kwin.txt)
 #endif
-  constexpr int kWin = is_sssp(OP) ? IRGL_KWIN_SSSP : IRGL_KWIN;
+  // (the multi-partition kernels keep 4: their remote staging leaves no registers for 8 — RMAT-24
+  // P=2 SSSP 5.94 -> 6.22 ms with 8)
+  constexpr int kWin = (is_sssp(OP) && !DIST) ? IRGL_KWIN_SSSP : IRGL_KWIN;
   for (uint32_t wb = 0; wb < total; wb += 32 * kWin) {
     uint32_t dst[kWin];
     int32_t wt[kWin], s[kWin], cur[kWin];

@@ -7,8 +7,12 @@ import bench
 import paper_1607_05707_b200 as irgl
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-for wt, ce in ((128, 512), (64, 512), (96, 512), (192, 512), (128, 256), (128, 1024)):
-    ctx = irgl.Context(warp_threshold=wt, chunk_edges=ce, cta_threshold=max(256, wt))
+combos = [(128, 512, 256), (64, 512, 256), (96, 512, 256), (192, 512, 256), (256, 512, 256),
+          (128, 256, 256), (128, 1024, 256)]
+if os.environ.get("SCHED"):  # SCHED="warp_t:chunk_edges:cta_t,..."
+    combos = [tuple(int(x) for x in c.split(":")) for c in os.environ["SCHED"].split(",")]
+for wt, ce, cta in combos:
+    ctx = irgl.Context(warp_threshold=wt, chunk_edges=ce, cta_threshold=max(cta, wt))
     g = ctx.generate_rmat(scale)
     deg = np.diff(g.download()[0])
     srcs = bench.pick_sources(g.n, lambda x: int(deg[x]), count=8)
@@ -24,5 +28,5 @@ for wt, ce in ((128, 512), (64, 512), (96, 512), (192, 512), (128, 256), (128, 1
                 if rep:
                     t.append(st.kernel_ms)
         out.append(f"{name} {np.mean(t):.3f} ms")
-    print(f"RMAT-{scale} warp_t={wt} chunk={ce}: " + ", ".join(out), flush=True)
+    print(f"RMAT-{scale} warp_t={wt} chunk={ce} cta_t={max(cta, wt)}: " + ", ".join(out), flush=True)
     p.close(); g.close(); ctx.close()
