@@ -107,7 +107,7 @@ typedef struct irgl_config {
   int32_t logical_partitions;    /* >1: P vertex partitions inside this ctx (loopback exchange) */
   int32_t dense_div;             /* outlined rounds whose frontier has >= n/dense_div vertices run
                                     dense: relaxations mark (fire-and-forget stores / REDs) and a
-                                    compaction sweep builds the out worklist; 0 -> 16, <0 off    */
+                                    compaction sweep builds the out worklist; 0 -> 32, <0 off    */
   int32_t bfs_bitmap_min_n;      /* BFS tracks visited vertices in an n-bit bitmap (L2-resident)
                                     when n >= this: 0 -> 12M (level array > 48 MB), or always
                                     for a relabelled graph; <0 never                             */

@@ -1591,7 +1591,7 @@ static void fill_persist_args(irgl_ctx* ctx, irgl_pipe* pipe, irgl_graph* g, int
   pa->defer_k = op == IRGL_OP_SSSP ? nf.defer_k : 0;
   // dense rounds (mark + compaction sweep) once the frontier reaches n / dense_div
   {
-    const int32_t dd = ctx->cfg.dense_div == 0 ? 16 : ctx->cfg.dense_div;
+    const int32_t dd = ctx->cfg.dense_div == 0 ? 32 : ctx->cfg.dense_div;  // profiles/r2_dense_sweep.txt
     pa->dense_min = (dd > 0 && nf.delta <= 0) ? std::max<int64_t>(g->n / dd, 1) : 0;
   }
 }

@@ -7,7 +7,8 @@ import bench
 import paper_1607_05707_b200 as irgl
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 22
-for dd in (16, 4, 8, 32, 64, -1):
+DD = [int(x) for x in os.environ["DENSE"].split(",")] if os.environ.get("DENSE") else [16, 4, 8, 32, 64, -1]
+for dd in DD:
     ctx = irgl.Context(dense_div=dd)
     g = ctx.generate_rmat(scale)
     deg = np.diff(g.download()[0])
